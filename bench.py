@@ -1,0 +1,572 @@
+#!/usr/bin/env python
+"""Benchmark of the cafx-b200 compute-actor backend (BASELINE.json).
+
+Headline (one JSON line, rank 0): BASELINE config 3 -- one 16384x16384 fp32
+Mandelbrot request (max_iter 1000, x in [-0.75,-0.73], y in [0.10,0.12],
+pixel centres) sharded by cyclic 64-row bands over the ranks, metric Giter/s
+(sum of escape counts / time). A "step" is one pass of the hot path over the
+whole image.
+
+  value : device-resident: the escape kernel writing counts to HBM, CUDA-event
+          timed per step (L2 flushed between steps, not timed), max over ranks.
+  e2e   : through the public C ABI (cafxg_mandelbrot) into one pinned host
+          image (shared /dev/shm image registered with cafxg_host_register for
+          N>1): descriptors H2D, kernels, 1 GiB of counts D2H, wall clock.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+`--impl reference` times the reference's CPU path on the host cores: the
+oracle restatement of bench.cpp:367-390 generalised to this config (the
+reference itself hard-codes fp64 / [-1.5,0.5]x[-1,1], so it cannot run it),
+plus the unmodified reference's run_mandelbrot(16000, 500) at paper scale
+when oracle/_ref is present.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import mmap
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W_IMG = H_IMG = 16384
+MAX_ITER = 1000
+REGION = (-0.75, -0.73, 0.10, 0.12)
+BAND_ROWS = 64
+METRIC = "Mandelbrot Giter/s (BASELINE cfg3: 16384^2 fp32 max_iter=1000 zoom)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="cafxg", choices=["cafxg", "reference"])
+    p.add_argument("--no-secondary", action="store_true",
+                   help="skip the cfg1/cfg2/cfg4/cfg5 side measurements")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---- clocks during the timed region ------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.path = gpu, None, None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---- distributed helpers -------------------------------------------------------------
+
+class Dist:
+    def __init__(self, backend):
+        self.rank, self.world, self.local = env_rank()
+        self.on = self.world > 1
+        if self.on:
+            import torch.distributed as dist
+            dist.init_process_group(backend)
+            self.dist = dist
+
+    def barrier(self):
+        if self.on:
+            self.dist.barrier()
+
+    def allreduce(self, x: float, op: str) -> float:
+        if not self.on:
+            return x
+        import torch
+        dev = f"cuda:{self.local}" if self.dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op={"max": self.dist.ReduceOp.MAX,
+                                    "sum": self.dist.ReduceOp.SUM}[op])
+        return float(t.item())
+
+    def close(self):
+        if self.on:
+            self.dist.destroy_process_group()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---- CPU baselines (test infrastructure: oracle) ---------------------------------------
+
+def cpu_cfg3_sample(target_s: float = 8.0):
+    """Times the oracle restatement on a row sample of cfg3 with every host
+    thread; returns (Giter/s, cores, description)."""
+    from oracle import oracle
+    threads = os.cpu_count() or 1
+    x0, x1, y0, y1 = REGION
+
+    def run(stride):
+        t0 = time.perf_counter()
+        out = oracle.tile(x0, x1, y0, y1, W_IMG, H_IMG, MAX_ITER, fp64=False, centre=True,
+                          threads=threads, sample_stride=stride)
+        dt = time.perf_counter() - t0
+        return float(out[::stride].sum(dtype="uint64")), dt
+
+    iters, dt = run(1024)
+    rate = iters / dt
+    per_row = iters / (H_IMG // 1024)
+    rows = max(16, min(H_IMG, int(target_s * rate / per_row)))
+    stride = max(1, H_IMG // rows)
+    iters, dt = run(stride)
+    return iters / dt / 1e9, threads, (
+        f"oracle port (cafx_oracle.c, -O3 -ffp-contract=off), every {stride}th row of cfg3 "
+        f"({H_IMG // stride} rows x {W_IMG} px, {iters:.3g} iterations in {dt:.2f} s), "
+        f"{threads} threads, rows dealt cyclically")
+
+
+def reference_paper_scale():
+    """The unmodified reference's run_mandelbrot(16000, 500) (bench.cpp:481),
+    all host threads, when oracle/_ref was built."""
+    import ctypes
+    from oracle import oracle
+    R = oracle.ref()
+    if R is None or os.environ.get("CAFXG_SKIP_PAPER_SCALE"):
+        return None
+    workers = os.cpu_count() or 1
+    ms = ctypes.c_double()
+    chk = R.ref_run_mandelbrot(16000, 500, workers, ctypes.byref(ms))
+    return {"call": "run_mandelbrot(16000, 500)", "wall_clock_ms": round(ms.value, 1),
+            "checksum": str(chk), "workers": workers,
+            "published": "3.2 s on 64 Opteron cores (PAPER.md:897)"}
+
+
+# ---- the reference arm ------------------------------------------------------------------
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from oracle import oracle
+    threads = os.cpu_count() or 1
+    x0, x1, y0, y1 = REGION
+    # size the per-step sample to ~4 s of CPU work
+    t0 = time.perf_counter()
+    probe = oracle.tile(x0, x1, y0, y1, W_IMG, H_IMG, MAX_ITER, fp64=False, centre=True,
+                        threads=threads, sample_stride=1024)
+    rate = float(probe[::1024].sum()) / (time.perf_counter() - t0)
+    per_row = float(probe[::1024].sum()) / (H_IMG // 1024)
+    stride = max(1, H_IMG // max(16, min(H_IMG, int(4.0 * rate / per_row))))
+    times, iters = [], 0.0
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        out = oracle.tile(x0, x1, y0, y1, W_IMG, H_IMG, MAX_ITER, fp64=False, centre=True,
+                          threads=threads, sample_stride=stride)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(dt)
+            iters = float(out[::stride].sum(dtype="uint64"))
+    step_s = statistics.mean(times)
+    value = iters / step_s / 1e9
+    sample = (f"every {stride}th row of cfg3 ({H_IMG // stride} rows x {W_IMG} px, "
+              f"{iters:.3g} iterations per step)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Giter/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(step_s * 1e3, 2), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (deterministic plane grid)",
+        "config": {"workload": "cfg3 16384x16384 fp32 max_iter=1000 x[-0.75,-0.73] "
+                               "y[0.10,0.12] pixel centres", "sample": sample},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Giter/s", "cores": threads,
+                         "kind": "port", "sample": sample + "; the reference hard-codes "
+                         "fp64 and [-1.5,0.5]x[-1,1] (bench.cpp:384-386), so its own "
+                         "code cannot run this config; paper-scale run below"},
+        "e2e": {"value": round(value, 4), "unit": "Giter/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    paper = reference_paper_scale()
+    if paper:
+        line["reference_paper_scale"] = paper
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm --------------------------------------------------------------------------------
+
+def shared_image(world, rank, dist):
+    """One host image all ranks gather into (/dev/shm for N>1)."""
+    import numpy as np
+    nbytes = W_IMG * H_IMG * 4
+    if world == 1:
+        return None, None
+    path = f"/dev/shm/cafxg_bench_{os.environ.get('MASTER_PORT', '0')}"
+    if rank == 0:
+        with open(path, "wb") as f:
+            f.truncate(nbytes)
+    dist.barrier()
+    f = open(path, "r+b")
+    mm = mmap.mmap(f.fileno(), nbytes)
+    arr = np.frombuffer(mm, dtype=np.uint32)
+    return arr, (f, mm, path)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1505_07368_b200 as pkg
+    from paper_1505_07368_b200.shard import band_tiles
+
+    D = Dist("nccl")
+    rank, world, local = D.rank, D.world, D.local
+    torch.cuda.set_device(local)
+    ctx = pkg.Context(device_mask=1 << local)
+    full = pkg.mandel_desc(*REGION, W_IMG, H_IMG, MAX_ITER)
+    tiles_local = band_tiles(full, world, rank, BAND_ROWS, global_offsets=False)
+    tiles_global = band_tiles(full, world, rank, BAND_ROWS, global_offsets=True)
+    npx = sum(t.nrows * t.ncols for t in tiles_local)
+    dev_out = torch.empty(npx, dtype=torch.int32, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def launch():
+        ctx.mandelbrot_device(tiles_local, dev_out.data_ptr(), sp)
+
+    for _ in range(max(args.warmup, 3)):
+        launch()
+    torch.cuda.synchronize()
+    iters_local = float(dev_out.to(torch.int64).sum().item())
+    iters_total = D.allreduce(iters_local, "sum")
+
+    # ---- timed: device-resident ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    D.barrier()
+    torch.cuda.synchronize()
+    st0 = ctx.stats()
+    clocks.start()
+    for k in range(args.steps):
+        flush.zero_()                 # L2 flush, outside the timed events
+        ev[k][0].record(stream)
+        launch()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    D.barrier()
+    st1 = ctx.stats()
+    kernel_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    step_ms = D.allreduce(kernel_ms, "max")
+    value = iters_total / (step_ms / 1e3) / 1e9
+    launches = int(st1.kernel_launches - st0.kernel_launches)
+
+    # ---- timed: end to end through the C ABI into one pinned host image ----
+    if world == 1:
+        host = ctx.pinned_empty(W_IMG * H_IMG, np.uint32)
+        shm = None
+    else:
+        host, shm = shared_image(world, rank, D)
+        ctx.host_register(host)
+    for _ in range(1):
+        ctx.mandelbrot(tiles_global, host)
+    D.barrier()
+    e2e_times = []
+    st2 = ctx.stats()
+    for _ in range(args.steps):
+        D.barrier()
+        t0 = time.perf_counter()
+        ctx.mandelbrot(tiles_global, host)
+        e2e_times.append(time.perf_counter() - t0)
+    D.barrier()
+    st3 = ctx.stats()
+    e2e_ms = D.allreduce(statistics.mean(e2e_times) * 1e3, "max")
+    e2e_value = iters_total / (e2e_ms / 1e3) / 1e9
+    h2d = D.allreduce(float(st3.h2d_bytes - st2.h2d_bytes) / args.steps, "sum")
+    d2h = D.allreduce(float(st3.d2h_bytes - st2.d2h_bytes) / args.steps, "sum")
+    # parity spot check of the gathered image (full image at N=1, bands at N>1)
+    spot_ok = True
+    if rank == 0:
+        from oracle import oracle
+        img = host.reshape(H_IMG, W_IMG)
+        for r in (0, 4097, H_IMG - 1):
+            ref = oracle.tile(*REGION, W_IMG, H_IMG, MAX_ITER, fp64=False, centre=True,
+                              row0=r, nrows=1)
+            spot_ok = spot_ok and bool(np.array_equal(img[r], ref[0]))
+
+    # ---- roofline of the escape kernel (per GPU) ----
+    pk = peaks()
+    sm_max = float(pk.get("sm_max_mhz") or 1965.0)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    peak_tops = sms * 128 * sm_max * 1e6 / 1e12
+    achieved = 8.0 * iters_local / (kernel_ms / 1e3) / 1e12
+    roof = {"bound": "fp32_pipe", "achieved": round(achieved, 3), "peak": round(peak_tops, 3),
+            "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4), "traffic": None,
+            "ops_per_launch": 8.0 * iters_local,
+            "peak_basis": f"{sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz of "
+                          "MEASURED_PEAKS.json); algorithmic 8 FP ops per escape iteration "
+                          "(3 mul + 5 add, SURVEY §8d)"}
+    if clk.get("sm_mhz"):
+        peak_clk = sms * 128 * clk["sm_mhz"] * 1e6 / 1e12
+        roof["frac_at_measured_clock"] = round(achieved / peak_clk, 4)
+
+    secondary = {}
+    if world == 1 and not args.no_secondary:
+        secondary = run_secondary(ctx, args)
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        v, cores, desc = cpu_cfg3_sample()
+        cpu = {"value": round(v, 4), "unit": "Giter/s", "cores": cores, "kind": "port",
+               "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Giter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (deterministic plane grid, BASELINE cfg3)",
+            "config": {"workload": "cfg3: one 16384x16384 fp32 Mandelbrot request, "
+                                   "max_iter=1000, x[-0.75,-0.73] y[0.10,0.12], pixel centres",
+                       "sharding": f"cyclic {BAND_ROWS}-row bands over {world} rank(s)",
+                       "iterations_per_step": iters_total,
+                       "l2": "256 MiB L2 flush between steps (untimed); output >= 128 MiB/rank",
+                       "bit_exact_spot_check": spot_ok},
+            "e2e": {"value": round(e2e_value, 3), "unit": "Giter/s",
+                    "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "path": "cafxg_mandelbrot (C ABI) -> pinned host image"},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "clocks": clk,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        if secondary:
+            line["secondary"] = secondary
+        print(json.dumps(line), flush=True)
+    if shm:
+        ctx.host_unregister(host)
+        del host
+        shm[1].close()
+        shm[0].close()
+        if rank == 0:
+            try:
+                os.unlink(shm[2])
+            except OSError:
+                pass
+    ctx.close()
+    D.close()
+
+
+def run_secondary(ctx, args):
+    """cfg1, cfg2/cfg5 (matmul), cfg4 (request storm) at N=1; few steps each."""
+    import numpy as np
+    import torch
+
+    import paper_1505_07368_b200 as pkg
+    from oracle import oracle
+    out = {}
+    stream = torch.cuda.current_stream()
+    steps = max(3, min(args.steps, 10))
+
+    def dev_time(fn, n):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    # cfg1: 1920x1080 fp32 it=100, one request
+    d1 = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)
+    o1 = torch.empty(1920 * 1080, dtype=torch.int32, device="cuda")
+    ms = dev_time(lambda: ctx.mandelbrot_device(d1, o1.data_ptr(), stream.cuda_stream), 20)
+    it1 = float(o1.to(torch.int64).sum().item())
+    h1 = ctx.pinned_empty(1920 * 1080, np.uint32)
+    ctx.mandelbrot(d1, h1)
+    t0 = time.perf_counter()
+    for _ in range(20):
+        ctx.mandelbrot(d1, h1)
+    e2e = (time.perf_counter() - t0) / 20 * 1e3
+    ctx.pinned_free(h1)
+    out["cfg1_mandelbrot_1920x1080_fp32"] = {
+        "kernel_ms": round(ms, 4), "giter_s": round(it1 / ms / 1e6, 2),
+        "e2e_ms": round(e2e, 4), "e2e_giter_s": round(it1 / e2e / 1e6, 2)}
+
+    # cfg2 / cfg5: fp32 matmul
+    for n, label in [(1024, "cfg2_sgemm_1024"), (16384, "cfg5_sgemm_16384")]:
+        A = torch.from_numpy(oracle.fill_uniform(n * n, 1).reshape(n, n)).cuda()
+        B = torch.from_numpy(oracle.fill_uniform(n * n, 2).reshape(n, n)).cuda()
+        C = torch.empty(n, n, device="cuda")
+        reps = 20 if n <= 2048 else 3
+        ms = dev_time(lambda: ctx.sgemm_device(n, n, n, A.data_ptr(), B.data_ptr(),
+                                               C.data_ptr(), stream.cuda_stream), reps)
+        tflops = 2.0 * n ** 3 / (ms / 1e3) / 1e12
+        rows = np.arange(0, n, max(1, n // 16), dtype=np.uint32)
+        An, Bn, Cn = A.cpu().numpy(), B.cpu().numpy(), C.cpu().numpy()
+        R = oracle.sgemm_ref_rows(An, Bn, rows, n, n)
+        err = oracle.sgemm_rel_err(Cn, R, rows, n)
+        hA, hB = ctx.pinned_empty((n, n), np.float32), ctx.pinned_empty((n, n), np.float32)
+        hC = ctx.pinned_empty((n, n), np.float32)
+        hA[...] = An
+        hB[...] = Bn
+        ctx.sgemm(hA, hB, hC)
+        e2e_reps = 5 if n <= 2048 else 2
+        t0 = time.perf_counter()
+        for _ in range(e2e_reps):
+            ctx.sgemm(hA, hB, hC)
+        e2e = (time.perf_counter() - t0) / e2e_reps * 1e3
+        for h in (hA, hB, hC):
+            ctx.pinned_free(h)
+        out[label] = {"kernel_ms": round(ms, 3), "tflops": round(tflops, 2),
+                      "e2e_ms": round(e2e, 3),
+                      "e2e_tflops": round(2.0 * n ** 3 / (e2e / 1e3) / 1e12, 2),
+                      "max_rel_err_sampled_rows": err, "tolerance": 1e-5}
+        del A, B, C
+
+    out["cfg4_request_storm"] = run_storm(ctx)
+    return out
+
+
+def run_storm(ctx, clients=64, per=1600, seed=2024):
+    """64 client threads x 1600 requests, each a 64x64 fp64 tile (pitch 1/512,
+    max_iter 256) at a seeded offset; every reply lands in a pinned buffer.
+    Each client keeps all its requests in flight (async send with
+    sender-directed replies)."""
+    import numpy as np
+
+    import paper_1505_07368_b200 as pkg
+    from oracle import oracle
+    rng = np.random.default_rng(seed)
+    kx = rng.integers(0, 3 * 512 - 64 + 1, size=(clients, per))
+    ky = rng.integers(0, 2 * 512 - 64 + 1, size=(clients, per))
+    descs = (pkg.MandelDesc * (clients * per))()
+    for c in range(clients):
+        for i in range(per):
+            x0, y0 = -2.0 + kx[c, i] / 512, -1.0 + ky[c, i] / 512
+            descs[c * per + i] = pkg.mandel_desc(x0, x0 + 0.125, y0, y0 + 0.125, 64, 64, 256,
+                                                 fp64=True, centre=True)
+    replies = ctx.pinned_empty((clients * per, 4096), np.uint32)
+    actor = ctx.spawn("mandelbrot")
+    import ctypes as C
+    L = pkg.lib()
+    done_count = [0]
+    lock = threading.Lock()
+    all_done = threading.Event()
+    total = clients * per
+
+    @pkg.cafxg.DONE_FN
+    def on_done(user, status):
+        with lock:
+            done_count[0] += 1
+            if status != 0:
+                done_count.append(status)
+            if done_count[0] == total:
+                all_done.set()
+    size = C.c_size_t(C.sizeof(pkg.MandelDesc))
+    base = C.addressof(descs)
+    rbase = replies.ctypes.data
+
+    def client(c):
+        ptr = (C.c_void_p * 1)()
+        sz = (C.c_size_t * 1)(size)
+        for i in range(per):
+            k = c * per + i
+            ptr[0] = base + k * C.sizeof(pkg.MandelDesc)
+            rc = L.cafxg_actor_enqueue(actor.handle, ptr, sz, 1, rbase + k * 16384, 16384,
+                                       on_done, None)
+            assert rc == 0
+
+    st0 = ctx.stats()
+    t0 = time.perf_counter()
+    th = [threading.Thread(target=client, args=(c,)) for c in range(clients)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    all_done.wait(600)
+    dt = time.perf_counter() - t0
+    st1 = ctx.stats()
+    iters = float(replies.sum(dtype=np.uint64))
+    # per-tile check of a seeded sample of replies against the fp64 oracle
+    bad = 0
+    for k in np.random.default_rng(seed + 1).integers(0, total, size=128):
+        d = descs[int(k)]
+        ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, 64, 64, 256, fp64=True, centre=True,
+                          threads=1)
+        bad += int(not np.array_equal(replies[int(k)].reshape(64, 64), ref))
+    actor.release()
+    ctx.pinned_free(replies)
+    return {"requests": total, "clients": clients, "wall_ms": round(dt * 1e3, 2),
+            "requests_per_s": round(total / dt, 1), "giter_s": round(iters / dt / 1e9, 2),
+            "batches": int(st1.batches - st0.batches), "max_batch": int(st1.max_batch),
+            "kernel_launches": int(st1.kernel_launches - st0.kernel_launches),
+            "errors": len(done_count) - 1, "checked_tiles": 128, "mismatched_tiles": bad}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

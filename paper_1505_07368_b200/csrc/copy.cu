@@ -1,0 +1,43 @@
+// Reply scatter: copies each request's counts from the batch's device staging
+// buffer straight into its (mapped, pinned) host reply buffer, so a batch of
+// N small replies costs one launch instead of N cudaMemcpyAsync calls.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.hpp"
+
+namespace cafxg {
+namespace {
+
+__global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg* segs,
+                                                            uint32_t n) {
+  for (uint32_t s = blockIdx.x; s < n; s += gridDim.x) {
+    const CopySeg g = segs[s];
+    const uintptr_t a = (uintptr_t)g.src | (uintptr_t)g.dst | (uintptr_t)g.bytes;
+    if ((a & 15u) == 0) {
+      const uint4* src = (const uint4*)g.src;
+      uint4* dst = (uint4*)g.dst;
+      const uint64_t n16 = g.bytes >> 4;
+      for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x)
+        dst[i] = __ldg(src + i);
+    } else {
+      const uint8_t* src = (const uint8_t*)g.src;
+      uint8_t* dst = (uint8_t*)g.dst;
+      for (uint64_t i = threadIdx.x; i < g.bytes; i += blockDim.x)
+        dst[i] = src[i];
+    }
+  }
+}
+
+}  // namespace
+
+int copy_segments_launch(const CopySeg* segs_dev, uint32_t n, void* stream) {
+  if (n == 0)
+    return 0;
+  uint32_t grid = n < 4096 ? n : 4096;
+  copy_segments_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(segs_dev, n);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace cafxg

@@ -1,0 +1,390 @@
+// Escape-time (Mandelbrot) kernels for sm_100a.
+//
+// Reference semantics: cafx::bench::mandelbrot_cell
+// (/root/reference/proj/src/bench/bench.cpp:367-379), generalised per
+// SURVEY.md §8a row a2 (include/cafxg.h documents the coordinate contract).
+//
+// Design:
+//  * persistent grid; each warp pulls 512-pixel chunks from a global cursor
+//    and every lane carries TWO independent pixels ("slots"). In fp32 the two
+//    slots live in the halves of 64-bit registers and each escape step is
+//    issued as packed FADD2/FMUL2/FFMA2 instructions (f32x2, new in sm_100):
+//    7 packed FP instructions advance 2 pixels by one iteration;
+//  * bit-exact counting without per-step branches: a sticky escape predicate
+//    (FSETP.OR) and a counter that stops at the first escape. After the first
+//    escape z keeps iterating (to inf/NaN) but the predicate never clears, so
+//    `count = escaped ? steps_before + 1 : steps` equals the reference's
+//    early-exit loop, capped at max_iter (an escape exactly at max_iter also
+//    returns max_iter, as bench.cpp:378);
+//  * refill: every `ksteps` iterations the warp votes; lanes whose pixel is
+//    finished store the count and take the next pixel from the warp's chunk,
+//    so no lane idles behind a slow neighbour (divergence-free main loop);
+//  * every FP op is an explicit round-to-nearest intrinsic / `.rn` PTX op, so
+//    nvcc can never contract the reference's separate mul and add into FMA.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mandelbrot.cuh"
+
+namespace cafxg {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---- the escape-iteration block ----------------------------------------------
+// kSteps iterations of the reference loop (bench.cpp:370-377) for a lane's two
+// slots, written as one PTX block so the escape bookkeeping stays in
+// predicates: per slot and step one `setp.gt.or` (sticky escape flag) and one
+// predicated add (the count stops at the first escape). Reference order, with
+// the squares shared between the escape test and the next step exactly as the
+// compiled reference does:
+//   nr = (zr*zr - zi*zi) + re ; ni = (2*zr)*zi + im ; escape if nr^2+ni^2 > 4
+//
+// fp32 packs the two slots into the halves of 64-bit registers (f32x2, new in
+// sm_100): 7 packed FP instructions advance both pixels by one iteration.
+// Two ptxas facts shape the text:
+//  * ptxas 12.9 contracts `mul.rn.f32x2` + `add.rn.f32x2` into FFMA2 in spite
+//    of the explicit rounding (checked in SASS). Squares are therefore formed
+//    as fma(a, a, z) with z a RUNTIME +0.0 (MLaunch::zero): fl(a*a + 0) ==
+//    fl(a*a) and an FFMA2 result is never fused further;
+//  * the fast step folds `(2*zr)*zi + im` into fma(zr*zi, 2, im): fl(2zr)*zi
+//    rounds to 2*fl(zr*zi) (power-of-two scaling commutes with rounding) and
+//    fl(2v + im) with 2v exact is one fma. Bit-identical unless fl(zr*zi) is
+//    subnormal, which the host rules out per request; the
+//    `exact` step keeps the reference's 8 separate operations.
+
+#define CAFXG_F32_STEP_FAST                                 \
+  "sub.rn.f32x2 t, q, w;\n\t"                               \
+  "add.rn.f32x2 t, t, c;\n\t"                               \
+  "mul.rn.f32x2 v, x, y;\n\t"                               \
+  "fma.rn.f32x2 y, v, two, d;\n\t"                          \
+  "mov.b64 x, t;\n\t"                                       \
+  "fma.rn.f32x2 q, x, x, zz;\n\t"                           \
+  "fma.rn.f32x2 w, y, y, zz;\n\t"                           \
+  "add.rn.f32x2 s, q, w;\n\t"                               \
+  "mov.b64 {s0, s1}, s;\n\t"                                \
+  "setp.gt.or.f32 p0, s0, 0f40800000, p0;\n\t"              \
+  "setp.gt.or.f32 p1, s1, 0f40800000, p1;\n\t"              \
+  "@!p0 add.u32 %4, %4, 1;\n\t"                             \
+  "@!p1 add.u32 %5, %5, 1;\n\t"
+
+#define CAFXG_F32_STEP_EXACT                                \
+  "sub.rn.f32x2 t, q, w;\n\t"                               \
+  "add.rn.f32x2 t, t, c;\n\t"                               \
+  "add.rn.f32x2 v, x, x;\n\t"                               \
+  "fma.rn.f32x2 v, v, y, zz;\n\t"                           \
+  "add.rn.f32x2 y, v, d;\n\t"                               \
+  "mov.b64 x, t;\n\t"                                       \
+  "fma.rn.f32x2 q, x, x, zz;\n\t"                           \
+  "fma.rn.f32x2 w, y, y, zz;\n\t"                           \
+  "add.rn.f32x2 s, q, w;\n\t"                               \
+  "mov.b64 {s0, s1}, s;\n\t"                                \
+  "setp.gt.or.f32 p0, s0, 0f40800000, p0;\n\t"              \
+  "setp.gt.or.f32 p1, s1, 0f40800000, p1;\n\t"              \
+  "@!p0 add.u32 %4, %4, 1;\n\t"                             \
+  "@!p1 add.u32 %5, %5, 1;\n\t"
+
+// operands: %0,%1 zr; %2,%3 zi; %4 n0; %5 n1; %6 e0; %7 e1; %8,%9 zr^2;
+// %10,%11 zi^2; %12,%13 cr; %14,%15 ci; %16 runtime zero; %17 2.0f.
+#define CAFXG_F32_PROLOGUE                                  \
+  "{\n\t.reg .b64 x, y, q, w, c, d, t, v, s, two, zz;\n\t"  \
+  ".reg .f32 s0, s1;\n\t.reg .pred p0, p1;\n\t"             \
+  "mov.b64 x, {%0, %1};\n\tmov.b64 y, {%2, %3};\n\t"        \
+  "mov.b64 q, {%8, %9};\n\tmov.b64 w, {%10, %11};\n\t"      \
+  "mov.b64 c, {%12, %13};\n\tmov.b64 d, {%14, %15};\n\t"    \
+  "mov.b64 zz, {%16, %16};\n\t"                             \
+  "mov.b64 two, {%17, %17};\n\t"                            \
+  "setp.ne.u32 p0, %6, 0;\n\tsetp.ne.u32 p1, %7, 0;\n\t"
+
+#define CAFXG_F32_EPILOGUE                                  \
+  "mov.b64 {%0, %1}, x;\n\tmov.b64 {%2, %3}, y;\n\t"        \
+  "mov.b64 {%8, %9}, q;\n\tmov.b64 {%10, %11}, w;\n\t"      \
+  "selp.u32 %6, 1, 0, p0;\n\tselp.u32 %7, 1, 0, p1;\n\t}"
+
+#define CAFXG_X4(S) S S S S
+#define CAFXG_X16(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S)
+
+#define CAFXG_F32_OPERANDS                                                   \
+  : "+f"(zr.x), "+f"(zr.y), "+f"(zi.x), "+f"(zi.y), "+r"(n0), "+r"(n1),       \
+    "+r"(e0), "+r"(e1), "+f"(zr2.x), "+f"(zr2.y), "+f"(zi2.x), "+f"(zi2.y)    \
+  : "f"(cr.x), "f"(cr.y), "f"(ci.x), "f"(ci.y), "f"(zero), "f"(2.0f)
+
+struct F32Slots {
+  using S = float;
+  float2 zr{}, zi{}, zr2{}, zi2{}, cr{}, ci{};
+  float zero;
+
+  template <int kSteps, bool kExact>
+  __device__ __forceinline__ void run(uint32_t& n0, uint32_t& n1, uint32_t& e0,
+                                      uint32_t& e1) {
+    if constexpr (kSteps == 16 && !kExact)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X16(CAFXG_F32_STEP_FAST)
+                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
+    else if constexpr (kSteps == 16 && kExact)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X16(CAFXG_F32_STEP_EXACT)
+                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
+    else if constexpr (kSteps == 4 && !kExact)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP_FAST)
+                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
+    else
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP_EXACT)
+                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
+  }
+  __device__ __forceinline__ void start(int slot, double xr, double xi) {
+    float fr = __double2float_rn(xr), fi = __double2float_rn(xi);
+    if (slot == 0) {
+      cr.x = fr; ci.x = fi; zr.x = zi.x = zr2.x = zi2.x = 0.0f;
+    } else {
+      cr.y = fr; ci.y = fi; zr.y = zi.y = zr2.y = zi2.y = 0.0f;
+    }
+  }
+};
+
+// fp64: two scalar slots; scalar `.rn` ops are never contracted by ptxas.
+#define CAFXG_F64_STEP_FAST(X, Y, Q, W, C, D, P, N)                 \
+  "sub.rn.f64 t, " Q ", " W ";\n\t"                                  \
+  "add.rn.f64 t, t, " C ";\n\t"                                      \
+  "mul.rn.f64 v, " X ", " Y ";\n\t"                                  \
+  "fma.rn.f64 " Y ", v, 0d4000000000000000, " D ";\n\t"              \
+  "mov.f64 " X ", t;\n\t"                                            \
+  "mul.rn.f64 " Q ", " X ", " X ";\n\t"                              \
+  "mul.rn.f64 " W ", " Y ", " Y ";\n\t"                              \
+  "add.rn.f64 s, " Q ", " W ";\n\t"                                  \
+  "setp.gt.or.f64 " P ", s, 0d4010000000000000, " P ";\n\t"          \
+  "@!" P " add.u32 " N ", " N ", 1;\n\t"
+
+#define CAFXG_F64_STEP_EXACT(X, Y, Q, W, C, D, P, N)                \
+  "sub.rn.f64 t, " Q ", " W ";\n\t"                                  \
+  "add.rn.f64 t, t, " C ";\n\t"                                      \
+  "add.rn.f64 v, " X ", " X ";\n\t"                                  \
+  "mul.rn.f64 v, v, " Y ";\n\t"                                      \
+  "add.rn.f64 " Y ", v, " D ";\n\t"                                  \
+  "mov.f64 " X ", t;\n\t"                                            \
+  "mul.rn.f64 " Q ", " X ", " X ";\n\t"                              \
+  "mul.rn.f64 " W ", " Y ", " Y ";\n\t"                              \
+  "add.rn.f64 s, " Q ", " W ";\n\t"                                  \
+  "setp.gt.or.f64 " P ", s, 0d4010000000000000, " P ";\n\t"          \
+  "@!" P " add.u32 " N ", " N ", 1;\n\t"
+
+#define CAFXG_F64_PAIR(STEP)                                             \
+  STEP("%0", "%1", "%2", "%3", "%12", "%13", "p0", "%8")                 \
+  STEP("%4", "%5", "%6", "%7", "%14", "%15", "p1", "%9")
+
+#define CAFXG_F64_PROLOGUE                                               \
+  "{\n\t.reg .f64 t, v, s;\n\t.reg .pred p0, p1;\n\t"                    \
+  "setp.ne.u32 p0, %10, 0;\n\tsetp.ne.u32 p1, %11, 0;\n\t"
+#define CAFXG_F64_EPILOGUE                                               \
+  "selp.u32 %10, 1, 0, p0;\n\tselp.u32 %11, 1, 0, p1;\n\t}"
+#define CAFXG_F64_OPERANDS                                               \
+  : "+d"(zr.x), "+d"(zi.x), "+d"(zr2.x), "+d"(zi2.x), "+d"(zr.y),         \
+    "+d"(zi.y), "+d"(zr2.y), "+d"(zi2.y), "+r"(n0), "+r"(n1), "+r"(e0),   \
+    "+r"(e1)                                                            \
+  : "d"(cr.x), "d"(ci.x), "d"(cr.y), "d"(ci.y)
+
+struct F64Slots {
+  using S = double;
+  double2 zr{}, zi{}, zr2{}, zi2{}, cr{}, ci{};
+  float zero;
+
+  template <int kSteps, bool kExact>
+  __device__ __forceinline__ void run(uint32_t& n0, uint32_t& n1, uint32_t& e0,
+                                      uint32_t& e1) {
+    if constexpr (kSteps == 16 && !kExact)
+      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X16(CAFXG_F64_PAIR(
+          CAFXG_F64_STEP_FAST)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
+    else if constexpr (kSteps == 16 && kExact)
+      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X16(CAFXG_F64_PAIR(
+          CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
+    else if constexpr (kSteps == 4 && !kExact)
+      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X4(CAFXG_F64_PAIR(
+          CAFXG_F64_STEP_FAST)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
+    else
+      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X4(CAFXG_F64_PAIR(
+          CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
+  }
+  __device__ __forceinline__ void start(int slot, double xr, double xi) {
+    if (slot == 0) {
+      cr.x = xr; ci.x = xi; zr.x = zi.x = zr2.x = zi2.x = 0.0;
+    } else {
+      cr.y = xr; ci.y = xi; zr.y = zi.y = zr2.y = zi2.y = 0.0;
+    }
+  }
+};
+
+__device__ __forceinline__ const MTile* tile_ptr(const MLaunch& L, uint32_t t) {
+  return L.n <= (uint32_t)kInlineTiles ? &L.inl[t] : &L.tiles[t];
+}
+
+__device__ __forceinline__ uint32_t find_tile(const MLaunch& L, uint32_t chunk) {
+  uint32_t lo = 0, hi = L.n - 1;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi + 1) >> 1;
+    if (tile_ptr(L, mid)->chunk_begin <= chunk)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// Coordinates of pixel p (tile-local, row-major) of tile T, as the oracle
+// computes them: lo + ((i + s) * span) / n in fp64 with IEEE rounding.
+__device__ __forceinline__ void pixel_coord(const MTile* T, uint32_t p,
+                                            double& cr, double& ci) {
+  uint32_t row = p / T->ncols;
+  uint32_t col = p - row * T->ncols;
+  double kx = __dadd_rn((double)(T->col0 + col), T->s);
+  double ky = __dadd_rn((double)(T->row0 + row), T->s);
+  cr = __dadd_rn(T->x0, __ddiv_rn(__dmul_rn(kx, T->xspan), (double)T->width));
+  ci = __dadd_rn(T->y0, __ddiv_rn(__dmul_rn(ky, T->yspan), (double)T->height));
+}
+
+template <class Slots, int kSteps, bool kExact>
+__global__ void __launch_bounds__(kMandelThreads)
+    mandel_kernel(const __grid_constant__ MLaunch L) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+
+  // warp-uniform chunk cursor
+  uint32_t cur = 0, cend = 0;
+  const MTile* T = nullptr;
+  bool exhausted = false;
+
+  Slots sl;
+  sl.zero = L.zero;
+  uint32_t e0 = 0, e1 = 0;  // sticky escape flags (0/1)
+  uint32_t n0 = 0, n1 = 0;  // iterations completed without escape
+  uint32_t m0 = 0, m1 = 0;  // max_iter of the slot's pixel
+  bool live0 = false, live1 = false;
+  uint32_t *o0 = nullptr, *o1 = nullptr;
+
+  auto refill = [&]() {
+    while (true) {
+      uint32_t b0 = __ballot_sync(kFull, !live0);
+      uint32_t b1 = __ballot_sync(kFull, !live1);
+      uint32_t want = __popc(b0) + __popc(b1);
+      if (want == 0 || exhausted)
+        return;
+      if (cur == cend) {
+        uint32_t c = 0;
+        if (lane == 0)
+          c = atomicAdd(&L.sched[0], 1u);
+        c = __shfl_sync(kFull, c, 0);
+        if (c >= L.total_chunks) {
+          exhausted = true;
+          return;
+        }
+        uint32_t t = find_tile(L, c);
+        T = tile_ptr(L, t);
+        uint32_t npix = T->nrows * T->ncols;
+        cur = (c - T->chunk_begin) * kChunk;
+        cend = min(cur + kChunk, npix);
+        continue;
+      }
+      uint32_t avail = cend - cur;
+      uint32_t r0 = __popc(b0 & lt_mask);
+      uint32_t r1 = __popc(b0) + __popc(b1 & lt_mask);
+      if (!live0 && r0 < avail) {
+        double xr, xi;
+        uint32_t p = cur + r0;
+        pixel_coord(T, p, xr, xi);
+        sl.start(0, xr, xi);
+        e0 = 0;
+        n0 = 0;
+        m0 = T->max_iter;
+        o0 = T->out + p;
+        live0 = true;
+      }
+      if (!live1 && r1 < avail) {
+        double xr, xi;
+        uint32_t p = cur + r1;
+        pixel_coord(T, p, xr, xi);
+        sl.start(1, xr, xi);
+        e1 = 0;
+        n1 = 0;
+        m1 = T->max_iter;
+        o1 = T->out + p;
+        live1 = true;
+      }
+      cur += min(want, avail);
+    }
+  };
+
+  refill();
+  while (__any_sync(kFull, live0 || live1)) {
+    sl.template run<kSteps, kExact>(n0, n1, e0, e1);
+    bool d0 = live0 && (e0 || n0 >= m0);
+    bool d1 = live1 && (e1 || n1 >= m1);
+    if (__any_sync(kFull, d0 || d1)) {
+      if (d0) {
+        *o0 = min(e0 ? n0 + 1u : n0, m0);
+        live0 = false;
+      }
+      if (d1) {
+        *o1 = min(e1 ? n1 + 1u : n1, m1);
+        live1 = false;
+      }
+      refill();
+    }
+  }
+
+  // Self-resetting scheduler: the last block to finish zeroes the cursor so
+  // the slot can serve the next launch without a memset.
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    uint32_t prev = atomicAdd(&L.sched[1], 1u);
+    if (prev == gridDim.x - 1) {
+      L.sched[0] = 0;
+      L.sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+template <class A, int kSteps, bool kExact>
+int launch_t(const MLaunch& L, int grid, cudaStream_t s) {
+  mandel_kernel<A, kSteps, kExact><<<grid, kMandelThreads, 0, s>>>(L);
+  return (int)cudaGetLastError();
+}
+
+template <class A, int kSteps, bool kExact>
+int occ_t() {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &n, mandel_kernel<A, kSteps, kExact>, kMandelThreads, 0);
+  return n;
+}
+
+}  // namespace
+
+#define CAFXG_MANDEL_DISPATCH(FN, ...)                                  \
+  do {                                                                  \
+    if (precision == 0) {                                               \
+      if (ksteps <= 4)                                                  \
+        return exact ? FN<F32Slots, 4, true>(__VA_ARGS__)                  \
+                     : FN<F32Slots, 4, false>(__VA_ARGS__);                \
+      return exact ? FN<F32Slots, 16, true>(__VA_ARGS__)                   \
+                   : FN<F32Slots, 16, false>(__VA_ARGS__);                 \
+    }                                                                   \
+    if (ksteps <= 4)                                                    \
+      return exact ? FN<F64Slots, 4, true>(__VA_ARGS__)                    \
+                   : FN<F64Slots, 4, false>(__VA_ARGS__);                  \
+    return exact ? FN<F64Slots, 16, true>(__VA_ARGS__)                     \
+                 : FN<F64Slots, 16, false>(__VA_ARGS__);                   \
+  } while (0)
+
+int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,
+                  void* stream) {
+  const int ksteps = cfg.ksteps;
+  const bool exact = cfg.exact;
+  cudaStream_t s = (cudaStream_t)stream;
+  CAFXG_MANDEL_DISPATCH(launch_t, L, cfg.grid, s);
+}
+
+int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact) {
+  CAFXG_MANDEL_DISPATCH(occ_t);
+}
+
+}  // namespace cafxg

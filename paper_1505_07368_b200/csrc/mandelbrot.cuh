@@ -1,0 +1,49 @@
+// Device-side descriptors shared by the Mandelbrot kernels and the host
+// dispatcher (runtime.cpp).
+#pragma once
+#include <cstdint>
+
+namespace cafxg {
+
+// One tile of a batch, as the kernel sees it. Built on the host from
+// cafxg_mandel_desc (include/cafxg.h). Tiles are split into chunks of
+// kChunk pixels; chunks never straddle tiles, and chunk_begin is the global
+// index of the tile's first chunk (ascending across the batch).
+struct MTile {
+  double x0, xspan, y0, yspan;  // xspan = x1 - x0, yspan = y1 - y0 (fp64)
+  double s;                     // 0 (corner) or 0.5 (pixel centre)
+  uint32_t width, height;       // full image, for the coordinate mapping
+  uint32_t row0, col0;          // tile origin in the image
+  uint32_t nrows, ncols;
+  uint32_t max_iter;
+  uint32_t chunk_begin;
+  uint32_t* out;                // tile's first count; row-major, pitch ncols
+};
+
+constexpr int kInlineTiles = 8;    // tiles passed by value in the params
+constexpr uint32_t kChunk = 512;   // pixels per work chunk
+constexpr int kMandelThreads = 256;
+
+struct MLaunch {
+  MTile inl[kInlineTiles];
+  const MTile* tiles;   // device copy when n > kInlineTiles
+  uint32_t n;
+  uint32_t total_chunks;
+  uint32_t* sched;      // [0] chunk cursor, [1] finished blocks (self-reset)
+  float zero;           // always 0.0f; opaque to ptxas (see F32x2::mulz)
+};
+
+// Host launchers (mandelbrot.cu). precision: 0 = fp32, 1 = fp64.
+// `exact` selects the 8-op escape step; the default 7-op step folds
+// 2*zr*zi + ci into fma(zr*zi, 2, ci), which is bit-identical whenever no
+// row has 0 < |ci| < 2^-100 (fp32) / 2^-960 (fp64): see DESIGN.md §3.
+struct MandelLaunchCfg {
+  int grid;
+  int ksteps;      // unchecked steps between refills
+  bool exact;
+};
+int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,
+                  void* stream);
+int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact);
+
+}  // namespace cafxg

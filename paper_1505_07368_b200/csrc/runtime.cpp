@@ -1,0 +1,1453 @@
+// libcafxg.so host runtime: contexts, devices, pinned pool, completion
+// threads, multi-device request splitting, compute actors and the batching
+// dispatcher behind the C ABI of include/cafxg.h.
+//
+// Reference mapping (what each piece replaces in CAF's OpenCL path):
+//  * cafxg_spawn / cafxg_actor_enqueue  -> spawn_cl + the actor's enqueue
+//    (seam abstract_actor::enqueue, abstract_actor.hpp:36);
+//  * completion threads                 -> the reply path of local_actor::
+//    respond (local_actor.cpp:319-329), run off the scheduler workers;
+//  * the dispatcher's MPSC inbox        -> cached_stack_mailbox
+//    (mailbox.cpp:13-62): one CAS per enqueue, one exchange per drain;
+//  * cafxg_actor_quit                   -> hard-kill exit + request_down
+//    errors for pending requests (actor_system.cpp:243-258,
+//    abstract_actor.cpp:126-131).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "common.hpp"
+#include "mandelbrot.cuh"
+#include "sgemm.cuh"
+
+namespace cafxg {
+
+// ---- error context -----------------------------------------------------------
+
+static thread_local std::string t_last_error;
+
+void set_last_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+}
+
+void clear_last_error() { t_last_error.clear(); }
+
+// ---- pinned host pool -----------------------------------------------------------
+// Page-locked, portable, device-mapped buffers cached by power-of-two size
+// class. Reply buffers that live here are written by DMA or by the reply
+// scatter kernel directly.
+class PinnedPool {
+ public:
+  ~PinnedPool() {
+    std::lock_guard<std::mutex> g(mu_);
+    for (auto& kv : free_)
+      for (void* p : kv.second)
+        cudaFreeHost(p);
+    for (auto& kv : live_)
+      cudaFreeHost(kv.first);
+  }
+
+  void* alloc(size_t bytes) {
+    size_t cls = size_class(bytes);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      auto it = free_.find(cls);
+      if (it != free_.end() && !it->second.empty()) {
+        void* p = it->second.back();
+        it->second.pop_back();
+        live_[p] = cls;
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, cls, cudaHostAllocPortable | cudaHostAllocMapped) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    std::lock_guard<std::mutex> g(mu_);
+    live_[p] = cls;
+    return p;
+  }
+
+  bool free(void* p) {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = live_.find(p);
+    if (it == live_.end())
+      return false;
+    free_[it->second].push_back(p);
+    live_.erase(it);
+    return true;
+  }
+
+ private:
+  static size_t size_class(size_t bytes) {
+    size_t c = 4096;
+    while (c < bytes)
+      c <<= 1;
+    return c;
+  }
+  std::mutex mu_;
+  std::unordered_map<void*, size_t> live_;
+  std::map<size_t, std::vector<void*>> free_;
+};
+
+// True when [p, p+bytes) is page-locked host memory the device can address
+// (our pool, cudaHostRegister'ed or torch pin_memory buffers).
+static bool host_is_pinned(const void* p, size_t bytes) {
+  if (!p)
+    return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type != cudaMemoryTypeHost || a.devicePointer != p)
+    return false;
+  if (bytes > 1) {
+    cudaPointerAttributes b{};
+    const char* last = static_cast<const char*>(p) + bytes - 1;
+    if (cudaPointerGetAttributes(&b, last) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return b.type == cudaMemoryTypeHost && b.devicePointer == last;
+  }
+  return true;
+}
+
+// ---- NCCL (loaded lazily; only multi-device sgemm needs it) ------------------------
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t,
+                            ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  bool load() {
+    if (ok)
+      return true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h)
+      h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h)
+      return false;
+    CommInitAll = (decltype(CommInitAll))dlsym(h, "ncclCommInitAll");
+    AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+    GroupStart = (decltype(GroupStart))dlsym(h, "ncclGroupStart");
+    GroupEnd = (decltype(GroupEnd))dlsym(h, "ncclGroupEnd");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    ok = CommInitAll && AllGather && GroupStart && GroupEnd && CommDestroy;
+    return ok;
+  }
+};
+
+// ---- devices and completion -----------------------------------------------------------
+
+struct Completion {
+  cudaEvent_t ev;
+  std::function<void(int)> fn;
+};
+
+constexpr uint32_t kSchedSlots = 1024;
+
+struct Device {
+  int ordinal = 0;
+  int sms = 0;
+  cudaStream_t compute = nullptr, d2h = nullptr;
+  uint32_t* sched = nullptr;  // kSchedSlots x {cursor, finished}
+  std::atomic<uint32_t> sched_next{0};
+  std::mutex submit_mu;
+
+  std::mutex cq_mu;
+  std::condition_variable cq_cv;
+  std::deque<Completion> cq;
+  std::vector<cudaEvent_t> ev_free;
+  bool stop = false;
+  std::thread completer;
+  std::atomic<int> inflight{0};
+  int mandel_occ[2][2][2] = {};  // [precision][ksteps16][exact]
+
+  uint32_t* next_sched() {
+    uint32_t i = sched_next.fetch_add(1, std::memory_order_relaxed) % kSchedSlots;
+    return sched + 2 * i;
+  }
+};
+
+}  // namespace cafxg
+
+using namespace cafxg;
+
+struct Request;
+
+struct cafxg_ctx {
+  std::vector<std::unique_ptr<Device>> devs;
+  PinnedPool pinned;
+  // outstanding completion records (cafxg_sync)
+  std::mutex sync_mu;
+  std::condition_variable sync_cv;
+  uint64_t submitted = 0, completed = 0;
+  // statistics
+  std::atomic<uint64_t> st_requests{0}, st_batches{0}, st_launches{0},
+      st_h2d{0}, st_d2h{0}, st_max_batch{0};
+  // actor dispatcher
+  std::atomic<Request*> inbox{nullptr};
+  std::mutex disp_mu;
+  std::condition_variable disp_cv;
+  bool disp_stop = false;
+  bool disp_wake = false;
+  std::thread dispatcher;
+  std::atomic<uint32_t> rr{0};
+  std::atomic<uint64_t> actor_open{0};  // enqueued, not yet completed
+  bool force_exact = false;  // CAFXG_EXACT_STEP=1: always the 8-op step
+  // NCCL communicators for multi-device sgemm (one per device)
+  std::mutex nccl_mu;
+  NcclApi nccl;
+  std::vector<ncclComm_t> comms;
+};
+
+namespace cafxg {
+
+static void note_max_batch(cafxg_ctx* ctx, uint64_t n) {
+  uint64_t cur = ctx->st_max_batch.load();
+  while (n > cur && !ctx->st_max_batch.compare_exchange_weak(cur, n)) {
+  }
+}
+
+static void completion_loop(cafxg_ctx* ctx, Device* d) {
+  cudaSetDevice(d->ordinal);
+  while (true) {
+    Completion c;
+    {
+      std::unique_lock<std::mutex> lk(d->cq_mu);
+      d->cq_cv.wait(lk, [&] { return d->stop || !d->cq.empty(); });
+      if (d->cq.empty())
+        return;
+      c = std::move(d->cq.front());
+      d->cq.pop_front();
+    }
+    cudaError_t e = cudaEventSynchronize(c.ev);
+    int status = CAFXG_OK;
+    if (e != cudaSuccess)
+      status = cuda_status(e, "device work failed");
+    c.fn(status);
+    {
+      std::lock_guard<std::mutex> lk(d->cq_mu);
+      d->ev_free.push_back(c.ev);
+    }
+    d->inflight.fetch_sub(1);
+    {
+      std::lock_guard<std::mutex> lk(ctx->sync_mu);
+      ++ctx->completed;
+    }
+    ctx->sync_cv.notify_all();
+    ctx->disp_cv.notify_all();
+  }
+}
+
+// Records an event on `stream` and hands `fn` to the device's completion
+// thread. Caller holds d->submit_mu (so records stay in stream order).
+static int push_completion(cafxg_ctx* ctx, Device* d, cudaStream_t stream,
+                           std::function<void(int)> fn) {
+  cudaEvent_t ev = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(d->cq_mu);
+    if (!d->ev_free.empty()) {
+      ev = d->ev_free.back();
+      d->ev_free.pop_back();
+    }
+  }
+  if (!ev)
+    CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CAFXG_CUDA_TRY(cudaEventRecord(ev, stream));
+  {
+    std::lock_guard<std::mutex> lk(ctx->sync_mu);
+    ++ctx->submitted;
+  }
+  d->inflight.fetch_add(1);
+  {
+    std::lock_guard<std::mutex> lk(d->cq_mu);
+    d->cq.push_back(Completion{ev, std::move(fn)});
+  }
+  d->cq_cv.notify_one();
+  return CAFXG_OK;
+}
+
+// Joins the per-device parts of one request; the last part reports.
+struct Join {
+  std::atomic<int> remaining{0};
+  std::atomic<int> status{CAFXG_OK};
+  cafxg_done_fn done = nullptr;
+  void* user = nullptr;
+  std::function<void()> on_ok;  // runs before done when every part succeeded
+
+  void part_done(int s) {
+    if (s != CAFXG_OK) {
+      int expected = CAFXG_OK;
+      status.compare_exchange_strong(expected, s);
+    }
+    if (remaining.fetch_sub(1) == 1) {
+      int st = status.load();
+      if (st == CAFXG_OK && on_ok)
+        on_ok();
+      if (done)
+        done(user, st);
+      delete this;
+    }
+  }
+};
+
+// ---- Mandelbrot planning -----------------------------------------------------------
+
+static int validate_mandel(const cafxg_mandel_desc& t) {
+  if (!std::isfinite(t.x0) || !std::isfinite(t.x1) || !std::isfinite(t.y0) ||
+      !std::isfinite(t.y1))
+    return fail(CAFXG_E_CONFIG, "mandelbrot: region must be finite");
+  if (t.width == 0 || t.height == 0)
+    return fail(CAFXG_E_OUT_OF_RANGE, "mandelbrot: empty image");
+  if ((uint64_t)t.row0 + t.nrows > t.height || (uint64_t)t.col0 + t.ncols > t.width)
+    return fail(CAFXG_E_OUT_OF_RANGE, "mandelbrot: tile outside the image");
+  if (t.precision > 1 || t.sampling > 1)
+    return fail(CAFXG_E_CONFIG, "mandelbrot: bad precision or sampling");
+  if (t.max_iter > (1u << 30))
+    return fail(CAFXG_E_OUT_OF_RANGE, "mandelbrot: max_iter above 2^30");
+  if ((uint64_t)t.nrows * t.ncols > 0xffffffffull)
+    return fail(CAFXG_E_OUT_OF_RANGE, "mandelbrot: tile above 2^32 pixels");
+  return CAFXG_OK;
+}
+
+static double coord(double lo, double hi, uint32_t i, uint32_t n, double s) {
+  volatile double k = (double)i + s;  // volatile: keep every rounding explicit
+  volatile double p = k * (hi - lo);
+  volatile double q = p / (double)n;
+  return lo + q;
+}
+
+// Smallest nonzero |ci| the tile's rows produce, in the request precision.
+// The map row -> ci is monotone, so the minimum sits next to the zero
+// crossing or at an end row.
+static double min_abs_ci(const cafxg_mandel_desc& t) {
+  double s = t.sampling ? 0.5 : 0.0;
+  std::vector<int64_t> cand = {(int64_t)t.row0, (int64_t)t.row0 + t.nrows - 1};
+  double span = t.y1 - t.y0;
+  if (span != 0.0) {
+    double r = -t.y0 * (double)t.height / span - s;
+    if (std::isfinite(r)) {
+      for (int64_t k = (int64_t)std::floor(r) - 2; k <= (int64_t)std::floor(r) + 3; ++k)
+        cand.push_back(k);
+    }
+  }
+  double best = INFINITY;
+  for (int64_t r : cand) {
+    if (r < (int64_t)t.row0 || r >= (int64_t)t.row0 + t.nrows)
+      continue;
+    double ci = coord(t.y0, t.y1, (uint32_t)r, t.height, s);
+    double v = t.precision ? std::fabs(ci) : std::fabs((double)(float)ci);
+    if (v > 0.0 && v < best)
+      best = v;
+  }
+  return best;
+}
+
+// The 7-op escape step is bit-identical unless a row has a tiny nonzero ci
+// (DESIGN.md §3): fp32 needs |ci| >= 2^-100, fp64 |ci| >= 2^-960.
+static bool needs_exact_step(const cafxg_mandel_desc& t);
+static bool use_exact(cafxg_ctx* ctx, const cafxg_mandel_desc& t) {
+  return ctx->force_exact || needs_exact_step(t);
+}
+static bool needs_exact_step(const cafxg_mandel_desc& t) {
+  double lim = t.precision ? std::ldexp(1.0, -960) : std::ldexp(1.0, -100);
+  return min_abs_ci(t) < lim;
+}
+
+struct SubTile {
+  cafxg_mandel_desc d;  // row0/nrows narrowed; out_offset = host offset
+  uint64_t pixels;
+};
+
+static void fill_mtile(MTile& m, const cafxg_mandel_desc& d, uint32_t* out,
+                       uint32_t chunk_begin) {
+  m.x0 = d.x0;
+  m.xspan = d.x1 - d.x0;
+  m.y0 = d.y0;
+  m.yspan = d.y1 - d.y0;
+  m.s = d.sampling ? 0.5 : 0.0;
+  m.width = d.width;
+  m.height = d.height;
+  m.row0 = d.row0;
+  m.col0 = d.col0;
+  m.nrows = d.nrows;
+  m.ncols = d.ncols;
+  m.max_iter = d.max_iter;
+  m.chunk_begin = chunk_begin;
+  m.out = out;
+}
+
+static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
+                                  bool exact, uint64_t pixels) {
+  MandelLaunchCfg c;
+  c.ksteps = max_iter >= 256 ? 16 : 4;
+  c.exact = exact;
+  int& occ = d->mandel_occ[precision][c.ksteps == 16][exact];
+  if (occ == 0)
+    occ = std::max(1, mandel_max_blocks_per_sm(precision, c.ksteps, exact));
+  uint64_t want = (pixels + 2 * kMandelThreads - 1) / (2 * kMandelThreads);
+  uint64_t full = (uint64_t)d->sms * occ;
+  c.grid = (int)std::max<uint64_t>(1, std::min(want, full));
+  return c;
+}
+
+// Enqueues one Mandelbrot launch over `tiles` (all the same precision) on
+// `stream`; descriptors beyond the inline capacity are uploaded first.
+static int launch_mandel(cafxg_ctx* ctx, Device* d,
+                         const std::vector<MTile>& tiles, uint32_t total_chunks,
+                         int precision, uint32_t max_iter, bool exact,
+                         uint64_t pixels, cudaStream_t stream) {
+  if (total_chunks == 0)
+    return CAFXG_OK;
+  MLaunch L{};
+  L.n = (uint32_t)tiles.size();
+  L.total_chunks = total_chunks;
+  L.sched = d->next_sched();
+  L.zero = 0.0f;
+  MTile* dev_tiles = nullptr;
+  if (tiles.size() <= (size_t)kInlineTiles) {
+    for (size_t i = 0; i < tiles.size(); ++i)
+      L.inl[i] = tiles[i];
+  } else {
+    size_t bytes = tiles.size() * sizeof(MTile);
+    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dev_tiles, bytes, stream));
+    // pageable source: cudaMemcpyAsync stages it before returning
+    CAFXG_CUDA_TRY(cudaMemcpyAsync(dev_tiles, tiles.data(), bytes,
+                                   cudaMemcpyHostToDevice, stream));
+    ctx->st_h2d += bytes;
+    L.tiles = dev_tiles;
+  }
+  MandelLaunchCfg cfg = mandel_cfg(d, precision, max_iter, exact, pixels);
+  int e = mandel_launch(L, precision, cfg, stream);
+  if (e != 0)
+    return cuda_status((cudaError_t)e, "mandelbrot launch");
+  ctx->st_launches++;
+  if (dev_tiles)
+    CAFXG_CUDA_TRY(cudaFreeAsync(dev_tiles, stream));
+  return CAFXG_OK;
+}
+
+// Splits the request's tiles into row-band sub-tiles dealt cyclically to the
+// devices (contiguous bands are load-imbalanced up to 1.15x).
+static std::vector<std::vector<SubTile>> plan_mandel(
+    const cafxg_mandel_desc* tiles, size_t n, size_t ndev) {
+  std::vector<std::vector<SubTile>> per(ndev);
+  uint64_t total = 0;
+  for (size_t i = 0; i < n; ++i)
+    total += (uint64_t)tiles[i].nrows * tiles[i].ncols;
+  // band size: ~1M pixels when the request is large enough to share
+  const uint64_t band_px = (ndev > 1 || total > (64ull << 20)) ? (1ull << 20) : UINT64_MAX;
+  size_t next = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const cafxg_mandel_desc& t = tiles[i];
+    uint64_t px = (uint64_t)t.nrows * t.ncols;
+    if (px == 0)
+      continue;
+    uint32_t rows_per = band_px == UINT64_MAX
+                            ? t.nrows
+                            : (uint32_t)std::max<uint64_t>(1, band_px / t.ncols);
+    for (uint32_t r = 0; r < t.nrows; r += rows_per) {
+      SubTile s;
+      s.d = t;
+      s.d.row0 = t.row0 + r;
+      s.d.nrows = std::min(rows_per, t.nrows - r);
+      s.d.out_offset = t.out_offset + (uint64_t)r * t.ncols;
+      s.pixels = (uint64_t)s.d.nrows * s.d.ncols;
+      per[next % ndev].push_back(s);
+      ++next;
+    }
+  }
+  return per;
+}
+
+// Submits one device's share: waves of sub-tiles, each a single launch into a
+// device staging buffer followed by the copy-out on the d2h stream, so the
+// PCIe transfer of wave w overlaps the compute of wave w+1.
+static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
+                                const std::vector<SubTile>& subs,
+                                uint32_t* host_out, bool out_pinned,
+                                bool exact, Join* join) {
+  cudaSetDevice(d->ordinal);
+  std::lock_guard<std::mutex> g(d->submit_mu);
+  const uint64_t wave_px = 16ull << 20;
+  uint32_t* staging = nullptr;  // pinned bounce buffer for pageable outputs
+  uint64_t dev_px_total = 0;
+  for (auto& s : subs)
+    dev_px_total += s.pixels;
+  if (!out_pinned) {
+    staging = (uint32_t*)ctx->pinned.alloc(dev_px_total * 4);
+    if (!staging)
+      return fail(CAFXG_E_CONFIG, "mandelbrot: pinned staging allocation failed");
+  }
+  uint64_t staged = 0;
+  std::vector<std::array<uint64_t, 3>> scat;  // (staging off, host off, px)
+  size_t i = 0;
+  while (i < subs.size()) {
+    // group a wave (same precision)
+    size_t j = i;
+    uint64_t px = 0;
+    int prec = subs[i].d.precision;
+    while (j < subs.size() && subs[j].d.precision == prec &&
+           (px == 0 || px + subs[j].pixels <= wave_px)) {
+      px += subs[j].pixels;
+      ++j;
+    }
+    uint32_t* dout = nullptr;
+    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dout, px * 4, d->compute));
+    std::vector<MTile> mt(j - i);
+    uint32_t chunks = 0, maxit = 0;
+    uint64_t off = 0;
+    for (size_t k = i; k < j; ++k) {
+      fill_mtile(mt[k - i], subs[k].d, dout + off, chunks);
+      chunks += (uint32_t)((subs[k].pixels + kChunk - 1) / kChunk);
+      maxit = std::max(maxit, subs[k].d.max_iter);
+      off += subs[k].pixels;
+    }
+    CAFXG_TRY(launch_mandel(ctx, d, mt, chunks, prec, maxit, exact, px, d->compute));
+    cudaEvent_t ev;
+    CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CAFXG_CUDA_TRY(cudaEventRecord(ev, d->compute));
+    CAFXG_CUDA_TRY(cudaStreamWaitEvent(d->d2h, ev, 0));
+    cudaEventDestroy(ev);  // destruction is deferred until the event completes
+    off = 0;
+    for (size_t k = i; k < j; ++k) {
+      uint64_t bytes = subs[k].pixels * 4;
+      void* dst;
+      if (out_pinned) {
+        dst = host_out + subs[k].d.out_offset;
+      } else {
+        dst = staging + staged;
+        scat.push_back({staged, subs[k].d.out_offset, subs[k].pixels});
+        staged += subs[k].pixels;
+      }
+      CAFXG_CUDA_TRY(cudaMemcpyAsync(dst, dout + off, bytes,
+                                     cudaMemcpyDeviceToHost, d->d2h));
+      ctx->st_d2h += bytes;
+      off += subs[k].pixels;
+    }
+    CAFXG_CUDA_TRY(cudaFreeAsync(dout, d->d2h));
+    i = j;
+  }
+  return push_completion(ctx, d, d->d2h,
+                         [ctx, staging, scat = std::move(scat), host_out, join](int st) {
+                           if (staging) {
+                             if (st == CAFXG_OK)
+                               for (auto& s : scat)
+                                 std::memcpy(host_out + s[1], staging + s[0], s[2] * 4);
+                             ctx->pinned.free(staging);
+                           }
+                           join->part_done(st);
+                         });
+}
+
+static int mandel_submit_impl(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles,
+                              size_t n, uint32_t* host_out, cafxg_done_fn done,
+                              void* user) {
+  if (!ctx || (n && !tiles) || (n && !host_out))
+    return fail(CAFXG_E_CONFIG, "mandelbrot_submit: null argument");
+  uint64_t out_elems = 0;
+  bool exact = false;
+  for (size_t i = 0; i < n; ++i) {
+    CAFXG_TRY(validate_mandel(tiles[i]));
+    out_elems = std::max<uint64_t>(
+        out_elems, tiles[i].out_offset + (uint64_t)tiles[i].nrows * tiles[i].ncols);
+    exact = exact || use_exact(ctx, tiles[i]);
+  }
+  bool pinned = host_is_pinned(host_out, out_elems * 4);
+  auto plan = plan_mandel(tiles, n, ctx->devs.size());
+  Join* join = new Join;
+  join->done = done;
+  join->user = user;
+  int parts = 0;
+  for (auto& p : plan)
+    parts += !p.empty();
+  if (parts == 0) {
+    // nothing to compute: complete through device 0's completion thread so
+    // the callback still runs off the caller's thread
+    join->remaining = 1;
+    Device* d = ctx->devs[0].get();
+    cudaSetDevice(d->ordinal);
+    std::lock_guard<std::mutex> g(d->submit_mu);
+    return push_completion(ctx, d, d->compute, [join](int st) { join->part_done(st); });
+  }
+  join->remaining = parts;
+  ctx->st_requests++;
+  for (size_t k = 0; k < plan.size(); ++k) {
+    if (plan[k].empty())
+      continue;
+    int s = submit_mandel_device(ctx, ctx->devs[k].get(), plan[k], host_out,
+                                 pinned, exact, join);
+    if (s != CAFXG_OK) {
+      // parts already submitted still report through the join
+      std::string err = t_last_error;
+      join->part_done(s);
+      for (size_t r = k + 1; r < plan.size(); ++r)
+        if (!plan[r].empty())
+          join->part_done(s);
+      t_last_error = err;
+      return CAFXG_OK;  // the error is delivered through `done`
+    }
+  }
+  return CAFXG_OK;
+}
+
+// ---- sgemm ---------------------------------------------------------------------------
+
+static int validate_sgemm(cafxg_sgemm_desc& d) {
+  if (d.lda == 0) d.lda = d.K;
+  if (d.ldb == 0) d.ldb = d.N;
+  if (d.ldc == 0) d.ldc = d.N;
+  if (d.lda < d.K || d.ldb < d.N || d.ldc < d.N)
+    return fail(CAFXG_E_OUT_OF_RANGE, "sgemm: leading dimension below extent");
+  if (d.mode > CAFXG_SGEMM_3XTF32)
+    return fail(CAFXG_E_CONFIG, "sgemm: bad mode");
+  if (d.M > (1u << 30) || d.N > (1u << 30) || d.K > (1u << 30))
+    return fail(CAFXG_E_OUT_OF_RANGE, "sgemm: dimension too large");
+  return CAFXG_OK;
+}
+
+// Runs C = A*B on one device with device pointers.
+static int sgemm_on_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
+                           const float* A, const float* B, float* C,
+                           cudaStream_t stream) {
+  if (g.M == 0 || g.N == 0)
+    return CAFXG_OK;
+  if (g.K == 0) {
+    for (uint32_t r = 0; r < g.M; ++r)
+      CAFXG_CUDA_TRY(cudaMemsetAsync(C + (size_t)r * g.ldc, 0, g.N * 4, stream));
+    return CAFXG_OK;
+  }
+  bool tc = g.mode != CAFXG_SGEMM_FFMA &&
+            sgemm_tc_supported(g.M, g.N, g.K, g.lda, g.ldb, g.ldc);
+  if (g.mode == CAFXG_SGEMM_3XTF32 && !tc)
+    return fail(CAFXG_E_CONFIG,
+                "sgemm: shape not supported by the 3xTF32 kernel (see cafxg.h)");
+  if (tc) {
+    size_t sb = sgemm_tc_scratch_bytes(g.M, g.N, g.K);
+    void* scratch = nullptr;
+    CAFXG_CUDA_TRY(cudaMallocAsync(&scratch, sb, stream));
+    int launches = 0;
+    int e = sgemm_tc_launch(A, B, C, g.M, g.N, g.K, g.lda, g.ldb, g.ldc, scratch,
+                            d->sms, stream, &launches);
+    ctx->st_launches += launches;
+    CAFXG_CUDA_TRY(cudaFreeAsync(scratch, stream));
+    if (e != 0)
+      return cuda_status((cudaError_t)e, "sgemm 3xtf32 launch");
+    return CAFXG_OK;
+  }
+  int e = sgemm_simt_launch(A, B, C, g.M, g.N, g.K, g.lda, g.ldb, g.ldc, stream);
+  if (e != 0)
+    return cuda_status((cudaError_t)e, "sgemm simt launch");
+  ctx->st_launches++;
+  return CAFXG_OK;
+}
+
+static int ensure_nccl(cafxg_ctx* ctx) {
+  std::lock_guard<std::mutex> g(ctx->nccl_mu);
+  if (!ctx->comms.empty())
+    return CAFXG_OK;
+  if (!ctx->nccl.load())
+    return fail(CAFXG_E_SPAWN, "libnccl.so.2 not loadable");
+  std::vector<int> ords;
+  for (auto& d : ctx->devs)
+    ords.push_back(d->ordinal);
+  std::vector<ncclComm_t> comms(ords.size());
+  ncclResult_t r = ctx->nccl.CommInitAll(comms.data(), (int)ords.size(), ords.data());
+  if (r != ncclSuccess)
+    return fail(CAFXG_E_SPAWN, "ncclCommInitAll failed: %s",
+                ctx->nccl.GetErrorString ? ctx->nccl.GetErrorString(r) : "?");
+  ctx->comms = comms;
+  return CAFXG_OK;
+}
+
+// Host-to-host sgemm. One device: H2D A,B -> GEMM -> D2H C. G devices: A is
+// split into row blocks; each device uploads 1/G of B's rows and an NCCL
+// all-gather over NVLink completes B everywhere; each device returns its C
+// rows.
+static int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
+                             const float* A, const float* B, float* C,
+                             cafxg_done_fn done, void* user) {
+  if (!ctx || !desc)
+    return fail(CAFXG_E_CONFIG, "sgemm_submit: null argument");
+  cafxg_sgemm_desc g = *desc;
+  CAFXG_TRY(validate_sgemm(g));
+  if ((g.M && g.K && !A) || (g.K && g.N && !B) || (g.M && g.N && !C))
+    return fail(CAFXG_E_CONFIG, "sgemm_submit: null matrix");
+  size_t G = ctx->devs.size();
+  // devices used: only split when every block gets rows and K divides evenly
+  size_t use = 1;
+  if (G > 1 && g.M >= G * 128 && g.K % G == 0 && g.ldb == g.N) {
+    if (ensure_nccl(ctx) == CAFXG_OK)
+      use = G;
+  }
+  Join* join = new Join;
+  join->done = done;
+  join->user = user;
+  join->remaining = (int)use;
+  ctx->st_requests++;
+  const size_t bytesB = (size_t)g.K * g.ldb * 4;
+  const uint32_t rows_per = (uint32_t)((g.M + use - 1) / use);
+  // allocation + upload of B slices on every used device
+  std::vector<float*> dB(use, nullptr);
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (size_t k = 0; k < use; ++k)
+    locks.emplace_back(ctx->devs[k]->submit_mu);
+  int status = CAFXG_OK;
+  for (size_t k = 0; k < use && status == CAFXG_OK; ++k) {
+    Device* d = ctx->devs[k].get();
+    cudaSetDevice(d->ordinal);
+    if (cudaMallocAsync((void**)&dB[k], std::max<size_t>(bytesB, 4), d->compute) != cudaSuccess) {
+      status = cuda_status(cudaGetLastError(), "sgemm: device B allocation");
+      break;
+    }
+    size_t k0 = use == 1 ? 0 : (size_t)g.K / use * k;
+    size_t kn = use == 1 ? g.K : (size_t)g.K / use;
+    if (kn && cudaMemcpyAsync(dB[k] + k0 * g.ldb, B + k0 * g.ldb, kn * g.ldb * 4,
+                              cudaMemcpyHostToDevice, d->compute) != cudaSuccess)
+      status = cuda_status(cudaGetLastError(), "sgemm: B upload");
+    ctx->st_h2d += kn * g.ldb * 4;
+  }
+  if (status == CAFXG_OK && use > 1) {
+    ctx->nccl.GroupStart();
+    for (size_t k = 0; k < use; ++k) {
+      size_t cnt = (size_t)g.K / use * g.ldb;
+      ctx->nccl.AllGather(dB[k] + cnt * k, dB[k], cnt, ncclFloat32, ctx->comms[k],
+                          ctx->devs[k]->compute);
+    }
+    if (ctx->nccl.GroupEnd() != ncclSuccess)
+      status = fail(CAFXG_E_DOWN, "sgemm: NCCL all-gather of B failed");
+  }
+  for (size_t k = 0; k < use; ++k) {
+    Device* d = ctx->devs[k].get();
+    cudaSetDevice(d->ordinal);
+    int s = status;
+    uint32_t r0 = (uint32_t)std::min<uint64_t>(g.M, (uint64_t)rows_per * k);
+    uint32_t r1 = (uint32_t)std::min<uint64_t>(g.M, (uint64_t)rows_per * (k + 1));
+    cafxg_sgemm_desc part = g;
+    part.M = r1 - r0;
+    part.lda = g.K;
+    part.ldc = g.N;
+    float *dA = nullptr, *dC = nullptr;
+    if (s == CAFXG_OK && part.M) {
+      if (cudaMallocAsync((void**)&dA, (size_t)part.M * g.K * 4 + 4, d->compute) != cudaSuccess ||
+          cudaMallocAsync((void**)&dC, (size_t)part.M * g.N * 4 + 4, d->compute) != cudaSuccess)
+        s = cuda_status(cudaGetLastError(), "sgemm: device allocation");
+      if (s == CAFXG_OK && g.K) {
+        if (g.lda == g.K)
+          s = cuda_status(cudaMemcpyAsync(dA, A + (size_t)r0 * g.lda, (size_t)part.M * g.K * 4,
+                                          cudaMemcpyHostToDevice, d->compute), "sgemm: A upload");
+        else
+          s = cuda_status(cudaMemcpy2DAsync(dA, (size_t)g.K * 4, A + (size_t)r0 * g.lda,
+                                            (size_t)g.lda * 4, (size_t)g.K * 4, part.M,
+                                            cudaMemcpyHostToDevice, d->compute), "sgemm: A upload");
+        ctx->st_h2d += (size_t)part.M * g.K * 4;
+      }
+      if (s == CAFXG_OK)
+        s = sgemm_on_device(ctx, d, part, dA, dB[k], dC, d->compute);
+      if (s == CAFXG_OK) {
+        s = cuda_status(cudaMemcpy2DAsync(C + (size_t)r0 * g.ldc, (size_t)g.ldc * 4, dC,
+                                          (size_t)g.N * 4, (size_t)g.N * 4, part.M,
+                                          cudaMemcpyDeviceToHost, d->compute), "sgemm: C download");
+        ctx->st_d2h += (size_t)part.M * g.N * 4;
+      }
+    }
+    if (dA) cudaFreeAsync(dA, d->compute);
+    if (dC) cudaFreeAsync(dC, d->compute);
+    if (dB[k]) cudaFreeAsync(dB[k], d->compute);
+    if (s != CAFXG_OK) {
+      // still route the failure through the completion thread
+      push_completion(ctx, d, d->compute, [join, s](int) { join->part_done(s); });
+    } else {
+      int ps = push_completion(ctx, d, d->compute, [join](int st) { join->part_done(st); });
+      if (ps != CAFXG_OK)
+        join->part_done(ps);
+    }
+  }
+  return CAFXG_OK;
+}
+
+// ---- compute actors + dispatcher ---------------------------------------------------
+
+enum class Kernel : uint32_t { mandelbrot = 1, matrix_multiply = 2 };
+
+}  // namespace cafxg
+
+struct cafxg_actor {
+  cafxg_ctx* ctx;
+  Kernel kernel;
+  uint64_t dims[3] = {0, 0, 0};
+  size_t ndims = 0;
+  std::atomic<bool> alive{true};
+  std::atomic<int> refs{1};
+  std::atomic<uint64_t> pending{0};
+};
+
+struct Request {
+  Request* next = nullptr;
+  cafxg_actor* actor = nullptr;
+  std::vector<cafxg_mandel_desc> tiles;  // mandelbrot
+  const float* a = nullptr;              // matrix_multiply
+  const float* b = nullptr;
+  void* out = nullptr;
+  size_t out_bytes = 0;
+  uint64_t pixels = 0;
+  cafxg_done_fn done = nullptr;
+  void* user = nullptr;
+};
+
+namespace cafxg {
+
+static void actor_unref(cafxg_actor* a) {
+  if (a->refs.fetch_sub(1) == 1)
+    delete a;
+}
+
+static void finish_request(Request* r, int status) {
+  cafxg_actor* a = r->actor;
+  if (r->done)
+    r->done(r->user, status);
+  a->pending.fetch_sub(1);
+  a->ctx->st_requests++;
+  a->ctx->actor_open.fetch_sub(1);
+  a->ctx->sync_cv.notify_all();
+  actor_unref(a);
+  delete r;
+}
+
+// One batch of Mandelbrot requests (same precision) on one device: one launch
+// over every tile of every request into a device staging buffer, then one
+// scatter launch straight into the pinned reply buffers (or one D2H into a
+// pinned bounce buffer + host memcpy for pageable replies).
+static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> batch) {
+  cudaSetDevice(d->ordinal);
+  std::lock_guard<std::mutex> g(d->submit_mu);
+  uint64_t px = 0;
+  uint32_t maxit = 0;
+  bool exact = false;
+  int prec = batch[0]->tiles[0].precision;
+  bool all_pinned = true;
+  size_t ntiles = 0;
+  for (Request* r : batch) {
+    px += r->pixels;
+    for (auto& t : r->tiles) {
+      maxit = std::max(maxit, t.max_iter);
+      exact = exact || use_exact(ctx, t);
+      ++ntiles;
+    }
+    all_pinned = all_pinned && host_is_pinned(r->out, r->out_bytes);
+  }
+  int status = CAFXG_OK;
+  uint32_t* dout = nullptr;
+  uint32_t* bounce = nullptr;
+  CopySeg* dsegs = nullptr;
+  auto fail_all = [&](int s) {
+    std::string err = t_last_error;
+    for (Request* r : batch)
+      push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); });
+    t_last_error = err;
+  };
+  if (cudaMallocAsync((void**)&dout, px * 4 + 16, d->compute) != cudaSuccess) {
+    fail_all(cuda_status(cudaGetLastError(), "batch staging allocation"));
+    return;
+  }
+  std::vector<MTile> mt;
+  mt.reserve(ntiles);
+  std::vector<CopySeg> segs;
+  uint32_t chunks = 0;
+  uint64_t off = 0;
+  for (Request* r : batch) {
+    uint64_t roff = off;
+    for (auto& t : r->tiles) {
+      MTile m;
+      fill_mtile(m, t, dout + off, chunks);
+      mt.push_back(m);
+      uint64_t tp = (uint64_t)t.nrows * t.ncols;
+      chunks += (uint32_t)((tp + kChunk - 1) / kChunk);
+      off += tp;
+    }
+    segs.push_back(CopySeg{dout + roff, r->out, (off - roff) * 4});
+  }
+  status = launch_mandel(ctx, d, mt, chunks, prec, maxit, exact, px, d->compute);
+  if (status == CAFXG_OK && px) {
+    if (all_pinned) {
+      size_t sb = segs.size() * sizeof(CopySeg);
+      status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, d->compute), "segs alloc");
+      if (status == CAFXG_OK)
+        status = cuda_status(cudaMemcpyAsync(dsegs, segs.data(), sb,
+                                             cudaMemcpyHostToDevice, d->compute), "segs upload");
+      if (status == CAFXG_OK) {
+        int e = copy_segments_launch(dsegs, (uint32_t)segs.size(), d->compute);
+        status = cuda_status((cudaError_t)e, "reply scatter launch");
+        ctx->st_launches++;
+      }
+      if (dsegs)
+        cudaFreeAsync(dsegs, d->compute);
+    } else {
+      bounce = (uint32_t*)ctx->pinned.alloc(px * 4);
+      if (!bounce)
+        status = fail(CAFXG_E_CONFIG, "pinned bounce allocation failed");
+      else
+        status = cuda_status(cudaMemcpyAsync(bounce, dout, px * 4, cudaMemcpyDeviceToHost,
+                                             d->compute), "batch download");
+    }
+    ctx->st_d2h += px * 4;
+  }
+  cudaFreeAsync(dout, d->compute);
+  ctx->st_batches++;
+  note_max_batch(ctx, batch.size());
+  if (status != CAFXG_OK) {
+    if (bounce)
+      ctx->pinned.free(bounce);
+    fail_all(status);
+    return;
+  }
+  push_completion(ctx, d, d->compute,
+                  [ctx, batch = std::move(batch), bounce](int st) {
+                    uint64_t o = 0;
+                    for (Request* r : batch) {
+                      if (bounce && st == CAFXG_OK)
+                        std::memcpy(r->out, bounce + o, r->pixels * 4);
+                      o += r->pixels;
+                      finish_request(r, st);
+                    }
+                    if (bounce)
+                      ctx->pinned.free(bounce);
+                  });
+}
+
+static Device* pick_device(cafxg_ctx* ctx) {
+  // least in-flight work, round-robin among ties
+  size_t n = ctx->devs.size();
+  uint32_t start = ctx->rr.fetch_add(1);
+  Device* best = nullptr;
+  for (size_t i = 0; i < n; ++i) {
+    Device* d = ctx->devs[(start + i) % n].get();
+    if (!best || d->inflight.load() < best->inflight.load())
+      best = d;
+  }
+  return best;
+}
+
+static void dispatcher_loop(cafxg_ctx* ctx) {
+  const int kMaxInflight = 4;            // batches per device before holding
+  const uint64_t kMaxBatchPx = 64ull << 20;
+  std::deque<Request*> queue;
+  while (true) {
+    {
+      std::unique_lock<std::mutex> lk(ctx->disp_mu);
+      ctx->disp_cv.wait(lk, [&] {
+        if (ctx->disp_stop)
+          return true;
+        if (ctx->inbox.load(std::memory_order_acquire) != nullptr && queue.empty())
+          return true;
+        if (!queue.empty()) {
+          for (auto& d : ctx->devs)
+            if (d->inflight.load() < kMaxInflight)
+              return true;
+          return false;
+        }
+        return ctx->disp_wake;
+      });
+      ctx->disp_wake = false;
+      if (ctx->disp_stop && queue.empty() && ctx->inbox.load() == nullptr)
+        return;
+    }
+    // drain the inbox (LIFO stack) and append in FIFO order
+    Request* head = ctx->inbox.exchange(nullptr, std::memory_order_acq_rel);
+    std::vector<Request*> fresh;
+    for (Request* r = head; r; r = r->next)
+      fresh.push_back(r);
+    for (auto it = fresh.rbegin(); it != fresh.rend(); ++it)
+      queue.push_back(*it);
+    if (queue.empty())
+      continue;
+    Device* d = pick_device(ctx);
+    if (d->inflight.load() >= kMaxInflight && !ctx->disp_stop)
+      continue;  // wait for a completion; meanwhile the batch keeps growing
+    // assemble one batch: leading requests of one kernel kind / precision
+    std::vector<Request*> batch;
+    uint64_t px = 0;
+    while (!queue.empty()) {
+      Request* r = queue.front();
+      if (!r->actor->alive.load()) {
+        queue.pop_front();
+        push_completion(ctx, d, d->compute, [r](int) { finish_request(r, CAFXG_E_DOWN); });
+        continue;
+      }
+      if (r->actor->kernel == Kernel::matrix_multiply) {
+        if (!batch.empty())
+          break;
+        queue.pop_front();
+        cafxg_sgemm_desc g{};
+        g.M = g.N = g.K = (uint32_t)r->actor->dims[0];
+        g.mode = CAFXG_SGEMM_AUTO;
+        int s = sgemm_submit_impl(
+            ctx, &g, r->a, r->b, (float*)r->out,
+            [](void* u, int st) { finish_request((Request*)u, st); }, r);
+        if (s != CAFXG_OK)
+          push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); });
+        ctx->st_requests--;  // counted by finish_request
+        break;
+      }
+      if (!batch.empty() &&
+          (r->tiles[0].precision != batch[0]->tiles[0].precision ||
+           px + r->pixels > kMaxBatchPx))
+        break;
+      queue.pop_front();
+      batch.push_back(r);
+      px += r->pixels;
+    }
+    if (!batch.empty())
+      run_mandel_batch(ctx, d, std::move(batch));
+  }
+}
+
+static void wake_dispatcher(cafxg_ctx* ctx) {
+  {
+    std::lock_guard<std::mutex> lk(ctx->disp_mu);
+    ctx->disp_wake = true;
+  }
+  ctx->disp_cv.notify_one();
+}
+
+}  // namespace cafxg
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+
+extern "C" {
+
+int cafxg_abi_version(void) { return CAFXG_ABI_VERSION; }
+
+const char* cafxg_status_string(int s) {
+  switch (s) {
+    case CAFXG_OK: return "none";
+    case CAFXG_E_UNKNOWN_TYPE: return "unknown_type";
+    case CAFXG_E_OUT_OF_RANGE: return "out_of_range";
+    case CAFXG_E_TYPE_MISMATCH: return "type_mismatch";
+    case CAFXG_E_INTERFACE_MISMATCH: return "interface_mismatch";
+    case CAFXG_E_CONFIG: return "config_error";
+    case CAFXG_E_SPAWN: return "spawn_error";
+    case CAFXG_E_TIMEOUT: return "request_timeout";
+    case CAFXG_E_DOWN: return "request_down";
+    default: return "unknown";
+  }
+}
+
+const char* cafxg_last_error(void) { return t_last_error.c_str(); }
+
+int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
+  if (!out)
+    return fail(CAFXG_E_CONFIG, "open: null out");
+  *out = nullptr;
+  try {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      return fail(CAFXG_E_SPAWN, "no CUDA device visible (%s)",
+                  e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
+    }
+    auto ctx = std::make_unique<cafxg_ctx>();
+    for (int i = 0; i < n && i < 64; ++i) {
+      if (device_mask && !(device_mask >> i & 1))
+        continue;
+      auto d = std::make_unique<Device>();
+      d->ordinal = i;
+      CAFXG_CUDA_TRY(cudaSetDevice(i));
+      cudaDeviceProp prop{};
+      CAFXG_CUDA_TRY(cudaGetDeviceProperties(&prop, i));
+      if (prop.major != 10)
+        return fail(CAFXG_E_SPAWN, "device %d is sm_%d%d; libcafxg is built for sm_100a",
+                    i, prop.major, prop.minor);
+      d->sms = prop.multiProcessorCount;
+      CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->compute, cudaStreamNonBlocking));
+      CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking));
+      CAFXG_CUDA_TRY(cudaMalloc(&d->sched, kSchedSlots * 2 * sizeof(uint32_t)));
+      CAFXG_CUDA_TRY(cudaMemset(d->sched, 0, kSchedSlots * 2 * sizeof(uint32_t)));
+      cudaMemPool_t pool;
+      CAFXG_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, i));
+      uint64_t thr = UINT64_MAX;
+      CAFXG_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      ctx->devs.push_back(std::move(d));
+    }
+    if (ctx->devs.empty())
+      return fail(CAFXG_E_SPAWN, "device_mask selects no visible device");
+    const char* ex = getenv("CAFXG_EXACT_STEP");
+    ctx->force_exact = ex && ex[0] == '1';
+    cafxg_ctx* c = ctx.release();
+    for (auto& d : c->devs)
+      d->completer = std::thread(completion_loop, c, d.get());
+    c->dispatcher = std::thread(dispatcher_loop, c);
+    *out = c;
+    return CAFXG_OK;
+  } catch (const std::exception& ex) {
+    return fail(CAFXG_E_SPAWN, "open: %s", ex.what());
+  }
+}
+
+int cafxg_sync(cafxg_ctx* ctx) {
+  if (!ctx)
+    return fail(CAFXG_E_CONFIG, "sync: null ctx");
+  std::unique_lock<std::mutex> lk(ctx->sync_mu);
+  while (!(ctx->completed == ctx->submitted && ctx->actor_open.load() == 0))
+    ctx->sync_cv.wait_for(lk, std::chrono::milliseconds(1));
+  return CAFXG_OK;
+}
+
+int cafxg_close(cafxg_ctx* ctx) {
+  if (!ctx)
+    return CAFXG_OK;
+  {
+    std::lock_guard<std::mutex> lk(ctx->disp_mu);
+    ctx->disp_stop = true;
+  }
+  ctx->disp_cv.notify_all();
+  if (ctx->dispatcher.joinable())
+    ctx->dispatcher.join();
+  for (auto& d : ctx->devs) {
+    {
+      std::lock_guard<std::mutex> lk(d->cq_mu);
+      d->stop = true;
+    }
+    d->cq_cv.notify_all();
+    if (d->completer.joinable())
+      d->completer.join();
+  }
+  for (auto& d : ctx->devs) {
+    cudaSetDevice(d->ordinal);
+    cudaStreamSynchronize(d->compute);
+    cudaStreamSynchronize(d->d2h);
+    for (auto ev : d->ev_free)
+      cudaEventDestroy(ev);
+    cudaFree(d->sched);
+    cudaStreamDestroy(d->compute);
+    cudaStreamDestroy(d->d2h);
+  }
+  if (!ctx->comms.empty())
+    for (auto c : ctx->comms)
+      ctx->nccl.CommDestroy(c);
+  delete ctx;
+  return CAFXG_OK;
+}
+
+int cafxg_device_count(const cafxg_ctx* ctx) { return ctx ? (int)ctx->devs.size() : 0; }
+
+int cafxg_host_alloc(cafxg_ctx* ctx, size_t bytes, void** ptr) {
+  if (!ctx || !ptr)
+    return fail(CAFXG_E_CONFIG, "host_alloc: null argument");
+  *ptr = ctx->pinned.alloc(bytes ? bytes : 1);
+  if (!*ptr)
+    return fail(CAFXG_E_OUT_OF_RANGE, "host_alloc: cudaHostAlloc of %zu bytes failed", bytes);
+  return CAFXG_OK;
+}
+
+int cafxg_host_free(cafxg_ctx* ctx, void* ptr) {
+  if (!ctx)
+    return fail(CAFXG_E_CONFIG, "host_free: null ctx");
+  if (!ptr)
+    return CAFXG_OK;
+  return ctx->pinned.free(ptr) ? CAFXG_OK
+                               : fail(CAFXG_E_CONFIG, "host_free: pointer not from host_alloc");
+}
+
+int cafxg_host_register(cafxg_ctx* ctx, void* ptr, size_t bytes) {
+  if (!ctx || !ptr || !bytes)
+    return fail(CAFXG_E_CONFIG, "host_register: bad argument");
+  CAFXG_CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+  return CAFXG_OK;
+}
+
+int cafxg_host_unregister(cafxg_ctx* ctx, void* ptr) {
+  if (!ctx || !ptr)
+    return fail(CAFXG_E_CONFIG, "host_unregister: bad argument");
+  CAFXG_CUDA_TRY(cudaHostUnregister(ptr));
+  return CAFXG_OK;
+}
+
+int cafxg_mandelbrot_submit(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles, size_t n,
+                            uint32_t* host_out, cafxg_done_fn done, void* user) {
+  try {
+    return mandel_submit_impl(ctx, tiles, n, host_out, done, user);
+  } catch (const std::exception& ex) {
+    return fail(CAFXG_E_CONFIG, "mandelbrot_submit: %s", ex.what());
+  }
+}
+
+namespace {
+struct Waiter {
+  std::mutex mu;
+  std::condition_variable cv;
+  bool fired = false;
+  int status = CAFXG_OK;
+  std::string err;
+  static void cb(void* u, int s) {
+    auto* w = static_cast<Waiter*>(u);
+    std::lock_guard<std::mutex> g(w->mu);
+    w->fired = true;
+    w->status = s;
+    if (s != CAFXG_OK)
+      w->err = t_last_error;
+    w->cv.notify_all();
+  }
+  int wait() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return fired; });
+    if (status != CAFXG_OK)
+      set_last_error("%s", err.c_str());
+    return status;
+  }
+};
+}  // namespace
+
+int cafxg_mandelbrot(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles, size_t n,
+                     uint32_t* host_out) {
+  Waiter w;
+  int s = cafxg_mandelbrot_submit(ctx, tiles, n, host_out, &Waiter::cb, &w);
+  if (s != CAFXG_OK)
+    return s;
+  return w.wait();
+}
+
+int cafxg_mandelbrot_device(cafxg_ctx* ctx, int device, const cafxg_mandel_desc* tiles,
+                            size_t n, uint32_t* dev_out, void* stream) {
+  if (!ctx || device < 0 || device >= (int)ctx->devs.size() || (n && (!tiles || !dev_out)))
+    return fail(CAFXG_E_CONFIG, "mandelbrot_device: bad argument");
+  try {
+    Device* d = ctx->devs[device].get();
+    bool exact = false;
+    std::vector<MTile> mt(n);
+    uint32_t chunks = 0, maxit = 0;
+    uint64_t px = 0;
+    int prec = n ? (int)tiles[0].precision : 0;
+    for (size_t i = 0; i < n; ++i) {
+      CAFXG_TRY(validate_mandel(tiles[i]));
+      if ((int)tiles[i].precision != prec)
+        return fail(CAFXG_E_CONFIG, "mandelbrot_device: mixed precisions in one launch");
+      exact = exact || use_exact(ctx, tiles[i]);
+      fill_mtile(mt[i], tiles[i], dev_out + tiles[i].out_offset, chunks);
+      uint64_t tp = (uint64_t)tiles[i].nrows * tiles[i].ncols;
+      chunks += (uint32_t)((tp + kChunk - 1) / kChunk);
+      maxit = std::max(maxit, tiles[i].max_iter);
+      px += tp;
+    }
+    // drop empty tiles (they own no chunks and would confuse find_tile)
+    mt.erase(std::remove_if(mt.begin(), mt.end(),
+                            [](const MTile& m) { return m.nrows == 0 || m.ncols == 0; }),
+             mt.end());
+    cudaSetDevice(d->ordinal);
+    cudaStream_t s = stream ? (cudaStream_t)stream : d->compute;
+    return launch_mandel(ctx, d, mt, chunks, prec, maxit, exact, px, s);
+  } catch (const std::exception& ex) {
+    return fail(CAFXG_E_CONFIG, "mandelbrot_device: %s", ex.what());
+  }
+}
+
+int cafxg_sgemm_submit(cafxg_ctx* ctx, const cafxg_sgemm_desc* d, const float* A,
+                       const float* B, float* C, cafxg_done_fn done, void* user) {
+  try {
+    return sgemm_submit_impl(ctx, d, A, B, C, done, user);
+  } catch (const std::exception& ex) {
+    return fail(CAFXG_E_CONFIG, "sgemm_submit: %s", ex.what());
+  }
+}
+
+int cafxg_sgemm(cafxg_ctx* ctx, const cafxg_sgemm_desc* d, const float* A, const float* B,
+                float* C) {
+  Waiter w;
+  int s = cafxg_sgemm_submit(ctx, d, A, B, C, &Waiter::cb, &w);
+  if (s != CAFXG_OK)
+    return s;
+  return w.wait();
+}
+
+int cafxg_sgemm_device(cafxg_ctx* ctx, int device, const cafxg_sgemm_desc* desc,
+                       const float* A, const float* B, float* C, void* stream) {
+  if (!ctx || !desc || device < 0 || device >= (int)ctx->devs.size())
+    return fail(CAFXG_E_CONFIG, "sgemm_device: bad argument");
+  cafxg_sgemm_desc g = *desc;
+  CAFXG_TRY(validate_sgemm(g));
+  Device* d = ctx->devs[device].get();
+  cudaSetDevice(d->ordinal);
+  return sgemm_on_device(ctx, d, g, A, B, C, stream ? (cudaStream_t)stream : d->compute);
+}
+
+// ---- actors --------------------------------------------------------------------
+
+int cafxg_spawn(cafxg_ctx* ctx, const char* kernel_name, const uint64_t* dims, size_t ndims,
+                cafxg_actor** out) {
+  if (!ctx || !kernel_name || !out)
+    return fail(CAFXG_E_CONFIG, "spawn: null argument");
+  *out = nullptr;
+  Kernel k;
+  if (!std::strcmp(kernel_name, "mandelbrot")) {
+    k = Kernel::mandelbrot;
+  } else if (!std::strcmp(kernel_name, "matrix_multiply")) {
+    k = Kernel::matrix_multiply;
+    // spawn_cl<float*(float*,float*)>(src, "matrix_multiply", {size, size})
+    if (ndims != 2 || !dims || dims[0] == 0 || dims[0] != dims[1] || dims[0] > (1u << 16))
+      return fail(CAFXG_E_INTERFACE_MISMATCH,
+                  "spawn: matrix_multiply takes dims {size, size}");
+  } else {
+    return fail(CAFXG_E_UNKNOWN_TYPE, "spawn: no kernel named '%s'", kernel_name);
+  }
+  auto* a = new cafxg_actor;
+  a->ctx = ctx;
+  a->kernel = k;
+  a->ndims = std::min<size_t>(ndims, 3);
+  for (size_t i = 0; i < a->ndims; ++i)
+    a->dims[i] = dims[i];
+  *out = a;
+  return CAFXG_OK;
+}
+
+static int actor_check(cafxg_actor* a, const void* const* in, const size_t* in_bytes,
+                       size_t n_in, size_t* reply_bytes) {
+  if (!a)
+    return fail(CAFXG_E_CONFIG, "enqueue: null actor");
+  if (n_in && (!in || !in_bytes))
+    return fail(CAFXG_E_CONFIG, "enqueue: null inputs");
+  if (a->kernel == Kernel::mandelbrot) {
+    if (n_in != 1)
+      return fail(CAFXG_E_INTERFACE_MISMATCH, "mandelbrot takes one descriptor buffer");
+    if (in_bytes[0] == 0 || in_bytes[0] % sizeof(cafxg_mandel_desc) != 0 || !in[0])
+      return fail(CAFXG_E_TYPE_MISMATCH,
+                  "mandelbrot input must hold whole cafxg_mandel_desc records");
+    const auto* t = static_cast<const cafxg_mandel_desc*>(in[0]);
+    size_t n = in_bytes[0] / sizeof(cafxg_mandel_desc);
+    uint64_t px = 0;
+    int prec = t[0].precision;
+    for (size_t i = 0; i < n; ++i) {
+      CAFXG_TRY(validate_mandel(t[i]));
+      if ((int)t[i].precision != prec)
+        return fail(CAFXG_E_CONFIG, "mandelbrot: one precision per request");
+      px += (uint64_t)t[i].nrows * t[i].ncols;
+    }
+    if (px == 0)
+      return fail(CAFXG_E_OUT_OF_RANGE, "mandelbrot: request without pixels");
+    *reply_bytes = px * 4;
+    return CAFXG_OK;
+  }
+  size_t sz = a->dims[0];
+  size_t mb = sz * sz * sizeof(float);
+  if (n_in != 2)
+    return fail(CAFXG_E_INTERFACE_MISMATCH, "matrix_multiply takes (matrix1, matrix2)");
+  if (in_bytes[0] != mb || in_bytes[1] != mb || !in[0] || !in[1])
+    return fail(CAFXG_E_TYPE_MISMATCH, "matrix_multiply inputs must be size*size floats");
+  *reply_bytes = mb;
+  return CAFXG_OK;
+}
+
+size_t cafxg_actor_reply_bytes(cafxg_actor* a, const void* const* in, const size_t* in_bytes,
+                               size_t n_in) {
+  size_t rb = 0;
+  return actor_check(a, in, in_bytes, n_in, &rb) == CAFXG_OK ? rb : 0;
+}
+
+int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in, const size_t* in_bytes,
+                        size_t n_in, void* out, size_t out_bytes, cafxg_done_fn done,
+                        void* user) {
+  size_t rb = 0;
+  CAFXG_TRY(actor_check(a, in, in_bytes, n_in, &rb));
+  if (!a->alive.load())
+    return fail(CAFXG_E_DOWN, "enqueue: actor terminated");
+  if (!out || out_bytes != rb)
+    return fail(CAFXG_E_TYPE_MISMATCH, "enqueue: reply buffer must be %zu bytes", rb);
+  auto* r = new Request;
+  r->actor = a;
+  r->out = out;
+  r->out_bytes = out_bytes;
+  r->done = done;
+  r->user = user;
+  if (a->kernel == Kernel::mandelbrot) {
+    const auto* t = static_cast<const cafxg_mandel_desc*>(in[0]);
+    size_t n = in_bytes[0] / sizeof(cafxg_mandel_desc);
+    r->tiles.assign(t, t + n);
+    uint64_t off = 0;
+    for (auto& x : r->tiles) {
+      x.out_offset = off;  // tiles packed in order in the reply
+      off += (uint64_t)x.nrows * x.ncols;
+    }
+    r->pixels = off;
+  } else {
+    r->a = static_cast<const float*>(in[0]);
+    r->b = static_cast<const float*>(in[1]);
+  }
+  a->refs.fetch_add(1);
+  a->pending.fetch_add(1);
+  cafxg_ctx* ctx = a->ctx;
+  ctx->actor_open.fetch_add(1);
+  Request* head = ctx->inbox.load(std::memory_order_relaxed);
+  do {
+    r->next = head;
+  } while (!ctx->inbox.compare_exchange_weak(head, r, std::memory_order_release,
+                                             std::memory_order_relaxed));
+  if (head == nullptr)  // empty -> non-empty: the dispatcher may sleep
+    wake_dispatcher(ctx);
+  return CAFXG_OK;
+}
+
+int cafxg_actor_quit(cafxg_actor* a) {
+  if (!a)
+    return fail(CAFXG_E_CONFIG, "quit: null actor");
+  a->alive.store(false);
+  wake_dispatcher(a->ctx);
+  return CAFXG_OK;
+}
+
+int cafxg_actor_release(cafxg_actor* a) {
+  if (!a)
+    return CAFXG_OK;
+  a->alive.store(false);
+  wake_dispatcher(a->ctx);
+  actor_unref(a);
+  return CAFXG_OK;
+}
+
+int cafxg_get_stats(cafxg_ctx* ctx, cafxg_stats* out) {
+  if (!ctx || !out)
+    return fail(CAFXG_E_CONFIG, "get_stats: null argument");
+  out->requests = ctx->st_requests.load();
+  out->batches = ctx->st_batches.load();
+  out->kernel_launches = ctx->st_launches.load();
+  out->h2d_bytes = ctx->st_h2d.load();
+  out->d2h_bytes = ctx->st_d2h.load();
+  out->max_batch = ctx->st_max_batch.load();
+  return CAFXG_OK;
+}
+
+}  // extern "C"

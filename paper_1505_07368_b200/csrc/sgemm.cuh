@@ -1,0 +1,21 @@
+// fp32 GEMM launchers for the `matrix_multiply` compute actor.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace cafxg {
+
+// Register-tiled FFMA kernel; any shape, any leading dims.
+int sgemm_simt_launch(const float* A, const float* B, float* C, int M, int N,
+                      int K, int lda, int ldb, int ldc, void* stream);
+
+// 3xTF32 tcgen05 path (sgemm_tc.cu). Shape constraints are checked by
+// sgemm_tc_supported; scratch holds the tf32 hi/lo splits of A and B^T
+// (sgemm_tc_scratch_bytes).
+bool sgemm_tc_supported(int M, int N, int K, int lda, int ldb, int ldc);
+size_t sgemm_tc_scratch_bytes(int M, int N, int K);
+int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N,
+                    int K, int lda, int ldb, int ldc, void* scratch,
+                    int sm_count, void* stream, int* launches);
+
+}  // namespace cafxg

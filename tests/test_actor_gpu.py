@@ -1,0 +1,145 @@
+"""GPU: the spawn_cl facade (cafxg_spawn / cafxg_actor_enqueue): replies,
+batching of request bursts, error replies, termination."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def storm_tile(rng, it=256):
+    # 64x64 fp64 tile at a seeded offset on the 1/512 grid inside [-2,1]x[-1,1]
+    kx = int(rng.integers(0, 3 * 512 - 64 + 1))
+    ky = int(rng.integers(0, 2 * 512 - 64 + 1))
+    x0, y0 = -2.0 + kx / 512, -1.0 + ky / 512
+    return pkg.mandel_desc(x0, x0 + 0.125, y0, y0 + 0.125, 64, 64, it, fp64=True, centre=True)
+
+
+def test_mandelbrot_actor_request(ctx):
+    a = ctx.spawn("mandelbrot")
+    d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 320, 200, 120)
+    desc = (pkg.MandelDesc * 1)(d)
+    assert a.reply_bytes([desc]) == 320 * 200 * 4
+    out = np.zeros(320 * 200, dtype=np.uint32)
+    a.request([desc], out).result(timeout=60)
+    ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 320, 200, 120, fp64=False, centre=True)
+    assert np.array_equal(out.reshape(200, 320), ref)
+    a.release()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_request_burst_from_many_clients(ctx, pinned):
+    """16 client threads x 40 storm tiles; every reply checked per tile."""
+    a = ctx.spawn("mandelbrot")
+    clients, per = 16, 40
+    rng = np.random.default_rng(99)
+    descs = [[storm_tile(rng) for _ in range(per)] for _ in range(clients)]
+    outs = [[(ctx.pinned_empty(4096, np.uint32) if pinned else np.zeros(4096, np.uint32))
+             for _ in range(per)] for _ in range(clients)]
+    before = ctx.stats()
+    errors = []
+
+    def client(c):
+        try:
+            futs = [a.request([(pkg.MandelDesc * 1)(descs[c][i])], outs[c][i])
+                    for i in range(per)]
+            for f in futs:
+                f.result(timeout=120)
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+    th = [threading.Thread(target=client, args=(c,)) for c in range(clients)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
+    after = ctx.stats()
+    n = clients * per
+    assert after.requests - before.requests == n
+    # bursts are batched: far fewer launches than requests
+    assert after.batches - before.batches < n
+    for c in range(clients):
+        for i in range(per):
+            d = descs[c][i]
+            ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, 64, 64, 256, fp64=True, centre=True)
+            assert np.array_equal(outs[c][i].reshape(64, 64), ref)
+    if pinned:
+        for row in outs:
+            for o in row:
+                ctx.pinned_free(o)
+    a.release()
+
+
+def test_multi_tile_request(ctx):
+    a = ctx.spawn("mandelbrot")
+    rng = np.random.default_rng(5)
+    ds = [storm_tile(rng, it=100) for _ in range(3)]
+    arr = (pkg.MandelDesc * 3)(*ds)
+    out = np.zeros(3 * 4096, dtype=np.uint32)
+    a.request([arr], out).result(timeout=60)
+    for k, d in enumerate(ds):
+        ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, 64, 64, 100, fp64=True, centre=True)
+        assert np.array_equal(out[k * 4096:(k + 1) * 4096].reshape(64, 64), ref)
+    a.release()
+
+
+def test_matrix_multiply_actor(ctx):
+    size = 256
+    a = ctx.spawn("matrix_multiply", (size, size))
+    A = oracle.fill_uniform(size * size, 7)
+    B = oracle.fill_uniform(size * size, 8)
+    C = np.zeros(size * size, dtype=np.float32)
+    a.request([A, B], C).result(timeout=60)
+    rows = np.arange(0, size, 9, dtype=np.uint32)
+    R = oracle.sgemm_ref_rows(A.reshape(size, size), B.reshape(size, size), rows, size, size)
+    assert oracle.sgemm_rel_err(C.reshape(size, size), R, rows, size) <= 1e-5
+    a.release()
+
+
+def test_interface_errors(ctx):
+    with pytest.raises(pkg.CafxgError) as e:
+        ctx.spawn("no_such_kernel")
+    assert e.value.code == 2          # unknown_type
+    with pytest.raises(pkg.CafxgError) as e:
+        ctx.spawn("matrix_multiply", (4, 5))
+    assert e.value.code == 6          # interface_mismatch
+    mm = ctx.spawn("matrix_multiply", (8, 8))
+    A = np.zeros(64, np.float32)
+    with pytest.raises(pkg.CafxgError) as e:
+        mm.request([A], np.zeros(64, np.float32))
+    assert e.value.code == 6
+    with pytest.raises(pkg.CafxgError) as e:
+        mm.request([A, np.zeros(63, np.float32)], np.zeros(64, np.float32))
+    assert e.value.code == 5          # type_mismatch
+    mm.release()
+    m = ctx.spawn("mandelbrot")
+    with pytest.raises(pkg.CafxgError) as e:
+        m.request([np.zeros(7, np.uint8)], np.zeros(1, np.uint32))
+    assert e.value.code == 5
+    m.release()
+
+
+def test_quit_fails_later_requests(ctx):
+    a = ctx.spawn("mandelbrot")
+    d = (pkg.MandelDesc * 1)(pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 16, 16, 10))
+    out = np.zeros(256, np.uint32)
+    a.request([d], out).result(timeout=60)
+    a.quit()
+    with pytest.raises(pkg.CafxgError) as e:
+        a.request([d], out)
+    assert e.value.code == 14         # request_down
+    a.release()
+
+
+def test_sync_waits_for_actor_requests(ctx):
+    a = ctx.spawn("mandelbrot")
+    rng = np.random.default_rng(1)
+    outs = [np.zeros(4096, np.uint32) for _ in range(50)]
+    futs = [a.request([(pkg.MandelDesc * 1)(storm_tile(rng))], o) for o in outs]
+    ctx.sync()
+    assert all(f.done() for f in futs)
+    a.release()

@@ -1,0 +1,212 @@
+"""GPU parity: the sm_100a escape-time kernels through the C ABI against the
+reference's goldens (bit-exact, fp64 reference mode) and against the oracle
+restatement (fp32/fp64, generalised regions), plus size-independent
+properties at the BASELINE sizes."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("size,it", [(64, 50), (96, 60), (256, 100), (1024, 500),
+                                     (2048, 500), (4096, 500)])
+def test_reference_mode_checksums(ctx, golden, size, it):
+    """run_mandelbrot(size, it) checksum (bench.cpp:481-505), bit-exact."""
+    want = int([g for g in golden["run_mandelbrot"]
+                if g["size"] == size and g["max_iter"] == it][0]["checksum"])
+    out = ctx.mandelbrot(pkg.reference_desc(size, it))
+    assert oracle.fnv1a_u32(out) == want
+
+
+def test_reference_rows(ctx, golden):
+    for r in golden["rows"]:
+        d = pkg.reference_desc(r["size"], r["max_iter"])
+        d.row0, d.nrows = r["y"], 1
+        row = ctx.mandelbrot(d)
+        assert int(row.sum()) == r["sum"]
+        assert oracle.fnv1a_u32(row) == int(r["fnv"])
+
+
+def test_cells(ctx, golden):
+    # single-pixel images whose centre-free corner sample is the cell's c
+    for c in golden["cells"]:
+        d = pkg.mandel_desc(c["re"], c["re"] + 1.0, c["im"], c["im"] + 1.0, 1, 1,
+                            c["max_iter"], fp64=True, centre=False)
+        assert int(ctx.mandelbrot(d)[0]) == c["count"], c
+
+
+def test_cfg1_fp32_full_image(ctx):
+    """BASELINE config 1: 1920x1080, [-2,1]x[-1,1], centres, fp32, it=100."""
+    d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)
+    out = ctx.mandelbrot(d).reshape(1080, 1920)
+    ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100, fp64=False, centre=True)
+    assert np.array_equal(out, ref), int((out != ref).sum())
+    assert 6.0e7 < int(out.sum(dtype=np.uint64)) < 6.6e7   # 6.29e7
+
+
+def test_cfg3_sampled_rows(ctx):
+    """BASELINE config 3 (16384^2, fp32, it=1000, boundary zoom): full image on
+    the GPU, every 256th row checked bit-exactly against the oracle."""
+    W = H = 16384
+    d = pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, W, H, 1000)
+    out = ctx.pinned_empty((H, W), np.uint32)
+    try:
+        ctx.mandelbrot(d, out)
+        ref = oracle.tile(-0.75, -0.73, 0.10, 0.12, W, H, 1000, fp64=False, centre=True,
+                          sample_stride=256)
+        for r in range(0, H, 256):
+            assert np.array_equal(out[r], ref[r]), r
+        mean = float(out[::64].mean())
+        assert 600 < mean < 760   # mean 678.6
+    finally:
+        ctx.pinned_free(out)
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+@pytest.mark.parametrize("centre", [False, True])
+def test_random_regions_vs_oracle(ctx, fp64, centre):
+    rng = np.random.default_rng(11 + fp64 * 2 + centre)
+    for _ in range(6):
+        w, h = int(rng.integers(1, 300)), int(rng.integers(1, 200))
+        x0 = float(rng.uniform(-2.2, 0.5)); y0 = float(rng.uniform(-1.2, 0.8))
+        span = float(10 ** rng.uniform(-4, 0.5))
+        it = int(rng.integers(0, 700))
+        d = pkg.mandel_desc(x0, x0 + span, y0, y0 + span * h / max(w, 1), w, h, it,
+                            fp64=fp64, centre=centre)
+        out = ctx.mandelbrot(d).reshape(h, w) if w * h else ctx.mandelbrot(d)
+        ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, w, h, it, fp64=fp64, centre=centre)
+        assert np.array_equal(out, ref), (w, h, x0, y0, span, it)
+
+
+def test_edges(ctx):
+    # max_iter 0 and 1, 1x1, one column, one row, non-chunk-multiple sizes
+    for (w, h, it) in [(1, 1, 0), (1, 1, 1), (5, 3, 0), (1, 777, 50), (777, 1, 50),
+                       (513, 3, 30), (1023, 5, 1)]:
+        for fp64 in (False, True):
+            d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, w, h, it, fp64=fp64)
+            out = ctx.mandelbrot(d).reshape(h, w)
+            ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, w, h, it, fp64=fp64, centre=True)
+            assert np.array_equal(out, ref), (w, h, it, fp64)
+    # c = -2: |z|^2 == 4 forever, never escapes (strict >)
+    d = pkg.mandel_desc(-2.0, -1.0, 0.0, 1.0, 1, 1, 3000, fp64=True, centre=False)
+    assert int(ctx.mandelbrot(d)[0]) == 3000
+    d.precision = pkg.FP32
+    assert int(ctx.mandelbrot(d)[0]) == 3000
+
+
+def test_tiny_imaginary_rows_use_exact_step(ctx):
+    """Rows with 0 < |ci| < 2^-100 route to the 8-op step."""
+    for fp64, lim in [(False, 1e-33), (True, 1e-300)]:
+        d = pkg.mandel_desc(-1.9, 0.4, -lim, lim, 64, 6, 400, fp64=fp64, centre=True)
+        out = ctx.mandelbrot(d).reshape(6, 64)
+        ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, 64, 6, 400, fp64=fp64, centre=True)
+        assert np.array_equal(out, ref)
+
+
+def test_exact_and_fast_steps_agree():
+    """The 7-op (fma-folded) and the 8-op step give identical counts."""
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+with pkg.Context(1) as c:
+    outs = []
+    for d in [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 640, 360, 300),
+              pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 512, 512, 1000),
+              pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 320, 180, 300, fp64=True)]:
+        outs.append(c.mandelbrot(d))
+    np.save(sys.argv[1], np.concatenate(outs))
+""" % ROOT
+    res = {}
+    for mode in ("0", "1"):
+        path = f"/tmp/cafxg_step_{mode}.npy"
+        env = dict(os.environ, CAFXG_EXACT_STEP=mode)
+        subprocess.check_call([sys.executable, "-c", code, path], env=env)
+        res[mode] = np.load(path)
+    assert np.array_equal(res["0"], res["1"])
+
+
+def test_multi_tile_batch_and_offsets(ctx):
+    tiles, refs, off = [], [], 0
+    rng = np.random.default_rng(3)
+    for k in range(20):   # > kInlineTiles: descriptors go through the upload path
+        w, h = int(rng.integers(1, 90)), int(rng.integers(1, 40))
+        d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 300, 200, int(rng.integers(1, 400)),
+                            fp64=bool(k & 1), row0=int(rng.integers(0, 200 - h)), nrows=h,
+                            col0=int(rng.integers(0, 300 - w)), ncols=w, out_offset=off)
+        tiles.append(d)
+        refs.append(oracle.tile(-2.0, 1.0, -1.0, 1.0, 300, 200, d.max_iter, fp64=bool(k & 1),
+                                centre=True, row0=d.row0, nrows=h, col0=d.col0, ncols=w))
+        off += w * h + 5   # gaps must stay untouched
+    out = np.full(off, 0xDEADBEEF, dtype=np.uint32)
+    ctx.mandelbrot(tiles, out)
+    pos = 0
+    for d, r in zip(tiles, refs):
+        n = d.nrows * d.ncols
+        assert np.array_equal(out[pos:pos + n].reshape(d.nrows, d.ncols), r)
+        assert np.all(out[pos + n:pos + n + 5] == 0xDEADBEEF)
+        pos += n + 5
+
+
+def test_pinned_and_pageable_outputs_agree(ctx):
+    d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 2000, 900, 200)
+    page = ctx.mandelbrot(d)
+    pin = ctx.pinned_empty(2000 * 900, np.uint32)
+    ctx.mandelbrot(d, pin)
+    assert np.array_equal(page, pin)
+    ctx.pinned_free(pin)
+
+
+def test_device_api_with_torch(ctx):
+    import torch
+    d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 640, 480, 150)
+    out = torch.zeros(640 * 480, dtype=torch.int32, device="cuda:0")
+    s = torch.cuda.current_stream()
+    ctx.mandelbrot_device(d, out.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 640, 480, 150, fp64=False, centre=True)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32).reshape(480, 640), ref)
+    # repeated launches reuse the self-resetting scheduler slots
+    for _ in range(2100):
+        ctx.mandelbrot_device(pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 64, 8, 20), out.data_ptr(),
+                              s.cuda_stream)
+    ctx.mandelbrot_device(d, out.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32).reshape(480, 640), ref)
+
+
+def test_async_submit_callback_runs_off_thread(ctx):
+    import threading
+    d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 300, 300, 100)
+    out = np.zeros(300 * 300, dtype=np.uint32)
+    seen = {}
+    ev = threading.Event()
+
+    def done(st):
+        seen["status"] = st
+        seen["thread"] = threading.get_ident()
+        ev.set()
+    ctx.mandelbrot_submit(d, out, done)
+    assert ev.wait(30)
+    assert seen["status"] == 0 and seen["thread"] != threading.get_ident()
+    ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 300, 300, 100, fp64=False, centre=True)
+    assert np.array_equal(out.reshape(300, 300), ref)
+
+
+def test_bad_requests_fail_synchronously(ctx):
+    bad = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 10, 10, 5, row0=8, nrows=5)
+    with pytest.raises(pkg.CafxgError) as e:
+        ctx.mandelbrot(bad)
+    assert e.value.code == 4
+    nan = pkg.mandel_desc(float("nan"), 1.0, -1.0, 1.0, 10, 10, 5)
+    with pytest.raises(pkg.CafxgError) as e:
+        ctx.mandelbrot(nan)
+    assert e.value.code == 8

@@ -1,0 +1,60 @@
+"""GPU parity for the matrix_multiply kernels: sampled rows against the
+fp64-accumulated check, normwise max_j|dC| / max_j|R| <= 1e-5 (BASELINE.json
+config 2/5 tolerance)."""
+import numpy as np
+import pytest
+
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def check(A, B, C, nrows=48, seed=0):
+    M, N = C.shape
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([[0, M - 1], rng.integers(0, M, nrows)])).astype(np.uint32)
+    R = oracle.sgemm_ref_rows(np.ascontiguousarray(A), np.ascontiguousarray(B), rows, N,
+                              A.shape[1])
+    return oracle.sgemm_rel_err(np.ascontiguousarray(C), R, rows, N)
+
+
+@pytest.mark.parametrize("mode", [pkg.SGEMM_FFMA, pkg.SGEMM_AUTO])
+@pytest.mark.parametrize("M,N,K", [(1024, 1024, 1024), (256, 256, 256), (100, 77, 33),
+                                   (1, 1, 1), (129, 257, 65), (512, 128, 2048)])
+def test_sgemm_shapes(ctx, mode, M, N, K):
+    A = oracle.fill_uniform(M * K, 1).reshape(M, K)
+    B = oracle.fill_uniform(K * N, 2).reshape(K, N)
+    C = ctx.sgemm(A, B, mode=mode)
+    assert check(A, B, C) <= TOL
+
+
+def test_sgemm_leading_dims(ctx):
+    M, N, K = 200, 150, 96
+    Abig = oracle.fill_uniform(M * (K + 7), 3).reshape(M, K + 7)
+    Bbig = oracle.fill_uniform(K * (N + 5), 4).reshape(K, N + 5)
+    A, B = Abig[:, :K], Bbig[:, :N]
+    C = np.zeros((M, N + 3), dtype=np.float32)[:, :N]
+    ctx.sgemm(A, B, C, mode=pkg.SGEMM_FFMA)
+    assert check(A, B, C) <= TOL
+
+
+def test_sgemm_k_zero(ctx):
+    A = np.zeros((8, 0), dtype=np.float32)
+    B = np.zeros((0, 9), dtype=np.float32)
+    C = np.full((8, 9), 3.0, dtype=np.float32)
+    ctx.sgemm(A, B, C)
+    assert np.all(C == 0)
+
+
+def test_sgemm_device_api(ctx):
+    import torch
+    M = N = K = 512
+    A = torch.from_numpy(oracle.fill_uniform(M * K, 5).reshape(M, K)).cuda()
+    B = torch.from_numpy(oracle.fill_uniform(K * N, 6).reshape(K, N)).cuda()
+    C = torch.empty(M, N, device="cuda")
+    ctx.sgemm_device(M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+                     torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert check(A.cpu().numpy(), B.cpu().numpy(), C.cpu().numpy()) <= TOL
