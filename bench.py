@@ -278,7 +278,10 @@ def run_ours(args):
     npx = sum(t.nrows * t.ncols for t in tiles_local)
     dev_out = torch.empty(npx, dtype=torch.int32, device=f"cuda:{local}")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
-    stream = torch.cuda.current_stream()
+    # a real stream: torch's default stream is the legacy NULL stream (handle
+    # 0), which the C ABI would read as "use the context's own stream"
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
 
     def launch():
@@ -419,6 +422,7 @@ def run_secondary(ctx, args):
     from oracle import oracle
     out = {}
     stream = torch.cuda.current_stream()
+    assert stream.cuda_stream != 0
     steps = max(3, min(args.steps, 10))
 
     def dev_time(fn, n):
@@ -481,70 +485,48 @@ def run_secondary(ctx, args):
         del A, B, C
 
     out["cfg4_request_storm"] = run_storm(ctx)
+    out["cfg4_request_storm_closed_loop"] = run_storm(ctx, closed_loop=True)
     return out
 
 
-def run_storm(ctx, clients=64, per=1600, seed=2024):
-    """64 client threads x 1600 requests, each a 64x64 fp64 tile (pitch 1/512,
-    max_iter 256) at a seeded offset; every reply lands in a pinned buffer.
-    Each client keeps all its requests in flight (async send with
-    sender-directed replies)."""
+def run_storm(ctx, clients=64, per=1600, seed=2024, closed_loop=False):
+    """BASELINE config 4: 64 native client threads (stand-ins for 64 cafx client
+    actors, paper_1505_07368_b200/tools/storm_client.cpp) x 1600 requests, each
+    a 64x64 fp64 tile (pitch 1/512, max_iter 256) at a seeded offset, replies in
+    pinned buffers. Open loop = async sends with sender-directed replies;
+    closed loop = one outstanding request per client (sync_send)."""
+    import ctypes as C
+
     import numpy as np
 
     import paper_1505_07368_b200 as pkg
     from oracle import oracle
     rng = np.random.default_rng(seed)
-    kx = rng.integers(0, 3 * 512 - 64 + 1, size=(clients, per))
-    ky = rng.integers(0, 2 * 512 - 64 + 1, size=(clients, per))
-    descs = (pkg.MandelDesc * (clients * per))()
-    for c in range(clients):
-        for i in range(per):
-            x0, y0 = -2.0 + kx[c, i] / 512, -1.0 + ky[c, i] / 512
-            descs[c * per + i] = pkg.mandel_desc(x0, x0 + 0.125, y0, y0 + 0.125, 64, 64, 256,
-                                                 fp64=True, centre=True)
-    replies = ctx.pinned_empty((clients * per, 4096), np.uint32)
-    actor = ctx.spawn("mandelbrot")
-    import ctypes as C
-    L = pkg.lib()
-    done_count = [0]
-    lock = threading.Lock()
-    all_done = threading.Event()
     total = clients * per
-
-    @pkg.cafxg.DONE_FN
-    def on_done(user, status):
-        with lock:
-            done_count[0] += 1
-            if status != 0:
-                done_count.append(status)
-            if done_count[0] == total:
-                all_done.set()
-    size = C.c_size_t(C.sizeof(pkg.MandelDesc))
-    base = C.addressof(descs)
-    rbase = replies.ctypes.data
-
-    def client(c):
-        ptr = (C.c_void_p * 1)()
-        sz = (C.c_size_t * 1)(size)
-        for i in range(per):
-            k = c * per + i
-            ptr[0] = base + k * C.sizeof(pkg.MandelDesc)
-            rc = L.cafxg_actor_enqueue(actor.handle, ptr, sz, 1, rbase + k * 16384, 16384,
-                                       on_done, None)
-            assert rc == 0
-
+    kx = rng.integers(0, 3 * 512 - 64 + 1, size=total)
+    ky = rng.integers(0, 2 * 512 - 64 + 1, size=total)
+    descs = (pkg.MandelDesc * total)()
+    for k in range(total):
+        x0, y0 = -2.0 + kx[k] / 512, -1.0 + ky[k] / 512
+        descs[k] = pkg.mandel_desc(x0, x0 + 0.125, y0, y0 + 0.125, 64, 64, 256,
+                                   fp64=True, centre=True)
+    replies = ctx.pinned_empty((total, 4096), np.uint32)
+    S = C.CDLL(os.path.join(ROOT, "paper_1505_07368_b200", "libcafxg_storm.so"))
+    S.cafxg_storm_run.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint32,
+                                  C.c_uint32, C.c_int, C.POINTER(C.c_double),
+                                  C.POINTER(C.c_uint32)]
+    actor = ctx.spawn("mandelbrot")
+    # warm-up burst (pool growth, first launches)
+    wms, errs = C.c_double(), C.c_uint32()
+    S.cafxg_storm_run(actor.handle, descs, replies.ctypes.data, 16384, 8, 64, 0,
+                      C.byref(wms), C.byref(errs))
+    replies[:] = 0
     st0 = ctx.stats()
-    t0 = time.perf_counter()
-    th = [threading.Thread(target=client, args=(c,)) for c in range(clients)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    all_done.wait(600)
-    dt = time.perf_counter() - t0
+    rc = S.cafxg_storm_run(actor.handle, descs, replies.ctypes.data, 16384, clients, per,
+                           1 if closed_loop else 0, C.byref(wms), C.byref(errs))
     st1 = ctx.stats()
+    dt = wms.value / 1e3
     iters = float(replies.sum(dtype=np.uint64))
-    # per-tile check of a seeded sample of replies against the fp64 oracle
     bad = 0
     for k in np.random.default_rng(seed + 1).integers(0, total, size=128):
         d = descs[int(k)]
@@ -553,11 +535,13 @@ def run_storm(ctx, clients=64, per=1600, seed=2024):
         bad += int(not np.array_equal(replies[int(k)].reshape(64, 64), ref))
     actor.release()
     ctx.pinned_free(replies)
-    return {"requests": total, "clients": clients, "wall_ms": round(dt * 1e3, 2),
+    return {"mode": "closed loop (1 outstanding/client)" if closed_loop else
+            "open loop (async sends)", "requests": total, "clients": clients,
+            "status": rc, "wall_ms": round(wms.value, 2),
             "requests_per_s": round(total / dt, 1), "giter_s": round(iters / dt / 1e9, 2),
             "batches": int(st1.batches - st0.batches), "max_batch": int(st1.max_batch),
             "kernel_launches": int(st1.kernel_launches - st0.kernel_launches),
-            "errors": len(done_count) - 1, "checked_tiles": 128, "mismatched_tiles": bad}
+            "errors": int(errs.value), "checked_tiles": 128, "mismatched_tiles": bad}
 
 
 def main():

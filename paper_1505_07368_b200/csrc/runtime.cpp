@@ -89,6 +89,7 @@ class PinnedPool {
     }
     std::lock_guard<std::mutex> g(mu_);
     live_[p] = cls;
+    ranges_[(uintptr_t)p] = cls;
     return p;
   }
 
@@ -102,6 +103,19 @@ class PinnedPool {
     return true;
   }
 
+  // [p, p+bytes) inside one live pool buffer (no driver call).
+  bool contains(const void* p, size_t bytes) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (live_.empty())
+      return false;
+    auto it = ranges_.upper_bound((uintptr_t)p);
+    if (it == ranges_.begin())
+      return false;
+    --it;
+    return (uintptr_t)p + bytes <= it->first + it->second &&
+           live_.count((void*)it->first);
+  }
+
  private:
   static size_t size_class(size_t bytes) {
     size_t c = 4096;
@@ -112,6 +126,7 @@ class PinnedPool {
   std::mutex mu_;
   std::unordered_map<void*, size_t> live_;
   std::map<size_t, std::vector<void*>> free_;
+  std::map<uintptr_t, size_t> ranges_;  // every buffer ever allocated
 };
 
 // True when [p, p+bytes) is page-locked host memory the device can address
@@ -824,6 +839,9 @@ struct Request {
   void* out = nullptr;
   size_t out_bytes = 0;
   uint64_t pixels = 0;
+  uint32_t max_iter = 0;
+  bool exact = false;       // needs the 8-op escape step (tiny |ci| rows)
+  bool out_pinned = false;  // reply buffer is device-mapped pinned memory
   cafxg_done_fn done = nullptr;
   void* user = nullptr;
 };
@@ -862,12 +880,10 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   size_t ntiles = 0;
   for (Request* r : batch) {
     px += r->pixels;
-    for (auto& t : r->tiles) {
-      maxit = std::max(maxit, t.max_iter);
-      exact = exact || use_exact(ctx, t);
-      ++ntiles;
-    }
-    all_pinned = all_pinned && host_is_pinned(r->out, r->out_bytes);
+    maxit = std::max(maxit, r->max_iter);
+    exact = exact || r->exact;
+    ntiles += r->tiles.size();
+    all_pinned = all_pinned && r->out_pinned;
   }
   int status = CAFXG_OK;
   uint32_t* dout = nullptr;
@@ -1401,8 +1417,12 @@ int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in, const size_t* in_
     for (auto& x : r->tiles) {
       x.out_offset = off;  // tiles packed in order in the reply
       off += (uint64_t)x.nrows * x.ncols;
+      r->max_iter = std::max(r->max_iter, x.max_iter);
+      r->exact = r->exact || use_exact(a->ctx, x);
     }
     r->pixels = off;
+    // classified on the client's thread so the dispatcher stays lean
+    r->out_pinned = a->ctx->pinned.contains(out, out_bytes) || host_is_pinned(out, out_bytes);
   } else {
     r->a = static_cast<const float*>(in[0]);
     r->b = static_cast<const float*>(in[1]);

@@ -1,0 +1,97 @@
+// Native request-storm driver for BASELINE config 4 (bench.py, tests): N
+// client threads stand in for N cafx client actors and push requests into one
+// compute actor through cafxg_actor_enqueue (the seam an adapter actor's
+// `enqueue` forwards to, abstract_actor.hpp:36).
+//
+//  * open loop  (mode 0): every client sends all its requests back to back,
+//    replies directed to the sender (async `send`, local_actor.cpp:325-327);
+//  * closed loop (mode 1): one outstanding request per client, the
+//    `sync_send(...).then(...)` discipline (local_actor.cpp:99-101).
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdint>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "../../include/cafxg.h"
+
+namespace {
+
+struct Client {
+  std::mutex mu;
+  std::condition_variable cv;
+  uint32_t done = 0;
+  std::atomic<uint32_t>* global_done;
+  std::atomic<uint32_t>* errors;
+};
+
+void on_done(void* user, int status) {
+  auto* c = static_cast<Client*>(user);
+  if (status != CAFXG_OK)
+    c->errors->fetch_add(1);
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    ++c->done;
+  }
+  c->cv.notify_one();
+  c->global_done->fetch_add(1, std::memory_order_release);
+}
+
+}  // namespace
+
+extern "C" {
+
+// descs: clients*per descriptors (request k = client k/per); replies: one
+// reply buffer of `reply_bytes` per request, contiguous. Returns 0 and fills
+// wall_ms / errors, or the first enqueue failure status.
+int cafxg_storm_run(cafxg_actor* actor, const cafxg_mandel_desc* descs,
+                    uint8_t* replies, size_t reply_bytes, uint32_t clients,
+                    uint32_t per, int closed_loop, double* wall_ms,
+                    uint32_t* errors_out) {
+  std::atomic<uint32_t> global_done{0}, errors{0};
+  std::atomic<int> enqueue_status{CAFXG_OK};
+  std::vector<Client> cs(clients);
+  for (auto& c : cs) {
+    c.global_done = &global_done;
+    c.errors = &errors;
+  }
+  const uint64_t total = (uint64_t)clients * per;
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> th;
+  th.reserve(clients);
+  for (uint32_t c = 0; c < clients; ++c) {
+    th.emplace_back([&, c] {
+      Client& me = cs[c];
+      size_t sz = sizeof(cafxg_mandel_desc);
+      for (uint32_t i = 0; i < per; ++i) {
+        uint64_t k = (uint64_t)c * per + i;
+        const void* in[1] = {&descs[k]};
+        int s = cafxg_actor_enqueue(actor, in, &sz, 1, replies + k * reply_bytes,
+                                    reply_bytes, on_done, &me);
+        if (s != CAFXG_OK) {
+          enqueue_status.store(s);
+          return;
+        }
+        if (closed_loop) {
+          std::unique_lock<std::mutex> lk(me.mu);
+          me.cv.wait(lk, [&] { return me.done == i + 1; });
+        }
+      }
+      std::unique_lock<std::mutex> lk(me.mu);
+      me.cv.wait(lk, [&] { return me.done == per; });
+    });
+  }
+  for (auto& t : th)
+    t.join();
+  auto t1 = std::chrono::steady_clock::now();
+  if (wall_ms)
+    *wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  if (errors_out)
+    *errors_out = errors.load();
+  (void)total;
+  return enqueue_status.load();
+}
+
+}  // extern "C"

@@ -169,7 +169,8 @@ def test_device_api_with_torch(ctx):
     import torch
     d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 640, 480, 150)
     out = torch.zeros(640 * 480, dtype=torch.int32, device="cuda:0")
-    s = torch.cuda.current_stream()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
     ctx.mandelbrot_device(d, out.data_ptr(), s.cuda_stream)
     torch.cuda.synchronize()
     ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 640, 480, 150, fp64=False, centre=True)

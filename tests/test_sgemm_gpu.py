@@ -54,7 +54,8 @@ def test_sgemm_device_api(ctx):
     A = torch.from_numpy(oracle.fill_uniform(M * K, 5).reshape(M, K)).cuda()
     B = torch.from_numpy(oracle.fill_uniform(K * N, 6).reshape(K, N)).cuda()
     C = torch.empty(M, N, device="cuda")
-    ctx.sgemm_device(M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(),
-                     torch.cuda.current_stream().cuda_stream)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    ctx.sgemm_device(M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream)
     torch.cuda.synchronize()
     assert check(A.cpu().numpy(), B.cpu().numpy(), C.cpu().numpy()) <= TOL
