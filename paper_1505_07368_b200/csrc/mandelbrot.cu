@@ -131,8 +131,10 @@ struct F32Slots {
       asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP_EXACT)
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
   }
-  __device__ __forceinline__ void start(int slot, double xr, double xi) {
-    float fr = __double2float_rn(xr), fi = __double2float_rn(xi);
+  __device__ __forceinline__ void start(int slot, const void* cx, const void* cy,
+                                        uint32_t col, uint32_t row) {
+    float fr = __ldg(static_cast<const float*>(cx) + col);
+    float fi = __ldg(static_cast<const float*>(cy) + row);
     if (slot == 0) {
       cr.x = fr; ci.x = fi; zr.x = zi.x = zr2.x = zi2.x = 0.0f;
     } else {
@@ -203,7 +205,10 @@ struct F64Slots {
       asm volatile(CAFXG_F64_PROLOGUE CAFXG_X4(CAFXG_F64_PAIR(
           CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
   }
-  __device__ __forceinline__ void start(int slot, double xr, double xi) {
+  __device__ __forceinline__ void start(int slot, const void* cx, const void* cy,
+                                        uint32_t col, uint32_t row) {
+    double xr = __ldg(static_cast<const double*>(cx) + col);
+    double xi = __ldg(static_cast<const double*>(cy) + row);
     if (slot == 0) {
       cr.x = xr; ci.x = xi; zr.x = zi.x = zr2.x = zi2.x = 0.0;
     } else {
@@ -228,20 +233,38 @@ __device__ __forceinline__ uint32_t find_tile(const MLaunch& L, uint32_t chunk) 
   return lo;
 }
 
-// Coordinates of pixel p (tile-local, row-major) of tile T, as the oracle
-// computes them: lo + ((i + s) * span) / n in fp64 with IEEE rounding.
-__device__ __forceinline__ void pixel_coord(const MTile* T, uint32_t p,
-                                            double& cr, double& ci) {
-  uint32_t row = p / T->ncols;
-  uint32_t col = p - row * T->ncols;
-  double kx = __dadd_rn((double)(T->col0 + col), T->s);
-  double ky = __dadd_rn((double)(T->row0 + row), T->s);
-  cr = __dadd_rn(T->x0, __ddiv_rn(__dmul_rn(kx, T->xspan), (double)T->width));
-  ci = __dadd_rn(T->y0, __ddiv_rn(__dmul_rn(ky, T->yspan), (double)T->height));
+// Coordinates as the oracle computes them (cafx_oracle.c oracle_coord):
+// lo + ((i + s) * span) / n in fp64 with IEEE rounding, then rounded to the
+// request precision. Computed once per column / row by the prologue kernel.
+__device__ __forceinline__ double grid_coord(double lo, double span, double s,
+                                             uint32_t i, uint32_t n) {
+  double k = __dadd_rn((double)i, s);
+  return __dadd_rn(lo, __ddiv_rn(__dmul_rn(k, span), (double)n));
 }
 
+template <class T>
+__global__ void __launch_bounds__(256)
+    coords_kernel(const __grid_constant__ MLaunch L) {
+  const MTile* t = tile_ptr(L, blockIdx.y);
+  T* cx = static_cast<T*>(t->cx);
+  T* cy = static_cast<T*>(t->cy);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < t->ncols + t->nrows;
+       i += gridDim.x * blockDim.x) {
+    if (i < t->ncols)
+      cx[i] = (T)grid_coord(t->x0, t->xspan, t->s, t->col0 + i, t->width);
+    else
+      cy[i - t->ncols] =
+          (T)grid_coord(t->y0, t->yspan, t->s, t->row0 + (i - t->ncols), t->height);
+  }
+}
+
+// fp32: 6 CTAs x 256 threads per SM (40 registers) so each scheduler holds
+// 12 warps to cover the FP2 dependency chains; fp64 is bound by the FP64 pipe.
+template <class Slots>
+constexpr int kMinBlocks = sizeof(typename Slots::S) == 4 ? 6 : 4;
+
 template <class Slots, int kSteps, bool kExact>
-__global__ void __launch_bounds__(kMandelThreads)
+__global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
     mandel_kernel(const __grid_constant__ MLaunch L) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -286,10 +309,9 @@ __global__ void __launch_bounds__(kMandelThreads)
       uint32_t r0 = __popc(b0 & lt_mask);
       uint32_t r1 = __popc(b0) + __popc(b1 & lt_mask);
       if (!live0 && r0 < avail) {
-        double xr, xi;
         uint32_t p = cur + r0;
-        pixel_coord(T, p, xr, xi);
-        sl.start(0, xr, xi);
+        uint32_t row = p / T->ncols;
+        sl.start(0, T->cx, T->cy, p - row * T->ncols, row);
         e0 = 0;
         n0 = 0;
         m0 = T->max_iter;
@@ -297,10 +319,9 @@ __global__ void __launch_bounds__(kMandelThreads)
         live0 = true;
       }
       if (!live1 && r1 < avail) {
-        double xr, xi;
         uint32_t p = cur + r1;
-        pixel_coord(T, p, xr, xi);
-        sl.start(1, xr, xi);
+        uint32_t row = p / T->ncols;
+        sl.start(1, T->cx, T->cy, p - row * T->ncols, row);
         e1 = 0;
         n1 = 0;
         m1 = T->max_iter;
@@ -381,6 +402,20 @@ int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,
   const bool exact = cfg.exact;
   cudaStream_t s = (cudaStream_t)stream;
   CAFXG_MANDEL_DISPATCH(launch_t, L, cfg.grid, s);
+}
+
+int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
+                         void* stream) {
+  if (L.n == 0)
+    return 0;
+  dim3 grid((max_extent + 255) / 256, L.n);
+  if (grid.x > 64)
+    grid.x = 64;
+  if (precision == 0)
+    coords_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(L);
+  else
+    coords_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(L);
+  return (int)cudaGetLastError();
 }
 
 int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact) {

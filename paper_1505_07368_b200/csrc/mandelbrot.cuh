@@ -18,6 +18,11 @@ struct MTile {
   uint32_t max_iter;
   uint32_t chunk_begin;
   uint32_t* out;                // tile's first count; row-major, pitch ncols
+  // Coordinate tables (filled by the prologue kernel): cx[ncols] real parts
+  // of the tile's columns, cy[nrows] imaginary parts of its rows, stored in
+  // the request precision (float or double).
+  void* cx;
+  void* cy;
 };
 
 constexpr int kInlineTiles = 8;    // tiles passed by value in the params
@@ -44,6 +49,9 @@ struct MandelLaunchCfg {
 };
 int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,
                   void* stream);
+// Prologue: fills every tile's cx/cy tables (grid.y = tile).
+int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
+                         void* stream);
 int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact);
 
 }  // namespace cafxg

@@ -442,11 +442,28 @@ static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
 // Enqueues one Mandelbrot launch over `tiles` (all the same precision) on
 // `stream`; descriptors beyond the inline capacity are uploaded first.
 static int launch_mandel(cafxg_ctx* ctx, Device* d,
-                         const std::vector<MTile>& tiles, uint32_t total_chunks,
+                         const std::vector<MTile>& tiles_in, uint32_t total_chunks,
                          int precision, uint32_t max_iter, bool exact,
                          uint64_t pixels, cudaStream_t stream) {
   if (total_chunks == 0)
     return CAFXG_OK;
+  // coordinate tables: one column table and one row table per tile
+  std::vector<MTile> tiles = tiles_in;
+  const size_t esz = precision ? sizeof(double) : sizeof(float);
+  uint64_t ncoord = 0;
+  uint32_t max_extent = 0;
+  for (auto& t : tiles) {
+    ncoord += (uint64_t)t.ncols + t.nrows;
+    max_extent = std::max(max_extent, t.ncols + t.nrows);
+  }
+  uint8_t* coords = nullptr;
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&coords, ncoord * esz + 16, stream));
+  uint64_t off = 0;
+  for (auto& t : tiles) {
+    t.cx = coords + off * esz;
+    t.cy = coords + (off + t.ncols) * esz;
+    off += (uint64_t)t.ncols + t.nrows;
+  }
   MLaunch L{};
   L.n = (uint32_t)tiles.size();
   L.total_chunks = total_chunks;
@@ -465,11 +482,15 @@ static int launch_mandel(cafxg_ctx* ctx, Device* d,
     ctx->st_h2d += bytes;
     L.tiles = dev_tiles;
   }
+  int e = mandel_coords_launch(L, precision, max_extent, stream);
+  if (e != 0)
+    return cuda_status((cudaError_t)e, "mandelbrot coordinate launch");
   MandelLaunchCfg cfg = mandel_cfg(d, precision, max_iter, exact, pixels);
-  int e = mandel_launch(L, precision, cfg, stream);
+  e = mandel_launch(L, precision, cfg, stream);
   if (e != 0)
     return cuda_status((cudaError_t)e, "mandelbrot launch");
-  ctx->st_launches++;
+  ctx->st_launches += 2;
+  CAFXG_CUDA_TRY(cudaFreeAsync(coords, stream));
   if (dev_tiles)
     CAFXG_CUDA_TRY(cudaFreeAsync(dev_tiles, stream));
   return CAFXG_OK;
