@@ -85,29 +85,32 @@ constexpr unsigned kFull = 0xffffffffu;
   "@!p0 add.u32 %4, %4, 1;\n\t"                             \
   "@!p1 add.u32 %5, %5, 1;\n\t"
 
-// operands: %0,%1 zr; %2,%3 zi; %4 n0; %5 n1; %6 e0; %7 e1; %8,%9 zr^2;
-// %10,%11 zi^2; %12,%13 cr; %14,%15 ci; %16 runtime zero; %17 2.0f.
+// operands: %0,%1 zr; %2,%3 zi; %4 n0; %5 n1; %6,%7 zr^2; %8,%9 zi^2;
+// %10,%11 cr; %12,%13 ci; %14 runtime zero; %15 2.0f. Bit 31 of a count is
+// the slot's sticky escape flag (max_iter <= 2^30 keeps it free).
 #define CAFXG_F32_PROLOGUE                                  \
   "{\n\t.reg .b64 x, y, q, w, c, d, t, v, s, two, zz;\n\t"  \
   ".reg .f32 s0, s1;\n\t.reg .pred p0, p1;\n\t"             \
   "mov.b64 x, {%0, %1};\n\tmov.b64 y, {%2, %3};\n\t"        \
-  "mov.b64 q, {%8, %9};\n\tmov.b64 w, {%10, %11};\n\t"      \
-  "mov.b64 c, {%12, %13};\n\tmov.b64 d, {%14, %15};\n\t"    \
-  "mov.b64 zz, {%16, %16};\n\t"                             \
-  "mov.b64 two, {%17, %17};\n\t"                            \
-  "setp.ne.u32 p0, %6, 0;\n\tsetp.ne.u32 p1, %7, 0;\n\t"
+  "mov.b64 q, {%6, %7};\n\tmov.b64 w, {%8, %9};\n\t"        \
+  "mov.b64 c, {%10, %11};\n\tmov.b64 d, {%12, %13};\n\t"    \
+  "mov.b64 zz, {%14, %14};\n\t"                             \
+  "mov.b64 two, {%15, %15};\n\t"                            \
+  "setp.lt.s32 p0, %4, 0;\n\tsetp.lt.s32 p1, %5, 0;\n\t"
 
 #define CAFXG_F32_EPILOGUE                                  \
   "mov.b64 {%0, %1}, x;\n\tmov.b64 {%2, %3}, y;\n\t"        \
-  "mov.b64 {%8, %9}, q;\n\tmov.b64 {%10, %11}, w;\n\t"      \
-  "selp.u32 %6, 1, 0, p0;\n\tselp.u32 %7, 1, 0, p1;\n\t}"
+  "mov.b64 {%6, %7}, q;\n\tmov.b64 {%8, %9}, w;\n\t"        \
+  "@p0 or.b32 %4, %4, 0x80000000;\n\t"                      \
+  "@p1 or.b32 %5, %5, 0x80000000;\n\t}"
 
 #define CAFXG_X4(S) S S S S
 #define CAFXG_X16(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S)
+#define CAFXG_X32(S) CAFXG_X16(S) CAFXG_X16(S)
 
 #define CAFXG_F32_OPERANDS                                                   \
   : "+f"(zr.x), "+f"(zr.y), "+f"(zi.x), "+f"(zi.y), "+r"(n0), "+r"(n1),       \
-    "+r"(e0), "+r"(e1), "+f"(zr2.x), "+f"(zr2.y), "+f"(zi2.x), "+f"(zi2.y)    \
+    "+f"(zr2.x), "+f"(zr2.y), "+f"(zi2.x), "+f"(zi2.y)                        \
   : "f"(cr.x), "f"(cr.y), "f"(ci.x), "f"(ci.y), "f"(zero), "f"(2.0f)
 
 struct F32Slots {
@@ -116,9 +119,14 @@ struct F32Slots {
   float zero;
 
   template <int kSteps, bool kExact>
-  __device__ __forceinline__ void run(uint32_t& n0, uint32_t& n1, uint32_t& e0,
-                                      uint32_t& e1) {
-    if constexpr (kSteps == 16 && !kExact)
+  __device__ __forceinline__ void run(uint32_t& n0, uint32_t& n1) {
+    if constexpr (kSteps == 32 && !kExact)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X32(CAFXG_F32_STEP_FAST)
+                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
+    else if constexpr (kSteps == 32 && kExact)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X32(CAFXG_F32_STEP_EXACT)
+                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
+    else if constexpr (kSteps == 16 && !kExact)
       asm volatile(CAFXG_F32_PROLOGUE CAFXG_X16(CAFXG_F32_STEP_FAST)
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
     else if constexpr (kSteps == 16 && kExact)
@@ -170,18 +178,18 @@ struct F32Slots {
   "@!" P " add.u32 " N ", " N ", 1;\n\t"
 
 #define CAFXG_F64_PAIR(STEP)                                             \
-  STEP("%0", "%1", "%2", "%3", "%12", "%13", "p0", "%8")                 \
-  STEP("%4", "%5", "%6", "%7", "%14", "%15", "p1", "%9")
+  STEP("%0", "%1", "%2", "%3", "%10", "%11", "p0", "%8")                 \
+  STEP("%4", "%5", "%6", "%7", "%12", "%13", "p1", "%9")
 
 #define CAFXG_F64_PROLOGUE                                               \
   "{\n\t.reg .f64 t, v, s;\n\t.reg .pred p0, p1;\n\t"                    \
-  "setp.ne.u32 p0, %10, 0;\n\tsetp.ne.u32 p1, %11, 0;\n\t"
+  "setp.lt.s32 p0, %8, 0;\n\tsetp.lt.s32 p1, %9, 0;\n\t"
 #define CAFXG_F64_EPILOGUE                                               \
-  "selp.u32 %10, 1, 0, p0;\n\tselp.u32 %11, 1, 0, p1;\n\t}"
+  "@p0 or.b32 %8, %8, 0x80000000;\n\t"                                 \
+  "@p1 or.b32 %9, %9, 0x80000000;\n\t}"
 #define CAFXG_F64_OPERANDS                                               \
   : "+d"(zr.x), "+d"(zi.x), "+d"(zr2.x), "+d"(zi2.x), "+d"(zr.y),         \
-    "+d"(zi.y), "+d"(zr2.y), "+d"(zi2.y), "+r"(n0), "+r"(n1), "+r"(e0),   \
-    "+r"(e1)                                                            \
+    "+d"(zi.y), "+d"(zr2.y), "+d"(zi2.y), "+r"(n0), "+r"(n1)              \
   : "d"(cr.x), "d"(ci.x), "d"(cr.y), "d"(ci.y)
 
 struct F64Slots {
@@ -190,9 +198,14 @@ struct F64Slots {
   float zero;
 
   template <int kSteps, bool kExact>
-  __device__ __forceinline__ void run(uint32_t& n0, uint32_t& n1, uint32_t& e0,
-                                      uint32_t& e1) {
-    if constexpr (kSteps == 16 && !kExact)
+  __device__ __forceinline__ void run(uint32_t& n0, uint32_t& n1) {
+    if constexpr (kSteps == 32 && !kExact)
+      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X32(CAFXG_F64_PAIR(
+          CAFXG_F64_STEP_FAST)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
+    else if constexpr (kSteps == 32 && kExact)
+      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X32(CAFXG_F64_PAIR(
+          CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
+    else if constexpr (kSteps == 16 && !kExact)
       asm volatile(CAFXG_F64_PROLOGUE CAFXG_X16(CAFXG_F64_PAIR(
           CAFXG_F64_STEP_FAST)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
     else if constexpr (kSteps == 16 && kExact)
@@ -269,18 +282,20 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
 
-  // warp-uniform chunk cursor
-  uint32_t cur = 0, cend = 0;
+  // warp-uniform cursor: columns [cur, cend) of row `crow` of tile T. Chunks
+  // never straddle rows, so a lane's pixel is (crow, cur + rank): no division
+  // and one shared row coordinate per chunk.
+  uint32_t cur = 0, cend = 0, crow = 0;
   const MTile* T = nullptr;
   bool exhausted = false;
 
   Slots sl;
   sl.zero = L.zero;
-  uint32_t e0 = 0, e1 = 0;  // sticky escape flags (0/1)
-  uint32_t n0 = 0, n1 = 0;  // iterations completed without escape
+  // iterations completed without escape; bit 31 = sticky escape flag
+  uint32_t n0 = 0, n1 = 0;
   uint32_t m0 = 0, m1 = 0;  // max_iter of the slot's pixel
   bool live0 = false, live1 = false;
-  uint32_t *o0 = nullptr, *o1 = nullptr;
+  uint32_t o0 = 0, o1 = 0;  // output element offsets from L.out
 
   auto refill = [&]() {
     while (true) {
@@ -298,34 +313,29 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
           exhausted = true;
           return;
         }
-        uint32_t t = find_tile(L, c);
-        T = tile_ptr(L, t);
-        uint32_t npix = T->nrows * T->ncols;
-        cur = (c - T->chunk_begin) * kChunk;
-        cend = min(cur + kChunk, npix);
+        T = tile_ptr(L, find_tile(L, c));
+        uint32_t local = c - T->chunk_begin;
+        crow = local / T->chunks_per_row;
+        cur = (local - crow * T->chunks_per_row) * kChunk;
+        cend = min(cur + kChunk, T->ncols);
         continue;
       }
       uint32_t avail = cend - cur;
       uint32_t r0 = __popc(b0 & lt_mask);
       uint32_t r1 = __popc(b0) + __popc(b1 & lt_mask);
+      uint32_t orow = T->out_off + crow * T->ncols;
       if (!live0 && r0 < avail) {
-        uint32_t p = cur + r0;
-        uint32_t row = p / T->ncols;
-        sl.start(0, T->cx, T->cy, p - row * T->ncols, row);
-        e0 = 0;
+        sl.start(0, T->cx, T->cy, cur + r0, crow);
         n0 = 0;
         m0 = T->max_iter;
-        o0 = T->out + p;
+        o0 = orow + cur + r0;
         live0 = true;
       }
       if (!live1 && r1 < avail) {
-        uint32_t p = cur + r1;
-        uint32_t row = p / T->ncols;
-        sl.start(1, T->cx, T->cy, p - row * T->ncols, row);
-        e1 = 0;
+        sl.start(1, T->cx, T->cy, cur + r1, crow);
         n1 = 0;
         m1 = T->max_iter;
-        o1 = T->out + p;
+        o1 = orow + cur + r1;
         live1 = true;
       }
       cur += min(want, avail);
@@ -334,16 +344,20 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
 
   refill();
   while (__any_sync(kFull, live0 || live1)) {
-    sl.template run<kSteps, kExact>(n0, n1, e0, e1);
-    bool d0 = live0 && (e0 || n0 >= m0);
-    bool d1 = live1 && (e1 || n1 >= m1);
+    sl.template run<kSteps, kExact>(n0, n1);
+    // escaped (bit 31) or reached max_iter; an escape at step i leaves i-1
+    // non-escaped steps counted, so the reference's return value is n+1
+    bool d0 = live0 && (n0 >= m0);
+    bool d1 = live1 && (n1 >= m1);
     if (__any_sync(kFull, d0 || d1)) {
       if (d0) {
-        *o0 = min(e0 ? n0 + 1u : n0, m0);
+        uint32_t c = (int32_t)n0 < 0 ? (n0 & 0x7fffffffu) + 1u : n0;
+        L.out[o0] = min(c, m0);
         live0 = false;
       }
       if (d1) {
-        *o1 = min(e1 ? n1 + 1u : n1, m1);
+        uint32_t c = (int32_t)n1 < 0 ? (n1 & 0x7fffffffu) + 1u : n1;
+        L.out[o1] = min(c, m1);
         live1 = false;
       }
       refill();
@@ -380,20 +394,18 @@ int occ_t() {
 
 }  // namespace
 
-#define CAFXG_MANDEL_DISPATCH(FN, ...)                                  \
-  do {                                                                  \
-    if (precision == 0) {                                               \
-      if (ksteps <= 4)                                                  \
-        return exact ? FN<F32Slots, 4, true>(__VA_ARGS__)                  \
-                     : FN<F32Slots, 4, false>(__VA_ARGS__);                \
-      return exact ? FN<F32Slots, 16, true>(__VA_ARGS__)                   \
-                   : FN<F32Slots, 16, false>(__VA_ARGS__);                 \
-    }                                                                   \
-    if (ksteps <= 4)                                                    \
-      return exact ? FN<F64Slots, 4, true>(__VA_ARGS__)                    \
-                   : FN<F64Slots, 4, false>(__VA_ARGS__);                  \
-    return exact ? FN<F64Slots, 16, true>(__VA_ARGS__)                     \
-                 : FN<F64Slots, 16, false>(__VA_ARGS__);                   \
+#define CAFXG_MANDEL_K(FN, SL, K, ...)                                 \
+  return exact ? FN<SL, K, true>(__VA_ARGS__) : FN<SL, K, false>(__VA_ARGS__)
+#define CAFXG_MANDEL_DISPATCH(FN, ...)                                 \
+  do {                                                                 \
+    if (precision == 0) {                                              \
+      if (ksteps <= 4) CAFXG_MANDEL_K(FN, F32Slots, 4, __VA_ARGS__);   \
+      if (ksteps <= 16) CAFXG_MANDEL_K(FN, F32Slots, 16, __VA_ARGS__); \
+      CAFXG_MANDEL_K(FN, F32Slots, 32, __VA_ARGS__);                   \
+    }                                                                  \
+    if (ksteps <= 4) CAFXG_MANDEL_K(FN, F64Slots, 4, __VA_ARGS__);     \
+    if (ksteps <= 16) CAFXG_MANDEL_K(FN, F64Slots, 16, __VA_ARGS__);   \
+    CAFXG_MANDEL_K(FN, F64Slots, 32, __VA_ARGS__);                     \
   } while (0)
 
 int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,

@@ -17,7 +17,9 @@ struct MTile {
   uint32_t nrows, ncols;
   uint32_t max_iter;
   uint32_t chunk_begin;
-  uint32_t* out;                // tile's first count; row-major, pitch ncols
+  uint32_t chunks_per_row;      // ceil(ncols / kChunk); chunks never straddle rows
+  uint32_t out_off;             // tile's first count in MLaunch::out (row-major,
+                                // pitch ncols); launch total < 2^32 elements
   // Coordinate tables (filled by the prologue kernel): cx[ncols] real parts
   // of the tile's columns, cy[nrows] imaginary parts of its rows, stored in
   // the request precision (float or double).
@@ -32,6 +34,7 @@ constexpr int kMandelThreads = 256;
 struct MLaunch {
   MTile inl[kInlineTiles];
   const MTile* tiles;   // device copy when n > kInlineTiles
+  uint32_t* out;        // counts of every tile (MTile::out_off)
   uint32_t n;
   uint32_t total_chunks;
   uint32_t* sched;      // [0] chunk cursor, [1] finished blocks (self-reset)

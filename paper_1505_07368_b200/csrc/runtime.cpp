@@ -407,7 +407,13 @@ struct SubTile {
   uint64_t pixels;
 };
 
-static void fill_mtile(MTile& m, const cafxg_mandel_desc& d, uint32_t* out,
+// Work chunks of a tile: rows x ceil(ncols / kChunk) (chunks never straddle
+// rows, see mandel_kernel).
+static uint32_t tile_chunks(uint32_t nrows, uint32_t ncols) {
+  return nrows * ((ncols + kChunk - 1) / kChunk);
+}
+
+static void fill_mtile(MTile& m, const cafxg_mandel_desc& d, uint64_t out_off,
                        uint32_t chunk_begin) {
   m.x0 = d.x0;
   m.xspan = d.x1 - d.x0;
@@ -422,13 +428,14 @@ static void fill_mtile(MTile& m, const cafxg_mandel_desc& d, uint32_t* out,
   m.ncols = d.ncols;
   m.max_iter = d.max_iter;
   m.chunk_begin = chunk_begin;
-  m.out = out;
+  m.chunks_per_row = (d.ncols + kChunk - 1) / kChunk;
+  m.out_off = (uint32_t)out_off;
 }
 
 static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
                                   bool exact, uint64_t pixels) {
   MandelLaunchCfg c;
-  c.ksteps = max_iter >= 256 ? 16 : 4;
+  c.ksteps = max_iter >= 512 ? 32 : max_iter >= 128 ? 16 : 4;
   c.exact = exact;
   int& occ = d->mandel_occ[precision][c.ksteps == 16][exact];
   if (occ == 0)
@@ -441,7 +448,7 @@ static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
 
 // Enqueues one Mandelbrot launch over `tiles` (all the same precision) on
 // `stream`; descriptors beyond the inline capacity are uploaded first.
-static int launch_mandel(cafxg_ctx* ctx, Device* d,
+static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                          const std::vector<MTile>& tiles_in, uint32_t total_chunks,
                          int precision, uint32_t max_iter, bool exact,
                          uint64_t pixels, cudaStream_t stream) {
@@ -467,6 +474,7 @@ static int launch_mandel(cafxg_ctx* ctx, Device* d,
   MLaunch L{};
   L.n = (uint32_t)tiles.size();
   L.total_chunks = total_chunks;
+  L.out = out_base;
   L.sched = d->next_sched();
   L.zero = 0.0f;
   MTile* dev_tiles = nullptr;
@@ -567,12 +575,12 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
     uint32_t chunks = 0, maxit = 0;
     uint64_t off = 0;
     for (size_t k = i; k < j; ++k) {
-      fill_mtile(mt[k - i], subs[k].d, dout + off, chunks);
-      chunks += (uint32_t)((subs[k].pixels + kChunk - 1) / kChunk);
+      fill_mtile(mt[k - i], subs[k].d, off, chunks);
+      chunks += tile_chunks(subs[k].d.nrows, subs[k].d.ncols);
       maxit = std::max(maxit, subs[k].d.max_iter);
       off += subs[k].pixels;
     }
-    CAFXG_TRY(launch_mandel(ctx, d, mt, chunks, prec, maxit, exact, px, d->compute));
+    CAFXG_TRY(launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, d->compute));
     cudaEvent_t ev;
     CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     CAFXG_CUDA_TRY(cudaEventRecord(ev, d->compute));
@@ -929,15 +937,15 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     uint64_t roff = off;
     for (auto& t : r->tiles) {
       MTile m;
-      fill_mtile(m, t, dout + off, chunks);
+      fill_mtile(m, t, off, chunks);
       mt.push_back(m);
       uint64_t tp = (uint64_t)t.nrows * t.ncols;
-      chunks += (uint32_t)((tp + kChunk - 1) / kChunk);
+      chunks += tile_chunks(t.nrows, t.ncols);
       off += tp;
     }
     segs.push_back(CopySeg{dout + roff, r->out, (off - roff) * 4});
   }
-  status = launch_mandel(ctx, d, mt, chunks, prec, maxit, exact, px, d->compute);
+  status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, d->compute);
   if (status == CAFXG_OK && px) {
     if (all_pinned) {
       size_t sb = segs.size() * sizeof(CopySeg);
@@ -1287,28 +1295,40 @@ int cafxg_mandelbrot_device(cafxg_ctx* ctx, int device, const cafxg_mandel_desc*
   try {
     Device* d = ctx->devs[device].get();
     bool exact = false;
-    std::vector<MTile> mt(n);
+    std::vector<MTile> mt;
+    mt.reserve(n);
     uint32_t chunks = 0, maxit = 0;
-    uint64_t px = 0;
+    uint64_t px = 0, lo = UINT64_MAX, hi = 0;
     int prec = n ? (int)tiles[0].precision : 0;
     for (size_t i = 0; i < n; ++i) {
       CAFXG_TRY(validate_mandel(tiles[i]));
       if ((int)tiles[i].precision != prec)
         return fail(CAFXG_E_CONFIG, "mandelbrot_device: mixed precisions in one launch");
-      exact = exact || use_exact(ctx, tiles[i]);
-      fill_mtile(mt[i], tiles[i], dev_out + tiles[i].out_offset, chunks);
       uint64_t tp = (uint64_t)tiles[i].nrows * tiles[i].ncols;
-      chunks += (uint32_t)((tp + kChunk - 1) / kChunk);
+      if (tp == 0)
+        continue;  // empty tiles own no chunks
+      lo = std::min<uint64_t>(lo, tiles[i].out_offset);
+      hi = std::max<uint64_t>(hi, tiles[i].out_offset + tp);
+    }
+    if (hi > lo && hi - lo >= (1ull << 32))
+      return fail(CAFXG_E_OUT_OF_RANGE, "mandelbrot_device: one launch spans >= 2^32 counts");
+    for (size_t i = 0; i < n; ++i) {
+      uint64_t tp = (uint64_t)tiles[i].nrows * tiles[i].ncols;
+      if (tp == 0)
+        continue;
+      exact = exact || use_exact(ctx, tiles[i]);
+      MTile m;
+      fill_mtile(m, tiles[i], tiles[i].out_offset - lo, chunks);
+      mt.push_back(m);
+      chunks += tile_chunks(tiles[i].nrows, tiles[i].ncols);
       maxit = std::max(maxit, tiles[i].max_iter);
       px += tp;
     }
-    // drop empty tiles (they own no chunks and would confuse find_tile)
-    mt.erase(std::remove_if(mt.begin(), mt.end(),
-                            [](const MTile& m) { return m.nrows == 0 || m.ncols == 0; }),
-             mt.end());
+    if (mt.empty())
+      return CAFXG_OK;
     cudaSetDevice(d->ordinal);
     cudaStream_t s = stream ? (cudaStream_t)stream : d->compute;
-    return launch_mandel(ctx, d, mt, chunks, prec, maxit, exact, px, s);
+    return launch_mandel(ctx, d, dev_out + lo, mt, chunks, prec, maxit, exact, px, s);
   } catch (const std::exception& ex) {
     return fail(CAFXG_E_CONFIG, "mandelbrot_device: %s", ex.what());
   }
