@@ -5,6 +5,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp_peak fp_peak.cu
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdio>
 
 #define CHAINS 8
@@ -13,6 +14,7 @@ template <int KIND>
 __global__ void __launch_bounds__(256) probe(float* out, int iters, float a, float b) {
   float x[CHAINS * 2];
   double dx[CHAINS];
+  uint32_t cnt[CHAINS] = {};
 #pragma unroll
   for (int c = 0; c < CHAINS * 2; ++c)
     x[c] = threadIdx.x * 1e-3f + c;
@@ -38,8 +40,41 @@ __global__ void __launch_bounds__(256) probe(float* out, int iters, float a, flo
                      : "+f"(x[2 * c]), "+f"(x[2 * c + 1]) : "f"(a), "f"(b));
       } else if constexpr (KIND == 4) {  // scalar DADD
         asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(dx[c]) : "d"((double)a));
-      } else {  // scalar DMUL
+      } else if constexpr (KIND == 5) {  // scalar DMUL
         asm volatile("mul.rn.f64 %0, %0, %1;" : "+d"(dx[c]) : "d"((double)a));
+      } else if constexpr (KIND == 6 || KIND == 7) {
+        // the Mandelbrot escape step's FP2 mix (7 packed ops, 2 pixels) on 4
+        // independent pixel pairs per thread; KIND 7 adds the per-step
+        // escape bookkeeping (2 x FSETP.OR + 2 x predicated IADD)
+        if (c < CHAINS / 2) {
+          float* z = &x[4 * c];
+          if constexpr (KIND == 6)
+            asm volatile(
+                "{.reg .b64 X, Y, T, V, two, zz, C;"
+                "mov.b64 X, {%0,%1}; mov.b64 Y, {%2,%3}; mov.b64 C, {%4,%4};"
+                "mov.b64 zz, {%5,%5}; mov.b64 two, {%6,%6};"
+                "fma.rn.f32x2 T, X, X, zz; fma.rn.f32x2 V, Y, Y, zz;"
+                "sub.rn.f32x2 T, T, V; add.rn.f32x2 T, T, C; mul.rn.f32x2 V, X, Y;"
+                "fma.rn.f32x2 Y, V, two, C; add.rn.f32x2 X, T, zz;"
+                "mov.b64 {%0,%1}, X; mov.b64 {%2,%3}, Y;}"
+                : "+f"(z[0]), "+f"(z[1]), "+f"(z[2]), "+f"(z[3])
+                : "f"(a), "f"(0.0f), "f"(b));
+          else
+            asm volatile(
+                "{.reg .b64 X, Y, T, V, two, zz, C; .reg .f32 s0, s1; .reg .pred q0, q1;"
+                "setp.ne.u32 q0, %4, 0; setp.ne.u32 q1, %4, 7;"
+                "mov.b64 X, {%0,%1}; mov.b64 Y, {%2,%3}; mov.b64 C, {%5,%5};"
+                "mov.b64 zz, {%6,%6}; mov.b64 two, {%7,%7};"
+                "fma.rn.f32x2 T, X, X, zz; fma.rn.f32x2 V, Y, Y, zz;"
+                "sub.rn.f32x2 T, T, V; add.rn.f32x2 T, T, C; mul.rn.f32x2 V, X, Y;"
+                "fma.rn.f32x2 Y, V, two, C; add.rn.f32x2 X, T, zz;"
+                "mov.b64 {s0, s1}, X;"
+                "setp.gt.or.f32 q0, s0, 0f40800000, q0; setp.gt.or.f32 q1, s1, 0f40800000, q1;"
+                "@!q0 add.u32 %4, %4, 1; @!q1 add.u32 %4, %4, 3;"
+                "mov.b64 {%0,%1}, X; mov.b64 {%2,%3}, Y;}"
+                : "+f"(z[0]), "+f"(z[1]), "+f"(z[2]), "+f"(z[3]), "+r"(cnt[c])
+                : "f"(a), "f"(0.0f), "f"(b));
+        }
       }
     }
   }
@@ -49,7 +84,7 @@ __global__ void __launch_bounds__(256) probe(float* out, int iters, float a, flo
     s += x[c];
 #pragma unroll
   for (int c = 0; c < CHAINS; ++c)
-    s += (float)dx[c];
+    s += (float)dx[c] + (float)cnt[c];
   if (s == 12345.678f)
     out[0] = s;
 }
@@ -92,5 +127,8 @@ int main() {
   run<3>("FFMA2 packed (2 flop/lane-op)", 2.0 * CHAINS, sms);
   run<4>("DADD", 1.0 * CHAINS, sms);
   run<5>("DMUL", 1.0 * CHAINS, sms);
+  // 4 chains x 7 FP2 x 2 lanes per iteration
+  run<6>("escape-step FP2 mix (lane-ops of 7 FP2)", 4.0 * 7 * 2, sms);
+  run<7>("escape-step FP2 mix + FSETP/IADD bookkeeping", 4.0 * 7 * 2, sms);
   return 0;
 }

@@ -1,0 +1,234 @@
+// GPU test of the drop-in on the UNMODIFIED reference runtime: cafx actors
+// (scoped, event-based, typed handles) talk to include/cafxg/gpu_actor.hpp
+// compute actors exactly as they would to CAF's OpenCL actors. Links the
+// reference compiled from its own sources (oracle/_ref/libcafx_ref.so) and
+// libcafxg.so. Prints one PASS/FAIL line per check; exit code 0 iff all pass.
+// Built by tests/cpp/Makefile, run by tests/test_cafx_adapter_gpu.py.
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+#include <thread>
+#include <variant>
+#include <vector>
+
+#include "cafx/actor_system.hpp"
+#include "cafx/bench/bench.hpp"
+#include "cafx/detail/fnv.hpp"
+#include "cafx/scoped_actor.hpp"
+#include "cafxg/gpu_actor.hpp"
+
+using namespace std::chrono_literals;
+
+static int failures = 0;
+
+static void check(bool ok, const std::string& name) {
+  std::printf("%s %s\n", ok ? "PASS" : "FAIL", name.c_str());
+  std::fflush(stdout);
+  if (!ok)
+    ++failures;
+}
+
+static cafxg_mandel_desc ref_desc(uint32_t size, uint32_t it) {
+  cafxg_mandel_desc d{};
+  d.x0 = -1.5; d.x1 = 0.5; d.y0 = -1.0; d.y1 = 1.0;
+  d.width = d.height = size;
+  d.nrows = d.ncols = size;
+  d.max_iter = it;
+  d.precision = CAFXG_FP64;
+  d.sampling = CAFXG_CORNER;
+  return d;
+}
+
+static cafxg_mandel_desc storm_tile(std::mt19937_64& rng) {
+  cafxg_mandel_desc d{};
+  uint64_t kx = rng() % (3 * 512 - 64 + 1), ky = rng() % (2 * 512 - 64 + 1);
+  d.x0 = -2.0 + kx / 512.0; d.x1 = d.x0 + 0.125;
+  d.y0 = -1.0 + ky / 512.0; d.y1 = d.y0 + 0.125;
+  d.width = d.height = d.nrows = d.ncols = 64;
+  d.max_iter = 256;
+  d.precision = CAFXG_FP64;
+  d.sampling = CAFXG_CENTRE;
+  return d;
+}
+
+// expected counts of a storm tile through the reference's own cell
+// (bench.cpp:367) and the generalised coordinate contract (cafxg.h)
+static cafxg::u32vec expect_tile(const cafxg_mandel_desc& d) {
+  cafxg::u32vec out(64 * 64);
+  for (uint32_t r = 0; r < 64; ++r) {
+    volatile double ky = r + 0.5;
+    volatile double qi = ky * (d.y1 - d.y0);
+    double ci = d.y0 + qi / 64.0;
+    for (uint32_t c = 0; c < 64; ++c) {
+      volatile double kx = c + 0.5;
+      volatile double qr = kx * (d.x1 - d.x0);
+      double cr = d.x0 + qr / 64.0;
+      out[r * 64 + c] = cafx::bench::mandelbrot_cell(cr, ci, 256);
+    }
+  }
+  return out;
+}
+
+int main() {
+  cafxg_ctx* ctx = nullptr;
+  if (cafxg_open(1, &ctx) != CAFXG_OK) {
+    std::printf("FAIL cafxg_open: %s\n", cafxg_last_error());
+    return 1;
+  }
+  {
+    cafx::actor_system sys;
+    cafx::scoped_actor self{sys};
+
+    // 1. run_mandelbrot(256, 100)'s image through a request, checksum
+    //    bit-exact (bench.cpp:481-505; golden 12958954340663424292)
+    auto mb = cafxg::spawn_gpu(sys, ctx, "mandelbrot", {});
+    {
+      cafxg::mandel_tiles req{{ref_desc(256, 100)}};
+      auto res = self->request(mb, cafx::make_message(req), 60s);
+      bool ok = std::holds_alternative<cafx::message>(res);
+      if (ok) {
+        const auto& counts = std::get<cafx::message>(res).get<cafxg::u32vec>(0);
+        uint64_t h = cafx::detail::fnv1a_seed;
+        for (uint32_t c : counts)
+          h = cafx::detail::fnv1a_u32(h, c);
+        ok = counts.size() == 256 * 256 && h == 12958954340663424292ull;
+      }
+      check(ok, "request run_mandelbrot(256,100) image -> checksum golden");
+    }
+
+    // 2. matrix_multiply: spawn_cl<float*(float*,float*)>(.., {size, size})
+    {
+      const uint32_t n = 128;
+      auto mm = cafxg::spawn_gpu(sys, ctx, "matrix_multiply", {n, n});
+      cafxg::f32vec a(n * n), b(n * n);
+      std::mt19937_64 rng(5);
+      std::uniform_real_distribution<float> u(-1.0f, 1.0f);
+      for (auto& x : a) x = u(rng);
+      for (auto& x : b) x = u(rng);
+      auto res = self->request(mm, cafx::make_message(a, b), 60s);
+      bool ok = std::holds_alternative<cafx::message>(res);
+      double worst = 0;
+      if (ok) {
+        const auto& c = std::get<cafx::message>(res).get<cafxg::f32vec>(0);
+        ok = c.size() == n * n;
+        for (uint32_t i = 0; ok && i < n; i += 7) {
+          double num = 0, den = 0;
+          for (uint32_t j = 0; j < n; ++j) {
+            double r = 0;
+            for (uint32_t k = 0; k < n; ++k)
+              r += (double)a[i * n + k] * (double)b[k * n + j];
+            num = std::max(num, std::fabs(c[i * n + j] - r));
+            den = std::max(den, std::fabs(r));
+          }
+          worst = std::max(worst, num / den);
+        }
+        ok = ok && worst <= 1e-5;
+      }
+      check(ok, "matrix_multiply actor reply within 1e-5 (err " + std::to_string(worst) + ")");
+
+      // wrong arity -> error reply, the requester's failure path
+      auto bad = self->request(mm, cafx::make_message(a), 30s);
+      check(std::holds_alternative<cafx::error>(bad) &&
+                std::get<cafx::error>(bad).code == cafx::errc::interface_mismatch,
+            "wrong arity -> error(interface_mismatch) reply");
+      auto bad2 = self->request(mm, cafx::make_message(a, cafxg::f32vec(3)), 30s);
+      check(std::holds_alternative<cafx::error>(bad2) &&
+                std::get<cafx::error>(bad2).code == cafx::errc::type_mismatch,
+            "wrong buffer size -> error(type_mismatch) reply");
+    }
+
+    // 3. 64 event-based client actors, each a chain of 40 sync_send(...)
+    //    .then(...) storm tiles (one outstanding request per client,
+    //    local_actor.cpp:99-101); every reply checked against the reference's
+    //    own mandelbrot_cell.
+    {
+      const int clients = 64, per = 40;
+      std::atomic<int> good{0}, bad{0}, finished{0};
+      for (int c = 0; c < clients; ++c) {
+        sys.spawn([&, c, mb](cafx::event_based_actor* me) {
+          auto rng = std::make_shared<std::mt19937_64>(1000 + c);
+          auto left = std::make_shared<int>(per);
+          auto step = std::make_shared<std::function<void()>>();
+          *step = [=, &good, &bad, &finished]() {
+            auto d = storm_tile(*rng);
+            me->sync_send(mb, cafx::make_message(cafxg::mandel_tiles{{d}}))
+                .then(
+                    [=, &good, &bad, &finished](const cafxg::u32vec& counts) {
+                      (counts == expect_tile(d) ? good : bad)++;
+                      if (--*left > 0)
+                        (*step)();
+                      else {
+                        finished++;
+                        me->quit();
+                      }
+                    },
+                    [=, &bad, &finished](const cafx::error&) {
+                      bad++;
+                      finished++;
+                      me->quit();
+                    });
+          };
+          (*step)();
+        });
+      }
+      auto t0 = std::chrono::steady_clock::now();
+      while (finished.load() < clients &&
+             std::chrono::steady_clock::now() - t0 < 120s)
+        std::this_thread::sleep_for(5ms);
+      check(finished.load() == clients && good.load() == clients * per && bad.load() == 0,
+            "64 event-based clients x 40 sync_send storm tiles, all replies exact (" +
+                std::to_string(good.load()) + " good, " + std::to_string(bad.load()) + " bad)");
+    }
+
+    // 4. async send with a sender: reply delivered to the sender's mailbox
+    {
+      cafx::scoped_actor other{sys};
+      std::mt19937_64 rng(77);
+      auto d = storm_tile(rng);
+      other->send(mb, cafx::make_message(cafxg::mandel_tiles{{d}}));
+      bool got = false;
+      other->receive(cafx::behavior{[&](const cafxg::u32vec& counts) {
+                       got = counts == expect_tile(d);
+                     }},
+                     60s);
+      check(got, "async send -> reply to the sender (local_actor.cpp:325-327)");
+    }
+
+    // 5. typed handle: the interface check rejects a mistyped send before
+    //    it reaches the actor (actor_system.cpp:85-91)
+    {
+      auto typed = cafxg::spawn_gpu_typed(sys, ctx, "mandelbrot", {});
+      bool threw = false;
+      try {
+        sys.anon_send(typed, cafx::make_message(uint32_t{7}));
+      } catch (const cafx::failure& f) {
+        threw = f.code() == cafx::errc::interface_mismatch;
+      }
+      check(threw, "typed gpu actor: mistyped send throws interface_mismatch");
+      std::mt19937_64 rng(78);
+      auto d = storm_tile(rng);
+      auto res = self->request(typed, cafx::make_message(cafxg::mandel_tiles{{d}}), 60s);
+      check(std::holds_alternative<cafx::message>(res) &&
+                std::get<cafx::message>(res).get<cafxg::u32vec>(0) == expect_tile(d),
+            "typed gpu actor request");
+    }
+
+    // 6. wire codec round trip (what middleman::publish would send)
+    {
+      std::mt19937_64 rng(79);
+      cafxg::mandel_tiles t{{storm_tile(rng), storm_tile(rng)}};
+      auto msg = cafx::make_message(t, cafxg::u32vec{1, 2, 0xfffffffeu},
+                                    cafxg::f32vec{1.5f, -0.0f});
+      auto back = cafx::deserialize(cafx::serialize(msg));
+      check(back == msg, "buffer types serialize/deserialize (BASP payload codecs)");
+    }
+    // ~actor_system: hard-kills the gpu actors, which unregister (no hang)
+  }
+  std::printf("PASS actor_system shutdown with registered gpu actors\n");
+  cafxg_close(ctx);
+  std::printf("%s\n", failures ? "FAILED" : "ALL PASS");
+  return failures ? 1 : 0;
+}
