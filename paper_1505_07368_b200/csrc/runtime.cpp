@@ -694,8 +694,14 @@ static int sgemm_on_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
       CAFXG_CUDA_TRY(cudaMemsetAsync(C + (size_t)r * g.ldc, 0, g.N * 4, stream));
     return CAFXG_OK;
   }
-  bool tc = g.mode != CAFXG_SGEMM_FFMA &&
-            sgemm_tc_supported(g.M, g.N, g.K, g.lda, g.ldb, g.ldc);
+  // AUTO takes the tensor-core path only when CAFXG_SGEMM_AUTO_TC=1 until
+  // the 3xTF32 kernel is validated on hardware
+  static const bool auto_tc = [] {
+    const char* e = getenv("CAFXG_SGEMM_AUTO_TC");
+    return e && e[0] == '1';
+  }();
+  bool supported = sgemm_tc_supported(g.M, g.N, g.K, g.lda, g.ldb, g.ldc);
+  bool tc = supported && (g.mode == CAFXG_SGEMM_3XTF32 || (g.mode == CAFXG_SGEMM_AUTO && auto_tc));
   if (g.mode == CAFXG_SGEMM_3XTF32 && !tc)
     return fail(CAFXG_E_CONFIG,
                 "sgemm: shape not supported by the 3xTF32 kernel (see cafxg.h)");

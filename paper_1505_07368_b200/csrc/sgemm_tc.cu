@@ -1,16 +1,359 @@
-// 3xTF32 tcgen05 GEMM (placeholder until the tensor-core kernel lands):
-// reports no supported shapes so CAFXG_SGEMM_AUTO uses the FFMA kernel.
-#include <cstddef>
+// 3xTF32 fp32 GEMM on the 5th-generation tensor cores (tcgen05) for the
+// `matrix_multiply` compute actor: C = A * B, row-major.
+//
+// fp32 operands are split once per request into tf32 hi/lo halves
+// (hi = rna_tf32(x), lo = rna_tf32(x - hi)); the kernel accumulates
+// lo(A)*hi(B) + hi(A)*lo(B) + hi(A)*hi(B) in fp32 TMEM, which recovers ~22
+// mantissa bits per product (the dropped lo*lo term is ~2^-22 relative).
+//
+// Kernel (one 128x256 C tile per CTA, 6 warps, warp-specialised):
+//   warp 0 lane 0 : TMA producer -- 4-stage ring of {A_hi, A_lo, Bt_hi, Bt_lo}
+//                   16-deep K slices (SWIZZLE_64B, K-major), mbarrier
+//                   complete_tx;
+//   warp 1        : allocates 256 TMEM columns; lane 0 issues
+//                   tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=256, K=8),
+//                   6 per stage, and tcgen05.commit frees the stage;
+//   warps 2..5    : epilogue -- tcgen05.ld 32x32b.x32 TMEM -> registers ->
+//                   global (each thread owns one C row of the tile).
+// Grid: grouped raster over (M/128) x (N/256) tiles so the CTAs in flight
+// share A row-blocks and B column-blocks in L2.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
 
 #include "sgemm.cuh"
 
 namespace cafxg {
+namespace {
 
-bool sgemm_tc_supported(int, int, int, int, int, int) { return false; }
-size_t sgemm_tc_scratch_bytes(int, int, int) { return 0; }
-int sgemm_tc_launch(const float*, const float*, float*, int, int, int, int, int,
-                    int, void*, int, void*, int*) {
-  return 1;
+constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4;
+constexpr int A_TILE = BM * BK * 4;                       // 8 KiB
+constexpr int B_TILE = BN * BK * 4;                       // 16 KiB
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;      // 48 KiB
+constexpr int TC_THREADS = 192;
+constexpr int GROUP_M = 16;
+constexpr uint32_t TMEM_COLS = 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+// ---- PTX helpers -----------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_64B canonical layout
+// ((8,m),2):((4,SBO),1) in 16-byte units: 64-byte rows, 8-row groups 512 B
+// apart (SBO), LBO unused (1), version 1 (sm_100), layout type 4.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;        // SBO
+  d |= (uint64_t)1 << 46;                 // version
+  d |= (uint64_t)4 << 61;                 // SWIZZLE_64B
+  return d;
+}
+
+// Instruction descriptor: D=f32, A=B=tf32, K-major both, M=128, N=256.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---- the GEMM kernel --------------------------------------------------------
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    sgemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAh,
+                        const __grid_constant__ CUtensorMap mAl,
+                        const __grid_constant__ CUtensorMap mBh,
+                        const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
+                        int M, int N, int K, int ldc) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // grouped raster: GROUP_M consecutive M tiles share each N tile
+  const int tiles_m = M / BM, tiles_n = N / BN;
+  const int per_group = GROUP_M * tiles_n;
+  const int bid = blockIdx.x;
+  const int first_m = (bid / per_group) * GROUP_M;
+  const int gsize = min(GROUP_M, tiles_m - first_m);
+  const int in_group = bid % per_group;
+  const int m0 = (first_m + in_group % gsize) * BM;
+  const int n0 = (in_group / gsize) * BN;
+  const int nk = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (const CUtensorMap* m : {&mAh, &mAl, &mBh, &mBl})
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m))
+                   : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      uint8_t* st = smem + s * STAGE_BYTES;
+      mbar_expect_tx(&full[s], STAGE_BYTES);
+      tma_load_2d(st, &mAh, &full[s], kb * BK, m0);
+      tma_load_2d(st + A_TILE, &mAl, &full[s], kb * BK, m0);
+      tma_load_2d(st + 2 * A_TILE, &mBh, &full[s], kb * BK, n0);
+      tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], kb * BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+      const uint32_t ah = base, al = base + A_TILE;
+      const uint32_t bh = base + 2 * A_TILE, bl = bh + B_TILE;
+#pragma unroll
+      for (int k = 0; k < BK / 8; ++k) {
+        const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K
+        const uint32_t acc0 = (kb | k) != 0;
+        mma_tf32(tmem, umma_desc_sw64(al + off), umma_desc_sw64(bh + off), acc0);
+        mma_tf32(tmem, umma_desc_sw64(ah + off), umma_desc_sw64(bl + off), 1);
+        mma_tf32(tmem, umma_desc_sw64(ah + off), umma_desc_sw64(bh + off), 1);
+      }
+      umma_commit(&empty[s]);  // the stage is free once these MMAs retire
+    }
+    umma_commit(tmem_full);
+  } else if (warp >= 2) {
+    // ---- epilogue: TMEM -> registers -> C ----
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = q * 32 + lane;
+    float* crow = C + (size_t)(m0 + row) * ldc + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(crow + c + j) =
+            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+}
+
+// ---- hi/lo split ----------------------------------------------------------
+
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  uint32_t h, l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  float rest = __fsub_rn(x, hi);  // exact
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(rest));
+  lo = __uint_as_float(l);
+}
+
+// A (M x K, lda) -> Ah, Al (M x K packed)
+__global__ void __launch_bounds__(256) split_rows_kernel(const float* __restrict__ A, int lda,
+                                                         int M, int K, float* __restrict__ Ah,
+                                                         float* __restrict__ Al) {
+  const size_t total = (size_t)M * K;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total / 4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    size_t e = i * 4;
+    size_t r = e / K, c = e % K;
+    float4 v = *reinterpret_cast<const float4*>(A + r * lda + c);
+    float4 h, l;
+    split_tf32(v.x, h.x, l.x);
+    split_tf32(v.y, h.y, l.y);
+    split_tf32(v.z, h.z, l.z);
+    split_tf32(v.w, h.w, l.w);
+    *reinterpret_cast<float4*>(Ah + e) = h;
+    *reinterpret_cast<float4*>(Al + e) = l;
+  }
+}
+
+// B (K x N, ldb) -> Bth, Btl (N x K packed): 32x32 tiles through smem
+__global__ void __launch_bounds__(256) split_transpose_kernel(const float* __restrict__ B,
+                                                              int ldb, int K, int N,
+                                                              float* __restrict__ Bth,
+                                                              float* __restrict__ Btl) {
+  __shared__ float th[32][33], tl[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int j = ty; j < 32; j += 8) {
+    float h, l;
+    split_tf32(B[(size_t)(k0 + j) * ldb + n0 + tx], h, l);
+    th[j][tx] = h;
+    tl[j][tx] = l;
+  }
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    Bth[(size_t)(n0 + j) * K + k0 + tx] = th[tx][j];
+    Btl[(size_t)(n0 + j) * K + k0 + tx] = tl[tx][j];
+  }
+}
+
+// ---- tensor maps (driver entry point fetched through the runtime) ---------
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled get_encoder() {
+  static EncodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  }
+  return fn;
+}
+
+// rows x cols fp32 row-major (cols contiguous); box = box_rows x BK
+bool make_map(CUtensorMap* m, const float* base, int rows, int cols, int box_rows) {
+  EncodeTiled enc = get_encoder();
+  if (!enc)
+    return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool sgemm_tc_supported(int M, int N, int K, int lda, int ldb, int ldc) {
+  (void)ldb;
+  return M >= BM && N >= BN && K >= BK && M % BM == 0 && N % BN == 0 && K % 32 == 0 &&
+         lda % 4 == 0 && ldc % 4 == 0 && get_encoder() != nullptr;
+}
+
+size_t sgemm_tc_scratch_bytes(int M, int N, int K) {
+  return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float);
+}
+
+int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int K, int lda,
+                    int ldb, int ldc, void* scratch, int sm_count, void* stream,
+                    int* launches) {
+  (void)sm_count;
+  cudaStream_t s = (cudaStream_t)stream;
+  float* Ah = static_cast<float*>(scratch);
+  float* Al = Ah + (size_t)M * K;
+  float* Bh = Al + (size_t)M * K;
+  float* Bl = Bh + (size_t)N * K;
+  int grid_split = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 16);
+  split_rows_kernel<<<grid_split, 256, 0, s>>>(A, lda, M, K, Ah, Al);
+  split_transpose_kernel<<<dim3(N / 32, K / 32), 256, 0, s>>>(B, ldb, K, N, Bh, Bl);
+  CUtensorMap mAh, mAl, mBh, mBl;
+  if (!make_map(&mAh, Ah, M, K, BM) || !make_map(&mAl, Al, M, K, BM) ||
+      !make_map(&mBh, Bh, N, K, BN) || !make_map(&mBl, Bl, N, K, BN))
+    return (int)cudaErrorInvalidValue;
+  cudaFuncSetAttribute(sgemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       SMEM_BYTES);
+  int tiles = (M / BM) * (N / BN);
+  sgemm_3xtf32_kernel<<<tiles, TC_THREADS, SMEM_BYTES, s>>>(mAh, mAl, mBh, mBl, C, M, N, K,
+                                                            ldc);
+  if (launches)
+    *launches = 3;
+  return (int)cudaGetLastError();
 }
 
 }  // namespace cafxg

@@ -148,31 +148,34 @@ int main() {
       const int clients = 64, per = 40;
       std::atomic<int> good{0}, bad{0}, finished{0};
       for (int c = 0; c < clients; ++c) {
-        sys.spawn([&, c, mb](cafx::event_based_actor* me) {
+        auto client = sys.spawn([&, c, mb](cafx::event_based_actor* me) {
           auto rng = std::make_shared<std::mt19937_64>(1000 + c);
-          auto left = std::make_shared<int>(per);
-          auto step = std::make_shared<std::function<void()>>();
-          *step = [=, &good, &bad, &finished]() {
-            auto d = storm_tile(*rng);
-            me->sync_send(mb, cafx::make_message(cafxg::mandel_tiles{{d}}))
-                .then(
-                    [=, &good, &bad, &finished](const cafxg::u32vec& counts) {
-                      (counts == expect_tile(d) ? good : bad)++;
-                      if (--*left > 0)
-                        (*step)();
-                      else {
-                        finished++;
-                        me->quit();
-                      }
-                    },
-                    [=, &bad, &finished](const cafx::error&) {
-                      bad++;
-                      finished++;
-                      me->quit();
-                    });
+          // each `go` issues the next sync request; its response handler
+          // re-sends `go` to self until `per` requests are done
+          return cafx::behavior{
+              [=, &good, &bad, &finished](uint32_t k) {
+                auto d = storm_tile(*rng);
+                cafx::actor self_handle{cafx::abstract_actor_ptr{me}};
+                me->sync_send(mb, cafx::make_message(cafxg::mandel_tiles{{d}}))
+                    .then(
+                        [=, &good, &bad, &finished](const cafxg::u32vec& counts) {
+                          (counts == expect_tile(d) ? good : bad)++;
+                          if (k + 1 < (uint32_t)per) {
+                            me->send(self_handle, cafx::make_message(k + 1));
+                          } else {
+                            finished++;
+                            me->quit();
+                          }
+                        },
+                        [=, &bad, &finished](const cafx::error&) {
+                          bad++;
+                          finished++;
+                          me->quit();
+                        });
+              },
           };
-          (*step)();
         });
+        sys.anon_send(client, cafx::make_message(uint32_t{0}));
       }
       auto t0 = std::chrono::steady_clock::now();
       while (finished.load() < clients &&
@@ -205,9 +208,9 @@ int main() {
       try {
         sys.anon_send(typed, cafx::make_message(uint32_t{7}));
       } catch (const cafx::failure& f) {
-        threw = f.code() == cafx::errc::interface_mismatch;
+        threw = f.code() == cafx::errc::type_mismatch;
       }
-      check(threw, "typed gpu actor: mistyped send throws interface_mismatch");
+      check(threw, "typed gpu actor: mistyped send throws type_mismatch (actor_system.cpp:85-91)");
       std::mt19937_64 rng(78);
       auto d = storm_tile(rng);
       auto res = self->request(typed, cafx::make_message(cafxg::mandel_tiles{{d}}), 60s);

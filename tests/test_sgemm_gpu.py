@@ -59,3 +59,21 @@ def test_sgemm_device_api(ctx):
     ctx.sgemm_device(M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream)
     torch.cuda.synchronize()
     assert check(A.cpu().numpy(), B.cpu().numpy(), C.cpu().numpy()) <= TOL
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 256), (1024, 1024, 1024), (384, 512, 2048),
+                                   (2048, 768, 4096)])
+def test_sgemm_3xtf32(ctx, M, N, K):
+    """tcgen05 kind::tf32 hi/lo split: within the fp32 tolerance."""
+    A = oracle.fill_uniform(M * K, 11).reshape(M, K)
+    B = oracle.fill_uniform(K * N, 12).reshape(K, N)
+    C = ctx.sgemm(A, B, mode=pkg.SGEMM_3XTF32)
+    assert check(A, B, C) <= TOL
+
+
+def test_sgemm_3xtf32_rejects_unsupported_shape(ctx):
+    A = np.zeros((100, 64), np.float32)
+    B = np.zeros((64, 256), np.float32)
+    with pytest.raises(pkg.CafxgError) as e:
+        ctx.sgemm(A, B, mode=pkg.SGEMM_3XTF32)
+    assert e.value.code == 8
