@@ -10,11 +10,15 @@
 //   warp 0 lane 0 : TMA producer -- 4-stage ring of {A_hi, A_lo, Bt_hi, Bt_lo}
 //                   16-deep K slices (SWIZZLE_64B, K-major), mbarrier
 //                   complete_tx;
-//   warp 1        : allocates 256 TMEM columns; lane 0 issues
-//                   tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=256, K=8),
-//                   6 per stage, and tcgen05.commit frees the stage;
-//   warps 2..5    : epilogue -- tcgen05.ld 32x32b.x32 TMEM -> registers ->
-//                   global (each thread owns one C row of the tile).
+//   warp 1        : allocates 512 TMEM columns (two 128x256 fp32
+//                   accumulators); lane 0 issues tcgen05.mma.cta_group::1
+//                   .kind::tf32 (M=128, N=256, K=8), 6 per stage, alternating
+//                   accumulators every 128 K; tcgen05.commit frees stages and
+//                   hands finished chunks to the epilogue;
+//   warps 2..9    : epilogue -- tcgen05.ld 32x32b.x32 TMEM -> registers,
+//                   fp32 round-to-nearest sum of the K chunks (the tensor
+//                   core accumulates with truncation), then global stores
+//                   (each thread owns half a C row of the tile).
 // Grid: grouped raster over (M/128) x (N/256) tiles so the CTAs in flight
 // share A row-blocks and B column-blocks in L2.
 #include <cuda.h>
@@ -33,9 +37,16 @@ constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4;
 constexpr int A_TILE = BM * BK * 4;                       // 8 KiB
 constexpr int B_TILE = BN * BK * 4;                       // 16 KiB
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;      // 48 KiB
-constexpr int TC_THREADS = 192;
+constexpr int EPI_WARPS = 8;                              // 2 per TMEM lane quadrant
+constexpr int TC_THREADS = 64 + EPI_WARPS * 32;           // TMA + MMA + epilogue
 constexpr int GROUP_M = 16;
-constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t TMEM_COLS = 512;                       // 2 x 256-column accumulators
+// K chunk per accumulator: the tensor core's fp32 accumulation rounds toward
+// zero, so its error grows linearly with the number of MMAs into one
+// accumulator (measured: 3.9e-5 normwise at K=4096 with a single
+// accumulator). Chunks of 128 K are summed by the epilogue in fp32 with
+// round-to-nearest, which keeps the error at the per-chunk level.
+constexpr int CHUNK_KB = 8;                               // k-blocks per chunk (128 K)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 // ---- PTX helpers -----------------------------------------------------------
@@ -134,8 +145,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + STAGES;    // [2] chunk accumulated (MMA -> epilogue)
+  uint64_t* acc_empty = acc_full + 2;     // [2] chunk consumed (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -158,7 +170,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -190,6 +205,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
+      const int chunk = kb / CHUNK_KB, kin = kb % CHUNK_KB;
+      const uint32_t acc = tmem + (uint32_t)(chunk & 1) * 256;
+      if (kin == 0)  // the epilogue must have drained this accumulator
+        mbar_wait(&acc_empty[chunk & 1], ((chunk >> 1) & 1) ^ 1);
       mbar_wait(&full[s], ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
@@ -198,31 +217,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
       for (int k = 0; k < BK / 8; ++k) {
         const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K
-        const uint32_t acc0 = (kb | k) != 0;
-        mma_tf32(tmem, umma_desc_sw64(al + off), umma_desc_sw64(bh + off), acc0);
-        mma_tf32(tmem, umma_desc_sw64(ah + off), umma_desc_sw64(bl + off), 1);
-        mma_tf32(tmem, umma_desc_sw64(ah + off), umma_desc_sw64(bh + off), 1);
+        const uint32_t acc0 = (kin | k) != 0;
+        mma_tf32(acc, umma_desc_sw64(al + off), umma_desc_sw64(bh + off), acc0);
+        mma_tf32(acc, umma_desc_sw64(ah + off), umma_desc_sw64(bl + off), 1);
+        mma_tf32(acc, umma_desc_sw64(ah + off), umma_desc_sw64(bh + off), 1);
       }
       umma_commit(&empty[s]);  // the stage is free once these MMAs retire
+      if (kin == CHUNK_KB - 1 || kb == nk - 1)
+        umma_commit(&acc_full[chunk & 1]);
     }
-    umma_commit(tmem_full);
   } else if (warp >= 2) {
-    // ---- epilogue: TMEM -> registers -> C ----
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    // ---- epilogue: sum the chunk accumulators in fp32 (RN), then store ----
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;       // which 128 columns of the tile
     const int row = q * 32 + lane;
-    float* crow = C + (size_t)(m0 + row) * ldc + n0;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    float sum[128];
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(crow + c + j) =
-            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+    for (int j = 0; j < 128; ++j)
+      sum[j] = 0.0f;
+    const int nchunks = (nk + CHUNK_KB - 1) / CHUNK_KB;
+    for (int chunk = 0; chunk < nchunks; ++chunk) {
+      const int b = chunk & 1;
+      mbar_wait(&acc_full[b], (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + (uint32_t)(b * 256 + half * 128 + c * 32), r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          sum[c * 32 + j] = __fadd_rn(sum[c * 32 + j], __uint_as_float(r[j]));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&acc_empty[b]))
+                     : "memory");
     }
+    float* crow = C + (size_t)(m0 + row) * ldc + n0 + half * 128;
+#pragma unroll
+    for (int j = 0; j < 128; j += 4)
+      *reinterpret_cast<float4*>(crow + j) =
+          make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
