@@ -478,7 +478,15 @@ def run_secondary(ctx, args):
         e2e = (time.perf_counter() - t0) / e2e_reps * 1e3
         for h in (hA, hB, hC):
             ctx.pinned_free(h)
+        bf16 = float(peaks().get("bf16_tflops") or 1590.0)
+        peak3 = bf16 / 2 / 3   # tf32 runs at half the bf16 rate; 3 MMAs per product
         out[label] = {"kernel_ms": round(ms, 3), "tflops": round(tflops, 2),
+                      "path": "3xTF32 tcgen05 (split + GEMM launches)",
+                      "roofline": {"bound": "tensor", "achieved": round(tflops, 2),
+                                   "peak": round(peak3, 1), "unit": "TFLOP/s",
+                                   "frac": round(tflops / peak3, 4),
+                                   "peak_basis": f"measured bf16 {bf16} TF/s / 2 (tf32) / 3 "
+                                                 "(hi*hi + hi*lo + lo*hi)"},
                       "e2e_ms": round(e2e, 3),
                       "e2e_tflops": round(2.0 * n ** 3 / (e2e / 1e3) / 1e12, 2),
                       "max_rel_err_sampled_rows": err, "tolerance": 1e-5}

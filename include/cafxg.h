@@ -126,6 +126,20 @@ int cafxg_mandelbrot_device(cafxg_ctx* ctx, int device,
                             const cafxg_mandel_desc* tiles, size_t n,
                             uint32_t* dev_out, void* stream);
 
+/* FNV-1a-64 of `n` device-resident u32 cells hashed as big-endian bytes
+ * (cafx::detail::fnv1a_u32, fnv.hpp:23-28) starting from `seed`; blocks until
+ * the hash is in *hash. Parallelised through the low-byte/affine decomposition
+ * of the FNV state; bit-identical to the serial loop. */
+int cafxg_fnv1a_u32_device(cafxg_ctx* ctx, int device, const uint32_t* cells,
+                           uint64_t n, uint64_t seed, uint64_t* hash,
+                           void* stream);
+/* The reference's run_mandelbrot(size, max_iter) (bench.cpp:481-505): the
+ * fp64 reference-mode image over [-1.5,0.5]x[-1,1] computed on the context's
+ * devices and its collector checksum (bench.cpp:329-331) computed on device.
+ * Blocking; *wall_ms (may be NULL) is request-to-checksum wall clock. */
+int cafxg_run_mandelbrot(cafxg_ctx* ctx, uint32_t size, uint32_t max_iter,
+                         uint64_t* checksum, double* wall_ms);
+
 /* ---- fp32 matrix multiply --------------------------------------------------
  * C = A * B, row-major, the OpenCL `matrix_multiply(matrix1, matrix2, output)`
  * contract. */

@@ -37,6 +37,7 @@ EXPORTS = [
     "cafxg_open", "cafxg_close", "cafxg_device_count", "cafxg_sync",
     "cafxg_host_alloc", "cafxg_host_free", "cafxg_host_register", "cafxg_host_unregister",
     "cafxg_mandelbrot_submit", "cafxg_mandelbrot", "cafxg_mandelbrot_device",
+    "cafxg_fnv1a_u32_device", "cafxg_run_mandelbrot",
     "cafxg_sgemm_submit", "cafxg_sgemm", "cafxg_sgemm_device",
     "cafxg_spawn", "cafxg_actor_enqueue", "cafxg_actor_reply_bytes",
     "cafxg_actor_quit", "cafxg_actor_release", "cafxg_get_stats",
@@ -102,6 +103,9 @@ def lib() -> C.CDLL:
         L.cafxg_mandelbrot_submit.argtypes = [vp, C.POINTER(MandelDesc), sz, vp, DONE_FN, vp]
         L.cafxg_mandelbrot.argtypes = [vp, C.POINTER(MandelDesc), sz, vp]
         L.cafxg_mandelbrot_device.argtypes = [vp, i, C.POINTER(MandelDesc), sz, vp, vp]
+        L.cafxg_fnv1a_u32_device.argtypes = [vp, i, vp, u64, u64, C.POINTER(u64), vp]
+        L.cafxg_run_mandelbrot.argtypes = [vp, C.c_uint32, C.c_uint32, C.POINTER(u64),
+                                           C.POINTER(C.c_double)]
         L.cafxg_sgemm_submit.argtypes = [vp, C.POINTER(SgemmDesc), vp, vp, vp, DONE_FN, vp]
         L.cafxg_sgemm.argtypes = [vp, C.POINTER(SgemmDesc), vp, vp, vp]
         L.cafxg_sgemm_device.argtypes = [vp, i, C.POINTER(SgemmDesc), vp, vp, vp, vp]
@@ -297,6 +301,20 @@ class Context:
         arr, n = _desc_array(tiles)
         _check(lib().cafxg_mandelbrot_device(self.handle, device, arr, n, dev_ptr,
                                              stream or None), "mandelbrot_device")
+
+    def fnv1a_u32_device(self, dev_ptr: int, n: int, seed: int = 0xCBF29CE484222325,
+                         stream: int = 0, device: int = 0) -> int:
+        h = C.c_uint64()
+        _check(lib().cafxg_fnv1a_u32_device(self.handle, device, dev_ptr, n, seed, C.byref(h),
+                                            stream or None), "fnv1a_u32_device")
+        return h.value
+
+    def run_mandelbrot(self, size: int, max_iter: int):
+        """(checksum, wall_ms) of the reference's run_mandelbrot(size, max_iter)."""
+        h, ms = C.c_uint64(), C.c_double()
+        _check(lib().cafxg_run_mandelbrot(self.handle, size, max_iter, C.byref(h), C.byref(ms)),
+               "run_mandelbrot")
+        return h.value, ms.value
 
     # -- sgemm
     def sgemm(self, A: np.ndarray, B: np.ndarray, C_: np.ndarray | None = None,

@@ -1506,6 +1506,103 @@ int cafxg_actor_release(cafxg_actor* a) {
   return CAFXG_OK;
 }
 
+int cafxg_fnv1a_u32_device(cafxg_ctx* ctx, int device, const uint32_t* cells, uint64_t n,
+                           uint64_t seed, uint64_t* hash, void* stream) {
+  if (!ctx || !hash || device < 0 || device >= (int)ctx->devs.size() || (n && !cells))
+    return fail(CAFXG_E_CONFIG, "fnv1a_u32_device: bad argument");
+  Device* d = ctx->devs[device].get();
+  cudaSetDevice(d->ordinal);
+  cudaStream_t s = stream ? (cudaStream_t)stream : d->compute;
+  void* scratch = nullptr;
+  uint64_t* dhash = nullptr;
+  CAFXG_CUDA_TRY(cudaMallocAsync(&scratch, fnv_scratch_bytes(n, d->sms), s));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dhash, sizeof(uint64_t), s));
+  int launches = 0;
+  int e = fnv_launch(cells, n, seed, dhash, scratch, d->sms, s, &launches);
+  if (e != 0)
+    return cuda_status((cudaError_t)e, "fnv launch");
+  ctx->st_launches += launches;
+  CAFXG_CUDA_TRY(cudaMemcpyAsync(hash, dhash, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  CAFXG_CUDA_TRY(cudaFreeAsync(scratch, s));
+  CAFXG_CUDA_TRY(cudaFreeAsync(dhash, s));
+  CAFXG_CUDA_TRY(cudaStreamSynchronize(s));
+  return CAFXG_OK;
+}
+
+// run_mandelbrot(size, max_iter) (bench.cpp:481-505) on the context's devices:
+// the reference-mode image (fp64, corner sampling, [-1.5,0.5]x[-1,1]) is
+// computed in HBM in contiguous row blocks per device, each device hashes its
+// block with the segment-table FNV (fnv.cu), and the per-device hashes are
+// chained on the host in row order: the checksum is the reference's
+// collector hash (bench.cpp:329-331) without moving the image off the GPUs.
+int cafxg_run_mandelbrot(cafxg_ctx* ctx, uint32_t size, uint32_t max_iter, uint64_t* checksum,
+                         double* wall_ms) {
+  if (!ctx || !checksum || size == 0)
+    return fail(CAFXG_E_CONFIG, "run_mandelbrot: bad argument");
+  auto t0 = std::chrono::steady_clock::now();
+  const size_t G = std::min<size_t>(ctx->devs.size(), size);
+  std::vector<uint32_t*> img(G, nullptr);
+  std::vector<uint64_t*> dh(G, nullptr);
+  std::vector<uint64_t> hh(G, 0);
+  std::vector<uint32_t> r0(G + 1);
+  for (size_t g = 0; g <= G; ++g)
+    r0[g] = (uint32_t)((uint64_t)size * g / G);
+  // pass 1: image + FNV tables of each block with seed 0 placeholder; the
+  // chaining needs the previous block's hash, so blocks are hashed in order
+  // below (the walk is cheap; the tables are the work).
+  std::vector<void*> scratch(G, nullptr);
+  for (size_t g = 0; g < G; ++g) {
+    Device* d = ctx->devs[g].get();
+    cudaSetDevice(d->ordinal);
+    uint64_t rows = r0[g + 1] - r0[g];
+    uint64_t n = rows * size;
+    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&img[g], n * 4 + 16, d->compute));
+    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dh[g], 8, d->compute));
+    CAFXG_CUDA_TRY(cudaMallocAsync(&scratch[g], fnv_scratch_bytes(n, d->sms), d->compute));
+    cafxg_mandel_desc t{};
+    t.x0 = -1.5; t.x1 = 0.5; t.y0 = -1.0; t.y1 = 1.0;
+    t.width = t.height = size;
+    t.row0 = r0[g];
+    t.nrows = (uint32_t)rows;
+    t.ncols = size;
+    t.max_iter = max_iter;
+    t.precision = CAFXG_FP64;
+    t.sampling = CAFXG_CORNER;
+    CAFXG_TRY(validate_mandel(t));
+    MTile m;
+    fill_mtile(m, t, 0, 0);
+    CAFXG_TRY(launch_mandel(ctx, d, img[g], {m}, tile_chunks(t.nrows, t.ncols), CAFXG_FP64,
+                            max_iter, use_exact(ctx, t), n, d->compute));
+  }
+  // pass 2: hash the blocks in row order, each seeded with the previous hash
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (size_t g = 0; g < G; ++g) {
+    Device* d = ctx->devs[g].get();
+    cudaSetDevice(d->ordinal);
+    uint64_t n = (uint64_t)(r0[g + 1] - r0[g]) * size;
+    int launches = 0;
+    int e = fnv_launch(img[g], n, h, dh[g], scratch[g], d->sms, d->compute, &launches);
+    if (e != 0)
+      return cuda_status((cudaError_t)e, "fnv launch");
+    ctx->st_launches += launches;
+    CAFXG_CUDA_TRY(cudaMemcpyAsync(&hh[g], dh[g], 8, cudaMemcpyDeviceToHost, d->compute));
+    CAFXG_CUDA_TRY(cudaStreamSynchronize(d->compute));
+    h = hh[g];
+  }
+  for (size_t g = 0; g < G; ++g) {
+    Device* d = ctx->devs[g].get();
+    cudaSetDevice(d->ordinal);
+    cudaFreeAsync(img[g], d->compute);
+    cudaFreeAsync(dh[g], d->compute);
+    cudaFreeAsync(scratch[g], d->compute);
+  }
+  *checksum = h;
+  if (wall_ms)
+    *wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                   .count();
+  return CAFXG_OK;
+}
+
 int cafxg_get_stats(cafxg_ctx* ctx, cafxg_stats* out) {
   if (!ctx || !out)
     return fail(CAFXG_E_CONFIG, "get_stats: null argument");

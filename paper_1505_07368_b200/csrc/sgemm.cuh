@@ -18,4 +18,10 @@ int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N,
                     int K, int lda, int ldb, int ldc, void* scratch,
                     int sm_count, void* stream, int* launches);
 
+// Device FNV-1a-64 over u32 cells hashed big-endian (fnv.cu).
+uint64_t fnv_segment_cells(uint64_t n, int sms);
+size_t fnv_scratch_bytes(uint64_t n, int sms);
+int fnv_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out,
+               void* scratch, int sms, void* stream, int* launches);
+
 }  // namespace cafxg

@@ -211,3 +211,26 @@ def test_bad_requests_fail_synchronously(ctx):
     with pytest.raises(pkg.CafxgError) as e:
         ctx.mandelbrot(nan)
     assert e.value.code == 8
+
+
+@pytest.mark.parametrize("n", [0, 1, 255, 256, 257, 4099, 1 << 20, 3_000_001])
+def test_device_fnv_matches_serial(ctx, n):
+    """Segment-table FNV-1a (fnv.cu) == the serial fnv1a_u32 loop."""
+    import torch
+    rng = np.random.default_rng(n)
+    cells = rng.integers(0, 2 ** 32, size=n, dtype=np.uint64).astype(np.uint32)
+    dev = torch.from_numpy(cells.view(np.int32)).cuda() if n else torch.zeros(1, device="cuda")
+    torch.cuda.synchronize()
+    for seed in (0xCBF29CE484222325, 0, 12345):
+        assert ctx.fnv1a_u32_device(dev.data_ptr(), n, seed) == oracle.fnv1a_u32(cells, seed)
+
+
+@pytest.mark.parametrize("size,it", [(64, 50), (96, 60), (256, 100), (1024, 500), (2048, 500),
+                                     (4096, 500)])
+def test_run_mandelbrot_on_device(ctx, golden, size, it):
+    """cafxg_run_mandelbrot == the reference's run_mandelbrot checksum."""
+    want = int([g for g in golden["run_mandelbrot"]
+                if g["size"] == size and g["max_iter"] == it][0]["checksum"])
+    chk, ms = ctx.run_mandelbrot(size, it)
+    assert chk == want
+    assert ms > 0
