@@ -492,6 +492,19 @@ def run_secondary(ctx, args):
                       "max_rel_err_sampled_rows": err, "tolerance": 1e-5}
         del A, B, C
 
+    # the reference's own benchmark at paper scale, on GPU
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_mandelbrot.json")))
+    want = [g for g in golden["run_mandelbrot"] if g["size"] == 16000][0]
+    ctx.run_mandelbrot(16000, 500)
+    runs = [ctx.run_mandelbrot(16000, 500) for _ in range(3)]
+    out["paper_scale_run_mandelbrot_16000_500"] = {
+        "wall_clock_ms": round(min(r[1] for r in runs), 3),
+        "checksum": str(runs[0][0]), "checksum_matches_reference": runs[0][0] == int(want["checksum"]),
+        "path": "cafxg_run_mandelbrot: fp64 reference-mode image in HBM + device FNV-1a",
+        "reference": "3.2 s on 64 Opteron cores (PAPER.md:897); "
+                     f"{want['wall_clock_ms_8_workers_here'] / 1e3:.1f} s for the unmodified "
+                     "reference on the 8-core build container"}
+
     out["cfg4_request_storm"] = run_storm(ctx)
     out["cfg4_request_storm_closed_loop"] = run_storm(ctx, closed_loop=True)
     return out

@@ -21,7 +21,9 @@ assert R is not None, "build the reference first: make -C oracle ref"
 out = {"source": "oracle/_ref/libcafx_ref.so (reference proj/src compiled -O3 -DNDEBUG)",
        "run_mandelbrot": [], "cells": [], "rows": []}
 
-for size, it in [(64, 50), (96, 60), (256, 100), (1024, 500), (2048, 500), (4096, 500)]:
+# (16000, 500) is the paper's scale; ~30 s on 8 cores
+for size, it in [(64, 50), (96, 60), (256, 100), (1024, 500), (2048, 500), (4096, 500),
+                 (16000, 500)]:
     sums = set()
     for w in ([1, 2, 4, 8] if size <= 256 else [8]):
         sums.add(R.ref_run_mandelbrot(size, it, w, None))
