@@ -114,7 +114,11 @@ class ClockSampler:
 # ---- distributed helpers -------------------------------------------------------------
 
 class Dist:
-    def __init__(self, backend):
+    """Control plane only (barriers, max/sum of scalars): the Mandelbrot path
+    shards without any data-path collective, so a CPU (gloo) group suffices
+    and ranks may even share a GPU when testing the N>1 path on one device."""
+
+    def __init__(self, backend="gloo"):
         self.rank, self.world, self.local = env_rank()
         self.on = self.world > 1
         if self.on:
@@ -268,19 +272,20 @@ def run_ours(args):
     import paper_1505_07368_b200 as pkg
     from paper_1505_07368_b200.shard import band_tiles
 
-    D = Dist("nccl")
+    D = Dist()
     rank, world, local = D.rank, D.world, D.local
-    torch.cuda.set_device(local)
-    ctx = pkg.Context(device_mask=1 << local)
+    gpu = local % torch.cuda.device_count()   # ranks share a GPU only in tests
+    torch.cuda.set_device(gpu)
+    ctx = pkg.Context(device_mask=1 << gpu)
     full = pkg.mandel_desc(*REGION, W_IMG, H_IMG, MAX_ITER)
     tiles_local = band_tiles(full, world, rank, BAND_ROWS, global_offsets=False)
     tiles_global = band_tiles(full, world, rank, BAND_ROWS, global_offsets=True)
     npx = sum(t.nrows * t.ncols for t in tiles_local)
-    dev_out = torch.empty(npx, dtype=torch.int32, device=f"cuda:{local}")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    dev_out = torch.empty(npx, dtype=torch.int32, device=f"cuda:{gpu}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{gpu}")
     # a real stream: torch's default stream is the legacy NULL stream (handle
     # 0), which the C ABI would read as "use the context's own stream"
-    stream = torch.cuda.Stream(device=local)
+    stream = torch.cuda.Stream(device=gpu)
     torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
 
@@ -296,7 +301,7 @@ def run_ours(args):
     # ---- timed: device-resident ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     D.barrier()
     torch.cuda.synchronize()
     st0 = ctx.stats()
@@ -351,7 +356,7 @@ def run_ours(args):
     # ---- roofline of the escape kernel (per GPU) ----
     pk = peaks()
     sm_max = float(pk.get("sm_max_mhz") or 1965.0)
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    sms = torch.cuda.get_device_properties(gpu).multi_processor_count
     peak_tops = sms * 128 * sm_max * 1e6 / 1e12
     achieved = 8.0 * iters_local / (kernel_ms / 1e3) / 1e12
     roof = {"bound": "fp32_pipe", "achieved": round(achieved, 3), "peak": round(peak_tops, 3),
