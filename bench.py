@@ -406,9 +406,8 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if shm:
         ctx.host_unregister(host)
-        del host
-        shm[1].close()
-        shm[0].close()
+        D.barrier()
+        # the mapping stays until exit (numpy views of it may still be alive)
         if rank == 0:
             try:
                 os.unlink(shm[2])
