@@ -139,10 +139,8 @@ struct F32Slots {
       asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP_EXACT)
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
   }
-  __device__ __forceinline__ void start(int slot, const void* cx, const void* cy,
-                                        uint32_t col, uint32_t row) {
-    float fr = __ldg(static_cast<const float*>(cx) + col);
-    float fi = __ldg(static_cast<const float*>(cy) + row);
+  using C = float;  // coordinate table element
+  __device__ __forceinline__ void start(int slot, float fr, float fi) {
     if (slot == 0) {
       cr.x = fr; ci.x = fi; zr.x = zi.x = zr2.x = zi2.x = 0.0f;
     } else {
@@ -218,10 +216,8 @@ struct F64Slots {
       asm volatile(CAFXG_F64_PROLOGUE CAFXG_X4(CAFXG_F64_PAIR(
           CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
   }
-  __device__ __forceinline__ void start(int slot, const void* cx, const void* cy,
-                                        uint32_t col, uint32_t row) {
-    double xr = __ldg(static_cast<const double*>(cx) + col);
-    double xi = __ldg(static_cast<const double*>(cy) + row);
+  using C = double;
+  __device__ __forceinline__ void start(int slot, double xr, double xi) {
     if (slot == 0) {
       cr.x = xr; ci.x = xi; zr.x = zi.x = zr2.x = zi2.x = 0.0;
     } else {
@@ -282,18 +278,21 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
 
-  // warp-uniform cursor: columns [cur, cend) of row `crow` of tile T. Chunks
-  // never straddle rows, so a lane's pixel is (crow, cur + rank): no division
-  // and one shared row coordinate per chunk.
-  uint32_t cur = 0, cend = 0, crow = 0;
-  const MTile* T = nullptr;
+  // warp-uniform cursor: columns [cur, cend) of one row of one tile. Chunks
+  // never straddle rows, so everything a new pixel needs besides its column
+  // coordinate is chunk state held in registers: the row's imaginary part,
+  // the column table and the output row base.
+  using Cd = typename Slots::C;
+  uint32_t cur = 0, cend = 0, orow = 0;
+  const Cd* cxp = nullptr;
+  Cd ci_row = Cd(0);
   bool exhausted = false;
+  const uint32_t maxit = L.max_iter;  // uniform per launch
 
   Slots sl;
   sl.zero = L.zero;
   // iterations completed without escape; bit 31 = sticky escape flag
   uint32_t n0 = 0, n1 = 0;
-  uint32_t m0 = 0, m1 = 0;  // max_iter of the slot's pixel
   bool live0 = false, live1 = false;
   uint32_t o0 = 0, o1 = 0;  // output element offsets from L.out
 
@@ -313,28 +312,30 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
           exhausted = true;
           return;
         }
-        T = tile_ptr(L, find_tile(L, c));
+        const MTile* T = tile_ptr(L, find_tile(L, c));
         uint32_t local = c - T->chunk_begin;
-        crow = local / T->chunks_per_row;
-        cur = (local - crow * T->chunks_per_row) * kChunk;
-        cend = min(cur + kChunk, T->ncols);
+        uint32_t cpr = T->chunks_per_row;
+        uint32_t crow = local / cpr;
+        uint32_t ncols = T->ncols;
+        cur = (local - crow * cpr) * kChunk;
+        cend = min(cur + kChunk, ncols);
+        cxp = static_cast<const Cd*>(T->cx);
+        ci_row = __ldg(static_cast<const Cd*>(T->cy) + crow);
+        orow = T->out_off + crow * ncols;
         continue;
       }
       uint32_t avail = cend - cur;
       uint32_t r0 = __popc(b0 & lt_mask);
       uint32_t r1 = __popc(b0) + __popc(b1 & lt_mask);
-      uint32_t orow = T->out_off + crow * T->ncols;
       if (!live0 && r0 < avail) {
-        sl.start(0, T->cx, T->cy, cur + r0, crow);
+        sl.start(0, __ldg(cxp + cur + r0), ci_row);
         n0 = 0;
-        m0 = T->max_iter;
         o0 = orow + cur + r0;
         live0 = true;
       }
       if (!live1 && r1 < avail) {
-        sl.start(1, T->cx, T->cy, cur + r1, crow);
+        sl.start(1, __ldg(cxp + cur + r1), ci_row);
         n1 = 0;
-        m1 = T->max_iter;
         o1 = orow + cur + r1;
         live1 = true;
       }
@@ -347,17 +348,17 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
     sl.template run<kSteps, kExact>(n0, n1);
     // escaped (bit 31) or reached max_iter; an escape at step i leaves i-1
     // non-escaped steps counted, so the reference's return value is n+1
-    bool d0 = live0 && (n0 >= m0);
-    bool d1 = live1 && (n1 >= m1);
+    bool d0 = live0 && (n0 >= maxit);
+    bool d1 = live1 && (n1 >= maxit);
     if (__any_sync(kFull, d0 || d1)) {
       if (d0) {
         uint32_t c = (int32_t)n0 < 0 ? (n0 & 0x7fffffffu) + 1u : n0;
-        L.out[o0] = min(c, m0);
+        L.out[o0] = min(c, maxit);
         live0 = false;
       }
       if (d1) {
         uint32_t c = (int32_t)n1 < 0 ? (n1 & 0x7fffffffu) + 1u : n1;
-        L.out[o1] = min(c, m1);
+        L.out[o1] = min(c, maxit);
         live1 = false;
       }
       refill();

@@ -37,6 +37,7 @@ struct MLaunch {
   uint32_t* out;        // counts of every tile (MTile::out_off)
   uint32_t n;
   uint32_t total_chunks;
+  uint32_t max_iter;    // one max_iter per launch (the host splits batches)
   uint32_t* sched;      // [0] chunk cursor, [1] finished blocks (self-reset)
   float zero;           // always 0.0f; opaque to ptxas (see F32x2::mulz)
 };

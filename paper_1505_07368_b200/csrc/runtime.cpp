@@ -446,23 +446,28 @@ static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
   return c;
 }
 
-// Enqueues one Mandelbrot launch over `tiles` (all the same precision) on
-// `stream`; descriptors beyond the inline capacity are uploaded first.
+// Enqueues the Mandelbrot launches for `tiles` (all the same precision) on
+// `stream`: one coordinate-table launch, then one escape launch per distinct
+// max_iter (the kernel keeps max_iter launch-uniform). Descriptors beyond the
+// inline capacity are uploaded first.
+static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
+                               std::vector<MTile>& tiles, int precision, bool exact,
+                               cudaStream_t stream, bool coords_only, bool skip_coords);
+
 static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                          const std::vector<MTile>& tiles_in, uint32_t total_chunks,
                          int precision, uint32_t max_iter, bool exact,
                          uint64_t pixels, cudaStream_t stream) {
+  (void)max_iter;
+  (void)pixels;
   if (total_chunks == 0)
     return CAFXG_OK;
   // coordinate tables: one column table and one row table per tile
   std::vector<MTile> tiles = tiles_in;
   const size_t esz = precision ? sizeof(double) : sizeof(float);
   uint64_t ncoord = 0;
-  uint32_t max_extent = 0;
-  for (auto& t : tiles) {
+  for (auto& t : tiles)
     ncoord += (uint64_t)t.ncols + t.nrows;
-    max_extent = std::max(max_extent, t.ncols + t.nrows);
-  }
   uint8_t* coords = nullptr;
   CAFXG_CUDA_TRY(cudaMallocAsync((void**)&coords, ncoord * esz + 16, stream));
   uint64_t off = 0;
@@ -471,9 +476,40 @@ static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
     t.cy = coords + (off + t.ncols) * esz;
     off += (uint64_t)t.ncols + t.nrows;
   }
+  CAFXG_TRY(launch_mandel_group(ctx, d, out_base, tiles, precision, exact, stream, true, false));
+  // group by max_iter (stable), re-basing the chunk numbering per group
+  std::vector<uint32_t> its;
+  for (auto& t : tiles)
+    if (std::find(its.begin(), its.end(), t.max_iter) == its.end())
+      its.push_back(t.max_iter);
+  for (uint32_t it : its) {
+    std::vector<MTile> grp;
+    for (auto& t : tiles)
+      if (t.max_iter == it)
+        grp.push_back(t);
+    CAFXG_TRY(launch_mandel_group(ctx, d, out_base, grp, precision, exact, stream, false, true));
+  }
+  CAFXG_CUDA_TRY(cudaFreeAsync(coords, stream));
+  return CAFXG_OK;
+}
+
+static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
+                               std::vector<MTile>& tiles, int precision, bool exact,
+                               cudaStream_t stream, bool coords_only, bool skip_coords) {
+  uint32_t chunks = 0, max_extent = 0;
+  uint64_t pixels = 0;
+  for (auto& t : tiles) {
+    t.chunk_begin = chunks;
+    chunks += tile_chunks(t.nrows, t.ncols);
+    pixels += (uint64_t)t.nrows * t.ncols;
+    max_extent = std::max(max_extent, t.ncols + t.nrows);
+  }
+  if (chunks == 0)
+    return CAFXG_OK;
   MLaunch L{};
   L.n = (uint32_t)tiles.size();
-  L.total_chunks = total_chunks;
+  L.total_chunks = chunks;
+  L.max_iter = tiles[0].max_iter;
   L.out = out_base;
   L.sched = d->next_sched();
   L.zero = 0.0f;
@@ -490,15 +526,19 @@ static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
     ctx->st_h2d += bytes;
     L.tiles = dev_tiles;
   }
-  int e = mandel_coords_launch(L, precision, max_extent, stream);
-  if (e != 0)
-    return cuda_status((cudaError_t)e, "mandelbrot coordinate launch");
-  MandelLaunchCfg cfg = mandel_cfg(d, precision, max_iter, exact, pixels);
-  e = mandel_launch(L, precision, cfg, stream);
-  if (e != 0)
-    return cuda_status((cudaError_t)e, "mandelbrot launch");
-  ctx->st_launches += 2;
-  CAFXG_CUDA_TRY(cudaFreeAsync(coords, stream));
+  if (!skip_coords) {
+    int e = mandel_coords_launch(L, precision, max_extent, stream);
+    if (e != 0)
+      return cuda_status((cudaError_t)e, "mandelbrot coordinate launch");
+    ctx->st_launches++;
+  }
+  if (!coords_only) {
+    MandelLaunchCfg cfg = mandel_cfg(d, precision, L.max_iter, exact, pixels);
+    int e = mandel_launch(L, precision, cfg, stream);
+    if (e != 0)
+      return cuda_status((cudaError_t)e, "mandelbrot launch");
+    ctx->st_launches++;
+  }
   if (dev_tiles)
     CAFXG_CUDA_TRY(cudaFreeAsync(dev_tiles, stream));
   return CAFXG_OK;
