@@ -5,11 +5,13 @@
 // SURVEY.md §8a row a2 (include/cafxg.h documents the coordinate contract).
 //
 // Design:
-//  * persistent grid; each warp pulls 512-pixel chunks from a global cursor
-//    and every lane carries TWO independent pixels ("slots"). In fp32 the two
-//    slots live in the halves of 64-bit registers and each escape step is
-//    issued as packed FADD2/FMUL2/FFMA2 instructions (f32x2, new in sm_100):
-//    7 packed FP instructions advance 2 pixels by one iteration;
+//  * persistent grid; each warp pulls 512-pixel chunks (never straddling a
+//    row) from a global cursor and every lane carries several independent
+//    pixels ("slots"). In fp32 two slots share the halves of 64-bit registers
+//    and each escape step is issued as packed FADD2/FMUL2/FFMA2 instructions
+//    (f32x2, new in sm_100): 7 packed FP instructions advance 2 pixels by one
+//    iteration; a lane runs two such pairs (4 pixels) so each warp has two
+//    independent dependency chains in flight;
 //  * bit-exact counting without per-step branches: a sticky escape predicate
 //    (FSETP.OR) and a counter that stops at the first escape. After the first
 //    escape z keeps iterating (to inf/NaN) but the predicate never clears, so
@@ -19,8 +21,8 @@
 //  * refill: every `ksteps` iterations the warp votes; lanes whose pixel is
 //    finished store the count and take the next pixel from the warp's chunk,
 //    so no lane idles behind a slow neighbour (divergence-free main loop);
-//  * every FP op is an explicit round-to-nearest intrinsic / `.rn` PTX op, so
-//    nvcc can never contract the reference's separate mul and add into FMA.
+//  * every FP op is an explicit round-to-nearest `.rn` PTX op, so nothing can
+//    contract the reference's separate mul and add into one FMA.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -33,7 +35,7 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 
 // ---- the escape-iteration block ----------------------------------------------
-// kSteps iterations of the reference loop (bench.cpp:370-377) for a lane's two
+// kSteps iterations of the reference loop (bench.cpp:370-377) for a lane's
 // slots, written as one PTX block so the escape bookkeeping stays in
 // predicates: per slot and step one `setp.gt.or` (sticky escape flag) and one
 // predicated add (the count stops at the first escape). Reference order, with
@@ -41,111 +43,125 @@ constexpr unsigned kFull = 0xffffffffu;
 // compiled reference does:
 //   nr = (zr*zr - zi*zi) + re ; ni = (2*zr)*zi + im ; escape if nr^2+ni^2 > 4
 //
-// fp32 packs the two slots into the halves of 64-bit registers (f32x2, new in
-// sm_100): 7 packed FP instructions advance both pixels by one iteration.
 // Two ptxas facts shape the text:
 //  * ptxas 12.9 contracts `mul.rn.f32x2` + `add.rn.f32x2` into FFMA2 in spite
-//    of the explicit rounding (checked in SASS). Squares are therefore formed
-//    as fma(a, a, z) with z a RUNTIME +0.0 (MLaunch::zero): fl(a*a + 0) ==
-//    fl(a*a) and an FFMA2 result is never fused further;
+//    of the explicit rounding (checked in SASS; scalar .rn is respected).
+//    Squares are therefore formed as fma(a, a, z) with z a RUNTIME +0.0
+//    (MLaunch::zero): fl(a*a + 0) == fl(a*a) and an FFMA2 result is never
+//    fused further;
 //  * the fast step folds `(2*zr)*zi + im` into fma(zr*zi, 2, im): fl(2zr)*zi
 //    rounds to 2*fl(zr*zi) (power-of-two scaling commutes with rounding) and
 //    fl(2v + im) with 2v exact is one fma. Bit-identical unless fl(zr*zi) is
 //    subnormal, which the host rules out per request; the
 //    `exact` step keeps the reference's 8 separate operations.
 
-#define CAFXG_F32_STEP_FAST                                 \
-  "sub.rn.f32x2 t, q, w;\n\t"                               \
-  "add.rn.f32x2 t, t, c;\n\t"                               \
-  "mul.rn.f32x2 v, x, y;\n\t"                               \
-  "fma.rn.f32x2 y, v, two, d;\n\t"                          \
-  "mov.b64 x, t;\n\t"                                       \
-  "fma.rn.f32x2 q, x, x, zz;\n\t"                           \
-  "fma.rn.f32x2 w, y, y, zz;\n\t"                           \
-  "add.rn.f32x2 s, q, w;\n\t"                               \
-  "mov.b64 {s0, s1}, s;\n\t"                                \
-  "setp.gt.or.f32 p0, s0, 0f40800000, p0;\n\t"              \
-  "setp.gt.or.f32 p1, s1, 0f40800000, p1;\n\t"              \
-  "@!p0 add.u32 %4, %4, 1;\n\t"                             \
-  "@!p1 add.u32 %5, %5, 1;\n\t"
+// One fp32 pair step. Register names: X zr, Y zi, Q zr^2, W zi^2 (packed
+// state), C cr, D ci (packed inputs), T/V/S temporaries, A0/A1 unpacked sums,
+// P0/P1 sticky predicates, N0/N1 counts.
+#define CAFXG_F32_FAST(X, Y, Q, W, C, D, T, V, S, A0, A1, P0, P1, N0, N1) \
+  "sub.rn.f32x2 " T ", " Q ", " W ";\n\t"                                 \
+  "add.rn.f32x2 " T ", " T ", " C ";\n\t"                                 \
+  "mul.rn.f32x2 " V ", " X ", " Y ";\n\t"                                 \
+  "fma.rn.f32x2 " Y ", " V ", two, " D ";\n\t"                            \
+  "mov.b64 " X ", " T ";\n\t"                                             \
+  "fma.rn.f32x2 " Q ", " X ", " X ", zz;\n\t"                             \
+  "fma.rn.f32x2 " W ", " Y ", " Y ", zz;\n\t"                             \
+  "add.rn.f32x2 " S ", " Q ", " W ";\n\t"                                 \
+  "mov.b64 {" A0 ", " A1 "}, " S ";\n\t"                                  \
+  "setp.gt.or.f32 " P0 ", " A0 ", 0f40800000, " P0 ";\n\t"                \
+  "setp.gt.or.f32 " P1 ", " A1 ", 0f40800000, " P1 ";\n\t"                \
+  "@!" P0 " add.u32 " N0 ", " N0 ", 1;\n\t"                               \
+  "@!" P1 " add.u32 " N1 ", " N1 ", 1;\n\t"
 
-#define CAFXG_F32_STEP_EXACT                                \
-  "sub.rn.f32x2 t, q, w;\n\t"                               \
-  "add.rn.f32x2 t, t, c;\n\t"                               \
-  "add.rn.f32x2 v, x, x;\n\t"                               \
-  "fma.rn.f32x2 v, v, y, zz;\n\t"                           \
-  "add.rn.f32x2 y, v, d;\n\t"                               \
-  "mov.b64 x, t;\n\t"                                       \
-  "fma.rn.f32x2 q, x, x, zz;\n\t"                           \
-  "fma.rn.f32x2 w, y, y, zz;\n\t"                           \
-  "add.rn.f32x2 s, q, w;\n\t"                               \
-  "mov.b64 {s0, s1}, s;\n\t"                                \
-  "setp.gt.or.f32 p0, s0, 0f40800000, p0;\n\t"              \
-  "setp.gt.or.f32 p1, s1, 0f40800000, p1;\n\t"              \
-  "@!p0 add.u32 %4, %4, 1;\n\t"                             \
-  "@!p1 add.u32 %5, %5, 1;\n\t"
+#define CAFXG_F32_EXACT(X, Y, Q, W, C, D, T, V, S, A0, A1, P0, P1, N0, N1) \
+  "sub.rn.f32x2 " T ", " Q ", " W ";\n\t"                                  \
+  "add.rn.f32x2 " T ", " T ", " C ";\n\t"                                  \
+  "add.rn.f32x2 " V ", " X ", " X ";\n\t"                                  \
+  "fma.rn.f32x2 " V ", " V ", " Y ", zz;\n\t"                              \
+  "add.rn.f32x2 " Y ", " V ", " D ";\n\t"                                  \
+  "mov.b64 " X ", " T ";\n\t"                                              \
+  "fma.rn.f32x2 " Q ", " X ", " X ", zz;\n\t"                              \
+  "fma.rn.f32x2 " W ", " Y ", " Y ", zz;\n\t"                              \
+  "add.rn.f32x2 " S ", " Q ", " W ";\n\t"                                  \
+  "mov.b64 {" A0 ", " A1 "}, " S ";\n\t"                                   \
+  "setp.gt.or.f32 " P0 ", " A0 ", 0f40800000, " P0 ";\n\t"                 \
+  "setp.gt.or.f32 " P1 ", " A1 ", 0f40800000, " P1 ";\n\t"                 \
+  "@!" P0 " add.u32 " N0 ", " N0 ", 1;\n\t"                                \
+  "@!" P1 " add.u32 " N1 ", " N1 ", 1;\n\t"
 
-// operands: %0,%1 zr; %2,%3 zi; %4 n0; %5 n1; %6,%7 zr^2; %8,%9 zi^2;
-// %10,%11 cr; %12,%13 ci; %14 runtime zero; %15 2.0f. Bit 31 of a count is
-// the slot's sticky escape flag (max_iter <= 2^30 keeps it free).
-#define CAFXG_F32_PROLOGUE                                  \
-  "{\n\t.reg .b64 x, y, q, w, c, d, t, v, s, two, zz;\n\t"  \
-  ".reg .f32 s0, s1;\n\t.reg .pred p0, p1;\n\t"             \
-  "mov.b64 x, {%0, %1};\n\tmov.b64 y, {%2, %3};\n\t"        \
-  "mov.b64 q, {%6, %7};\n\tmov.b64 w, {%8, %9};\n\t"        \
-  "mov.b64 c, {%10, %11};\n\tmov.b64 d, {%12, %13};\n\t"    \
-  "mov.b64 zz, {%14, %14};\n\t"                             \
-  "mov.b64 two, {%15, %15};\n\t"                            \
-  "setp.lt.s32 p0, %4, 0;\n\tsetp.lt.s32 p1, %5, 0;\n\t"
+// Both pairs of a lane, interleaved (two independent chains).
+// operands: %0..%3 pair A {zr, zi, zr^2, zi^2}; %4..%7 pair B; %8..%11
+// counts (A0, A1, B0, B1; bit 31 = sticky escape flag, max_iter <= 2^30
+// keeps it free); %12 crA, %13 ciA, %14 crB, %15 ciB; %16 runtime zero;
+// %17 2.0f.
+#define CAFXG_F32_STEP2(STEP)                                                  \
+  STEP("%0", "%1", "%2", "%3", "%12", "%13", "tA", "vA", "sA", "a0", "a1", "pA0", \
+       "pA1", "%8", "%9")                                                       \
+  STEP("%4", "%5", "%6", "%7", "%14", "%15", "tB", "vB", "sB", "b0", "b1", "pB0", \
+       "pB1", "%10", "%11")
 
-#define CAFXG_F32_EPILOGUE                                  \
-  "mov.b64 {%0, %1}, x;\n\tmov.b64 {%2, %3}, y;\n\t"        \
-  "mov.b64 {%6, %7}, q;\n\tmov.b64 {%8, %9}, w;\n\t"        \
-  "@p0 or.b32 %4, %4, 0x80000000;\n\t"                      \
-  "@p1 or.b32 %5, %5, 0x80000000;\n\t}"
+#define CAFXG_F32_PROLOGUE                                                 \
+  "{\n\t.reg .b64 tA, vA, sA, tB, vB, sB, two, zz;\n\t"                    \
+  ".reg .f32 a0, a1, b0, b1;\n\t.reg .pred pA0, pA1, pB0, pB1;\n\t"        \
+  "mov.b64 zz, {%16, %16};\n\tmov.b64 two, {%17, %17};\n\t"                \
+  "setp.lt.s32 pA0, %8, 0;\n\tsetp.lt.s32 pA1, %9, 0;\n\t"                 \
+  "setp.lt.s32 pB0, %10, 0;\n\tsetp.lt.s32 pB1, %11, 0;\n\t"
+
+#define CAFXG_F32_EPILOGUE                                                 \
+  "@pA0 or.b32 %8, %8, 0x80000000;\n\t@pA1 or.b32 %9, %9, 0x80000000;\n\t" \
+  "@pB0 or.b32 %10, %10, 0x80000000;\n\t@pB1 or.b32 %11, %11, 0x80000000;\n\t}"
 
 #define CAFXG_X4(S) S S S S
 #define CAFXG_X16(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S)
 #define CAFXG_X32(S) CAFXG_X16(S) CAFXG_X16(S)
 
-#define CAFXG_F32_OPERANDS                                                   \
-  : "+f"(zr.x), "+f"(zr.y), "+f"(zi.x), "+f"(zi.y), "+r"(n0), "+r"(n1),       \
-    "+f"(zr2.x), "+f"(zr2.y), "+f"(zi2.x), "+f"(zi2.y)                        \
-  : "f"(cr.x), "f"(cr.y), "f"(ci.x), "f"(ci.y), "f"(zero), "f"(2.0f)
+#define CAFXG_F32_OPERANDS                                                     \
+  : "+l"(zr[0]), "+l"(zi[0]), "+l"(zr2[0]), "+l"(zi2[0]), "+l"(zr[1]),         \
+    "+l"(zi[1]), "+l"(zr2[1]), "+l"(zi2[1]), "+r"(n[0]), "+r"(n[1]),           \
+    "+r"(n[2]), "+r"(n[3])                                                     \
+  : "l"(cr[0]), "l"(ci[0]), "l"(cr[1]), "l"(ci[1]), "f"(zero), "f"(2.0f)
+
+__device__ __forceinline__ uint64_t set_half(uint64_t v, int hi, float f) {
+  uint64_t b = __float_as_uint(f);
+  return hi ? ((v & 0xffffffffull) | (b << 32)) : ((v & 0xffffffff00000000ull) | b);
+}
 
 struct F32Slots {
-  using S = float;
-  float2 zr{}, zi{}, zr2{}, zi2{}, cr{}, ci{};
+  static constexpr int kSlots = 4;  // two packed pairs per lane
+  using C = float;                  // coordinate table element
+  uint64_t zr[2] = {}, zi[2] = {}, zr2[2] = {}, zi2[2] = {}, cr[2] = {}, ci[2] = {};
   float zero;
 
   template <int kSteps, bool kExact>
-  __device__ __forceinline__ void run(uint32_t& n0, uint32_t& n1) {
+  __device__ __forceinline__ void run(uint32_t (&n)[kSlots]) {
     if constexpr (kSteps == 32 && !kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X32(CAFXG_F32_STEP_FAST)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X32(CAFXG_F32_STEP2(CAFXG_F32_FAST))
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
     else if constexpr (kSteps == 32 && kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X32(CAFXG_F32_STEP_EXACT)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X32(CAFXG_F32_STEP2(CAFXG_F32_EXACT))
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
     else if constexpr (kSteps == 16 && !kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X16(CAFXG_F32_STEP_FAST)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X16(CAFXG_F32_STEP2(CAFXG_F32_FAST))
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
     else if constexpr (kSteps == 16 && kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X16(CAFXG_F32_STEP_EXACT)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X16(CAFXG_F32_STEP2(CAFXG_F32_EXACT))
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
     else if constexpr (kSteps == 4 && !kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP_FAST)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP2(CAFXG_F32_FAST))
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
     else
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP_EXACT)
+      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP2(CAFXG_F32_EXACT))
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
   }
-  using C = float;  // coordinate table element
-  __device__ __forceinline__ void start(int slot, float fr, float fi) {
-    if (slot == 0) {
-      cr.x = fr; ci.x = fi; zr.x = zi.x = zr2.x = zi2.x = 0.0f;
-    } else {
-      cr.y = fr; ci.y = fi; zr.y = zi.y = zr2.y = zi2.y = 0.0f;
-    }
+  // slot s lives in half (s & 1) of pair (s >> 1)
+  __device__ __forceinline__ void start(int s, float fr, float fi) {
+    const int p = s >> 1, h = s & 1;
+    cr[p] = set_half(cr[p], h, fr);
+    ci[p] = set_half(ci[p], h, fi);
+    zr[p] = set_half(zr[p], h, 0.0f);
+    zi[p] = set_half(zi[p], h, 0.0f);
+    zr2[p] = set_half(zr2[p], h, 0.0f);
+    zi2[p] = set_half(zi2[p], h, 0.0f);
   }
 };
 
@@ -187,16 +203,17 @@ struct F32Slots {
   "@p1 or.b32 %9, %9, 0x80000000;\n\t}"
 #define CAFXG_F64_OPERANDS                                               \
   : "+d"(zr.x), "+d"(zi.x), "+d"(zr2.x), "+d"(zi2.x), "+d"(zr.y),         \
-    "+d"(zi.y), "+d"(zr2.y), "+d"(zi2.y), "+r"(n0), "+r"(n1)              \
+    "+d"(zi.y), "+d"(zr2.y), "+d"(zi2.y), "+r"(n[0]), "+r"(n[1])          \
   : "d"(cr.x), "d"(ci.x), "d"(cr.y), "d"(ci.y)
 
 struct F64Slots {
-  using S = double;
+  static constexpr int kSlots = 2;
+  using C = double;
   double2 zr{}, zi{}, zr2{}, zi2{}, cr{}, ci{};
   float zero;
 
   template <int kSteps, bool kExact>
-  __device__ __forceinline__ void run(uint32_t& n0, uint32_t& n1) {
+  __device__ __forceinline__ void run(uint32_t (&n)[kSlots]) {
     if constexpr (kSteps == 32 && !kExact)
       asm volatile(CAFXG_F64_PROLOGUE CAFXG_X32(CAFXG_F64_PAIR(
           CAFXG_F64_STEP_FAST)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
@@ -216,9 +233,8 @@ struct F64Slots {
       asm volatile(CAFXG_F64_PROLOGUE CAFXG_X4(CAFXG_F64_PAIR(
           CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
   }
-  using C = double;
-  __device__ __forceinline__ void start(int slot, double xr, double xi) {
-    if (slot == 0) {
+  __device__ __forceinline__ void start(int s, double xr, double xi) {
+    if (s == 0) {
       cr.x = xr; ci.x = xi; zr.x = zi.x = zr2.x = zi2.x = 0.0;
     } else {
       cr.y = xr; ci.y = xi; zr.y = zi.y = zr2.y = zi2.y = 0.0;
@@ -267,14 +283,16 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// fp32: 6 CTAs x 256 threads per SM (40 registers) so each scheduler holds
-// 12 warps to cover the FP2 dependency chains; fp64 is bound by the FP64 pipe.
+// 4 CTAs x 256 threads per SM (<= 64 registers): 8 warps per scheduler, each
+// with two independent FP2 chains in fp32; fp64 is bound by the FP64 pipe.
 template <class Slots>
-constexpr int kMinBlocks = sizeof(typename Slots::S) == 4 ? 6 : 4;
+constexpr int kMinBlocks = 4;
 
 template <class Slots, int kSteps, bool kExact>
 __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
     mandel_kernel(const __grid_constant__ MLaunch L) {
+  constexpr int NS = Slots::kSlots;
+  using Cd = typename Slots::C;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
 
@@ -282,7 +300,6 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
   // never straddle rows, so everything a new pixel needs besides its column
   // coordinate is chunk state held in registers: the row's imaginary part,
   // the column table and the output row base.
-  using Cd = typename Slots::C;
   uint32_t cur = 0, cend = 0, orow = 0;
   const Cd* cxp = nullptr;
   Cd ci_row = Cd(0);
@@ -291,16 +308,24 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
 
   Slots sl;
   sl.zero = L.zero;
-  // iterations completed without escape; bit 31 = sticky escape flag
-  uint32_t n0 = 0, n1 = 0;
-  bool live0 = false, live1 = false;
-  uint32_t o0 = 0, o1 = 0;  // output element offsets from L.out
+  uint32_t n[NS];   // iterations completed without escape; bit 31 = escaped
+  uint32_t o[NS];   // output element offsets from L.out
+  uint32_t live = 0;  // bit s: slot s holds a pixel
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    n[s] = 0;
+    o[s] = 0;
+  }
 
   auto refill = [&]() {
     while (true) {
-      uint32_t b0 = __ballot_sync(kFull, !live0);
-      uint32_t b1 = __ballot_sync(kFull, !live1);
-      uint32_t want = __popc(b0) + __popc(b1);
+      uint32_t b[NS];
+      uint32_t want = 0;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        b[s] = __ballot_sync(kFull, !(live >> s & 1u));
+        want += __popc(b[s]);
+      }
       if (want == 0 || exhausted)
         return;
       if (cur == cend) {
@@ -324,43 +349,41 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
         orow = T->out_off + crow * ncols;
         continue;
       }
-      uint32_t avail = cend - cur;
-      uint32_t r0 = __popc(b0 & lt_mask);
-      uint32_t r1 = __popc(b0) + __popc(b1 & lt_mask);
-      if (!live0 && r0 < avail) {
-        sl.start(0, __ldg(cxp + cur + r0), ci_row);
-        n0 = 0;
-        o0 = orow + cur + r0;
-        live0 = true;
-      }
-      if (!live1 && r1 < avail) {
-        sl.start(1, __ldg(cxp + cur + r1), ci_row);
-        n1 = 0;
-        o1 = orow + cur + r1;
-        live1 = true;
+      const uint32_t avail = cend - cur;
+      uint32_t base = 0;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const uint32_t r = base + __popc(b[s] & lt_mask);
+        if (!(live >> s & 1u) && r < avail) {
+          sl.start(s, __ldg(cxp + cur + r), ci_row);
+          n[s] = 0;
+          o[s] = orow + cur + r;
+          live |= 1u << s;
+        }
+        base += __popc(b[s]);
       }
       cur += min(want, avail);
     }
   };
 
   refill();
-  while (__any_sync(kFull, live0 || live1)) {
-    sl.template run<kSteps, kExact>(n0, n1);
+  while (__any_sync(kFull, live != 0)) {
+    sl.template run<kSteps, kExact>(n);
     // escaped (bit 31) or reached max_iter; an escape at step i leaves i-1
     // non-escaped steps counted, so the reference's return value is n+1
-    bool d0 = live0 && (n0 >= maxit);
-    bool d1 = live1 && (n1 >= maxit);
-    if (__any_sync(kFull, d0 || d1)) {
-      if (d0) {
-        uint32_t c = (int32_t)n0 < 0 ? (n0 & 0x7fffffffu) + 1u : n0;
-        L.out[o0] = min(c, maxit);
-        live0 = false;
+    uint32_t done = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      done |= ((live >> s & 1u) && n[s] >= maxit) ? (1u << s) : 0u;
+    if (__any_sync(kFull, done != 0)) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (done >> s & 1u) {
+          uint32_t c = (int32_t)n[s] < 0 ? (n[s] & 0x7fffffffu) + 1u : n[s];
+          L.out[o[s]] = min(c, maxit);
+        }
       }
-      if (d1) {
-        uint32_t c = (int32_t)n1 < 0 ? (n1 & 0x7fffffffu) + 1u : n1;
-        L.out[o1] = min(c, maxit);
-        live1 = false;
-      }
+      live &= ~done;
       refill();
     }
   }
@@ -433,6 +456,10 @@ int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
 
 int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact) {
   CAFXG_MANDEL_DISPATCH(occ_t);
+}
+
+int mandel_slots_per_thread(int precision) {
+  return precision == 0 ? F32Slots::kSlots : F64Slots::kSlots;
 }
 
 }  // namespace cafxg

@@ -57,5 +57,6 @@ int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,
 int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
                          void* stream);
 int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact);
+int mandel_slots_per_thread(int precision);
 
 }  // namespace cafxg

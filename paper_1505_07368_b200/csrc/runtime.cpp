@@ -440,7 +440,8 @@ static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
   int& occ = d->mandel_occ[precision][c.ksteps == 16][exact];
   if (occ == 0)
     occ = std::max(1, mandel_max_blocks_per_sm(precision, c.ksteps, exact));
-  uint64_t want = (pixels + 2 * kMandelThreads - 1) / (2 * kMandelThreads);
+  const uint64_t per_block = (uint64_t)kMandelThreads * mandel_slots_per_thread(precision);
+  uint64_t want = (pixels + per_block - 1) / per_block;
   uint64_t full = (uint64_t)d->sms * occ;
   c.grid = (int)std::max<uint64_t>(1, std::min(want, full));
   return c;

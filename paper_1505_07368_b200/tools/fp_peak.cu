@@ -42,11 +42,11 @@ __global__ void __launch_bounds__(256) probe(float* out, int iters, float a, flo
         asm volatile("add.rn.f64 %0, %0, %1;" : "+d"(dx[c]) : "d"((double)a));
       } else if constexpr (KIND == 5) {  // scalar DMUL
         asm volatile("mul.rn.f64 %0, %0, %1;" : "+d"(dx[c]) : "d"((double)a));
-      } else if constexpr (KIND == 6 || KIND == 7) {
+      } else if constexpr (KIND >= 6) {
         // the Mandelbrot escape step's FP2 mix (7 packed ops, 2 pixels) on 4
         // independent pixel pairs per thread; KIND 7 adds the per-step
         // escape bookkeeping (2 x FSETP.OR + 2 x predicated IADD)
-        if (c < CHAINS / 2) {
+        if (c < (KIND == 8 ? 1 : KIND == 9 ? 2 : CHAINS / 2)) {
           float* z = &x[4 * c];
           if constexpr (KIND == 6)
             asm volatile(
@@ -130,5 +130,7 @@ int main() {
   // 4 chains x 7 FP2 x 2 lanes per iteration
   run<6>("escape-step FP2 mix (lane-ops of 7 FP2)", 4.0 * 7 * 2, sms);
   run<7>("escape-step FP2 mix + FSETP/IADD bookkeeping", 4.0 * 7 * 2, sms);
+  run<8>("escape-step + bookkeeping, 1 chain per thread", 1.0 * 7 * 2, sms);
+  run<9>("escape-step + bookkeeping, 2 chains per thread", 2.0 * 7 * 2, sms);
   return 0;
 }
