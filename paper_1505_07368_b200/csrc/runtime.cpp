@@ -600,13 +600,17 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
   uint64_t staged = 0;
   std::vector<std::array<uint64_t, 3>> scat;  // (staging off, host off, px)
   size_t i = 0;
+  // pixels still to schedule: waves shrink geometrically towards the end so
+  // the copy-out left exposed after the last kernel is small
+  uint64_t left = dev_px_total;
   while (i < subs.size()) {
     // group a wave (same precision)
     size_t j = i;
     uint64_t px = 0;
     int prec = subs[i].d.precision;
+    const uint64_t cap = std::max<uint64_t>(std::min<uint64_t>(wave_px, left / 4), 1);
     while (j < subs.size() && subs[j].d.precision == prec &&
-           (px == 0 || px + subs[j].pixels <= wave_px)) {
+           (px == 0 || px + subs[j].pixels <= cap)) {
       px += subs[j].pixels;
       ++j;
     }
@@ -644,6 +648,7 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
       off += subs[k].pixels;
     }
     CAFXG_CUDA_TRY(cudaFreeAsync(dout, d->d2h));
+    left -= px;
     i = j;
   }
   return push_completion(ctx, d, d->d2h,
