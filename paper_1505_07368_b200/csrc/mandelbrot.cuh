@@ -27,7 +27,7 @@ struct MTile {
   void* cy;
 };
 
-constexpr int kInlineTiles = 8;    // tiles passed by value in the params
+constexpr int kInlineTiles = 32;   // tiles passed by value in the params (< 4 KB)
 constexpr uint32_t kChunk = 512;   // pixels per work chunk
 constexpr int kMandelThreads = 256;
 

@@ -192,6 +192,8 @@ struct Completion {
 };
 
 constexpr uint32_t kSchedSlots = 1024;
+constexpr int kUpSlots = 16;
+constexpr size_t kUpSlotBytes = 2u << 20;
 
 struct Device {
   int ordinal = 0;
@@ -208,7 +210,14 @@ struct Device {
   bool stop = false;
   std::thread completer;
   std::atomic<int> inflight{0};
-  int mandel_occ[2][2][2] = {};  // [precision][ksteps16][exact]
+  int mandel_occ[2][3][2] = {};  // [precision][ksteps 4/16/32][exact]
+  // pinned staging ring for descriptor uploads (a pageable cudaMemcpyAsync
+  // may wait for earlier work on the stream, serialising host and device)
+  std::mutex up_mu;
+  uint8_t* up_base = nullptr;
+  cudaEvent_t up_ev[16] = {};
+  bool up_armed[16] = {};
+  uint32_t up_next = 0;
 
   uint32_t* next_sched() {
     uint32_t i = sched_next.fetch_add(1, std::memory_order_relaxed) % kSchedSlots;
@@ -312,6 +321,24 @@ static int push_completion(cafxg_ctx* ctx, Device* d, cudaStream_t stream,
     d->cq.push_back(Completion{ev, std::move(fn)});
   }
   d->cq_cv.notify_one();
+  return CAFXG_OK;
+}
+
+// Host -> device copy of small descriptor arrays through the device's pinned
+// staging ring, so the call never waits for earlier work on `stream`.
+static int upload(Device* d, void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+  if (bytes > kUpSlotBytes)
+    return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream),
+                       "descriptor upload");
+  std::lock_guard<std::mutex> g(d->up_mu);
+  uint32_t i = d->up_next++ % kUpSlots;
+  if (d->up_armed[i])
+    CAFXG_CUDA_TRY(cudaEventSynchronize(d->up_ev[i]));
+  uint8_t* p = d->up_base + (size_t)i * kUpSlotBytes;
+  std::memcpy(p, src, bytes);
+  CAFXG_CUDA_TRY(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, stream));
+  CAFXG_CUDA_TRY(cudaEventRecord(d->up_ev[i], stream));
+  d->up_armed[i] = true;
   return CAFXG_OK;
 }
 
@@ -437,7 +464,7 @@ static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
   MandelLaunchCfg c;
   c.ksteps = max_iter >= 512 ? 32 : max_iter >= 128 ? 16 : 4;
   c.exact = exact;
-  int& occ = d->mandel_occ[precision][c.ksteps == 16][exact];
+  int& occ = d->mandel_occ[precision][c.ksteps == 4 ? 0 : c.ksteps == 16 ? 1 : 2][exact];
   if (occ == 0)
     occ = std::max(1, mandel_max_blocks_per_sm(precision, c.ksteps, exact));
   const uint64_t per_block = (uint64_t)kMandelThreads * mandel_slots_per_thread(precision);
@@ -521,9 +548,7 @@ static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
   } else {
     size_t bytes = tiles.size() * sizeof(MTile);
     CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dev_tiles, bytes, stream));
-    // pageable source: cudaMemcpyAsync stages it before returning
-    CAFXG_CUDA_TRY(cudaMemcpyAsync(dev_tiles, tiles.data(), bytes,
-                                   cudaMemcpyHostToDevice, stream));
+    CAFXG_TRY(upload(d, dev_tiles, tiles.data(), bytes, stream));
     ctx->st_h2d += bytes;
     L.tiles = dev_tiles;
   }
@@ -1004,8 +1029,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
       size_t sb = segs.size() * sizeof(CopySeg);
       status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, d->compute), "segs alloc");
       if (status == CAFXG_OK)
-        status = cuda_status(cudaMemcpyAsync(dsegs, segs.data(), sb,
-                                             cudaMemcpyHostToDevice, d->compute), "segs upload");
+        status = upload(d, dsegs, segs.data(), sb, d->compute);
       if (status == CAFXG_OK) {
         int e = copy_segments_launch(dsegs, (uint32_t)segs.size(), d->compute);
         status = cuda_status((cudaError_t)e, "reply scatter launch");
@@ -1197,6 +1221,10 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
       CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking));
       CAFXG_CUDA_TRY(cudaMalloc(&d->sched, kSchedSlots * 2 * sizeof(uint32_t)));
       CAFXG_CUDA_TRY(cudaMemset(d->sched, 0, kSchedSlots * 2 * sizeof(uint32_t)));
+      CAFXG_CUDA_TRY(cudaHostAlloc((void**)&d->up_base, kUpSlots * kUpSlotBytes,
+                                   cudaHostAllocPortable));
+      for (auto& ev : d->up_ev)
+        CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       cudaMemPool_t pool;
       CAFXG_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, i));
       uint64_t thr = UINT64_MAX;
@@ -1252,6 +1280,9 @@ int cafxg_close(cafxg_ctx* ctx) {
     cudaStreamSynchronize(d->d2h);
     for (auto ev : d->ev_free)
       cudaEventDestroy(ev);
+    for (auto ev : d->up_ev)
+      cudaEventDestroy(ev);
+    cudaFreeHost(d->up_base);
     cudaFree(d->sched);
     cudaStreamDestroy(d->compute);
     cudaStreamDestroy(d->d2h);
