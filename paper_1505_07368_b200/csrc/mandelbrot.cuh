@@ -28,7 +28,10 @@ struct MTile {
 };
 
 constexpr int kInlineTiles = 32;   // tiles passed by value in the params (< 4 KB)
-constexpr uint32_t kChunk = 512;   // pixels per work chunk
+// Pixels per work chunk: one refill generation of a warp (32 lanes x 4
+// slots), so when the cursor runs dry no warp still holds unstarted pixels
+// (512-pixel chunks left ~0.2 ms tails per launch).
+constexpr uint32_t kChunk = 128;
 constexpr int kMandelThreads = 256;
 
 struct MLaunch {

@@ -628,12 +628,18 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
   // pixels still to schedule: waves shrink geometrically towards the end so
   // the copy-out left exposed after the last kernel is small
   uint64_t left = dev_px_total;
+  // CAFXG_TRACE=1: per-wave device timeline on stderr (debug aid)
+  static const bool trace = [] {
+    const char* e = getenv("CAFXG_TRACE");
+    return e && e[0] == '1';
+  }();
+  std::vector<std::array<cudaEvent_t, 3>> tev;
   while (i < subs.size()) {
     // group a wave (same precision)
     size_t j = i;
     uint64_t px = 0;
     int prec = subs[i].d.precision;
-    const uint64_t cap = std::max<uint64_t>(std::min<uint64_t>(wave_px, left / 4), 1);
+    const uint64_t cap = std::max<uint64_t>(std::min<uint64_t>(wave_px, left / 4), 4ull << 20);
     while (j < subs.size() && subs[j].d.precision == prec &&
            (px == 0 || px + subs[j].pixels <= cap)) {
       px += subs[j].pixels;
@@ -650,7 +656,15 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
       maxit = std::max(maxit, subs[k].d.max_iter);
       off += subs[k].pixels;
     }
+    if (trace) {
+      tev.push_back({});
+      for (auto& e : tev.back())
+        cudaEventCreate(&e);
+      cudaEventRecord(tev.back()[0], d->compute);
+    }
     CAFXG_TRY(launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, d->compute));
+    if (trace)
+      cudaEventRecord(tev.back()[1], d->compute);
     cudaEvent_t ev;
     CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     CAFXG_CUDA_TRY(cudaEventRecord(ev, d->compute));
@@ -673,8 +687,27 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
       off += subs[k].pixels;
     }
     CAFXG_CUDA_TRY(cudaFreeAsync(dout, d->d2h));
+    if (trace)
+      cudaEventRecord(tev.back()[2], d->d2h);
     left -= px;
     i = j;
+  }
+  if (trace && !tev.empty()) {
+    cudaError_t se = cudaEventSynchronize(tev.back()[2]);
+    for (size_t w = 0; w < tev.size(); ++w) {
+      float a = -1, b = -1, c = -1;
+      cudaError_t e1 = cudaEventElapsedTime(&a, tev[0][0], tev[w][0]);
+      cudaError_t e2 = cudaEventElapsedTime(&b, tev[0][0], tev[w][1]);
+      cudaError_t e3 = cudaEventElapsedTime(&c, tev[0][0], tev[w][2]);
+      if (se || e1 || e2 || e3)
+        fprintf(stderr, "cafxg trace errors %d %d %d %d\n", (int)se, (int)e1, (int)e2, (int)e3);
+      fprintf(stderr, "cafxg trace wave %zu: kernel %.3f..%.3f ms, copy done %.3f ms\n", w, a, b,
+              c);
+    }
+    for (auto& w : tev)
+      for (auto& e : w)
+        cudaEventDestroy(e);
+    cudaGetLastError();
   }
   return push_completion(ctx, d, d->d2h,
                          [ctx, staging, scat = std::move(scat), host_out, join](int st) {
