@@ -250,6 +250,12 @@ struct cafxg_ctx {
   std::thread dispatcher;
   std::atomic<uint32_t> rr{0};
   std::atomic<uint64_t> actor_open{0};  // enqueued, not yet completed
+  // reply-callback threads (finish_batch)
+  std::mutex cb_mu;
+  std::condition_variable cb_cv;
+  std::deque<std::function<void()>> cb_q;
+  bool cb_stop = false;
+  std::vector<std::thread> cb_threads;
   bool force_exact = false;  // CAFXG_EXACT_STEP=1: always the 8-op step
   // NCCL communicators for multi-device sgemm (one per device)
   std::mutex nccl_mu;
@@ -993,23 +999,110 @@ static void actor_unref(cafxg_actor* a) {
     delete a;
 }
 
-static void finish_request(Request* r, int status) {
+// Completes one actor request: the caller's callback, then the bookkeeping.
+// `account` = false when the caller settles the context counters for a whole
+// batch at once (st_requests / actor_open / the sync notification).
+static void finish_request(Request* r, int status, bool account = true) {
   cafxg_actor* a = r->actor;
+  cafxg_ctx* ctx = a->ctx;
   if (r->done)
     r->done(r->user, status);
   a->pending.fetch_sub(1);
-  a->ctx->st_requests++;
-  a->ctx->actor_open.fetch_sub(1);
-  a->ctx->sync_cv.notify_all();
   actor_unref(a);
   delete r;
+  if (account) {
+    ctx->st_requests++;
+    ctx->actor_open.fetch_sub(1);
+    ctx->sync_cv.notify_all();
+  }
 }
+
+// Runs a finished batch's reply callbacks. Large batches are split across the
+// context's callback threads (the per-request callback -- a cafx `deliver`
+// in the adapter -- would otherwise serialise on one completion thread).
+static void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* bounce,
+                         int status);
 
 // One batch of Mandelbrot requests (same precision) on one device: one launch
 // over every tile of every request into a device staging buffer, then one
 // scatter launch straight into the pinned reply buffers (or one D2H into a
 // pinned bounce buffer + host memcpy for pageable replies).
+static double trace_now_ms() {
+  static const auto t0 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+static bool trace_on() {
+  static const bool on = [] {
+    const char* e = getenv("CAFXG_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+static void callback_loop(cafxg_ctx* ctx) {
+  while (true) {
+    std::function<void()> job;
+    {
+      std::unique_lock<std::mutex> lk(ctx->cb_mu);
+      ctx->cb_cv.wait(lk, [&] { return ctx->cb_stop || !ctx->cb_q.empty(); });
+      if (ctx->cb_q.empty())
+        return;
+      job = std::move(ctx->cb_q.front());
+      ctx->cb_q.pop_front();
+    }
+    job();
+  }
+}
+
+static void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* bounce,
+                         int status) {
+  constexpr size_t kSlice = 1024;
+  const size_t n = batch.size();
+  auto run_slice = [ctx, status, bounce](Request* const* rs, size_t cnt, uint64_t pix_off) {
+    uint64_t o = pix_off;
+    for (size_t i = 0; i < cnt; ++i) {
+      Request* r = rs[i];
+      if (bounce && status == CAFXG_OK)
+        std::memcpy(r->out, bounce + o, r->pixels * 4);
+      o += r->pixels;
+      finish_request(r, status, false);
+    }
+    ctx->st_requests += cnt;
+    ctx->actor_open.fetch_sub(cnt);
+    ctx->sync_cv.notify_all();
+  };
+  if (n <= kSlice || ctx->cb_threads.empty()) {
+    run_slice(batch.data(), n, 0);
+    if (bounce)
+      ctx->pinned.free(bounce);
+    return;
+  }
+  // slices run on the callback threads; the last one frees the bounce buffer
+  auto shared = std::make_shared<std::vector<Request*>>(std::move(batch));
+  auto left = std::make_shared<std::atomic<size_t>>((n + kSlice - 1) / kSlice);
+  uint64_t pix = 0;
+  std::vector<std::function<void()>> jobs;
+  for (size_t b = 0; b < n; b += kSlice) {
+    size_t cnt = std::min(kSlice, n - b);
+    jobs.push_back([ctx, shared, left, b, cnt, pix, bounce, run_slice] {
+      run_slice(shared->data() + b, cnt, pix);
+      if (left->fetch_sub(1) == 1 && bounce)
+        ctx->pinned.free(bounce);
+    });
+    for (size_t i = b; i < b + cnt; ++i)
+      pix += (*shared)[i]->pixels;
+  }
+  {
+    std::lock_guard<std::mutex> g(ctx->cb_mu);
+    for (auto& j : jobs)
+      ctx->cb_q.push_back(std::move(j));
+  }
+  ctx->cb_cv.notify_all();
+}
+
 static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> batch) {
+  const double t_begin = trace_now_ms();
   cudaSetDevice(d->ordinal);
   std::lock_guard<std::mutex> g(d->submit_mu);
   uint64_t px = 0;
@@ -1090,16 +1183,16 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     return;
   }
   push_completion(ctx, d, d->compute,
-                  [ctx, batch = std::move(batch), bounce](int st) {
-                    uint64_t o = 0;
-                    for (Request* r : batch) {
-                      if (bounce && st == CAFXG_OK)
-                        std::memcpy(r->out, bounce + o, r->pixels * 4);
-                      o += r->pixels;
-                      finish_request(r, st);
-                    }
-                    if (bounce)
-                      ctx->pinned.free(bounce);
+                  [ctx, batch = std::move(batch), bounce, t_begin,
+                   t_sub = trace_now_ms()](int st) mutable {
+                    const double t_done = trace_now_ms();
+                    size_t n = batch.size();
+                    finish_batch(ctx, std::move(batch), bounce, st);
+                    if (trace_on())
+                      fprintf(stderr,
+                              "cafxg batch of %zu: build %.3f submit %.3f device-done %.3f "
+                              "callbacks-handed-off %.3f ms\n",
+                              n, t_begin, t_sub, t_done, trace_now_ms());
                   });
 }
 
@@ -1272,6 +1365,10 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
     for (auto& d : c->devs)
       d->completer = std::thread(completion_loop, c, d.get());
     c->dispatcher = std::thread(dispatcher_loop, c);
+    unsigned hw = std::thread::hardware_concurrency();
+    unsigned ncb = std::max(1u, std::min(8u, hw / 4));
+    for (unsigned i = 0; i < ncb; ++i)
+      c->cb_threads.emplace_back(callback_loop, c);
     *out = c;
     return CAFXG_OK;
   } catch (const std::exception& ex) {
@@ -1298,6 +1395,8 @@ int cafxg_close(cafxg_ctx* ctx) {
   ctx->disp_cv.notify_all();
   if (ctx->dispatcher.joinable())
     ctx->dispatcher.join();
+  // completion threads may still hand slices to the callback threads, so
+  // those stop last (after the completion threads below)
   for (auto& d : ctx->devs) {
     {
       std::lock_guard<std::mutex> lk(d->cq_mu);
@@ -1307,6 +1406,14 @@ int cafxg_close(cafxg_ctx* ctx) {
     if (d->completer.joinable())
       d->completer.join();
   }
+  {
+    std::lock_guard<std::mutex> lk(ctx->cb_mu);
+    ctx->cb_stop = true;
+  }
+  ctx->cb_cv.notify_all();
+  for (auto& t : ctx->cb_threads)
+    if (t.joinable())
+      t.join();
   for (auto& d : ctx->devs) {
     cudaSetDevice(d->ordinal);
     cudaStreamSynchronize(d->compute);

@@ -20,23 +20,26 @@
 namespace {
 
 struct Client {
-  std::mutex mu;
-  std::condition_variable cv;
-  uint32_t done = 0;
-  std::atomic<uint32_t>* global_done;
+  std::atomic<uint32_t> done{0};  // replies received (C++20 atomic wait)
   std::atomic<uint32_t>* errors;
 };
 
+// Runs on a libcafxg completion/callback thread: one atomic increment and a
+// futex wake only when the client is actually waiting.
 void on_done(void* user, int status) {
   auto* c = static_cast<Client*>(user);
   if (status != CAFXG_OK)
     c->errors->fetch_add(1);
-  {
-    std::lock_guard<std::mutex> g(c->mu);
-    ++c->done;
+  c->done.fetch_add(1, std::memory_order_release);
+  c->done.notify_one();
+}
+
+void wait_for(Client& c, uint32_t n) {
+  uint32_t v = c.done.load(std::memory_order_acquire);
+  while (v < n) {
+    c.done.wait(v, std::memory_order_acquire);
+    v = c.done.load(std::memory_order_acquire);
   }
-  c->cv.notify_one();
-  c->global_done->fetch_add(1, std::memory_order_release);
 }
 
 }  // namespace
@@ -50,13 +53,11 @@ int cafxg_storm_run(cafxg_actor* actor, const cafxg_mandel_desc* descs,
                     uint8_t* replies, size_t reply_bytes, uint32_t clients,
                     uint32_t per, int closed_loop, double* wall_ms,
                     uint32_t* errors_out) {
-  std::atomic<uint32_t> global_done{0}, errors{0};
+  std::atomic<uint32_t> errors{0};
   std::atomic<int> enqueue_status{CAFXG_OK};
   std::vector<Client> cs(clients);
-  for (auto& c : cs) {
-    c.global_done = &global_done;
+  for (auto& c : cs)
     c.errors = &errors;
-  }
   const uint64_t total = (uint64_t)clients * per;
   auto t0 = std::chrono::steady_clock::now();
   std::vector<std::thread> th;
@@ -74,13 +75,10 @@ int cafxg_storm_run(cafxg_actor* actor, const cafxg_mandel_desc* descs,
           enqueue_status.store(s);
           return;
         }
-        if (closed_loop) {
-          std::unique_lock<std::mutex> lk(me.mu);
-          me.cv.wait(lk, [&] { return me.done == i + 1; });
-        }
+        if (closed_loop)
+          wait_for(me, i + 1);
       }
-      std::unique_lock<std::mutex> lk(me.mu);
-      me.cv.wait(lk, [&] { return me.done == per; });
+      wait_for(me, per);
     });
   }
   for (auto& t : th)
