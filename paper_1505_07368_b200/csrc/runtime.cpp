@@ -1150,30 +1150,41 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     segs.push_back(CopySeg{dout + roff, r->out, (off - roff) * 4});
   }
   status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, d->compute);
+  // the reply copy-out runs on the copy stream so it overlaps the next
+  // batch's compute (a storm moves 16 KiB per request over PCIe)
+  if (status == CAFXG_OK && px) {
+    cudaEvent_t ev;
+    status = cuda_status(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    if (status == CAFXG_OK) {
+      cudaEventRecord(ev, d->compute);
+      cudaStreamWaitEvent(d->d2h, ev, 0);
+      cudaEventDestroy(ev);
+    }
+  }
   if (status == CAFXG_OK && px) {
     if (all_pinned) {
       size_t sb = segs.size() * sizeof(CopySeg);
-      status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, d->compute), "segs alloc");
+      status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, d->d2h), "segs alloc");
       if (status == CAFXG_OK)
-        status = upload(d, dsegs, segs.data(), sb, d->compute);
+        status = upload(d, dsegs, segs.data(), sb, d->d2h);
       if (status == CAFXG_OK) {
-        int e = copy_segments_launch(dsegs, (uint32_t)segs.size(), d->compute);
+        int e = copy_segments_launch(dsegs, (uint32_t)segs.size(), d->d2h);
         status = cuda_status((cudaError_t)e, "reply scatter launch");
         ctx->st_launches++;
       }
       if (dsegs)
-        cudaFreeAsync(dsegs, d->compute);
+        cudaFreeAsync(dsegs, d->d2h);
     } else {
       bounce = (uint32_t*)ctx->pinned.alloc(px * 4);
       if (!bounce)
         status = fail(CAFXG_E_CONFIG, "pinned bounce allocation failed");
       else
         status = cuda_status(cudaMemcpyAsync(bounce, dout, px * 4, cudaMemcpyDeviceToHost,
-                                             d->compute), "batch download");
+                                             d->d2h), "batch download");
     }
     ctx->st_d2h += px * 4;
   }
-  cudaFreeAsync(dout, d->compute);
+  cudaFreeAsync(dout, d->d2h);
   ctx->st_batches++;
   note_max_batch(ctx, batch.size());
   if (status != CAFXG_OK) {
@@ -1182,7 +1193,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     fail_all(status);
     return;
   }
-  push_completion(ctx, d, d->compute,
+  push_completion(ctx, d, d->d2h,
                   [ctx, batch = std::move(batch), bounce, t_begin,
                    t_sub = trace_now_ms()](int st) mutable {
                     const double t_done = trace_now_ms();
