@@ -288,7 +288,9 @@ __global__ void __launch_bounds__(256)
 template <class Slots>
 constexpr int kMinBlocks = 4;
 
-template <class Slots, int kSteps, bool kExact>
+// kInlineCoords: coordinates computed at pixel start (batches of small tiles)
+// instead of loaded from the tables of coords_kernel (big tiles).
+template <class Slots, int kSteps, bool kExact, bool kInlineCoords>
 __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
     mandel_kernel(const __grid_constant__ MLaunch L) {
   constexpr int NS = Slots::kSlots;
@@ -301,7 +303,8 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
   // coordinate is chunk state held in registers: the row's imaginary part,
   // the column table and the output row base.
   uint32_t cur = 0, cend = 0, orow = 0;
-  const Cd* cxp = nullptr;
+  const Cd* cxp = nullptr;     // column table, or null: coordinates inline
+  const MTile* Tc = nullptr;   // current tile (inline-coordinate mode)
   Cd ci_row = Cd(0);
   bool exhausted = false;
   const uint32_t maxit = L.max_iter;  // uniform per launch
@@ -344,8 +347,13 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
         uint32_t ncols = T->ncols;
         cur = (local - crow * cpr) * kChunk;
         cend = min(cur + kChunk, ncols);
-        cxp = static_cast<const Cd*>(T->cx);
-        ci_row = __ldg(static_cast<const Cd*>(T->cy) + crow);
+        if constexpr (kInlineCoords) {
+          Tc = T;
+          ci_row = (Cd)grid_coord(T->y0, T->yspan, T->s, T->row0 + crow, T->height);
+        } else {
+          cxp = static_cast<const Cd*>(T->cx);
+          ci_row = __ldg(static_cast<const Cd*>(T->cy) + crow);
+        }
         orow = T->out_off + crow * ncols;
         continue;
       }
@@ -355,7 +363,12 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
       for (int s = 0; s < NS; ++s) {
         const uint32_t r = base + __popc(b[s] & lt_mask);
         if (!(live >> s & 1u) && r < avail) {
-          sl.start(s, __ldg(cxp + cur + r), ci_row);
+          Cd cr;
+          if constexpr (kInlineCoords)
+            cr = (Cd)grid_coord(Tc->x0, Tc->xspan, Tc->s, Tc->col0 + cur + r, Tc->width);
+          else
+            cr = __ldg(cxp + cur + r);
+          sl.start(s, cr, ci_row);
           n[s] = 0;
           o[s] = orow + cur + r;
           live |= 1u << s;
@@ -404,7 +417,10 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
 
 template <class A, int kSteps, bool kExact>
 int launch_t(const MLaunch& L, int grid, cudaStream_t s) {
-  mandel_kernel<A, kSteps, kExact><<<grid, kMandelThreads, 0, s>>>(L);
+  if (L.inline_coords)
+    mandel_kernel<A, kSteps, kExact, true><<<grid, kMandelThreads, 0, s>>>(L);
+  else
+    mandel_kernel<A, kSteps, kExact, false><<<grid, kMandelThreads, 0, s>>>(L);
   return (int)cudaGetLastError();
 }
 
@@ -412,7 +428,7 @@ template <class A, int kSteps, bool kExact>
 int occ_t() {
   int n = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &n, mandel_kernel<A, kSteps, kExact>, kMandelThreads, 0);
+      &n, mandel_kernel<A, kSteps, kExact, false>, kMandelThreads, 0);
   return n;
 }
 

@@ -42,7 +42,8 @@ struct MLaunch {
   uint32_t total_chunks;
   uint32_t max_iter;    // one max_iter per launch (the host splits batches)
   uint32_t* sched;      // [0] chunk cursor, [1] finished blocks (self-reset)
-  float zero;           // always 0.0f; opaque to ptxas (see F32x2::mulz)
+  float zero;           // always 0.0f; opaque to ptxas (see the escape block)
+  uint32_t inline_coords;  // 1: tiles carry no coordinate tables (cx == cy == null)
 };
 
 // Host launchers (mandelbrot.cu). precision: 0 = fp32, 1 = fp64.

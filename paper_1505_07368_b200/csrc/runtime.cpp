@@ -496,21 +496,32 @@ static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
   (void)pixels;
   if (total_chunks == 0)
     return CAFXG_OK;
-  // coordinate tables: one column table and one row table per tile
+  // coordinate tables (one column and one row table per tile) pay off for
+  // big tiles; batches of small tiles (request storms) compute coordinates
+  // inline in the escape kernel and save the table launch
   std::vector<MTile> tiles = tiles_in;
-  const size_t esz = precision ? sizeof(double) : sizeof(float);
-  uint64_t ncoord = 0;
+  bool small = true;
   for (auto& t : tiles)
-    ncoord += (uint64_t)t.ncols + t.nrows;
+    small = small && (uint64_t)t.ncols * t.nrows <= (64u << 10);
   uint8_t* coords = nullptr;
-  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&coords, ncoord * esz + 16, stream));
-  uint64_t off = 0;
-  for (auto& t : tiles) {
-    t.cx = coords + off * esz;
-    t.cy = coords + (off + t.ncols) * esz;
-    off += (uint64_t)t.ncols + t.nrows;
+  if (!small) {
+    const size_t esz = precision ? sizeof(double) : sizeof(float);
+    uint64_t ncoord = 0;
+    for (auto& t : tiles)
+      ncoord += (uint64_t)t.ncols + t.nrows;
+    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&coords, ncoord * esz + 16, stream));
+    uint64_t off = 0;
+    for (auto& t : tiles) {
+      t.cx = coords + off * esz;
+      t.cy = coords + (off + t.ncols) * esz;
+      off += (uint64_t)t.ncols + t.nrows;
+    }
+    CAFXG_TRY(
+        launch_mandel_group(ctx, d, out_base, tiles, precision, exact, stream, true, false));
+  } else {
+    for (auto& t : tiles)
+      t.cx = t.cy = nullptr;
   }
-  CAFXG_TRY(launch_mandel_group(ctx, d, out_base, tiles, precision, exact, stream, true, false));
   // group by max_iter (stable), re-basing the chunk numbering per group
   std::vector<uint32_t> its;
   for (auto& t : tiles)
@@ -523,7 +534,8 @@ static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
         grp.push_back(t);
     CAFXG_TRY(launch_mandel_group(ctx, d, out_base, grp, precision, exact, stream, false, true));
   }
-  CAFXG_CUDA_TRY(cudaFreeAsync(coords, stream));
+  if (coords)
+    CAFXG_CUDA_TRY(cudaFreeAsync(coords, stream));
   return CAFXG_OK;
 }
 
@@ -547,6 +559,7 @@ static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
   L.out = out_base;
   L.sched = d->next_sched();
   L.zero = 0.0f;
+  L.inline_coords = tiles[0].cx == nullptr;
   MTile* dev_tiles = nullptr;
   if (tiles.size() <= (size_t)kInlineTiles) {
     for (size_t i = 0; i < tiles.size(); ++i)
@@ -977,9 +990,15 @@ struct cafxg_actor {
 };
 
 struct Request {
+  const cafxg_mandel_desc& tile(size_t i) const { return i == 0 ? tile0 : more[i - 1]; }
   Request* next = nullptr;
   cafxg_actor* actor = nullptr;
-  std::vector<cafxg_mandel_desc> tiles;  // mandelbrot
+  // mandelbrot tiles: the first inline (a storm request is one tile, so the
+  // dispatcher touches one cache-resident node per request), the rest behind
+  cafxg_mandel_desc tile0{};
+  std::vector<cafxg_mandel_desc> more;
+  uint32_t ntiles = 0;
+  int precision = 0;
   const float* a = nullptr;              // matrix_multiply
   const float* b = nullptr;
   void* out = nullptr;
@@ -1108,14 +1127,14 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   uint64_t px = 0;
   uint32_t maxit = 0;
   bool exact = false;
-  int prec = batch[0]->tiles[0].precision;
+  int prec = batch[0]->precision;
   bool all_pinned = true;
   size_t ntiles = 0;
   for (Request* r : batch) {
     px += r->pixels;
     maxit = std::max(maxit, r->max_iter);
     exact = exact || r->exact;
-    ntiles += r->tiles.size();
+    ntiles += r->ntiles;
     all_pinned = all_pinned && r->out_pinned;
   }
   int status = CAFXG_OK;
@@ -1139,7 +1158,8 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   uint64_t off = 0;
   for (Request* r : batch) {
     uint64_t roff = off;
-    for (auto& t : r->tiles) {
+    for (uint32_t k = 0; k < r->ntiles; ++k) {
+      const cafxg_mandel_desc& t = r->tile(k);
       MTile m;
       fill_mtile(m, t, off, chunks);
       mt.push_back(m);
@@ -1225,6 +1245,15 @@ static void dispatcher_loop(cafxg_ctx* ctx) {
   const uint64_t kMaxBatchPx = 64ull << 20;
   std::deque<Request*> queue;
   while (true) {
+    // brief spin before sleeping: request/reply round trips (sync_send
+    // clients) arrive within microseconds of the previous completion, and a
+    // futex sleep/wake pair would dominate their latency
+    if (queue.empty() && ctx->inbox.load(std::memory_order_acquire) == nullptr) {
+      auto until = std::chrono::steady_clock::now() + std::chrono::microseconds(50);
+      while (ctx->inbox.load(std::memory_order_acquire) == nullptr &&
+             std::chrono::steady_clock::now() < until && !ctx->disp_stop)
+        __builtin_ia32_pause();
+    }
     {
       std::unique_lock<std::mutex> lk(ctx->disp_mu);
       ctx->disp_cv.wait(lk, [&] {
@@ -1282,7 +1311,7 @@ static void dispatcher_loop(cafxg_ctx* ctx) {
         break;
       }
       if (!batch.empty() &&
-          (r->tiles[0].precision != batch[0]->tiles[0].precision ||
+          (r->precision != batch[0]->precision ||
            px + r->pixels > kMaxBatchPx))
         break;
       queue.pop_front();
@@ -1688,9 +1717,14 @@ int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in, const size_t* in_
   if (a->kernel == Kernel::mandelbrot) {
     const auto* t = static_cast<const cafxg_mandel_desc*>(in[0]);
     size_t n = in_bytes[0] / sizeof(cafxg_mandel_desc);
-    r->tiles.assign(t, t + n);
+    r->tile0 = t[0];
+    if (n > 1)
+      r->more.assign(t + 1, t + n);
+    r->ntiles = (uint32_t)n;
+    r->precision = (int)t[0].precision;
     uint64_t off = 0;
-    for (auto& x : r->tiles) {
+    for (size_t k = 0; k < n; ++k) {
+      cafxg_mandel_desc& x = k == 0 ? r->tile0 : r->more[k - 1];
       x.out_offset = off;  // tiles packed in order in the reply
       off += (uint64_t)x.nrows * x.ncols;
       r->max_iter = std::max(r->max_iter, x.max_iter);
