@@ -1245,15 +1245,6 @@ static void dispatcher_loop(cafxg_ctx* ctx) {
   const uint64_t kMaxBatchPx = 64ull << 20;
   std::deque<Request*> queue;
   while (true) {
-    // brief spin before sleeping: request/reply round trips (sync_send
-    // clients) arrive within microseconds of the previous completion, and a
-    // futex sleep/wake pair would dominate their latency
-    if (queue.empty() && ctx->inbox.load(std::memory_order_acquire) == nullptr) {
-      auto until = std::chrono::steady_clock::now() + std::chrono::microseconds(50);
-      while (ctx->inbox.load(std::memory_order_acquire) == nullptr &&
-             std::chrono::steady_clock::now() < until && !ctx->disp_stop)
-        __builtin_ia32_pause();
-    }
     {
       std::unique_lock<std::mutex> lk(ctx->disp_mu);
       ctx->disp_cv.wait(lk, [&] {
