@@ -198,7 +198,7 @@ constexpr size_t kUpSlotBytes = 2u << 20;
 struct Device {
   int ordinal = 0;
   int sms = 0;
-  cudaStream_t compute = nullptr, d2h = nullptr;
+  cudaStream_t compute = nullptr, d2h = nullptr, h2d = nullptr;
   uint32_t* sched = nullptr;  // kSchedSlots x {cursor, finished}
   std::atomic<uint32_t> sched_next{0};
   std::mutex submit_mu;
@@ -867,6 +867,106 @@ static int ensure_nccl(cafxg_ctx* ctx) {
   return CAFXG_OK;
 }
 
+// Streams `b` waits for what `a` has enqueued so far.
+static int stream_after(cudaStream_t b, cudaStream_t a) {
+  cudaEvent_t ev;
+  CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CAFXG_CUDA_TRY(cudaEventRecord(ev, a));
+  CAFXG_CUDA_TRY(cudaStreamWaitEvent(b, ev, 0));
+  cudaEventDestroy(ev);  // released once it completes
+  return CAFXG_OK;
+}
+
+// Host-request pipeline for one device's C rows [r0, r1) with B already in
+// device memory (dB, K x N): B is split once (tf32 hi/lo, transposed), then
+// per block of R rows: H2D of A_i on the upload stream -> hi/lo split + 3xTF32
+// GEMM on the compute stream -> D2H of C_i on the download stream. A and C
+// blocks are double-buffered, so PCIe traffic in both directions overlaps the
+// tensor-core work. Completion is recorded on d2h.
+static bool sgemm_pipeline_eligible(const cafxg_sgemm_desc& g, uint32_t rows) {
+  return g.mode != CAFXG_SGEMM_FFMA && rows >= 1024 && rows % 128 == 0 &&
+         sgemm_tc_supported(128, g.N, g.K, g.K, g.N, g.N);
+}
+
+static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
+                                 const float* A, const float* dB, float* C, uint32_t r0,
+                                 uint32_t r1) {
+  const size_t N = g.N, K = g.K;
+  const uint32_t rows = r1 - r0;
+  uint32_t R = ((rows + 7) / 8 + 127) / 128 * 128;  // ~8 blocks of whole 128-row tiles
+  R = std::max<uint32_t>(R, 512);
+  float *Bh = nullptr, *Bl = nullptr, *Ah = nullptr, *Al = nullptr;
+  float* dA[2] = {nullptr, nullptr};
+  float* dC[2] = {nullptr, nullptr};
+  cudaStream_t cs = d->compute;
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Bh, N * K * 4, cs));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Bl, N * K * 4, cs));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Ah, (size_t)R * K * 4, cs));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Al, (size_t)R * K * 4, cs));
+  for (int b = 0; b < 2; ++b) {
+    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dA[b], (size_t)R * K * 4, cs));
+    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dC[b], (size_t)R * N * 4, cs));
+  }
+  int e = sgemm_tc_split_b(dB, (int)N, (int)K, (int)N, Bh, Bl, cs);
+  if (e != 0)
+    return cuda_status((cudaError_t)e, "sgemm: B split");
+  ctx->st_launches++;
+  CAFXG_TRY(stream_after(d->h2d, cs));  // the buffers exist before uploads
+  std::vector<cudaEvent_t> ev_split, ev_gemm, ev_down;
+  auto mk = [](std::vector<cudaEvent_t>& v) {
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    v.push_back(ev);
+    return ev;
+  };
+  int status = CAFXG_OK;
+  uint32_t i = 0;
+  for (uint32_t b0 = 0; b0 < rows && status == CAFXG_OK; b0 += R, ++i) {
+    const uint32_t m = std::min(R, rows - b0);
+    const int slot = i & 1;
+    // upload A block (slot free once block i-2's split consumed it)
+    if (i >= 2)
+      cudaStreamWaitEvent(d->h2d, ev_split[i - 2], 0);
+    const float* src = A + (size_t)(r0 + b0) * g.lda;
+    if (g.lda == K)
+      status = cuda_status(cudaMemcpyAsync(dA[slot], src, (size_t)m * K * 4,
+                                           cudaMemcpyHostToDevice, d->h2d), "sgemm: A upload");
+    else
+      status = cuda_status(cudaMemcpy2DAsync(dA[slot], K * 4, src, (size_t)g.lda * 4, K * 4, m,
+                                             cudaMemcpyHostToDevice, d->h2d),
+                           "sgemm: A upload");
+    ctx->st_h2d += (size_t)m * K * 4;
+    CAFXG_TRY(stream_after(cs, d->h2d));
+    if (i >= 2)
+      cudaStreamWaitEvent(cs, ev_down[i - 2], 0);  // C slot drained
+    e = sgemm_tc_split_a(dA[slot], (int)K, (int)m, (int)K, Ah, Al, cs);
+    cudaEventRecord(mk(ev_split), cs);
+    if (e == 0)
+      e = sgemm_tc_gemm(Ah, Al, Bh, Bl, dC[slot], (int)m, (int)N, (int)K, (int)N, cs);
+    if (e != 0)
+      status = cuda_status((cudaError_t)e, "sgemm: 3xtf32 launch");
+    ctx->st_launches += 2;
+    cudaEventRecord(mk(ev_gemm), cs);
+    cudaStreamWaitEvent(d->d2h, ev_gemm.back(), 0);
+    if (status == CAFXG_OK)
+      status = cuda_status(cudaMemcpy2DAsync(C + (size_t)(r0 + b0) * g.ldc, (size_t)g.ldc * 4,
+                                             dC[slot], N * 4, N * 4, m,
+                                             cudaMemcpyDeviceToHost, d->d2h),
+                           "sgemm: C download");
+    ctx->st_d2h += (size_t)m * N * 4;
+    cudaEventRecord(mk(ev_down), d->d2h);
+  }
+  // everything is released on the download stream, which by now follows
+  // every upload and kernel of this request
+  CAFXG_TRY(stream_after(d->d2h, cs));
+  for (float* p : {Bh, Bl, Ah, Al, dA[0], dA[1], dC[0], dC[1]})
+    cudaFreeAsync(p, d->d2h);
+  for (auto* v : {&ev_split, &ev_gemm, &ev_down})
+    for (auto ev : *v)
+      cudaEventDestroy(ev);
+  return status;
+}
+
 // Host-to-host sgemm. One device: H2D A,B -> GEMM -> D2H C. G devices: A is
 // split into row blocks; each device uploads 1/G of B's rows and an NCCL
 // all-gather over NVLink completes B everywhere; each device returns its C
@@ -935,6 +1035,16 @@ static int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
     part.lda = g.K;
     part.ldc = g.N;
     float *dA = nullptr, *dC = nullptr;
+    if (s == CAFXG_OK && part.M && g.ldb == g.N && sgemm_pipeline_eligible(g, part.M)) {
+      s = sgemm_pipeline_device(ctx, d, g, A, dB[k], C, r0, r1);
+      cudaFreeAsync(dB[k], d->d2h);
+      if (s != CAFXG_OK)
+        push_completion(ctx, d, d->d2h, [join, s](int) { join->part_done(s); });
+      else if (push_completion(ctx, d, d->d2h, [join](int st) { join->part_done(st); }) !=
+               CAFXG_OK)
+        join->part_done(CAFXG_E_DOWN);
+      continue;
+    }
     if (s == CAFXG_OK && part.M) {
       if (cudaMallocAsync((void**)&dA, (size_t)part.M * g.K * 4 + 4, d->compute) != cudaSuccess ||
           cudaMallocAsync((void**)&dC, (size_t)part.M * g.N * 4 + 4, d->compute) != cudaSuccess)
@@ -1376,6 +1486,7 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
       d->sms = prop.multiProcessorCount;
       CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->compute, cudaStreamNonBlocking));
       CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking));
+      CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->h2d, cudaStreamNonBlocking));
       CAFXG_CUDA_TRY(cudaMalloc(&d->sched, kSchedSlots * 2 * sizeof(uint32_t)));
       CAFXG_CUDA_TRY(cudaMemset(d->sched, 0, kSchedSlots * 2 * sizeof(uint32_t)));
       CAFXG_CUDA_TRY(cudaHostAlloc((void**)&d->up_base, kUpSlots * kUpSlotBytes,
@@ -1455,8 +1566,10 @@ int cafxg_close(cafxg_ctx* ctx) {
       cudaEventDestroy(ev);
     cudaFreeHost(d->up_base);
     cudaFree(d->sched);
+    cudaStreamSynchronize(d->h2d);
     cudaStreamDestroy(d->compute);
     cudaStreamDestroy(d->d2h);
+    cudaStreamDestroy(d->h2d);
   }
   if (!ctx->comms.empty())
     for (auto c : ctx->comms)

@@ -17,6 +17,15 @@ size_t sgemm_tc_scratch_bytes(int M, int N, int K);
 int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N,
                     int K, int lda, int ldb, int ldc, void* scratch,
                     int sm_count, void* stream, int* launches);
+// The three stages separately (pipelined host requests): tf32 hi/lo split of
+// an A row block (M x K, packed out), split + transpose of B (to N x K), and
+// the GEMM on split operands.
+int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al,
+                     void* stream);
+int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl,
+                     void* stream);
+int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl,
+                  float* C, int M, int N, int K, int ldc, void* stream);
 
 // Device FNV-1a-64 over u32 cells hashed big-endian (fnv.cu).
 uint64_t fnv_segment_cells(uint64_t n, int sms);

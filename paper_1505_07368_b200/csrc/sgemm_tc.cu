@@ -367,18 +367,23 @@ size_t sgemm_tc_scratch_bytes(int M, int N, int K) {
   return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float);
 }
 
-int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int K, int lda,
-                    int ldb, int ldc, void* scratch, int sm_count, void* stream,
-                    int* launches) {
-  (void)sm_count;
-  cudaStream_t s = (cudaStream_t)stream;
-  float* Ah = static_cast<float*>(scratch);
-  float* Al = Ah + (size_t)M * K;
-  float* Bh = Al + (size_t)M * K;
-  float* Bl = Bh + (size_t)N * K;
-  int grid_split = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 16);
-  split_rows_kernel<<<grid_split, 256, 0, s>>>(A, lda, M, K, Ah, Al);
-  split_transpose_kernel<<<dim3(N / 32, K / 32), 256, 0, s>>>(B, ldb, K, N, Bh, Bl);
+int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al,
+                     void* stream) {
+  int grid = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 16);
+  if (grid > 0)
+    split_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al);
+  return (int)cudaGetLastError();
+}
+
+int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl,
+                     void* stream) {
+  split_transpose_kernel<<<dim3(N / 32, K / 32), 256, 0, (cudaStream_t)stream>>>(B, ldb, K, N,
+                                                                                Bh, Bl);
+  return (int)cudaGetLastError();
+}
+
+int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl, float* C,
+                  int M, int N, int K, int ldc, void* stream) {
   CUtensorMap mAh, mAl, mBh, mBl;
   if (!make_map(&mAh, Ah, M, K, BM) || !make_map(&mAl, Al, M, K, BM) ||
       !make_map(&mBh, Bh, N, K, BN) || !make_map(&mBl, Bl, N, K, BN))
@@ -386,11 +391,27 @@ int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int 
   cudaFuncSetAttribute(sgemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        SMEM_BYTES);
   int tiles = (M / BM) * (N / BN);
-  sgemm_3xtf32_kernel<<<tiles, TC_THREADS, SMEM_BYTES, s>>>(mAh, mAl, mBh, mBl, C, M, N, K,
-                                                            ldc);
+  sgemm_3xtf32_kernel<<<tiles, TC_THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
+      mAh, mAl, mBh, mBl, C, M, N, K, ldc);
+  return (int)cudaGetLastError();
+}
+
+int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int K, int lda,
+                    int ldb, int ldc, void* scratch, int sm_count, void* stream,
+                    int* launches) {
+  (void)sm_count;
+  float* Ah = static_cast<float*>(scratch);
+  float* Al = Ah + (size_t)M * K;
+  float* Bh = Al + (size_t)M * K;
+  float* Bl = Bh + (size_t)N * K;
+  int e = sgemm_tc_split_a(A, lda, M, K, Ah, Al, stream);
+  if (e == 0)
+    e = sgemm_tc_split_b(B, ldb, K, N, Bh, Bl, stream);
+  if (e == 0)
+    e = sgemm_tc_gemm(Ah, Al, Bh, Bl, C, M, N, K, ldc, stream);
   if (launches)
     *launches = 3;
-  return (int)cudaGetLastError();
+  return e;
 }
 
 }  // namespace cafxg

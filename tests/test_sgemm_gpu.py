@@ -71,6 +71,22 @@ def test_sgemm_3xtf32(ctx, M, N, K):
     assert check(A, B, C) <= TOL
 
 
+@pytest.mark.parametrize("M,N,K,pad", [(3072, 512, 256, 0), (1280, 256, 512, 8)])
+def test_sgemm_pipelined_host_request(ctx, M, N, K, pad):
+    """Host request >= 1024 rows: row-block pipeline (upload / 3xTF32 / download
+    overlapped), including a padded leading dimension of A and C."""
+    Abig = oracle.fill_uniform(M * (K + pad), 21).reshape(M, K + pad)
+    A = Abig[:, :K]
+    B = oracle.fill_uniform(K * N, 22).reshape(K, N)
+    Cbig = np.full((M, N + pad), np.nan, dtype=np.float32)
+    C = Cbig[:, :N]
+    ctx.sgemm(A, B, C)
+    assert not np.isnan(C).any()
+    assert check(np.ascontiguousarray(A), B, C) <= TOL
+    if pad:
+        assert np.isnan(Cbig[:, N:]).all()   # the padding is never written
+
+
 def test_sgemm_3xtf32_rejects_unsupported_shape(ctx):
     A = np.zeros((100, 64), np.float32)
     B = np.zeros((64, 256), np.float32)
