@@ -359,8 +359,14 @@ def run_ours(args):
     sms = torch.cuda.get_device_properties(gpu).multi_processor_count
     peak_tops = sms * 128 * sm_max * 1e6 / 1e12
     achieved = 8.0 * iters_local / (kernel_ms / 1e3) / 1e12
+    # DRAM traffic of the escape kernel from the committed ncu capture of the
+    # full-image launch (profiles/round1/mandel_cfg3_full.txt: 1.021780 GB
+    # written + 7.890176 MB read), scaled to this rank's share of the pixels
+    traffic = round((1.021780e9 + 7.890176e6) * npx / (W_IMG * H_IMG))
     roof = {"bound": "fp32_pipe", "achieved": round(achieved, 3), "peak": round(peak_tops, 3),
-            "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4), "traffic": None,
+            "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4), "traffic": traffic,
+            "traffic_note": "dram read+write bytes per launch (ncu, profiles/round1); "
+                            "algorithmic output is 4 B/pixel",
             "ops_per_launch": 8.0 * iters_local,
             "peak_basis": f"{sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz of "
                           "MEASURED_PEAKS.json); algorithmic 8 FP ops per escape iteration "
