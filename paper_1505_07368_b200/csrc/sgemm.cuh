@@ -25,7 +25,11 @@ int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al
 int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl,
                      void* stream);
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl,
-                  float* C, int M, int N, int K, int ldc, void* stream);
+                  float* C, int M, int N, int K, int ldc, void* stream, int splits = 1,
+                  float* work = nullptr);
+// split-K factor for small C grids and its workspace (splits * M * N floats)
+int sgemm_tc_splits(int M, int N, int K, int sms);
+size_t sgemm_tc_work_bytes(int M, int N, int K, int sms);
 
 // Device FNV-1a-64 over u32 cells hashed big-endian (fnv.cu).
 uint64_t fnv_segment_cells(uint64_t n, int sms);

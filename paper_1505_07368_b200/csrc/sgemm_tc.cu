@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         const __grid_constant__ CUtensorMap mAl,
                         const __grid_constant__ CUtensorMap mBh,
                         const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
-                        int M, int N, int K, int ldc) {
+                        int M, int N, int K, int ldc, int splits, float* __restrict__ work) {
+  // split-K: CTA z of `splits` covers K range [z*K/splits, (z+1)*K/splits) and
+  // writes its partial tile to work + z*M*N (summed by splitk_reduce_kernel)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -154,13 +156,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // grouped raster: GROUP_M consecutive M tiles share each N tile
   const int tiles_m = M / BM, tiles_n = N / BN;
   const int per_group = GROUP_M * tiles_n;
-  const int bid = blockIdx.x;
+  const int tiles = tiles_m * tiles_n;
+  const int kz = blockIdx.x / tiles;
+  const int bid = blockIdx.x % tiles;
   const int first_m = (bid / per_group) * GROUP_M;
   const int gsize = min(GROUP_M, tiles_m - first_m);
   const int in_group = bid % per_group;
   const int m0 = (first_m + in_group % gsize) * BM;
   const int n0 = (in_group / gsize) * BN;
-  const int nk = K / BK;
+  const int ksplit = K / splits;
+  const int k_base = kz * ksplit;
+  const int nk = ksplit / BK;
+  if (splits > 1) {
+    C = work + (size_t)kz * M * N;
+    ldc = N;
+  }
 
   if (warp == 0 && lane == 0) {
     for (const CUtensorMap* m : {&mAh, &mAl, &mBh, &mBl})
@@ -195,10 +205,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&empty[s], ph ^ 1);
       uint8_t* st = smem + s * STAGE_BYTES;
       mbar_expect_tx(&full[s], STAGE_BYTES);
-      tma_load_2d(st, &mAh, &full[s], kb * BK, m0);
-      tma_load_2d(st + A_TILE, &mAl, &full[s], kb * BK, m0);
-      tma_load_2d(st + 2 * A_TILE, &mBh, &full[s], kb * BK, n0);
-      tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], kb * BK, n0);
+      const int kx = k_base + kb * BK;
+      tma_load_2d(st, &mAh, &full[s], kx, m0);
+      tma_load_2d(st + A_TILE, &mAl, &full[s], kx, m0);
+      tma_load_2d(st + 2 * A_TILE, &mBh, &full[s], kx, n0);
+      tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], kx, n0);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer ----
@@ -266,6 +277,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
+}
+
+// C = sum of the split-K partials, in fixed order (deterministic)
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ work,
+                                                            int splits, int M, int N,
+                                                            float* __restrict__ C, int ldc) {
+  const size_t total = (size_t)M * N / 4;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(work)[i];
+    for (int z = 1; z < splits; ++z) {
+      float4 v = reinterpret_cast<const float4*>(work + (size_t)z * M * N)[i];
+      acc.x = __fadd_rn(acc.x, v.x);
+      acc.y = __fadd_rn(acc.y, v.y);
+      acc.z = __fadd_rn(acc.z, v.z);
+      acc.w = __fadd_rn(acc.w, v.w);
+    }
+    size_t e = i * 4, r = e / N, c = e % N;
+    *reinterpret_cast<float4*>(C + r * ldc + c) = acc;
+  }
 }
 
 // ---- hi/lo split ----------------------------------------------------------
@@ -364,7 +395,9 @@ bool sgemm_tc_supported(int M, int N, int K, int lda, int ldb, int ldc) {
 }
 
 size_t sgemm_tc_scratch_bytes(int M, int N, int K) {
-  return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float);
+  // hi/lo splits of A and B^T, plus the split-K workspace (148 SMs)
+  return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float) +
+         sgemm_tc_work_bytes(M, N, K, 148);
 }
 
 int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al,
@@ -382,17 +415,38 @@ int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl
   return (int)cudaGetLastError();
 }
 
+// Split-K factor that fills the GPU when the C tile grid alone cannot (each
+// split keeps >= 8 k-blocks of 16 and a multiple of 32 in K).
+int sgemm_tc_splits(int M, int N, int K, int sms) {
+  const int tiles = (M / BM) * (N / BN);
+  int s = 1;
+  while (s < 8 && tiles * s * 2 <= 2 * sms && K % (32 * s * 2) == 0 && K / (s * 2) >= 128)
+    s *= 2;
+  return s;
+}
+
+size_t sgemm_tc_work_bytes(int M, int N, int K, int sms) {
+  int s = sgemm_tc_splits(M, N, K, sms);
+  return s > 1 ? (size_t)s * M * N * sizeof(float) : 0;
+}
+
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl, float* C,
-                  int M, int N, int K, int ldc, void* stream) {
+                  int M, int N, int K, int ldc, void* stream, int splits, float* work) {
   CUtensorMap mAh, mAl, mBh, mBl;
   if (!make_map(&mAh, Ah, M, K, BM) || !make_map(&mAl, Al, M, K, BM) ||
       !make_map(&mBh, Bh, N, K, BN) || !make_map(&mBl, Bl, N, K, BN))
     return (int)cudaErrorInvalidValue;
   cudaFuncSetAttribute(sgemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        SMEM_BYTES);
+  if (splits < 1 || !work)
+    splits = 1;
   int tiles = (M / BM) * (N / BN);
-  sgemm_3xtf32_kernel<<<tiles, TC_THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
-      mAh, mAl, mBh, mBl, C, M, N, K, ldc);
+  sgemm_3xtf32_kernel<<<tiles * splits, TC_THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
+      mAh, mAl, mBh, mBl, C, M, N, K, ldc, splits, work);
+  if (splits > 1) {
+    int grid = (int)std::min<size_t>(((size_t)M * N / 4 + 255) / 256, 148 * 8);
+    splitk_reduce_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(work, splits, M, N, C, ldc);
+  }
   return (int)cudaGetLastError();
 }
 
@@ -404,13 +458,15 @@ int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int 
   float* Al = Ah + (size_t)M * K;
   float* Bh = Al + (size_t)M * K;
   float* Bl = Bh + (size_t)N * K;
+  const int splits = sgemm_tc_splits(M, N, K, 148);  // as sgemm_tc_scratch_bytes
+  float* work = splits > 1 ? Bl + (size_t)N * K : nullptr;
   int e = sgemm_tc_split_a(A, lda, M, K, Ah, Al, stream);
   if (e == 0)
     e = sgemm_tc_split_b(B, ldb, K, N, Bh, Bl, stream);
   if (e == 0)
-    e = sgemm_tc_gemm(Ah, Al, Bh, Bl, C, M, N, K, ldc, stream);
+    e = sgemm_tc_gemm(Ah, Al, Bh, Bl, C, M, N, K, ldc, stream, splits, work);
   if (launches)
-    *launches = 3;
+    *launches = splits > 1 ? 4 : 3;
   return e;
 }
 
