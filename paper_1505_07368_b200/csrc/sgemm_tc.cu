@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 
@@ -436,8 +437,17 @@ int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float
   if (!make_map(&mAh, Ah, M, K, BM) || !make_map(&mAl, Al, M, K, BM) ||
       !make_map(&mBh, Bh, N, K, BN) || !make_map(&mBl, Bl, N, K, BN))
     return (int)cudaErrorInvalidValue;
-  cudaFuncSetAttribute(sgemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       SMEM_BYTES);
+  {
+    // once per device (the attribute is per-device state)
+    static std::atomic<uint64_t> configured{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !(configured.load() >> dev & 1)) {
+      cudaFuncSetAttribute(sgemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SMEM_BYTES);
+      configured.fetch_or(1ull << dev);
+    }
+  }
   if (splits < 1 || !work)
     splits = 1;
   int tiles = (M / BM) * (N / BN);
