@@ -6,18 +6,22 @@
 // is parallelised through a decomposition of the state rather than of the
 // data. Write h = 256u + l with l the low byte. Because b < 256 and p is odd,
 //     (256u + (l ^ b)) * p = 256 (u*p + q) + r,   t = l ^ b, t*p = 256q + r,
-// so the low byte evolves on its own (l' = r, a permutation of 0..255) and the
-// high part is affine in u with slope p: u' = u*p + q(l, b). A segment of n
-// bytes therefore acts as
-//     l_end = L[l0],   u_end = p^n * u0 + Cs[l0]   (mod 2^56; computed mod 2^64)
-// for a 256-entry table pair (L, Cs). One CTA of 256 threads builds a
-// segment's tables (thread = starting low byte); a single thread then walks
-// the segments in order from the real seed. Work is 256x the serial hash but
-// spread over the whole GPU, and the result is bit-identical to the
-// reference's serial loop.
+// so the low byte evolves on its own, l' = (t * 179) mod 256 (435 = 179 mod
+// 256; a permutation of 0..255), and the high part is affine in u with slope
+// p: u' = u*p + q(l, b), q = (t << 32) + (t*435 >> 8) (p = 2^40 + 435).
 //
-// With p = 2^40 + 435:  t*p = t*2^40 + t*435, so q = (t << 32) + (t*435 >> 8)
-// and r = t*435 & 255 (t*435 < 2^17).
+// Three passes:
+//  1. low bytes only. A segment's 256 possible incoming low bytes are
+//     tracked at once, four per 32-bit register (byte-lane SIMD: one
+//     multiply per pair of lanes, 7 instructions per byte per 4 lanes), and
+//     the lanes are recorded at every sub-segment boundary;
+//  2. one thread walks the segments' low-byte permutations from the seed,
+//     giving each segment its real incoming low byte;
+//  3. one thread per sub-segment runs the full recurrence from its real
+//     incoming low byte (read from the pass-1 record) and returns the affine
+//     offset C_j; a final thread folds u = u * p^(n_j) + C_j in order.
+// Work is ~1.75x the serial byte count in pass 1 (256 lanes, 4 per slot) plus
+// 1x in pass 3, all parallel; the result is bit-identical to the serial loop.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -26,50 +30,155 @@ namespace cafxg {
 namespace {
 
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
-constexpr int kFnvThreads = 256;
-constexpr int kFnvTile = 2048;  // cells staged in smem per round
+constexpr int kP1Threads = 64;   // 64 threads x 4 byte lanes = 256 low bytes
+constexpr int kSubSegs = 32;     // sub-segments per segment (pass 3 threads)
+constexpr int kTile = 4096;      // cells staged in smem per round (pass 1)
 
-__global__ void __launch_bounds__(kFnvThreads)
-    fnv_segments_kernel(const uint32_t* __restrict__ cells, uint64_t n, uint64_t seg_cells,
-                        uint8_t* __restrict__ Lout, uint64_t* __restrict__ Cout) {
-  __shared__ uint32_t tile[kFnvTile];
+__device__ __forceinline__ uint32_t rep_byte(uint32_t x, int sh) {
+  // byte (x >> sh) & 255 replicated into all four lanes
+  return __byte_perm(x, 0, (sh >> 3) * 0x1111);
+}
+
+// Pass 1: per segment, the low byte after every sub-segment for all 256
+// incoming low bytes. rec[(seg * kSubSegs + j) * 64 + thread] holds lanes
+// 4*thread .. 4*thread+3 at the START of sub-segment j; L[seg * 256 + v] is
+// the outgoing low byte for incoming v.
+__global__ void __launch_bounds__(kP1Threads)
+    fnv_lowbyte_kernel(const uint32_t* __restrict__ cells, uint64_t n, uint64_t seg_cells,
+                       uint64_t sub_cells, uint32_t* __restrict__ rec,
+                       uint8_t* __restrict__ L) {
+  __shared__ uint32_t tile[kTile];
   const uint64_t begin = (uint64_t)blockIdx.x * seg_cells;
   const uint64_t end = begin + seg_cells < n ? begin + seg_cells : n;
-  uint32_t l = threadIdx.x;  // this thread's starting low byte
-  uint64_t c = 0;
-  for (uint64_t base = begin; base < end; base += kFnvTile) {
-    const uint32_t cnt = end - base < (uint64_t)kFnvTile ? (uint32_t)(end - base) : kFnvTile;
+  const uint32_t tid = threadIdx.x;
+  // lanes: incoming low bytes 4*tid + {0,1,2,3}
+  uint32_t w = (4 * tid) | ((4 * tid + 1) << 8) | ((4 * tid + 2) << 16) | ((4 * tid + 3) << 24);
+  uint32_t* myrec = rec + (size_t)blockIdx.x * kSubSegs * kP1Threads + tid;
+  uint64_t next_rec = begin;  // cell index of the next sub-segment start
+  uint32_t j = 0;
+  for (uint64_t base = begin; base < end; base += kTile) {
+    const uint32_t cnt = end - base < (uint64_t)kTile ? (uint32_t)(end - base) : kTile;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < cnt; i += kFnvThreads)
+    for (uint32_t i = tid; i < cnt; i += kP1Threads)
       tile[i] = __ldg(cells + base + i);
     __syncthreads();
     for (uint32_t i = 0; i < cnt; ++i) {
+      if (base + i == next_rec) {
+        myrec[(size_t)j * kP1Threads] = w;
+        ++j;
+        next_rec += sub_cells;
+      }
       const uint32_t x = tile[i];  // broadcast read
 #pragma unroll
       for (int sh = 24; sh >= 0; sh -= 8) {
-        const uint32_t t = l ^ ((x >> sh) & 255u);
-        const uint32_t m = t * 435u;
-        l = m & 255u;
-        c = c * kFnvPrime + (((uint64_t)t << 32) + (m >> 8));
+        const uint32_t bb = rep_byte(x, sh);
+        const uint32_t e = ((w ^ bb) & 0x00ff00ffu) * 179u;           // lanes 0, 2
+        const uint32_t o = (((w >> 8) ^ bb) & 0x00ff00ffu) * 45824u;  // lanes 1, 3 (179 << 8)
+        w = (e & 0x00ff00ffu) | (o & 0xff00ff00u);
       }
     }
   }
-  Lout[(size_t)blockIdx.x * 256 + threadIdx.x] = (uint8_t)l;
-  Cout[(size_t)blockIdx.x * 256 + threadIdx.x] = c;
+  for (; j < kSubSegs; ++j)  // empty trailing sub-segments start where we end
+    myrec[(size_t)j * kP1Threads] = w;
+  uint8_t* out = L + (size_t)blockIdx.x * 256 + 4 * tid;
+  out[0] = (uint8_t)w;
+  out[1] = (uint8_t)(w >> 8);
+  out[2] = (uint8_t)(w >> 16);
+  out[3] = (uint8_t)(w >> 24);
 }
 
-// Walks the segment tables from the seed: one thread, nseg steps.
-__global__ void fnv_walk_kernel(const uint8_t* __restrict__ L, const uint64_t* __restrict__ C,
-                                uint64_t nseg, uint64_t p_full, uint64_t p_last,
-                                uint64_t seed, uint64_t* out) {
+// Pass 2: the real incoming low byte of every segment, and the final one.
+// One CTA: the tables are staged through shared memory 32 segments at a time
+// so the single walking thread chases pointers in smem, not L2.
+__global__ void __launch_bounds__(256)
+    fnv_scan_kernel(const uint8_t* __restrict__ L, uint32_t nseg, uint64_t seed,
+                    uint8_t* __restrict__ lin) {
+  __shared__ uint32_t tab[32 * 64];
   uint32_t l = (uint32_t)(seed & 255u);
-  uint64_t u = seed >> 8;
-  for (uint64_t s = 0; s < nseg; ++s) {
-    const uint64_t pn = (s + 1 == nseg) ? p_last : p_full;
-    u = u * pn + C[s * 256 + l];
-    l = L[s * 256 + l];
+  for (uint32_t s0 = 0; s0 < nseg; s0 += 32) {
+    const uint32_t cnt = nseg - s0 < 32 ? nseg - s0 : 32;
+    __syncthreads();
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(L + (size_t)s0 * 256);
+    for (uint32_t i = threadIdx.x; i < cnt * 64; i += blockDim.x)
+      tab[i] = src[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint8_t* t = reinterpret_cast<const uint8_t*>(tab);
+      for (uint32_t k = 0; k < cnt; ++k) {
+        lin[s0 + k] = (uint8_t)l;
+        l = t[k * 256 + l];
+      }
+    }
   }
-  *out = ((u << 8) | l);
+  if (threadIdx.x == 0)
+    lin[nseg] = (uint8_t)l;
+}
+
+// Pass 3: thread = (segment, sub-segment): full recurrence from the real
+// incoming low byte; C[j] = affine offset of the sub-segment.
+__global__ void __launch_bounds__(256)
+    fnv_affine_kernel(const uint32_t* __restrict__ cells, uint64_t n, uint64_t seg_cells,
+                      uint64_t sub_cells, uint32_t nseg, const uint32_t* __restrict__ rec,
+                      const uint8_t* __restrict__ lin, uint64_t* __restrict__ C) {
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (uint64_t)nseg * kSubSegs)
+    return;
+  const uint32_t s = (uint32_t)(g / kSubSegs), j = (uint32_t)(g % kSubSegs);
+  const uint64_t seg_begin = (uint64_t)s * seg_cells;
+  const uint64_t seg_end = seg_begin + seg_cells < n ? seg_begin + seg_cells : n;
+  uint64_t b = seg_begin + (uint64_t)j * sub_cells;
+  uint64_t e = b + sub_cells;
+  if (b > seg_end) b = seg_end;
+  if (e > seg_end) e = seg_end;
+  const uint32_t v = lin[s];
+  const uint32_t word = rec[((size_t)s * kSubSegs + j) * kP1Threads + (v >> 2)];
+  uint32_t l = (word >> (8 * (v & 3))) & 255u;
+  uint64_t c = 0;
+  for (uint64_t i = b; i < e; ++i) {
+    const uint32_t x = __ldg(cells + i);
+#pragma unroll
+    for (int sh = 24; sh >= 0; sh -= 8) {
+      const uint32_t t = l ^ ((x >> sh) & 255u);
+      const uint32_t m = t * 435u;
+      l = m & 255u;
+      c = c * kFnvPrime + (((uint64_t)t << 32) + (m >> 8));
+    }
+  }
+  C[g] = c;
+}
+
+__device__ uint64_t pow_dev(uint64_t b, uint64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1)
+      r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+
+// Fold: u = u * p^(4 n_j) + C_j over all sub-segments in order.
+__global__ void fnv_fold_kernel(const uint64_t* __restrict__ C, uint64_t n, uint64_t seg_cells,
+                                uint64_t sub_cells, uint32_t nseg, uint64_t p_sub,
+                                uint64_t seed, const uint8_t* __restrict__ lin,
+                                uint64_t* out) {
+  uint64_t u = seed >> 8;
+  for (uint32_t s = 0; s < nseg; ++s) {
+    const uint64_t seg_begin = (uint64_t)s * seg_cells;
+    const uint64_t seg_end = seg_begin + seg_cells < n ? seg_begin + seg_cells : n;
+    for (uint32_t j = 0; j < kSubSegs; ++j) {
+      uint64_t b = seg_begin + (uint64_t)j * sub_cells, e = b + sub_cells;
+      if (b > seg_end) b = seg_end;
+      if (e > seg_end) e = seg_end;
+      const uint64_t len = e - b;
+      if (len == 0)
+        continue;
+      const uint64_t pn = len == sub_cells ? p_sub : pow_dev(kFnvPrime, 4 * len);
+      u = u * pn + C[(size_t)s * kSubSegs + j];
+    }
+  }
+  *out = (u << 8) | lin[nseg];
 }
 
 uint64_t pow_mod64(uint64_t b, uint64_t e) {
@@ -83,37 +192,58 @@ uint64_t pow_mod64(uint64_t b, uint64_t e) {
   return r;
 }
 
+struct FnvPlan {
+  uint64_t seg_cells, sub_cells;
+  uint32_t nseg;
+};
+
+FnvPlan plan(uint64_t n, int sms) {
+  FnvPlan p;
+  uint64_t want = (uint64_t)sms * 16;  // pass-1 CTAs: 16 per SM (2 warps each)
+  p.seg_cells = (n + want - 1) / want;
+  if (p.seg_cells < 4096)
+    p.seg_cells = 4096;
+  p.nseg = n ? (uint32_t)((n + p.seg_cells - 1) / p.seg_cells) : 0;
+  p.sub_cells = (p.seg_cells + kSubSegs - 1) / kSubSegs;
+  return p;
+}
+
 }  // namespace
+
+size_t fnv_scratch_bytes(uint64_t n, int sms) {
+  FnvPlan p = plan(n, sms);
+  size_t rec = (size_t)p.nseg * kSubSegs * kP1Threads * sizeof(uint32_t);
+  size_t L = (size_t)p.nseg * 256;
+  size_t C = (size_t)p.nseg * kSubSegs * sizeof(uint64_t);
+  return C + rec + L + p.nseg + 1 + 64;
+}
 
 // Enqueues the device FNV of `n` cells onto `stream`; the 64-bit hash lands
 // in device memory `out`. Scratch: fnv_scratch_bytes(n, sms).
-uint64_t fnv_segment_cells(uint64_t n, int sms) {
-  uint64_t want = (uint64_t)sms * 8;  // one wave of 8 CTAs per SM
-  uint64_t seg = (n + want - 1) / want;
-  return seg < 256 ? 256 : seg;
-}
-
-size_t fnv_scratch_bytes(uint64_t n, int sms) {
-  uint64_t seg = fnv_segment_cells(n, sms);
-  uint64_t nseg = n ? (n + seg - 1) / seg : 0;
-  return nseg * 256 * (sizeof(uint64_t) + 1) + 16;
-}
-
 int fnv_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out, void* scratch,
                int sms, void* stream, int* launches) {
-  cudaStream_t s = (cudaStream_t)stream;
-  uint64_t seg = fnv_segment_cells(n, sms);
-  uint64_t nseg = n ? (n + seg - 1) / seg : 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  FnvPlan p = plan(n, sms);
   uint64_t* C = static_cast<uint64_t*>(scratch);
-  uint8_t* L = reinterpret_cast<uint8_t*>(C + nseg * 256);
+  uint32_t* rec = reinterpret_cast<uint32_t*>(C + (size_t)p.nseg * kSubSegs);
+  uint8_t* L = reinterpret_cast<uint8_t*>(rec + (size_t)p.nseg * kSubSegs * kP1Threads);
+  uint8_t* lin = L + (size_t)p.nseg * 256;
   int k = 0;
-  if (nseg) {
-    fnv_segments_kernel<<<(unsigned)nseg, kFnvThreads, 0, s>>>(cells, n, seg, L, C);
+  if (p.nseg) {
+    fnv_lowbyte_kernel<<<p.nseg, kP1Threads, 0, st>>>(cells, n, p.seg_cells, p.sub_cells, rec,
+                                                       L);
     ++k;
   }
-  uint64_t last = nseg ? n - (nseg - 1) * seg : 0;
-  fnv_walk_kernel<<<1, 1, 0, s>>>(L, C, nseg, pow_mod64(kFnvPrime, 4 * seg),
-                                  pow_mod64(kFnvPrime, 4 * last), seed, out);
+  fnv_scan_kernel<<<1, 256, 0, st>>>(L, p.nseg, seed, lin);
+  ++k;
+  if (p.nseg) {
+    uint64_t threads = (uint64_t)p.nseg * kSubSegs;
+    fnv_affine_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+        cells, n, p.seg_cells, p.sub_cells, p.nseg, rec, lin, C);
+    ++k;
+  }
+  fnv_fold_kernel<<<1, 1, 0, st>>>(C, n, p.seg_cells, p.sub_cells, p.nseg,
+                                   pow_mod64(kFnvPrime, 4 * p.sub_cells), seed, lin, out);
   ++k;
   if (launches)
     *launches = k;

@@ -32,7 +32,6 @@ int sgemm_tc_splits(int M, int N, int K, int sms);
 size_t sgemm_tc_work_bytes(int M, int N, int K, int sms);
 
 // Device FNV-1a-64 over u32 cells hashed big-endian (fnv.cu).
-uint64_t fnv_segment_cells(uint64_t n, int sms);
 size_t fnv_scratch_bytes(uint64_t n, int sms);
 int fnv_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out,
                void* scratch, int sms, void* stream, int* launches);
