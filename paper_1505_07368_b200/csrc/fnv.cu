@@ -12,16 +12,17 @@
 //
 // Three passes:
 //  1. low bytes only. A segment's 256 possible incoming low bytes are
-//     tracked at once, four per 32-bit register (byte-lane SIMD: one
-//     multiply per pair of lanes, 7 instructions per byte per 4 lanes), and
-//     the lanes are recorded at every sub-segment boundary;
+//     tracked at once by one warp, two per 32-bit register (16-bit slots:
+//     one LOP3 + one IMAD advance two lanes by a byte), and recorded at
+//     every sub-segment boundary;
 //  2. one thread walks the segments' low-byte permutations from the seed,
 //     giving each segment its real incoming low byte;
 //  3. one thread per sub-segment runs the full recurrence from its real
-//     incoming low byte (read from the pass-1 record) and returns the affine
-//     offset C_j; a final thread folds u = u * p^(n_j) + C_j in order.
-// Work is ~1.75x the serial byte count in pass 1 (256 lanes, 4 per slot) plus
-// 1x in pass 3, all parallel; the result is bit-identical to the serial loop.
+//     incoming low byte (read from the pass-1 record); each warp composes its
+//     32 affine maps into the segment's, and a final thread folds the
+//     segments in order.
+// All passes are parallel except two short sequential walks over the
+// segments; the result is bit-identical to the serial loop.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -30,19 +31,19 @@ namespace cafxg {
 namespace {
 
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
-constexpr int kP1Threads = 64;   // 64 threads x 4 byte lanes = 256 low bytes
-constexpr int kSubSegs = 32;     // sub-segments per segment (pass 3 threads)
-constexpr int kTile = 4096;      // cells staged in smem per round (pass 1)
-
-__device__ __forceinline__ uint32_t rep_byte(uint32_t x, int sh) {
-  // byte (x >> sh) & 255 replicated into all four lanes
-  return __byte_perm(x, 0, (sh >> 3) * 0x1111);
-}
+constexpr int kP1Threads = 32;   // one warp per segment: 32 threads x 8 low bytes
+constexpr int kSubSegs = 32;     // sub-segments per segment (pass 3: one warp)
+constexpr int kTile = 1024;      // cells staged in smem per round (pass 1)
+constexpr int kRecWords = 64;    // 256 low bytes = 64 packed words per record
 
 // Pass 1: per segment, the low byte after every sub-segment for all 256
-// incoming low bytes. rec[(seg * kSubSegs + j) * 64 + thread] holds lanes
-// 4*thread .. 4*thread+3 at the START of sub-segment j; L[seg * 256 + v] is
-// the outgoing low byte for incoming v.
+// incoming low bytes. Thread t tracks incoming values 8t..8t+7 in four
+// registers, two 16-bit slots each (value in bits 0-7 / 16-23): one step is
+// r = ((r ^ b) & 0x00ff00ff) * 179 -- one LOP3 and one IMAD per two lanes
+// (179 * 255 < 2^16, so the slots never interfere; the next step's mask
+// drops the product's high byte). rec[(seg * kSubSegs + j) * 64 + w] holds
+// low bytes 4w..4w+3 at the START of sub-segment j; L[seg * 256 + v] is the
+// outgoing low byte for incoming v.
 __global__ void __launch_bounds__(kP1Threads)
     fnv_lowbyte_kernel(const uint32_t* __restrict__ cells, uint64_t n, uint64_t seg_cells,
                        uint64_t sub_cells, uint32_t* __restrict__ rec,
@@ -51,40 +52,46 @@ __global__ void __launch_bounds__(kP1Threads)
   const uint64_t begin = (uint64_t)blockIdx.x * seg_cells;
   const uint64_t end = begin + seg_cells < n ? begin + seg_cells : n;
   const uint32_t tid = threadIdx.x;
-  // lanes: incoming low bytes 4*tid + {0,1,2,3}
-  uint32_t w = (4 * tid) | ((4 * tid + 1) << 8) | ((4 * tid + 2) << 16) | ((4 * tid + 3) << 24);
-  uint32_t* myrec = rec + (size_t)blockIdx.x * kSubSegs * kP1Threads + tid;
+  uint32_t r[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    r[k] = (8 * tid + 2 * k) | ((8 * tid + 2 * k + 1) << 16);
+  uint32_t* myrec = rec + (size_t)blockIdx.x * kSubSegs * kRecWords + 2 * tid;
+  auto record = [&](uint32_t j) {
+    // low bytes of the slots, packed in incoming-value order
+    myrec[(size_t)j * kRecWords] = __byte_perm(r[0], r[1], 0x6420);
+    myrec[(size_t)j * kRecWords + 1] = __byte_perm(r[2], r[3], 0x6420);
+  };
   uint64_t next_rec = begin;  // cell index of the next sub-segment start
   uint32_t j = 0;
   for (uint64_t base = begin; base < end; base += kTile) {
     const uint32_t cnt = end - base < (uint64_t)kTile ? (uint32_t)(end - base) : kTile;
-    __syncthreads();
+    __syncwarp();
     for (uint32_t i = tid; i < cnt; i += kP1Threads)
       tile[i] = __ldg(cells + base + i);
-    __syncthreads();
+    __syncwarp();
     for (uint32_t i = 0; i < cnt; ++i) {
       if (base + i == next_rec) {
-        myrec[(size_t)j * kP1Threads] = w;
+        record(j);
         ++j;
         next_rec += sub_cells;
       }
       const uint32_t x = tile[i];  // broadcast read
 #pragma unroll
-      for (int sh = 24; sh >= 0; sh -= 8) {
-        const uint32_t bb = rep_byte(x, sh);
-        const uint32_t e = ((w ^ bb) & 0x00ff00ffu) * 179u;           // lanes 0, 2
-        const uint32_t o = (((w >> 8) ^ bb) & 0x00ff00ffu) * 45824u;  // lanes 1, 3 (179 << 8)
-        w = (e & 0x00ff00ffu) | (o & 0xff00ff00u);
+      for (int sh = 3; sh >= 0; --sh) {
+        // byte sh of x into both slots: selector picks x.byte[sh] / zero
+        const uint32_t bb = __byte_perm(x, 0, sh | (4 << 4) | (sh << 8) | (4 << 12));
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          r[k] = ((r[k] ^ bb) & 0x00ff00ffu) * 179u;
       }
     }
   }
   for (; j < kSubSegs; ++j)  // empty trailing sub-segments start where we end
-    myrec[(size_t)j * kP1Threads] = w;
-  uint8_t* out = L + (size_t)blockIdx.x * 256 + 4 * tid;
-  out[0] = (uint8_t)w;
-  out[1] = (uint8_t)(w >> 8);
-  out[2] = (uint8_t)(w >> 16);
-  out[3] = (uint8_t)(w >> 24);
+    record(j);
+  uint32_t* out = reinterpret_cast<uint32_t*>(L + (size_t)blockIdx.x * 256) + 2 * tid;
+  out[0] = __byte_perm(r[0], r[1], 0x6420);
+  out[1] = __byte_perm(r[2], r[3], 0x6420);
 }
 
 // Pass 2: the real incoming low byte of every segment, and the final one.
@@ -114,15 +121,30 @@ __global__ void __launch_bounds__(256)
     lin[nseg] = (uint8_t)l;
 }
 
-// Pass 3: thread = (segment, sub-segment): full recurrence from the real
-// incoming low byte; C[j] = affine offset of the sub-segment.
+__device__ __forceinline__ uint64_t pow_dev(uint64_t b, uint64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1)
+      r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+
+// Pass 3: thread = (segment, sub-segment) -- a warp is one segment: full
+// recurrence from the real incoming low byte gives the sub-segment's affine
+// map u -> p^(4 len) u + c; the warp composes its 32 maps in order
+// ((P1,C1) then (P2,C2) = (P1 P2, C1 P2 + C2)) and lane 0 stores the
+// segment's (P, C).
 __global__ void __launch_bounds__(256)
     fnv_affine_kernel(const uint32_t* __restrict__ cells, uint64_t n, uint64_t seg_cells,
                       uint64_t sub_cells, uint32_t nseg, const uint32_t* __restrict__ rec,
-                      const uint8_t* __restrict__ lin, uint64_t* __restrict__ C) {
+                      const uint8_t* __restrict__ lin, uint64_t* __restrict__ SP,
+                      uint64_t* __restrict__ SC) {
   const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (uint64_t)nseg * kSubSegs)
-    return;
+    return;  // whole warps only: nseg * 32 threads
   const uint32_t s = (uint32_t)(g / kSubSegs), j = (uint32_t)(g % kSubSegs);
   const uint64_t seg_begin = (uint64_t)s * seg_cells;
   const uint64_t seg_end = seg_begin + seg_cells < n ? seg_begin + seg_cells : n;
@@ -131,7 +153,7 @@ __global__ void __launch_bounds__(256)
   if (b > seg_end) b = seg_end;
   if (e > seg_end) e = seg_end;
   const uint32_t v = lin[s];
-  const uint32_t word = rec[((size_t)s * kSubSegs + j) * kP1Threads + (v >> 2)];
+  const uint32_t word = rec[((size_t)s * kSubSegs + j) * kRecWords + (v >> 2)];
   uint32_t l = (word >> (8 * (v & 3))) & 255u;
   uint64_t c = 0;
   for (uint64_t i = b; i < e; ++i) {
@@ -144,40 +166,30 @@ __global__ void __launch_bounds__(256)
       c = c * kFnvPrime + (((uint64_t)t << 32) + (m >> 8));
     }
   }
-  C[g] = c;
-}
-
-__device__ uint64_t pow_dev(uint64_t b, uint64_t e) {
-  uint64_t r = 1;
-  while (e) {
-    if (e & 1)
-      r *= b;
-    b *= b;
-    e >>= 1;
-  }
-  return r;
-}
-
-// Fold: u = u * p^(4 n_j) + C_j over all sub-segments in order.
-__global__ void fnv_fold_kernel(const uint64_t* __restrict__ C, uint64_t n, uint64_t seg_cells,
-                                uint64_t sub_cells, uint32_t nseg, uint64_t p_sub,
-                                uint64_t seed, const uint8_t* __restrict__ lin,
-                                uint64_t* out) {
-  uint64_t u = seed >> 8;
-  for (uint32_t s = 0; s < nseg; ++s) {
-    const uint64_t seg_begin = (uint64_t)s * seg_cells;
-    const uint64_t seg_end = seg_begin + seg_cells < n ? seg_begin + seg_cells : n;
-    for (uint32_t j = 0; j < kSubSegs; ++j) {
-      uint64_t b = seg_begin + (uint64_t)j * sub_cells, e = b + sub_cells;
-      if (b > seg_end) b = seg_end;
-      if (e > seg_end) e = seg_end;
-      const uint64_t len = e - b;
-      if (len == 0)
-        continue;
-      const uint64_t pn = len == sub_cells ? p_sub : pow_dev(kFnvPrime, 4 * len);
-      u = u * pn + C[(size_t)s * kSubSegs + j];
+  uint64_t P = pow_dev(kFnvPrime, 4 * (e - b));
+  const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint64_t P2 = __shfl_down_sync(0xffffffffu, P, off);
+    const uint64_t C2 = __shfl_down_sync(0xffffffffu, c, off);
+    if (lane + off < 32 && (lane & (2 * off - 1)) == 0) {
+      c = c * P2 + C2;
+      P = P * P2;
     }
   }
+  if (lane == 0) {
+    SP[s] = P;
+    SC[s] = c;
+  }
+}
+
+// Fold: u = u * P_s + C_s over the segments in order.
+__global__ void fnv_fold_kernel(const uint64_t* __restrict__ SP, const uint64_t* __restrict__ SC,
+                                uint32_t nseg, uint64_t seed, const uint8_t* __restrict__ lin,
+                                uint64_t* out) {
+  uint64_t u = seed >> 8;
+  for (uint32_t s = 0; s < nseg; ++s)
+    u = u * SP[s] + SC[s];
   *out = (u << 8) | lin[nseg];
 }
 
@@ -199,7 +211,7 @@ struct FnvPlan {
 
 FnvPlan plan(uint64_t n, int sms) {
   FnvPlan p;
-  uint64_t want = (uint64_t)sms * 16;  // pass-1 CTAs: 16 per SM (2 warps each)
+  uint64_t want = (uint64_t)sms * 32;  // pass-1 CTAs: 32 one-warp CTAs per SM
   p.seg_cells = (n + want - 1) / want;
   if (p.seg_cells < 4096)
     p.seg_cells = 4096;
@@ -212,10 +224,10 @@ FnvPlan plan(uint64_t n, int sms) {
 
 size_t fnv_scratch_bytes(uint64_t n, int sms) {
   FnvPlan p = plan(n, sms);
-  size_t rec = (size_t)p.nseg * kSubSegs * kP1Threads * sizeof(uint32_t);
+  size_t rec = (size_t)p.nseg * kSubSegs * kRecWords * sizeof(uint32_t);
   size_t L = (size_t)p.nseg * 256;
-  size_t C = (size_t)p.nseg * kSubSegs * sizeof(uint64_t);
-  return C + rec + L + p.nseg + 1 + 64;
+  size_t PC = (size_t)p.nseg * 2 * sizeof(uint64_t);
+  return PC + rec + L + p.nseg + 1 + 64;
 }
 
 // Enqueues the device FNV of `n` cells onto `stream`; the 64-bit hash lands
@@ -224,9 +236,10 @@ int fnv_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out, 
                int sms, void* stream, int* launches) {
   cudaStream_t st = (cudaStream_t)stream;
   FnvPlan p = plan(n, sms);
-  uint64_t* C = static_cast<uint64_t*>(scratch);
-  uint32_t* rec = reinterpret_cast<uint32_t*>(C + (size_t)p.nseg * kSubSegs);
-  uint8_t* L = reinterpret_cast<uint8_t*>(rec + (size_t)p.nseg * kSubSegs * kP1Threads);
+  uint64_t* SP = static_cast<uint64_t*>(scratch);
+  uint64_t* SC = SP + p.nseg;
+  uint32_t* rec = reinterpret_cast<uint32_t*>(SC + p.nseg);
+  uint8_t* L = reinterpret_cast<uint8_t*>(rec + (size_t)p.nseg * kSubSegs * kRecWords);
   uint8_t* lin = L + (size_t)p.nseg * 256;
   int k = 0;
   if (p.nseg) {
@@ -239,11 +252,10 @@ int fnv_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out, 
   if (p.nseg) {
     uint64_t threads = (uint64_t)p.nseg * kSubSegs;
     fnv_affine_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
-        cells, n, p.seg_cells, p.sub_cells, p.nseg, rec, lin, C);
+        cells, n, p.seg_cells, p.sub_cells, p.nseg, rec, lin, SP, SC);
     ++k;
   }
-  fnv_fold_kernel<<<1, 1, 0, st>>>(C, n, p.seg_cells, p.sub_cells, p.nseg,
-                                   pow_mod64(kFnvPrime, 4 * p.sub_cells), seed, lin, out);
+  fnv_fold_kernel<<<1, 1, 0, st>>>(SP, SC, p.nseg, seed, lin, out);
   ++k;
   if (launches)
     *launches = k;
