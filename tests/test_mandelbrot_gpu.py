@@ -234,3 +234,29 @@ def test_run_mandelbrot_on_device(ctx, golden, size, it):
     chk, ms = ctx.run_mandelbrot(size, it)
     assert chk == want
     assert ms > 0
+
+
+def test_concurrent_host_requests(ctx):
+    """Several host threads submitting to one context at once (the C ABI is
+    thread-safe; ctypes releases the GIL for the blocking call)."""
+    import threading
+    descs = [pkg.mandel_desc(-2.0 + 0.01 * k, 1.0, -1.0, 1.0, 400 + 17 * k, 150 + k,
+                             80 + 10 * k, fp64=bool(k & 1)) for k in range(8)]
+    refs = [oracle.tile(d.x0, d.x1, d.y0, d.y1, d.width, d.height, d.max_iter,
+                        fp64=bool(d.precision), centre=True) for d in descs]
+    errors = []
+
+    def worker(k):
+        try:
+            for _ in range(5):
+                out = ctx.mandelbrot(descs[k]).reshape(descs[k].height, descs[k].width)
+                if not np.array_equal(out, refs[k]):
+                    errors.append(k)
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
