@@ -66,3 +66,19 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(b.MandelDesc) == 4 * 8 + 10 * 4 + 8
     assert ctypes.sizeof(b.SgemmDesc) == 32
     assert ctypes.sizeof(b.Stats) == 48
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/cafxg.h compiles as C99 and a C program links libcafxg.so."""
+    import paper_1505_07368_b200.cafxg as b
+    exe = tmp_path / "abi_check"
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "c", "abi_check.c"),
+                        "-L", os.path.dirname(b.LIB_PATH), "-lcafxg",
+                        f"-Wl,-rpath,{os.path.dirname(b.LIB_PATH)}", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    import torch
+    if not torch.cuda.is_available():
+        out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+        assert out.returncode == 0 and "spawn_error" in out.stdout

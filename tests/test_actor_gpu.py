@@ -143,3 +143,18 @@ def test_sync_waits_for_actor_requests(ctx):
     ctx.sync()
     assert all(f.done() for f in futs)
     a.release()
+
+
+def test_c_program_through_the_abi(tmp_path):
+    """tests/c/abi_check.c: run_mandelbrot golden + one actor request, from C."""
+    import os
+    import subprocess
+    import paper_1505_07368_b200.cafxg as b
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "abi_check"
+    subprocess.check_call(["gcc", "-std=c99", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "tests", "c", "abi_check.c"),
+                           "-L", os.path.dirname(b.LIB_PATH), "-lcafxg",
+                           f"-Wl,-rpath,{os.path.dirname(b.LIB_PATH)}", "-o", str(exe)])
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "C ABI OK" in r.stdout, r.stdout + r.stderr
