@@ -257,8 +257,14 @@ struct cafxg_ctx {
   bool cb_stop = false;
   std::vector<std::thread> cb_threads;
   bool force_exact = false;  // CAFXG_EXACT_STEP=1: always the 8-op step
+  // CAFXG_VIRTUAL_DEVICES=V: V context devices on one physical GPU (own
+  // streams, scheduler ring and completion thread each) so the multi-device
+  // split/join logic runs on a single-GPU box; B is then replicated by
+  // device-to-device copies instead of NCCL (which rejects duplicate GPUs)
+  bool virtual_devs = false;
   // NCCL communicators for multi-device sgemm (one per device)
   std::mutex nccl_mu;
+  bool nccl_failed = false;
   NcclApi nccl;
   std::vector<ncclComm_t> comms;
 };
@@ -853,6 +859,11 @@ static int ensure_nccl(cafxg_ctx* ctx) {
   std::lock_guard<std::mutex> g(ctx->nccl_mu);
   if (!ctx->comms.empty())
     return CAFXG_OK;
+  if (ctx->virtual_devs)
+    return fail(CAFXG_E_CONFIG, "virtual devices share one GPU; NCCL not used");
+  if (ctx->nccl_failed)
+    return fail(CAFXG_E_SPAWN, "NCCL unavailable (first attempt failed)");
+  ctx->nccl_failed = true;  // cleared on success
   if (!ctx->nccl.load())
     return fail(CAFXG_E_SPAWN, "libnccl.so.2 not loadable");
   std::vector<int> ords;
@@ -864,6 +875,7 @@ static int ensure_nccl(cafxg_ctx* ctx) {
     return fail(CAFXG_E_SPAWN, "ncclCommInitAll failed: %s",
                 ctx->nccl.GetErrorString ? ctx->nccl.GetErrorString(r) : "?");
   ctx->comms = comms;
+  ctx->nccl_failed = false;
   return CAFXG_OK;
 }
 
@@ -983,9 +995,13 @@ static int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
   size_t G = ctx->devs.size();
   // devices used: only split when every block gets rows and K divides evenly
   size_t use = 1;
+  bool nccl = false;
   if (G > 1 && g.M >= G * 128 && g.K % G == 0 && g.ldb == g.N) {
-    if (ensure_nccl(ctx) == CAFXG_OK)
-      use = G;
+    use = G;
+    // NCCL all-gather over NVLink; without it (virtual devices, or NCCL not
+    // loadable) the slices are replicated by peer copies on the copy engines
+    nccl = ensure_nccl(ctx) == CAFXG_OK;
+    clear_last_error();
   }
   Join* join = new Join;
   join->done = done;
@@ -1014,7 +1030,47 @@ static int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
       status = cuda_status(cudaGetLastError(), "sgemm: B upload");
     ctx->st_h2d += kn * g.ldb * 4;
   }
-  if (status == CAFXG_OK && use > 1) {
+  if (status == CAFXG_OK && use > 1 && !nccl) {
+    // each device pulls the other devices' slices once they are uploaded
+    std::vector<cudaEvent_t> up(use, nullptr);
+    for (size_t k = 0; k < use && status == CAFXG_OK; ++k) {
+      cudaSetDevice(ctx->devs[k]->ordinal);
+      if (cudaEventCreateWithFlags(&up[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventRecord(up[k], ctx->devs[k]->compute) != cudaSuccess)
+        status = cuda_status(cudaGetLastError(), "sgemm: B slice event");
+    }
+    const size_t cnt = (size_t)g.K / use * g.ldb;
+    for (size_t k = 0; k < use && status == CAFXG_OK; ++k) {
+      Device* d = ctx->devs[k].get();
+      cudaSetDevice(d->ordinal);
+      for (size_t j = 0; j < use && status == CAFXG_OK; ++j) {
+        if (j == k)
+          continue;
+        cudaStreamWaitEvent(d->compute, up[j], 0);
+        status = cuda_status(cudaMemcpyPeerAsync(dB[k] + cnt * j, d->ordinal, dB[j] + cnt * j,
+                                                 ctx->devs[j]->ordinal, cnt * 4, d->compute),
+                             "sgemm: B slice peer copy");
+      }
+    }
+    // a device's own slice buffer must outlive the peers' reads of it
+    std::vector<cudaEvent_t> pulled(use, nullptr);
+    for (size_t k = 0; k < use && status == CAFXG_OK; ++k) {
+      cudaSetDevice(ctx->devs[k]->ordinal);
+      cudaEventCreateWithFlags(&pulled[k], cudaEventDisableTiming);
+      cudaEventRecord(pulled[k], ctx->devs[k]->compute);
+    }
+    for (size_t k = 0; k < use && status == CAFXG_OK; ++k) {
+      cudaSetDevice(ctx->devs[k]->ordinal);
+      for (size_t j = 0; j < use; ++j)
+        if (j != k)
+          cudaStreamWaitEvent(ctx->devs[k]->compute, pulled[j], 0);
+    }
+    for (auto* v : {&up, &pulled})
+      for (auto ev : *v)
+        if (ev)
+          cudaEventDestroy(ev);
+  }
+  if (status == CAFXG_OK && use > 1 && nccl) {
     ctx->nccl.GroupStart();
     for (size_t k = 0; k < use; ++k) {
       size_t cnt = (size_t)g.K / use * g.ldb;
@@ -1472,9 +1528,17 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
                   e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
     }
     auto ctx = std::make_unique<cafxg_ctx>();
-    for (int i = 0; i < n && i < 64; ++i) {
-      if (device_mask && !(device_mask >> i & 1))
-        continue;
+    std::vector<int> ords;
+    for (int i = 0; i < n && i < 64; ++i)
+      if (!device_mask || (device_mask >> i & 1))
+        ords.push_back(i);
+    const char* vd = getenv("CAFXG_VIRTUAL_DEVICES");
+    int vcount = vd ? atoi(vd) : 0;
+    if (vcount > 1 && ords.size() == 1) {
+      ords.assign(std::min(vcount, 64), ords[0]);
+      ctx->virtual_devs = true;
+    }
+    for (int i : ords) {
       auto d = std::make_unique<Device>();
       d->ordinal = i;
       CAFXG_CUDA_TRY(cudaSetDevice(i));

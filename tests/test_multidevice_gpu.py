@@ -1,0 +1,130 @@
+"""GPU: the multi-device paths of one context on a one-GPU box.
+
+CAFXG_VIRTUAL_DEVICES=V opens V context devices on the same physical GPU,
+each with its own streams, scheduler ring and completion thread, so the
+request splitting and joining that a G-GPU context does runs for real:
+cyclic row bands for Mandelbrot, per-device row blocks of A plus the
+replicated B for sgemm (peer copies stand in for the NCCL all-gather, which
+rejects duplicate GPUs), the in-order FNV chain of run_mandelbrot and the
+dispatcher's device choice for actor batches."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+V = 3
+
+
+@pytest.fixture(scope="module")
+def vctx():
+    os.environ["CAFXG_VIRTUAL_DEVICES"] = str(V)
+    try:
+        c = pkg.Context(device_mask=1)
+    finally:
+        del os.environ["CAFXG_VIRTUAL_DEVICES"]
+    yield c
+    c.close()
+
+
+def test_device_count(vctx):
+    assert vctx.device_count == V
+
+
+def test_mandelbrot_bands_over_devices(vctx):
+    # cfg1 geometry: every row band dealt cyclically over the 3 devices
+    d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)
+    out = vctx.mandelbrot(d).reshape(1080, 1920)
+    ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100, fp64=False, centre=True)
+    assert np.array_equal(out, ref), int((out != ref).sum())
+
+
+def test_multi_tile_request_over_devices(vctx):
+    rng = np.random.default_rng(21)
+    tiles, refs, off = [], [], 0
+    for _ in range(7):
+        w, h = int(rng.integers(1, 400)), int(rng.integers(1, 300))
+        x0, y0 = float(rng.uniform(-2.0, 0.3)), float(rng.uniform(-1.1, 0.9))
+        span = float(10 ** rng.uniform(-3, 0.3))
+        fp64 = bool(rng.integers(0, 2))
+        t = pkg.mandel_desc(x0, x0 + span, y0, y0 + span * h / w, w, h, 200, fp64=fp64)
+        t.out_offset = off
+        off += w * h
+        tiles.append(t)
+        refs.append(oracle.tile(t.x0, t.x1, t.y0, t.y1, w, h, 200, fp64=fp64, centre=True))
+    out = vctx.mandelbrot(tiles, np.zeros(off, np.uint32))
+    for t, r in zip(tiles, refs):
+        got = out[t.out_offset:t.out_offset + t.width * t.height].reshape(t.height, t.width)
+        assert np.array_equal(got, r)
+
+
+@pytest.mark.parametrize("size,it", [(256, 100), (1024, 500)])
+def test_run_mandelbrot_chain(vctx, golden, size, it):
+    """Blocks on different devices, FNV chained block to block in row order."""
+    want = int([g for g in golden["run_mandelbrot"]
+                if g["size"] == size and g["max_iter"] == it][0]["checksum"])
+    h, _ = vctx.run_mandelbrot(size, it)
+    assert h == want
+
+
+@pytest.mark.parametrize("M,N,K", [(768, 512, 384),      # one launch per device
+                                   (3072, 1024, 768),    # per-device H2D/GEMM/D2H pipeline
+                                   (3 * 128, 256, 3)])    # smallest split
+def test_sgemm_row_blocks(vctx, M, N, K):
+    A = oracle.fill_uniform(M * K, 31).reshape(M, K)
+    B = oracle.fill_uniform(K * N, 32).reshape(K, N)
+    before = vctx.stats()
+    C = vctx.sgemm(A, B)
+    after = vctx.stats()
+    # B crossed PCIe once in total (1/V per device), A once
+    assert after.h2d_bytes - before.h2d_bytes == (M * K + K * N) * 4
+    rows = np.unique(np.concatenate([np.arange(0, M, 61), [M // V - 1, M // V, M - 1]]))
+    R = oracle.sgemm_ref_rows(A, B, rows.astype(np.uint32), N, K)
+    assert oracle.sgemm_rel_err(C, R, rows.astype(np.uint32), N) <= 1e-5
+
+
+def test_sgemm_unsplit_shapes(vctx):
+    # K not divisible by the device count: one device does the whole product
+    M, N, K = 512, 128, 100
+    A = oracle.fill_uniform(M * K, 33).reshape(M, K)
+    B = oracle.fill_uniform(K * N, 34).reshape(K, N)
+    C = vctx.sgemm(A, B)
+    rows = np.arange(0, M, 17, dtype=np.uint32)
+    R = oracle.sgemm_ref_rows(A, B, rows, N, K)
+    assert oracle.sgemm_rel_err(C, R, rows, N) <= 1e-5
+
+
+def test_actor_batches_over_devices(vctx):
+    a = vctx.spawn("mandelbrot")
+    rng = np.random.default_rng(8)
+    descs, outs, futs = [], [], []
+    for _ in range(60):
+        kx, ky = int(rng.integers(0, 1472)), int(rng.integers(0, 960))
+        x0, y0 = -2.0 + kx / 512, -1.0 + ky / 512
+        d = pkg.mandel_desc(x0, x0 + 0.125, y0, y0 + 0.125, 64, 64, 150, fp64=True)
+        o = np.zeros(4096, np.uint32)
+        futs.append(a.request([(pkg.MandelDesc * 1)(d)], o))
+        descs.append(d)
+        outs.append(o)
+    for f in futs:
+        f.result(timeout=120)
+    for d, o in zip(descs, outs):
+        ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, 64, 64, 150, fp64=True, centre=True)
+        assert np.array_equal(o.reshape(64, 64), ref)
+    a.release()
+
+
+def test_matrix_multiply_actor_over_devices(vctx):
+    size = 3 * 256
+    a = vctx.spawn("matrix_multiply", (size, size))
+    A = oracle.fill_uniform(size * size, 41)
+    B = oracle.fill_uniform(size * size, 42)
+    C = np.zeros(size * size, dtype=np.float32)
+    a.request([A, B], C).result(timeout=60)
+    rows = np.arange(0, size, 13, dtype=np.uint32)
+    R = oracle.sgemm_ref_rows(A.reshape(size, size), B.reshape(size, size), rows, size, size)
+    assert oracle.sgemm_rel_err(C.reshape(size, size), R, rows, size) <= 1e-5
+    a.release()
