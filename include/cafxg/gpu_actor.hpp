@@ -34,6 +34,8 @@
 #include <cstring>
 #include <initializer_list>
 #include <memory>
+#include <new>
+#include <type_traits>
 #include <string>
 #include <utility>
 #include <vector>
@@ -51,8 +53,56 @@
 
 namespace cafxg {
 
-using f32vec = std::vector<float>;
-using u32vec = std::vector<uint32_t>;
+/// Allocator of the buffer types. Default-constructed it is the plain heap
+/// (wire decoding, user-built requests). Bound to a context it takes memory
+/// from the context's pinned, device-mapped pool (cafxg_host_alloc) and
+/// leaves elements uninitialised: the adapter sizes reply vectors with it, so
+/// the kernel writes counts straight into the vector the reply message owns
+/// (no zero-fill, no staging copy). Such a vector must not outlive its
+/// context. Users may bind it too, to make request payloads DMA-able.
+template <class T>
+struct host_allocator {
+  using value_type = T;
+  using propagate_on_container_copy_assignment = std::true_type;
+  using propagate_on_container_move_assignment = std::true_type;
+  using propagate_on_container_swap = std::true_type;
+  cafxg_ctx* ctx = nullptr;
+
+  host_allocator() noexcept = default;
+  explicit host_allocator(cafxg_ctx* c) noexcept : ctx(c) {}
+  template <class U>
+  host_allocator(const host_allocator<U>& o) noexcept : ctx(o.ctx) {}
+
+  T* allocate(size_t n) {
+    if (!ctx)
+      return std::allocator<T>{}.allocate(n);
+    void* p = nullptr;
+    if (cafxg_host_alloc(ctx, n * sizeof(T), &p) != CAFXG_OK)
+      throw std::bad_alloc{};
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t n) noexcept {
+    if (!ctx)
+      std::allocator<T>{}.deallocate(p, n);
+    else
+      cafxg_host_free(ctx, p);
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    if constexpr (sizeof...(Args) == 0) {
+      if (ctx) {
+        ::new (static_cast<void*>(p)) U;  // default-init: the device fills it
+        return;
+      }
+    }
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+  template <class U>
+  bool operator==(const host_allocator<U>& o) const noexcept { return ctx == o.ctx; }
+};
+
+using f32vec = std::vector<float, host_allocator<float>>;
+using u32vec = std::vector<uint32_t, host_allocator<uint32_t>>;
 
 /// Request payload of the "mandelbrot" kernel: one or more tiles; the reply
 /// is their counts packed in order.
@@ -154,8 +204,9 @@ inline void register_types(cafx::type_registry& reg = cafx::type_registry::globa
 /// A cafx actor whose behaviour is one sm_100a kernel.
 class gpu_actor final : public cafx::abstract_actor {
  public:
-  gpu_actor(cafx::actor_system& sys, cafxg_actor* backend, std::string kernel)
+  gpu_actor(cafx::actor_system& sys, cafxg_ctx* ctx, cafxg_actor* backend, std::string kernel)
       : cafx::abstract_actor(&sys, cafx::actor_addr{sys.node(), sys.next_actor_id()}),
+        ctx_(ctx),
         backend_(backend),
         kernel_(std::move(kernel)) {}
 
@@ -201,13 +252,21 @@ class gpu_actor final : public cafx::abstract_actor {
     size_t reply = cafxg_actor_reply_bytes(backend_, in, in_bytes, n_in);
     if (reply == 0)
       return fail(*env, static_cast<cafx::errc>(CAFXG_E_TYPE_MISMATCH), cafxg_last_error());
+    // the reply vector lives in the context's pinned pool: the device writes
+    // into it directly and it moves into the reply message unchanged
     void* out;
-    if (kernel_ == "mandelbrot") {
-      job->counts.resize(reply / sizeof(uint32_t));
-      out = job->counts.data();
-    } else {
-      job->floats.resize(reply / sizeof(float));
-      out = job->floats.data();
+    try {
+      if (kernel_ == "mandelbrot") {
+        job->counts = u32vec(host_allocator<uint32_t>{ctx_});
+        job->counts.resize(reply / sizeof(uint32_t));
+        out = job->counts.data();
+      } else {
+        job->floats = f32vec(host_allocator<float>{ctx_});
+        job->floats.resize(reply / sizeof(float));
+        out = job->floats.data();
+      }
+    } catch (const std::bad_alloc&) {
+      return fail(*env, cafx::errc::config_error, "pinned reply allocation failed");
     }
     job->env = std::move(env);  // keeps the request payload alive
     int s = cafxg_actor_enqueue(backend_, in, in_bytes, n_in, out, reply, &gpu_actor::on_done,
@@ -273,6 +332,7 @@ class gpu_actor final : public cafx::abstract_actor {
     home_system().unregister_actor(address().id);
   }
 
+  cafxg_ctx* ctx_;
   cafxg_actor* backend_;
   std::string kernel_;
   std::atomic<bool> quitting_{false};
@@ -290,7 +350,7 @@ inline cafx::actor spawn_gpu(cafx::actor_system& sys, cafxg_ctx* ctx,
   int s = cafxg_spawn(ctx, kernel.c_str(), d.data(), d.size(), &h);
   if (s != CAFXG_OK)
     throw cafx::failure{static_cast<cafx::errc>(s), cafxg_last_error()};
-  auto ptr = cafx::make_counted<gpu_actor>(sys, h, kernel);
+  auto ptr = cafx::make_counted<gpu_actor>(sys, ctx, h, kernel);
   sys.register_actor(cafx::abstract_actor_ptr{ptr.get()});
   return cafx::actor{cafx::abstract_actor_ptr{ptr.get()}};
 }

@@ -1244,12 +1244,14 @@ static void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* 
                          int status) {
   constexpr size_t kSlice = 1024;
   const size_t n = batch.size();
-  auto run_slice = [ctx, status, bounce](Request* const* rs, size_t cnt, uint64_t pix_off) {
+  // src: the staging buffer to copy replies out of (nullptr: already placed)
+  auto run_slice = [ctx, status](Request* const* rs, size_t cnt, uint64_t pix_off,
+                                 const uint32_t* src) {
     uint64_t o = pix_off;
     for (size_t i = 0; i < cnt; ++i) {
       Request* r = rs[i];
-      if (bounce && status == CAFXG_OK)
-        std::memcpy(r->out, bounce + o, r->pixels * 4);
+      if (src && status == CAFXG_OK)
+        std::memcpy(r->out, src + o, r->pixels * 4);
       o += r->pixels;
       finish_request(r, status, false);
     }
@@ -1257,8 +1259,50 @@ static void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* 
     ctx->actor_open.fetch_sub(cnt);
     ctx->sync_cv.notify_all();
   };
+  uint64_t total_px = 0;
+  for (Request* r : batch)
+    total_px += r->pixels;
+  constexpr uint64_t kPiece = 1 << 20;  // bytes per copy piece
+  if (bounce && status == CAFXG_OK && n <= kSlice && total_px * 4 >= 4 * kPiece &&
+      !ctx->cb_threads.empty()) {
+    // few large pageable replies (e.g. one 1920x1080 image): the staging
+    // copy-out is split into 1 MiB pieces over the callback threads and this
+    // thread; the last piece to finish completes the requests
+    struct Piece {
+      void* dst;
+      const void* src;
+      size_t bytes;
+    };
+    auto pieces = std::make_shared<std::vector<Piece>>();
+    uint64_t o = 0;
+    for (Request* r : batch) {
+      const size_t bytes = r->pixels * 4;
+      for (size_t b = 0; b < bytes; b += kPiece)
+        pieces->push_back({(char*)r->out + b, (const char*)(bounce + o) + b,
+                           std::min<size_t>(kPiece, bytes - b)});
+      o += r->pixels;
+    }
+    auto shared = std::make_shared<std::vector<Request*>>(std::move(batch));
+    auto left = std::make_shared<std::atomic<size_t>>(pieces->size());
+    auto piece_job = [ctx, shared, pieces, left, bounce, run_slice](size_t i) {
+      const Piece& p = (*pieces)[i];
+      std::memcpy(p.dst, p.src, p.bytes);
+      if (left->fetch_sub(1) == 1) {
+        run_slice(shared->data(), shared->size(), 0, nullptr);
+        ctx->pinned.free(bounce);
+      }
+    };
+    {
+      std::lock_guard<std::mutex> g(ctx->cb_mu);
+      for (size_t i = 1; i < pieces->size(); ++i)
+        ctx->cb_q.push_back([piece_job, i] { piece_job(i); });
+    }
+    ctx->cb_cv.notify_all();
+    piece_job(0);
+    return;
+  }
   if (n <= kSlice || ctx->cb_threads.empty()) {
-    run_slice(batch.data(), n, 0);
+    run_slice(batch.data(), n, 0, bounce);
     if (bounce)
       ctx->pinned.free(bounce);
     return;
@@ -1271,7 +1315,7 @@ static void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* 
   for (size_t b = 0; b < n; b += kSlice) {
     size_t cnt = std::min(kSlice, n - b);
     jobs.push_back([ctx, shared, left, b, cnt, pix, bounce, run_slice] {
-      run_slice(shared->data() + b, cnt, pix);
+      run_slice(shared->data() + b, cnt, pix, bounce);
       if (left->fetch_sub(1) == 1 && bounce)
         ctx->pinned.free(bounce);
     });

@@ -17,6 +17,7 @@
 #include "cafx/actor_system.hpp"
 #include "cafx/bench/bench.hpp"
 #include "cafx/detail/fnv.hpp"
+#include "cafx/io/middleman.hpp"
 #include "cafx/scoped_actor.hpp"
 #include "cafxg/gpu_actor.hpp"
 
@@ -227,6 +228,71 @@ int main() {
                                     cafxg::f32vec{1.5f, -0.0f});
       auto back = cafx::deserialize(cafx::serialize(msg));
       check(back == msg, "buffer types serialize/deserialize (BASP payload codecs)");
+    }
+
+    // 7. remote compute actors over BASP: a second
+    //    actor system reaches published GPU actors through the unmodified
+    //    middleman over TCP on 127.0.0.1; requests, replies and error replies
+    //    cross the wire through the registered codecs (middleman.cpp:421-447).
+    {
+      cafx::io::middleman server_mm{sys};
+      cafx::actor_system client_sys;
+      cafx::io::middleman client_mm{client_sys};
+      auto typed = cafxg::spawn_gpu_typed(sys, ctx, "mandelbrot", {});
+      auto port = server_mm.publish(typed, 0);
+      auto remote = client_mm.remote_actor("127.0.0.1", port, typed.interface());
+      cafx::scoped_actor cself{client_sys};
+      std::mt19937_64 rng(80);
+      const int n_remote = 200;
+      int good = 0;
+      auto t0 = std::chrono::steady_clock::now();
+      for (int i = 0; i < n_remote; ++i) {
+        cafxg::mandel_tiles t{{storm_tile(rng), storm_tile(rng)}};
+        auto res = cself->request(remote, cafx::make_message(t), 60s);
+        if (!std::holds_alternative<cafx::message>(res))
+          continue;
+        const auto& counts = std::get<cafx::message>(res).get<cafxg::u32vec>(0);
+        auto e0 = expect_tile(t.tiles[0]), e1 = expect_tile(t.tiles[1]);
+        e0.insert(e0.end(), e1.begin(), e1.end());
+        good += counts == e0;
+      }
+      double ms = std::chrono::duration<double, std::milli>(
+                      std::chrono::steady_clock::now() - t0).count();
+      check(good == n_remote, "remote typed gpu actor over TCP: " + std::to_string(good) + "/" +
+                                  std::to_string(n_remote) + " two-tile requests exact (" +
+                                  std::to_string(ms / n_remote) + " ms/request round trip)");
+
+      const uint32_t n = 256;
+      auto mm = cafxg::spawn_gpu(sys, ctx, "matrix_multiply", {n, n});
+      auto port2 = server_mm.publish(mm, 0);
+      auto rmm = client_mm.remote_actor("127.0.0.1", port2);
+      cafxg::f32vec a(n * n), b(n * n);
+      std::uniform_real_distribution<float> u(-1.0f, 1.0f);
+      for (auto& x : a) x = u(rng);
+      for (auto& x : b) x = u(rng);
+      auto res = cself->request(rmm, cafx::make_message(a, b), 60s);
+      double worst = 1;
+      if (std::holds_alternative<cafx::message>(res)) {
+        const auto& c = std::get<cafx::message>(res).get<cafxg::f32vec>(0);
+        worst = c.size() == n * n ? 0 : 1;
+        for (uint32_t i = 0; c.size() == n * n && i < n; i += 11) {
+          double num = 0, den = 0;
+          for (uint32_t j = 0; j < n; ++j) {
+            double r = 0;
+            for (uint32_t k = 0; k < n; ++k)
+              r += (double)a[i * n + k] * (double)b[k * n + j];
+            num = std::max(num, std::fabs(c[i * n + j] - r));
+            den = std::max(den, std::fabs(r));
+          }
+          worst = std::max(worst, num / den);
+        }
+      }
+      check(worst <= 1e-5, "remote matrix_multiply over TCP within 1e-5 (err " +
+                               std::to_string(worst) + ")");
+      auto bad = cself->request(rmm, cafx::make_message(a), 30s);
+      check(std::holds_alternative<cafx::error>(bad) &&
+                std::get<cafx::error>(bad).code == cafx::errc::interface_mismatch,
+            "remote wrong arity -> error(interface_mismatch) reply over the wire");
     }
     // ~actor_system: hard-kills the gpu actors, which unregister (no hang)
   }

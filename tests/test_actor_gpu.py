@@ -32,6 +32,24 @@ def test_mandelbrot_actor_request(ctx):
 
 
 @pytest.mark.parametrize("pinned", [False, True])
+def test_large_reply(ctx, pinned):
+    """cfg1-sized reply (8.3 MB): pageable replies are copied out of staging in
+    pieces on the callback threads, pinned ones written by the device."""
+    a = ctx.spawn("mandelbrot")
+    d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)
+    desc = (pkg.MandelDesc * 1)(d)
+    ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100, fp64=False, centre=True)
+    for _ in range(3):
+        out = ctx.pinned_empty(1920 * 1080, np.uint32) if pinned else \
+            np.full(1920 * 1080, 7, dtype=np.uint32)
+        a.request([desc], out).result(timeout=60)
+        assert np.array_equal(out.reshape(1080, 1920), ref)
+        if pinned:
+            ctx.pinned_free(out)
+    a.release()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
 def test_request_burst_from_many_clients(ctx, pinned):
     """16 client threads x 40 storm tiles; every reply checked per tile."""
     a = ctx.spawn("mandelbrot")
