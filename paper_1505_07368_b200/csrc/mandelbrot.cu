@@ -121,9 +121,48 @@ constexpr unsigned kFull = 0xffffffffu;
     "+r"(n[2]), "+r"(n[3])                                                     \
   : "l"(cr[0]), "l"(ci[0]), "l"(cr[1]), "l"(ci[1]), "f"(zero), "f"(2.0f)
 
+// ---- unchecked blocks (deferred escape test) --------------------------------
+// The same steps without the per-step test: 6 packed FP ops per pair and
+// step (7 with the reference's 8-op form). Escape is tested once per block;
+// see mandel_deferred_kernel for why that is exact.
+#define CAFXG_F32_FREE_FAST(X, Y, Q, W, C, D, T, V) \
+  "sub.rn.f32x2 " T ", " Q ", " W ";\n\t"           \
+  "add.rn.f32x2 " T ", " T ", " C ";\n\t"           \
+  "mul.rn.f32x2 " V ", " X ", " Y ";\n\t"           \
+  "fma.rn.f32x2 " Y ", " V ", two, " D ";\n\t"      \
+  "mov.b64 " X ", " T ";\n\t"                       \
+  "fma.rn.f32x2 " Q ", " X ", " X ", zz;\n\t"       \
+  "fma.rn.f32x2 " W ", " Y ", " Y ", zz;\n\t"
+
+#define CAFXG_F32_FREE_EXACT(X, Y, Q, W, C, D, T, V) \
+  "sub.rn.f32x2 " T ", " Q ", " W ";\n\t"            \
+  "add.rn.f32x2 " T ", " T ", " C ";\n\t"            \
+  "add.rn.f32x2 " V ", " X ", " X ";\n\t"            \
+  "fma.rn.f32x2 " V ", " V ", " Y ", zz;\n\t"        \
+  "add.rn.f32x2 " Y ", " V ", " D ";\n\t"            \
+  "mov.b64 " X ", " T ";\n\t"                        \
+  "fma.rn.f32x2 " Q ", " X ", " X ", zz;\n\t"        \
+  "fma.rn.f32x2 " W ", " Y ", " Y ", zz;\n\t"
+
+#define CAFXG_F32_FREE2(STEP)                                       \
+  STEP("%0", "%1", "%2", "%3", "%8", "%9", "tA", "vA")              \
+  STEP("%4", "%5", "%6", "%7", "%10", "%11", "tB", "vB")
+
+#define CAFXG_F32_FREE_PROLOGUE                                     \
+  "{\n\t.reg .b64 tA, vA, tB, vB, two, zz;\n\t"                     \
+  "mov.b64 zz, {%12, %12};\n\tmov.b64 two, {%13, %13};\n\t"
+#define CAFXG_F32_FREE_EPILOGUE "}"
+#define CAFXG_F32_FREE_OPERANDS                                             \
+  : "+l"(zr[0]), "+l"(zi[0]), "+l"(zr2[0]), "+l"(zi2[0]), "+l"(zr[1]),      \
+    "+l"(zi[1]), "+l"(zr2[1]), "+l"(zi2[1])                                 \
+  : "l"(cr[0]), "l"(ci[0]), "l"(cr[1]), "l"(ci[1]), "f"(zero), "f"(2.0f)
+
 __device__ __forceinline__ uint64_t set_half(uint64_t v, int hi, float f) {
   uint64_t b = __float_as_uint(f);
   return hi ? ((v & 0xffffffffull) | (b << 32)) : ((v & 0xffffffff00000000ull) | b);
+}
+__device__ __forceinline__ float get_half(uint64_t v, int hi) {
+  return __uint_as_float(hi ? (uint32_t)(v >> 32) : (uint32_t)v);
 }
 
 struct F32Slots {
@@ -153,6 +192,27 @@ struct F32Slots {
       asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP2(CAFXG_F32_EXACT))
                        CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
   }
+  template <int kSteps, bool kExact>
+  __device__ __forceinline__ void run_free() {
+    if constexpr (kSteps == 32 && !kExact)
+      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X32(CAFXG_F32_FREE2(CAFXG_F32_FREE_FAST))
+                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
+    else if constexpr (kSteps == 32 && kExact)
+      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X32(CAFXG_F32_FREE2(CAFXG_F32_FREE_EXACT))
+                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
+    else if constexpr (kSteps == 16 && !kExact)
+      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X16(CAFXG_F32_FREE2(CAFXG_F32_FREE_FAST))
+                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
+    else if constexpr (kSteps == 16 && kExact)
+      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X16(CAFXG_F32_FREE2(CAFXG_F32_FREE_EXACT))
+                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
+    else if constexpr (!kExact)
+      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X4(CAFXG_F32_FREE2(CAFXG_F32_FREE_FAST))
+                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
+    else
+      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X4(CAFXG_F32_FREE2(CAFXG_F32_FREE_EXACT))
+                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
+  }
   // slot s lives in half (s & 1) of pair (s >> 1)
   __device__ __forceinline__ void start(int s, float fr, float fi) {
     const int p = s >> 1, h = s & 1;
@@ -162,6 +222,31 @@ struct F32Slots {
     zi[p] = set_half(zi[p], h, 0.0f);
     zr2[p] = set_half(zr2[p], h, 0.0f);
     zi2[p] = set_half(zi2[p], h, 0.0f);
+  }
+  // resumes slot s at a saved z; the squares are recomputed exactly as the
+  // step forms them (fma(a, a, +0) == fl(a * a))
+  __device__ __forceinline__ void resume(int s, float r, float i, float fr, float fi) {
+    const int p = s >> 1, h = s & 1;
+    cr[p] = set_half(cr[p], h, fr);
+    ci[p] = set_half(ci[p], h, fi);
+    zr[p] = set_half(zr[p], h, r);
+    zi[p] = set_half(zi[p], h, i);
+    zr2[p] = set_half(zr2[p], h, __fmul_rn(r, r));
+    zi2[p] = set_half(zi2[p], h, __fmul_rn(i, i));
+  }
+  __device__ __forceinline__ float zr_of(int s) const { return get_half(zr[s >> 1], s & 1); }
+  __device__ __forceinline__ float zi_of(int s) const { return get_half(zi[s >> 1], s & 1); }
+  __device__ __forceinline__ float cr_of(int s) const { return get_half(cr[s >> 1], s & 1); }
+  __device__ __forceinline__ float ci_of(int s) const { return get_half(ci[s >> 1], s & 1); }
+  // bit s: fl(zr^2 + zi^2) > 4 or NaN (an orbit that overflowed)
+  __device__ __forceinline__ uint32_t escaped() const {
+    uint32_t m = 0;
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) {
+      float S = __fadd_rn(get_half(zr2[s >> 1], s & 1), get_half(zi2[s >> 1], s & 1));
+      m |= (!(S <= 4.0f)) ? (1u << s) : 0u;
+    }
+    return m;
   }
 };
 
@@ -206,6 +291,34 @@ struct F32Slots {
     "+d"(zi.y), "+d"(zr2.y), "+d"(zi2.y), "+r"(n[0]), "+r"(n[1])          \
   : "d"(cr.x), "d"(ci.x), "d"(cr.y), "d"(ci.y)
 
+#define CAFXG_F64_FREE_FAST(X, Y, Q, W, C, D)           \
+  "sub.rn.f64 t, " Q ", " W ";\n\t"                      \
+  "add.rn.f64 t, t, " C ";\n\t"                          \
+  "mul.rn.f64 v, " X ", " Y ";\n\t"                      \
+  "fma.rn.f64 " Y ", v, 0d4000000000000000, " D ";\n\t"  \
+  "mov.f64 " X ", t;\n\t"                                \
+  "mul.rn.f64 " Q ", " X ", " X ";\n\t"                  \
+  "mul.rn.f64 " W ", " Y ", " Y ";\n\t"
+
+#define CAFXG_F64_FREE_EXACT(X, Y, Q, W, C, D)          \
+  "sub.rn.f64 t, " Q ", " W ";\n\t"                      \
+  "add.rn.f64 t, t, " C ";\n\t"                          \
+  "add.rn.f64 v, " X ", " X ";\n\t"                      \
+  "mul.rn.f64 v, v, " Y ";\n\t"                          \
+  "add.rn.f64 " Y ", v, " D ";\n\t"                      \
+  "mov.f64 " X ", t;\n\t"                                \
+  "mul.rn.f64 " Q ", " X ", " X ";\n\t"                  \
+  "mul.rn.f64 " W ", " Y ", " Y ";\n\t"
+
+#define CAFXG_F64_FREE2(STEP)                          \
+  STEP("%0", "%1", "%2", "%3", "%8", "%9")             \
+  STEP("%4", "%5", "%6", "%7", "%10", "%11")
+#define CAFXG_F64_FREE_PROLOGUE "{\n\t.reg .f64 t, v;\n\t"
+#define CAFXG_F64_FREE_OPERANDS                                          \
+  : "+d"(zr.x), "+d"(zi.x), "+d"(zr2.x), "+d"(zi2.x), "+d"(zr.y),         \
+    "+d"(zi.y), "+d"(zr2.y), "+d"(zi2.y)                                  \
+  : "d"(cr.x), "d"(ci.x), "d"(cr.y), "d"(ci.y)
+
 struct F64Slots {
   static constexpr int kSlots = 2;
   using C = double;
@@ -233,12 +346,50 @@ struct F64Slots {
       asm volatile(CAFXG_F64_PROLOGUE CAFXG_X4(CAFXG_F64_PAIR(
           CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
   }
+  template <int kSteps, bool kExact>
+  __device__ __forceinline__ void run_free() {
+    if constexpr (kSteps == 32 && !kExact)
+      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X32(CAFXG_F64_FREE2(CAFXG_F64_FREE_FAST))
+                       "}" CAFXG_F64_FREE_OPERANDS);
+    else if constexpr (kSteps == 32 && kExact)
+      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X32(CAFXG_F64_FREE2(CAFXG_F64_FREE_EXACT))
+                       "}" CAFXG_F64_FREE_OPERANDS);
+    else if constexpr (kSteps == 16 && !kExact)
+      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X16(CAFXG_F64_FREE2(CAFXG_F64_FREE_FAST))
+                       "}" CAFXG_F64_FREE_OPERANDS);
+    else if constexpr (kSteps == 16 && kExact)
+      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X16(CAFXG_F64_FREE2(CAFXG_F64_FREE_EXACT))
+                       "}" CAFXG_F64_FREE_OPERANDS);
+    else if constexpr (!kExact)
+      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X4(CAFXG_F64_FREE2(CAFXG_F64_FREE_FAST))
+                       "}" CAFXG_F64_FREE_OPERANDS);
+    else
+      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X4(CAFXG_F64_FREE2(CAFXG_F64_FREE_EXACT))
+                       "}" CAFXG_F64_FREE_OPERANDS);
+  }
   __device__ __forceinline__ void start(int s, double xr, double xi) {
     if (s == 0) {
       cr.x = xr; ci.x = xi; zr.x = zi.x = zr2.x = zi2.x = 0.0;
     } else {
       cr.y = xr; ci.y = xi; zr.y = zi.y = zr2.y = zi2.y = 0.0;
     }
+  }
+  __device__ __forceinline__ void resume(int s, double r, double i, double xr, double xi) {
+    if (s == 0) {
+      cr.x = xr; ci.x = xi; zr.x = r; zi.x = i;
+      zr2.x = __dmul_rn(r, r); zi2.x = __dmul_rn(i, i);
+    } else {
+      cr.y = xr; ci.y = xi; zr.y = r; zi.y = i;
+      zr2.y = __dmul_rn(r, r); zi2.y = __dmul_rn(i, i);
+    }
+  }
+  __device__ __forceinline__ double zr_of(int s) const { return s ? zr.y : zr.x; }
+  __device__ __forceinline__ double zi_of(int s) const { return s ? zi.y : zi.x; }
+  __device__ __forceinline__ double cr_of(int s) const { return s ? cr.y : cr.x; }
+  __device__ __forceinline__ double ci_of(int s) const { return s ? ci.y : ci.x; }
+  __device__ __forceinline__ uint32_t escaped() const {
+    double s0 = __dadd_rn(zr2.x, zi2.x), s1 = __dadd_rn(zr2.y, zi2.y);
+    return ((!(s0 <= 4.0)) ? 1u : 0u) | ((!(s1 <= 4.0)) ? 2u : 0u);
   }
 };
 
@@ -283,44 +434,25 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// 4 CTAs x 256 threads per SM (<= 64 registers): 8 warps per scheduler, each
-// with two independent FP2 chains in fp32; fp64 is bound by the FP64 pipe.
-template <class Slots>
-constexpr int kMinBlocks = 4;
-
-// kInlineCoords: coordinates computed at pixel start (batches of small tiles)
-// instead of loaded from the tables of coords_kernel (big tiles).
-template <class Slots, int kSteps, bool kExact, bool kInlineCoords>
-__global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
-    mandel_kernel(const __grid_constant__ MLaunch L) {
-  constexpr int NS = Slots::kSlots;
+// ---- work distribution --------------------------------------------------------
+// Warp-uniform cursor over columns [cur, cend) of one row of one tile. Chunks
+// never straddle rows, so everything a new pixel needs besides its column
+// coordinate is chunk state held in registers: the row's imaginary part, the
+// column table and the output row base. refill() hands the next pixels to
+// the lane slots that are free (bit s of `live` clear).
+template <class Slots, bool kInlineCoords>
+struct Feeder {
   using Cd = typename Slots::C;
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-
-  // warp-uniform cursor: columns [cur, cend) of one row of one tile. Chunks
-  // never straddle rows, so everything a new pixel needs besides its column
-  // coordinate is chunk state held in registers: the row's imaginary part,
-  // the column table and the output row base.
+  static constexpr int NS = Slots::kSlots;
   uint32_t cur = 0, cend = 0, orow = 0;
-  const Cd* cxp = nullptr;     // column table, or null: coordinates inline
-  const MTile* Tc = nullptr;   // current tile (inline-coordinate mode)
+  const Cd* cxp = nullptr;    // column table (table mode)
+  const MTile* Tc = nullptr;  // current tile (inline-coordinate mode)
   Cd ci_row = Cd(0);
   bool exhausted = false;
-  const uint32_t maxit = L.max_iter;  // uniform per launch
 
-  Slots sl;
-  sl.zero = L.zero;
-  uint32_t n[NS];   // iterations completed without escape; bit 31 = escaped
-  uint32_t o[NS];   // output element offsets from L.out
-  uint32_t live = 0;  // bit s: slot s holds a pixel
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-    n[s] = 0;
-    o[s] = 0;
-  }
-
-  auto refill = [&]() {
+  __device__ __forceinline__ void refill(const MLaunch& L, Slots& sl, uint32_t (&n)[NS],
+                                         uint32_t (&o)[NS], uint32_t& live, uint32_t lt_mask) {
+    const uint32_t lane = threadIdx.x & 31u;
     while (true) {
       uint32_t b[NS];
       uint32_t want = 0;
@@ -377,9 +509,52 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
       }
       cur += min(want, avail);
     }
-  };
+  }
+};
 
-  refill();
+// Self-resetting scheduler: the last block to finish zeroes the cursor so
+// the slot can serve the next launch without a memset.
+__device__ __forceinline__ void retire_block(const MLaunch& L) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    uint32_t prev = atomicAdd(&L.sched[1], 1u);
+    if (prev == gridDim.x - 1) {
+      L.sched[0] = 0;
+      L.sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ---- checked kernel: escape tested at every step ------------------------------
+// 4 CTAs x 256 threads per SM (<= 64 registers): 8 warps per scheduler, each
+// with two independent FP2 chains in fp32; fp64 is bound by the FP64 pipe.
+// Used where the deferred kernel's precondition does not hold (tiles that
+// reach |c| ~ 2) and for small max_iter.
+// kInlineCoords: coordinates computed at pixel start (batches of small tiles)
+// instead of loaded from the tables of coords_kernel (big tiles).
+template <class Slots, int kSteps, bool kExact, bool kInlineCoords>
+__global__ void __launch_bounds__(kMandelThreads, 4)
+    mandel_kernel(const __grid_constant__ MLaunch L) {
+  constexpr int NS = Slots::kSlots;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint32_t maxit = L.max_iter;  // uniform per launch
+
+  Feeder<Slots, kInlineCoords> feed;
+  Slots sl;
+  sl.zero = L.zero;
+  uint32_t n[NS];   // iterations completed without escape; bit 31 = escaped
+  uint32_t o[NS];   // output element offsets from L.out
+  uint32_t live = 0;  // bit s: slot s holds a pixel
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    n[s] = 0;
+    o[s] = 0;
+  }
+
+  feed.refill(L, sl, n, o, live, lt_mask);
   while (__any_sync(kFull, live != 0)) {
     sl.template run<kSteps, kExact>(n);
     // escaped (bit 31) or reached max_iter; an escape at step i leaves i-1
@@ -397,40 +572,195 @@ __global__ void __launch_bounds__(kMandelThreads, kMinBlocks<Slots>)
         }
       }
       live &= ~done;
-      refill();
+      feed.refill(L, sl, n, o, live, lt_mask);
     }
   }
+  retire_block(L);
+}
 
-  // Self-resetting scheduler: the last block to finish zeroes the cursor so
-  // the slot can serve the next launch without a memset.
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    uint32_t prev = atomicAdd(&L.sched[1], 1u);
-    if (prev == gridDim.x - 1) {
-      L.sched[0] = 0;
-      L.sched[1] = 0;
-      __threadfence();
+// ---- deferred kernel: escape tested once per block ----------------------------
+// The main loop runs kSteps iterations with no escape test at all (6 packed
+// FP ops per pixel pair and step instead of 7 + FSETP + IADD), then tests
+// fl(zr^2 + zi^2) > 4 (or NaN) once. A pixel that passes has not escaped in
+// any of the kSteps steps; a pixel that fails is pushed -- with its z, c and
+// count from the START of the block -- on a per-warp replay queue in shared
+// memory and its slot is refilled. When the queue holds a full warp's worth
+// (32 x kSlots entries) the warp replays those blocks with the checked
+// per-step code, every lane busy; the replay evaluates the identical
+// operation sequence from the identical state, so it finds the reference's
+// escape step exactly.
+//
+// Why a block-end test sees every escape inside the block: once the reference
+// test fires at step i, the orbit keeps |z| > 2 (and overflows to inf / NaN,
+// which the unordered test also catches) for every later step, provided
+// |c| <= 2 - eta or |c| >= 2 + eta with eta far above the rounding error
+// (|z_{i+1}| >= |z_i|^2 - |c| > |z_i| + eta/2). The host runs this kernel only
+// for tiles whose coordinate box stays outside 2 - 2^-10 < |c| < 2 + 2^-10
+// (DESIGN.md §3.1); others take mandel_kernel. A block that crosses max_iter
+// is handled the same way: no escape by the block end means none by max_iter,
+// and a replayed pixel's count is clamped to max_iter as in mandel_kernel.
+//
+// 2 CTAs x 256 threads per SM: up to 128 registers, room for the replay
+// slots next to the live ones; 4 warps x 2 chains per scheduler still keep
+// the FP pipe saturated (6 FP2 ops of 2 cycles vs a 3-op dependency chain).
+template <class Slots>
+struct ReplayQueue {
+  using Cd = typename Slots::C;
+  static constexpr int kCap = 2 * 32 * Slots::kSlots;  // < 1 batch + 1 block of pushes
+  Cd zr[kCap], zi[kCap], cr[kCap], ci[kCap];
+  uint32_t n[kCap], o[kCap];
+};
+
+template <class Slots>
+constexpr size_t deferred_smem_bytes() {
+  return sizeof(ReplayQueue<Slots>) * (kMandelThreads / 32);
+}
+
+template <class Slots, int kSteps, bool kExact>
+__device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
+                                       uint32_t first, uint32_t count, uint32_t maxit) {
+  constexpr int NS = Slots::kSlots;
+  const uint32_t lane = threadIdx.x & 31u;
+  Slots rp;
+  rp.zero = L.zero;
+  uint32_t rn[NS], ro[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const uint32_t k = s * 32 + lane;
+    if (k < count) {
+      const uint32_t e = first + k;
+      rp.resume(s, q.zr[e], q.zi[e], q.cr[e], q.ci[e]);
+      rn[s] = q.n[e];
+      ro[s] = q.o[e];
+    } else {
+      rp.start(s, 0, 0);  // c = 0 never escapes; result discarded
+      rn[s] = 0;
+      ro[s] = 0xffffffffu;
+    }
+  }
+  __syncwarp();  // entries consumed before later pushes overwrite them
+  rp.template run<kSteps, kExact>(rn);
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    if (ro[s] != 0xffffffffu) {
+      uint32_t c = (int32_t)rn[s] < 0 ? (rn[s] & 0x7fffffffu) + 1u : rn[s];
+      L.out[ro[s]] = min(c, maxit);
     }
   }
 }
 
+template <class Slots, int kSteps, bool kExact, bool kInlineCoords>
+__global__ void __launch_bounds__(kMandelThreads, 2)
+    mandel_deferred_kernel(const __grid_constant__ MLaunch L) {
+  constexpr int NS = Slots::kSlots;
+  constexpr uint32_t kBatch = 32 * NS;
+  using Cd = typename Slots::C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ReplayQueue<Slots>& q = reinterpret_cast<ReplayQueue<Slots>*>(smem_raw)[threadIdx.x >> 5];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint32_t maxit = L.max_iter;
+
+  Feeder<Slots, kInlineCoords> feed;
+  Slots sl;
+  sl.zero = L.zero;
+  uint32_t n[NS];  // steps completed (a multiple of kSteps), all unescaped
+  uint32_t o[NS];
+  uint32_t live = 0;
+  uint32_t queued = 0;  // warp-uniform queue length
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    n[s] = 0;
+    o[s] = 0;
+  }
+
+  feed.refill(L, sl, n, o, live, lt_mask);
+  while (__any_sync(kFull, live != 0)) {
+    Cd szr[NS], szi[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      szr[s] = sl.zr_of(s);
+      szi[s] = sl.zi_of(s);
+    }
+    sl.template run_free<kSteps, kExact>();
+    const uint32_t esc = sl.escaped() & live;
+    uint32_t done = esc;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if ((live & ~esc) >> s & 1u) {
+        n[s] += kSteps;
+        if (n[s] >= maxit) {
+          L.out[o[s]] = maxit;
+          done |= 1u << s;
+        }
+      }
+    }
+    if (__any_sync(kFull, esc != 0)) {
+      uint32_t base = queued;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const uint32_t b = __ballot_sync(kFull, esc >> s & 1u);
+        if (esc >> s & 1u) {
+          const uint32_t e = base + __popc(b & lt_mask);
+          q.zr[e] = szr[s];
+          q.zi[e] = szi[s];
+          q.cr[e] = sl.cr_of(s);
+          q.ci[e] = sl.ci_of(s);
+          q.n[e] = n[s];
+          q.o[e] = o[s];
+        }
+        base += __popc(b);
+      }
+      queued = base;
+    }
+    if (__any_sync(kFull, done != 0)) {
+      live &= ~done;
+      feed.refill(L, sl, n, o, live, lt_mask);
+    }
+    if (queued >= kBatch) {
+      __syncwarp();
+      queued -= kBatch;
+      replay<Slots, kSteps, kExact>(L, q, queued, kBatch, maxit);
+    }
+  }
+  if (queued) {
+    __syncwarp();
+    replay<Slots, kSteps, kExact>(L, q, 0, queued, maxit);
+  }
+  retire_block(L);
+}
+
 template <class A, int kSteps, bool kExact>
-int launch_t(const MLaunch& L, int grid, cudaStream_t s) {
-  if (L.inline_coords)
+int launch_t(const MLaunch& L, int grid, bool deferred, cudaStream_t s) {
+  if (deferred) {
+    constexpr size_t smem = deferred_smem_bytes<A>();
+    if (L.inline_coords)
+      mandel_deferred_kernel<A, kSteps, kExact, true><<<grid, kMandelThreads, smem, s>>>(L);
+    else
+      mandel_deferred_kernel<A, kSteps, kExact, false><<<grid, kMandelThreads, smem, s>>>(L);
+  } else if (L.inline_coords) {
     mandel_kernel<A, kSteps, kExact, true><<<grid, kMandelThreads, 0, s>>>(L);
-  else
+  } else {
     mandel_kernel<A, kSteps, kExact, false><<<grid, kMandelThreads, 0, s>>>(L);
+  }
   return (int)cudaGetLastError();
 }
 
 template <class A, int kSteps, bool kExact>
-int occ_t() {
+int occ_t(bool deferred) {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &n, mandel_kernel<A, kSteps, kExact, false>, kMandelThreads, 0);
+  if (deferred)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &n, mandel_deferred_kernel<A, kSteps, kExact, false>, kMandelThreads,
+        deferred_smem_bytes<A>());
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &n, mandel_kernel<A, kSteps, kExact, false>, kMandelThreads, 0);
   return n;
 }
+
+static_assert(deferred_smem_bytes<F32Slots>() <= 48 * 1024, "replay queues exceed 48 KB");
+static_assert(deferred_smem_bytes<F64Slots>() <= 48 * 1024, "replay queues exceed 48 KB");
 
 }  // namespace
 
@@ -453,7 +783,7 @@ int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,
   const int ksteps = cfg.ksteps;
   const bool exact = cfg.exact;
   cudaStream_t s = (cudaStream_t)stream;
-  CAFXG_MANDEL_DISPATCH(launch_t, L, cfg.grid, s);
+  CAFXG_MANDEL_DISPATCH(launch_t, L, cfg.grid, cfg.deferred, s);
 }
 
 int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
@@ -470,8 +800,8 @@ int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
   return (int)cudaGetLastError();
 }
 
-int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact) {
-  CAFXG_MANDEL_DISPATCH(occ_t);
+int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact, bool deferred) {
+  CAFXG_MANDEL_DISPATCH(occ_t, deferred);
 }
 
 int mandel_slots_per_thread(int precision) {

@@ -50,17 +50,21 @@ struct MLaunch {
 // `exact` selects the 8-op escape step; the default 7-op step folds
 // 2*zr*zi + ci into fma(zr*zi, 2, ci), which is bit-identical whenever no
 // row has 0 < |ci| < 2^-100 (fp32) / 2^-960 (fp64): see DESIGN.md §3.
+// `deferred` selects mandel_deferred_kernel (escape tested once per block of
+// ksteps, escaped blocks replayed; valid only when no tile reaches
+// 2 - 2^-10 < |c| < 2 + 2^-10, see mandelbrot.cu).
 struct MandelLaunchCfg {
   int grid;
-  int ksteps;      // unchecked steps between refills
+  int ksteps;      // steps between refills
   bool exact;
+  bool deferred;
 };
 int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,
                   void* stream);
 // Prologue: fills every tile's cx/cy tables (grid.y = tile).
 int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
                          void* stream);
-int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact);
+int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact, bool deferred);
 int mandel_slots_per_thread(int precision);
 
 }  // namespace cafxg

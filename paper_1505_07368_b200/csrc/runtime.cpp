@@ -210,7 +210,7 @@ struct Device {
   bool stop = false;
   std::thread completer;
   std::atomic<int> inflight{0};
-  int mandel_occ[2][3][2] = {};  // [precision][ksteps 4/16/32][exact]
+  int mandel_occ[2][3][2][2] = {};  // [precision][ksteps 4/16/32][exact][deferred]
   // pinned staging ring for descriptor uploads (a pageable cudaMemcpyAsync
   // may wait for earlier work on the stream, serialising host and device)
   std::mutex up_mu;
@@ -471,14 +471,47 @@ static void fill_mtile(MTile& m, const cafxg_mandel_desc& d, uint64_t out_off,
   m.out_off = (uint32_t)out_off;
 }
 
+// Precondition of the deferred escape test (mandel_deferred_kernel): the
+// tile's coordinate box stays outside the annulus 2 - 2^-10 < |c| < 2 + 2^-10,
+// where an orbit could pass the reference's test and fall back below it.
+static bool deferred_safe(const MTile& t) {
+  auto at = [](double lo, double span, double s, uint32_t i, uint32_t n) {
+    return lo + (((double)i + s) * span) / n;
+  };
+  double xa = at(t.x0, t.xspan, t.s, t.col0, t.width);
+  double xb = at(t.x0, t.xspan, t.s, t.col0 + t.ncols - 1, t.width);
+  double ya = at(t.y0, t.yspan, t.s, t.row0, t.height);
+  double yb = at(t.y0, t.yspan, t.s, t.row0 + t.nrows - 1, t.height);
+  if (xa > xb) std::swap(xa, xb);
+  if (ya > yb) std::swap(ya, yb);
+  const double dx = xa > 0 ? xa : (xb < 0 ? -xb : 0.0);
+  const double dy = ya > 0 ? ya : (yb < 0 ? -yb : 0.0);
+  const double rmin = std::hypot(dx, dy);
+  const double rmax = std::hypot(std::max(std::fabs(xa), std::fabs(xb)),
+                                 std::max(std::fabs(ya), std::fabs(yb)));
+  const double eta = std::ldexp(1.0, -10), pad = 1e-6;  // pad: fp32 rounding of c
+  return rmax < 2.0 - eta - pad || rmin > 2.0 + eta + pad;
+}
+
+// CAFXG_DEFERRED=0 forces the per-step-checked kernel everywhere
+static bool deferred_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CAFXG_DEFERRED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
-                                  bool exact, uint64_t pixels) {
+                                  bool exact, bool safe, uint64_t pixels) {
   MandelLaunchCfg c;
   c.ksteps = max_iter >= 512 ? 32 : max_iter >= 128 ? 16 : 4;
   c.exact = exact;
-  int& occ = d->mandel_occ[precision][c.ksteps == 4 ? 0 : c.ksteps == 16 ? 1 : 2][exact];
+  c.deferred = safe && max_iter >= 256 && deferred_enabled();
+  int& occ = d->mandel_occ[precision][c.ksteps == 4 ? 0 : c.ksteps == 16 ? 1 : 2][exact]
+                          [c.deferred];
   if (occ == 0)
-    occ = std::max(1, mandel_max_blocks_per_sm(precision, c.ksteps, exact));
+    occ = std::max(1, mandel_max_blocks_per_sm(precision, c.ksteps, exact, c.deferred));
   const uint64_t per_block = (uint64_t)kMandelThreads * mandel_slots_per_thread(precision);
   uint64_t want = (pixels + per_block - 1) / per_block;
   uint64_t full = (uint64_t)d->sms * occ;
@@ -584,7 +617,10 @@ static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
     ctx->st_launches++;
   }
   if (!coords_only) {
-    MandelLaunchCfg cfg = mandel_cfg(d, precision, L.max_iter, exact, pixels);
+    bool safe = true;
+    for (auto& t : tiles)
+      safe = safe && deferred_safe(t);
+    MandelLaunchCfg cfg = mandel_cfg(d, precision, L.max_iter, exact, safe, pixels);
     int e = mandel_launch(L, precision, cfg, stream);
     if (e != 0)
       return cuda_status((cudaError_t)e, "mandelbrot launch");

@@ -1,0 +1,59 @@
+"""Device-resident timing of the escape kernel on a few workloads (CUDA events
+on the launching stream, mean of 5 after 2 warm-ups). Run twice with
+CAFXG_DEFERRED=0 / 1 to compare the per-step and the deferred escape test.
+    python paper_1505_07368_b200/tools/mandel_time.py
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
+import paper_1505_07368_b200 as pkg  # noqa: E402
+
+
+def storm(n, it):
+    rng = np.random.default_rng(7)
+    tiles = []
+    for k in range(n):
+        kx, ky = int(rng.integers(0, 1473)), int(rng.integers(0, 961))
+        x0, y0 = -2.0 + kx / 512, -1.0 + ky / 512
+        tiles.append(pkg.mandel_desc(x0, x0 + 0.125, y0, y0 + 0.125, 64, 64, it, fp64=True,
+                                     out_offset=k * 4096))
+    return tiles
+
+
+WORK = {
+    "cfg3_fp32_16384_it1000": [pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 16384, 16384, 1000)],
+    "ref_fp64_16000_it500": [pkg.reference_desc(16000, 500)],
+    "ref_fp64_4096_it500": [pkg.reference_desc(4096, 500)],
+    "deep_fp32_4096_it5000": [pkg.mandel_desc(-0.7487, -0.7485, 0.0650, 0.0652, 4096, 4096,
+                                              5000)],
+    "storm_fp64_4096x64sq_it256": storm(4096, 256),
+    "cfg1_fp32_1920x1080_it100": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)],
+}
+
+only = sys.argv[1:] or list(WORK)
+s = torch.cuda.Stream()
+with pkg.Context(1) as ctx:
+    for name in only:
+        tiles = WORK[name]
+        npx = sum(t.nrows * t.ncols for t in tiles)
+        out = torch.empty(npx, dtype=torch.int32, device="cuda")
+        ts = []
+        for k in range(7):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(s)
+            ctx.mandelbrot_device(tiles, out.data_ptr(), s.cuda_stream)
+            b.record(s)
+            torch.cuda.synchronize()
+            if k >= 2:
+                ts.append(a.elapsed_time(b))
+        iters = int(out.cpu().numpy().view(np.uint32).sum(dtype=np.uint64))
+        ms = sum(ts) / len(ts)
+        print(json.dumps({"work": name, "deferred": os.environ.get("CAFXG_DEFERRED", "1"),
+                          "ms": round(ms, 4), "giter_s": round(iters / ms / 1e6, 1),
+                          "iters": iters}))

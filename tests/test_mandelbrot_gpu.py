@@ -134,6 +134,59 @@ with pkg.Context(1) as c:
     assert np.array_equal(res["0"], res["1"])
 
 
+@pytest.mark.parametrize("fp64", [False, True])
+def test_deferred_kernel_vs_oracle(ctx, fp64):
+    """max_iter >= 256 on tiles clear of |c| ~ 2 takes the deferred-test
+    kernel (escape tested once per block, escaped blocks replayed): random
+    regions, max_iter not a multiple of the block, tiny tiles (partial replay
+    batches), a tile wholly outside |c| = 2 (every pixel escapes at step 1)
+    and tiles straddling |c| = 2 (routed to the per-step kernel)."""
+    rng = np.random.default_rng(41 + fp64)
+    cases = []
+    for _ in range(8):
+        w, h = int(rng.integers(1, 260)), int(rng.integers(1, 160))
+        x0, y0 = float(rng.uniform(-1.6, 0.2)), float(rng.uniform(-1.0, 0.8))
+        span = float(10 ** rng.uniform(-5, -0.5))
+        cases.append((x0, x0 + span, y0, y0 + span * h / w, w, h, int(rng.integers(256, 2500))))
+    cases += [(-0.75, -0.73, 0.10, 0.12, 1, 1, 1000),      # one pixel
+              (-0.75, -0.73, 0.10, 0.12, 3, 70, 777),
+              (2.5, 3.0, 0.0, 0.5, 97, 45, 600),           # |c| > 2 + eta
+              (-2.1, -1.9, -0.05, 0.05, 120, 60, 900),     # straddles |c| = 2
+              (-1.5, 0.5, -1.0, 1.0, 300, 300, 500)]       # reference region
+    for (x0, x1, y0, y1, w, h, it) in cases:
+        d = pkg.mandel_desc(x0, x1, y0, y1, w, h, it, fp64=fp64)
+        out = ctx.mandelbrot(d).reshape(h, w)
+        ref = oracle.tile(x0, x1, y0, y1, w, h, it, fp64=fp64, centre=True)
+        assert np.array_equal(out, ref), (x0, x1, y0, y1, w, h, it)
+
+
+def test_deferred_and_checked_kernels_agree():
+    """CAFXG_DEFERRED=0 (escape tested every step) and the default deferred
+    test give identical counts, fp32 and fp64, fast and exact steps."""
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+with pkg.Context(1) as c:
+    outs = []
+    for d in [pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 1024, 1024, 1000),
+              pkg.mandel_desc(-1.5, 0.5, -1.0, 1.0, 1000, 800, 500, fp64=True, centre=False),
+              pkg.mandel_desc(-0.7487, -0.7485, 0.0650, 0.0652, 700, 500, 4000),
+              pkg.mandel_desc(-0.16, -0.14, 1.03, 1.05, 500, 500, 3000, fp64=True)]:
+        outs.append(c.mandelbrot(d))
+    np.save(sys.argv[1], np.concatenate(outs))
+""" % ROOT
+    res = {}
+    for mode in ("0", "1"):
+        for exact in ("0", "1"):
+            path = f"/tmp/cafxg_deferred_{mode}{exact}.npy"
+            env = dict(os.environ, CAFXG_DEFERRED=mode, CAFXG_EXACT_STEP=exact)
+            subprocess.check_call([sys.executable, "-c", code, path], env=env)
+            res[mode + exact] = np.load(path)
+    for k in ("01", "10", "11"):
+        assert np.array_equal(res["00"], res[k]), k
+
+
 def test_multi_tile_batch_and_offsets(ctx):
     tiles, refs, off = [], [], 0
     rng = np.random.default_rng(3)
