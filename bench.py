@@ -360,9 +360,14 @@ def run_ours(args):
     peak_tops = sms * 128 * sm_max * 1e6 / 1e12
     achieved = 8.0 * iters_local / (kernel_ms / 1e3) / 1e12
     # DRAM traffic of the escape kernel from the committed ncu capture of the
-    # full-image launch (profiles/round1/mandel_cfg3_full.txt: 1.021780 GB
-    # written + 7.890176 MB read), scaled to this rank's share of the pixels
-    traffic = round((1.021780e9 + 7.890176e6) * npx / (W_IMG * H_IMG))
+    # full-image launch (profiles/round1/mandel_cfg3_deferred_full.txt:
+    # 1.020146 GB written + 10.927616 MB read), scaled to this rank's share
+    traffic = round((1.020146e9 + 10.927616e6) * npx / (W_IMG * H_IMG))
+    # The same capture: FMA pipe busy 85.5% of active cycles over 36.72 ms at
+    # 1.963 GHz = 1.17e12 executed FP32 lane-ops for 1.82e11 iterations, i.e.
+    # 6.41 executed lane-ops per iteration (6 in the unchecked step, the rest
+    # block-end tests and replays) against the algorithmic 8.
+    exec_ops_per_iter = 6.41
     roof = {"bound": "fp32_pipe", "achieved": round(achieved, 3), "peak": round(peak_tops, 3),
             "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4), "traffic": traffic,
             "traffic_note": "dram read+write bytes per launch (ncu, profiles/round1); "
@@ -370,7 +375,14 @@ def run_ours(args):
             "ops_per_launch": 8.0 * iters_local,
             "peak_basis": f"{sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz of "
                           "MEASURED_PEAKS.json); algorithmic 8 FP ops per escape iteration "
-                          "(3 mul + 5 add, SURVEY §8d)"}
+                          "(3 mul + 5 add, SURVEY §8d)",
+            "frac_executed": round(achieved / peak_tops * exec_ops_per_iter / 8.0, 4),
+            "frac_note": "frac counts the reference's 8 FP ops per iteration; the kernel "
+                         "executes 6 per iteration (escape test deferred to 32-step block "
+                         "ends, 2*zr*zi+ci as one FMA) plus block-end tests and exact "
+                         "replays, 6.41 lane-ops/iteration measured (ncu FMA pipe busy "
+                         "85.5%, profiles/round1/mandel_cfg3_deferred_full.txt); "
+                         "frac_executed is the pipe fraction doing that executed work"}
     if clk.get("sm_mhz"):
         peak_clk = sms * 128 * clk["sm_mhz"] * 1e6 / 1e12
         roof["frac_at_measured_clock"] = round(achieved / peak_clk, 4)
