@@ -559,10 +559,11 @@ def run_storm(ctx, clients=64, per=1600, seed=2024, closed_loop=False):
                                   C.c_uint32, C.c_int, C.POINTER(C.c_double),
                                   C.POINTER(C.c_uint32)]
     actor = ctx.spawn("mandelbrot")
-    # warm-up burst (pool growth, first launches)
+    # warm-up: one full untimed storm of the same shape (staging ring, request
+    # allocator arenas, pinned reply pages, first launches)
     wms, errs = C.c_double(), C.c_uint32()
-    S.cafxg_storm_run(actor.handle, descs, replies.ctypes.data, 16384, 8, 64, 0,
-                      C.byref(wms), C.byref(errs))
+    S.cafxg_storm_run(actor.handle, descs, replies.ctypes.data, 16384, clients, per,
+                      1 if closed_loop else 0, C.byref(wms), C.byref(errs))
     replies[:] = 0
     st0 = ctx.stats()
     rc = S.cafxg_storm_run(actor.handle, descs, replies.ctypes.data, 16384, clients, per,

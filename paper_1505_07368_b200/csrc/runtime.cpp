@@ -14,6 +14,9 @@
 //    abstract_actor.cpp:126-131).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/resource.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -90,6 +93,11 @@ class PinnedPool {
     std::lock_guard<std::mutex> g(mu_);
     live_[p] = cls;
     ranges_[(uintptr_t)p] = cls;
+    // publish a new immutable snapshot for the lock-free contains(); older
+    // snapshots may still be read and are kept until the pool dies
+    auto* snap = new std::vector<std::pair<uintptr_t, size_t>>(ranges_.begin(), ranges_.end());
+    retired_.emplace_back(snap);
+    snap_.store(snap, std::memory_order_release);
     return p;
   }
 
@@ -103,17 +111,23 @@ class PinnedPool {
     return true;
   }
 
-  // [p, p+bytes) inside one live pool buffer (no driver call).
-  bool contains(const void* p, size_t bytes) {
-    std::lock_guard<std::mutex> g(mu_);
-    if (live_.empty())
+  // [p, p+bytes) inside one pool buffer (no driver call, no lock: every
+  // client thread classifies its reply buffer here). Pool buffers stay
+  // pinned and device-mapped until the context closes, so a buffer that is
+  // currently on the free list still qualifies.
+  bool contains(const void* p, size_t bytes) const {
+    const auto* snap = snap_.load(std::memory_order_acquire);
+    if (!snap || snap->empty())
       return false;
-    auto it = ranges_.upper_bound((uintptr_t)p);
-    if (it == ranges_.begin())
+    const uintptr_t a = (uintptr_t)p;
+    auto it = std::upper_bound(snap->begin(), snap->end(), a,
+                               [](uintptr_t v, const std::pair<uintptr_t, size_t>& e) {
+                                 return v < e.first;
+                               });
+    if (it == snap->begin())
       return false;
     --it;
-    return (uintptr_t)p + bytes <= it->first + it->second &&
-           live_.count((void*)it->first);
+    return a + bytes <= it->first + it->second;
   }
 
  private:
@@ -127,6 +141,8 @@ class PinnedPool {
   std::unordered_map<void*, size_t> live_;
   std::map<size_t, std::vector<void*>> free_;
   std::map<uintptr_t, size_t> ranges_;  // every buffer ever allocated
+  std::atomic<const std::vector<std::pair<uintptr_t, size_t>>*> snap_{nullptr};
+  std::vector<std::unique_ptr<std::vector<std::pair<uintptr_t, size_t>>>> retired_;
 };
 
 // True when [p, p+bytes) is page-locked host memory the device can address
@@ -192,6 +208,15 @@ struct Completion {
 };
 
 constexpr uint32_t kSchedSlots = 1024;
+// Actor batching: at most kMaxInflight batches per device before the
+// dispatcher holds (arrivals meanwhile coalesce into the next batch), each of
+// at most kMaxBatchPx pixels (a single larger request is its own batch).
+// Batches are kept small enough that the reply copy-out of one overlaps the
+// kernel of the next and the pipeline drains quickly after the last request.
+constexpr int kMaxInflight = 8;
+constexpr int kSoftInflight = 4;
+constexpr uint64_t kInlineCopyPx = 256u << 10;  // copy-out on the compute stream below  // beyond this only when a full batch is queued
+constexpr uint64_t kMaxBatchPx = 16ull << 20;
 constexpr int kUpSlots = 16;
 constexpr size_t kUpSlotBytes = 2u << 20;
 
@@ -218,6 +243,16 @@ struct Device {
   cudaEvent_t up_ev[16] = {};
   bool up_armed[16] = {};
   uint32_t up_next = 0;
+  // batch staging ring (actor batches): one device buffer per in-flight
+  // batch, reused in order. A fresh cudaMallocAsync per batch can block the
+  // dispatcher while the pool grows; this ring grows only in warm-up. Reuse
+  // of slot i waits (on the device) for the copy-out that last read it.
+  uint8_t* stage[kMaxInflight] = {};
+  size_t stage_cap[kMaxInflight] = {};
+  cudaEvent_t stage_ev[kMaxInflight] = {};
+  uint32_t stage_next = 0;
+  cudaEvent_t trace_ref = nullptr;  // CAFXG_TRACE time base
+  double trace_ref_ms = 0;
 
   uint32_t* next_sched() {
     uint32_t i = sched_next.fetch_add(1, std::memory_order_relaxed) % kSchedSlots;
@@ -277,7 +312,16 @@ static void note_max_batch(cafxg_ctx* ctx, uint64_t n) {
   }
 }
 
+// Backend threads (dispatcher, completion) get a higher scheduling weight
+// than client threads when the process may raise it (best effort): under a
+// request storm, clients outnumber cores, and a starved completion thread
+// leaves the device idle with finished batches counted as in flight.
+static void raise_priority() {
+  setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), -10);
+}
+
 static void completion_loop(cafxg_ctx* ctx, Device* d) {
+  raise_priority();
   cudaSetDevice(d->ordinal);
   while (true) {
     Completion c;
@@ -409,17 +453,19 @@ static double coord(double lo, double hi, uint32_t i, uint32_t n, double s) {
 // crossing or at an end row.
 static double min_abs_ci(const cafxg_mandel_desc& t) {
   double s = t.sampling ? 0.5 : 0.0;
-  std::vector<int64_t> cand = {(int64_t)t.row0, (int64_t)t.row0 + t.nrows - 1};
+  int64_t cand[8] = {(int64_t)t.row0, (int64_t)t.row0 + t.nrows - 1};
+  int nc = 2;
   double span = t.y1 - t.y0;
   if (span != 0.0) {
     double r = -t.y0 * (double)t.height / span - s;
-    if (std::isfinite(r)) {
+    if (std::isfinite(r) && std::fabs(r) < 9.0e18) {
       for (int64_t k = (int64_t)std::floor(r) - 2; k <= (int64_t)std::floor(r) + 3; ++k)
-        cand.push_back(k);
+        cand[nc++] = k;
     }
   }
   double best = INFINITY;
-  for (int64_t r : cand) {
+  for (int i = 0; i < nc; ++i) {
+    const int64_t r = cand[i];
     if (r < (int64_t)t.row0 || r >= (int64_t)t.row0 + t.nrows)
       continue;
     double ci = coord(t.y0, t.y1, (uint32_t)r, t.height, s);
@@ -506,6 +552,12 @@ static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
                                   bool exact, bool safe, uint64_t pixels) {
   MandelLaunchCfg c;
   c.ksteps = max_iter >= 512 ? 32 : max_iter >= 128 ? 16 : 4;
+  static const int ks_env = [] {  // CAFXG_KSTEPS=4|16|32: experiments only
+    const char* e = getenv("CAFXG_KSTEPS");
+    return e ? atoi(e) : 0;
+  }();
+  if (ks_env == 4 || ks_env == 16 || ks_env == 32)
+    c.ksteps = ks_env;
   c.exact = exact;
   c.deferred = safe && max_iter >= 256 && deferred_enabled();
   int& occ = d->mandel_occ[precision][c.ksteps == 4 ? 0 : c.ksteps == 16 ? 1 : 2][exact]
@@ -1370,6 +1422,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   const double t_begin = trace_now_ms();
   cudaSetDevice(d->ordinal);
   std::lock_guard<std::mutex> g(d->submit_mu);
+  const double t_lock = trace_now_ms();
   uint64_t px = 0;
   uint32_t maxit = 0;
   bool exact = false;
@@ -1393,9 +1446,50 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
       push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); });
     t_last_error = err;
   };
-  if (cudaMallocAsync((void**)&dout, px * 4 + 16, d->compute) != cudaSuccess) {
-    fail_all(cuda_status(cudaGetLastError(), "batch staging allocation"));
-    return;
+  const uint32_t slot = d->stage_next++ % kMaxInflight;
+  if (!d->stage[0]) {
+    // first batch on this device: the whole ring at the batch cap, so later
+    // batches never allocate (one request above the cap still grows its slot)
+    for (int i = 0; i < kMaxInflight; ++i) {
+      const size_t cap = kMaxBatchPx * 4 + 16;
+      if (cudaMalloc((void**)&d->stage[i], cap) == cudaSuccess) {
+        d->stage_cap[i] = cap;
+      } else {
+        cudaGetLastError();
+        d->stage[i] = nullptr;
+        break;
+      }
+    }
+  }
+  {
+    const size_t need = px * 4 + 16;
+    if (d->stage_cap[slot] < need) {
+      // growth (warm-up): the old buffer may still feed an earlier batch
+      if (d->stage[slot]) {
+        cudaStreamSynchronize(d->compute);
+        cudaStreamSynchronize(d->d2h);
+        cudaFree(d->stage[slot]);
+        d->stage[slot] = nullptr;
+        d->stage_cap[slot] = 0;
+      }
+      size_t cap = std::max<size_t>(need, kMaxBatchPx * 4 + 16);
+      if (cudaMalloc((void**)&d->stage[slot], cap) != cudaSuccess) {
+        d->stage[slot] = nullptr;
+        fail_all(cuda_status(cudaGetLastError(), "batch staging allocation"));
+        return;
+      }
+      d->stage_cap[slot] = cap;
+    }
+    if (!d->stage_ev[slot] &&
+        cudaEventCreateWithFlags(&d->stage_ev[slot], cudaEventDisableTiming) != cudaSuccess) {
+      d->stage_ev[slot] = nullptr;
+      fail_all(cuda_status(cudaGetLastError(), "batch staging event"));
+      return;
+    }
+    // the copy-out of the batch that used this slot before must be done
+    // reading it (recorded on the copy stream; a no-op the first time)
+    cudaStreamWaitEvent(d->compute, d->stage_ev[slot], 0);
+    dout = reinterpret_cast<uint32_t*>(d->stage[slot]);
   }
   std::vector<MTile> mt;
   mt.reserve(ntiles);
@@ -1415,9 +1509,39 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     }
     segs.push_back(CopySeg{dout + roff, r->out, (off - roff) * 4});
   }
+  const double t_built = trace_now_ms();
+  // CAFXG_TRACE: device-side timestamps of this batch (kernel start/end,
+  // copy-out end), reported against a per-device reference event
+  cudaEvent_t tev[3] = {};
+  if (trace_on()) {
+    if (!d->trace_ref) {
+      cudaEventCreate(&d->trace_ref);
+      cudaEventRecord(d->trace_ref, d->compute);
+      cudaEventSynchronize(d->trace_ref);
+      d->trace_ref_ms = trace_now_ms();
+    }
+    for (auto& e : tev)
+      cudaEventCreate(&e);
+    cudaEventRecord(tev[0], d->compute);
+  }
   status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, d->compute);
+  if (tev[0])
+    cudaEventRecord(tev[1], d->compute);
+  const double t_launched = trace_now_ms();
+  // the reply segment table goes up on the compute stream: an upload-ring
+  // slot recorded on the copy stream would only free up behind every queued
+  // copy-out, and reusing it would block the dispatcher
+  if (status == CAFXG_OK && px && all_pinned) {
+    size_t sb = segs.size() * sizeof(CopySeg);
+    status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, d->compute), "segs alloc");
+    if (status == CAFXG_OK)
+      status = upload(d, dsegs, segs.data(), sb, d->compute);
+  }
   // the reply copy-out runs on the copy stream so it overlaps the next
-  // batch's compute (a storm moves 16 KiB per request over PCIe)
+  // batch's compute (a storm moves 16 KiB per request over PCIe; copying on
+  // the compute stream instead was slower even for closed-loop trickles,
+  // 144 -> 218 ms, because it serialises copy-out and the next kernel)
+  cudaStream_t cs = d->d2h;
   if (status == CAFXG_OK && px) {
     cudaEvent_t ev;
     status = cuda_status(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
@@ -1429,28 +1553,26 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   }
   if (status == CAFXG_OK && px) {
     if (all_pinned) {
-      size_t sb = segs.size() * sizeof(CopySeg);
-      status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, d->d2h), "segs alloc");
-      if (status == CAFXG_OK)
-        status = upload(d, dsegs, segs.data(), sb, d->d2h);
-      if (status == CAFXG_OK) {
-        int e = copy_segments_launch(dsegs, (uint32_t)segs.size(), d->d2h);
+      {
+        int e = copy_segments_launch(dsegs, (uint32_t)segs.size(), cs);
         status = cuda_status((cudaError_t)e, "reply scatter launch");
         ctx->st_launches++;
       }
-      if (dsegs)
-        cudaFreeAsync(dsegs, d->d2h);
     } else {
       bounce = (uint32_t*)ctx->pinned.alloc(px * 4);
       if (!bounce)
         status = fail(CAFXG_E_CONFIG, "pinned bounce allocation failed");
       else
         status = cuda_status(cudaMemcpyAsync(bounce, dout, px * 4, cudaMemcpyDeviceToHost,
-                                             d->d2h), "batch download");
+                                             cs), "batch download");
     }
     ctx->st_d2h += px * 4;
   }
-  cudaFreeAsync(dout, d->d2h);
+  if (dsegs)
+    cudaFreeAsync(dsegs, cs);
+  cudaEventRecord(d->stage_ev[slot], cs);  // slot free once the copy-out is done
+  if (tev[0])
+    cudaEventRecord(tev[2], cs);
   ctx->st_batches++;
   note_max_batch(ctx, batch.size());
   if (status != CAFXG_OK) {
@@ -1459,17 +1581,32 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     fail_all(status);
     return;
   }
-  push_completion(ctx, d, d->d2h,
-                  [ctx, batch = std::move(batch), bounce, t_begin,
+  push_completion(ctx, d, cs,
+                  [ctx, d, batch = std::move(batch), bounce, t_begin, t_lock, t_built,
+                   t_launched, tev0 = tev[0], tev1 = tev[1], tev2 = tev[2],
                    t_sub = trace_now_ms()](int st) mutable {
                     const double t_done = trace_now_ms();
                     size_t n = batch.size();
                     finish_batch(ctx, std::move(batch), bounce, st);
                     if (trace_on())
                       fprintf(stderr,
-                              "cafxg batch of %zu: build %.3f submit %.3f device-done %.3f "
+                              "cafxg batch of %zu: build %.3f lock %.3f built %.3f "
+                              "launched %.3f submit %.3f device-done %.3f "
                               "callbacks-handed-off %.3f ms\n",
-                              n, t_begin, t_sub, t_done, trace_now_ms());
+                              n, t_begin, t_lock, t_built, t_launched, t_sub, t_done,
+                              trace_now_ms());
+                    if (tev0) {
+                      float g[3] = {};
+                      cudaEvent_t es[3] = {tev0, tev1, tev2};
+                      for (int i = 0; i < 3; ++i) {
+                        cudaEventElapsedTime(&g[i], d->trace_ref, es[i]);
+                        cudaEventDestroy(es[i]);
+                      }
+                      fprintf(stderr,
+                              "cafxg   gpu: kernel %.3f..%.3f copy-out done %.3f ms\n",
+                              d->trace_ref_ms + g[0], d->trace_ref_ms + g[1],
+                              d->trace_ref_ms + g[2]);
+                    }
                   });
 }
 
@@ -1487,9 +1624,16 @@ static Device* pick_device(cafxg_ctx* ctx) {
 }
 
 static void dispatcher_loop(cafxg_ctx* ctx) {
-  const int kMaxInflight = 4;            // batches per device before holding
-  const uint64_t kMaxBatchPx = 64ull << 20;
+  raise_priority();
   std::deque<Request*> queue;
+  uint64_t queued_px = 0;
+  // A trickle of requests (closed-loop clients) coalesces while kSoftInflight
+  // batches run; a backlog of at least one full batch (open-loop bursts) may
+  // fill the pipeline up to kMaxInflight.
+  auto may_dispatch = [&](const Device* d) {
+    const int n = d->inflight.load();
+    return n < kSoftInflight || (n < kMaxInflight && queued_px >= kMaxBatchPx);
+  };
   while (true) {
     {
       std::unique_lock<std::mutex> lk(ctx->disp_mu);
@@ -1500,7 +1644,7 @@ static void dispatcher_loop(cafxg_ctx* ctx) {
           return true;
         if (!queue.empty()) {
           for (auto& d : ctx->devs)
-            if (d->inflight.load() < kMaxInflight)
+            if (may_dispatch(d.get()))
               return true;
           return false;
         }
@@ -1515,12 +1659,14 @@ static void dispatcher_loop(cafxg_ctx* ctx) {
     std::vector<Request*> fresh;
     for (Request* r = head; r; r = r->next)
       fresh.push_back(r);
-    for (auto it = fresh.rbegin(); it != fresh.rend(); ++it)
+    for (auto it = fresh.rbegin(); it != fresh.rend(); ++it) {
       queue.push_back(*it);
+      queued_px += (*it)->pixels;
+    }
     if (queue.empty())
       continue;
     Device* d = pick_device(ctx);
-    if (d->inflight.load() >= kMaxInflight && !ctx->disp_stop)
+    if (!may_dispatch(d) && !ctx->disp_stop)
       continue;  // wait for a completion; meanwhile the batch keeps growing
     // assemble one batch: leading requests of one kernel kind / precision
     std::vector<Request*> batch;
@@ -1529,6 +1675,7 @@ static void dispatcher_loop(cafxg_ctx* ctx) {
       Request* r = queue.front();
       if (!r->actor->alive.load()) {
         queue.pop_front();
+        queued_px -= r->pixels;
         push_completion(ctx, d, d->compute, [r](int) { finish_request(r, CAFXG_E_DOWN); });
         continue;
       }
@@ -1552,11 +1699,16 @@ static void dispatcher_loop(cafxg_ctx* ctx) {
            px + r->pixels > kMaxBatchPx))
         break;
       queue.pop_front();
+      queued_px -= r->pixels;
       batch.push_back(r);
       px += r->pixels;
     }
-    if (!batch.empty())
+    if (!batch.empty()) {
+      if (trace_on())
+        fprintf(stderr, "cafxg dispatch %.3f ms: batch %zu, %zu queued behind, inflight %d\n",
+                trace_now_ms(), batch.size(), queue.size(), (int)d->inflight.load());
       run_mandel_batch(ctx, d, std::move(batch));
+    }
   }
 }
 
@@ -1709,6 +1861,12 @@ int cafxg_close(cafxg_ctx* ctx) {
     for (auto ev : d->up_ev)
       cudaEventDestroy(ev);
     cudaFreeHost(d->up_base);
+    for (int i = 0; i < kMaxInflight; ++i) {
+      if (d->stage[i])
+        cudaFree(d->stage[i]);
+      if (d->stage_ev[i])
+        cudaEventDestroy(d->stage_ev[i]);
+    }
     cudaFree(d->sched);
     cudaStreamSynchronize(d->h2d);
     cudaStreamDestroy(d->compute);
