@@ -112,8 +112,27 @@ constexpr unsigned kFull = 0xffffffffu;
   "@pB0 or.b32 %10, %10, 0x80000000;\n\t@pB1 or.b32 %11, %11, 0x80000000;\n\t}"
 
 #define CAFXG_X4(S) S S S S
+#define CAFXG_X8(S) CAFXG_X4(S) CAFXG_X4(S)
 #define CAFXG_X16(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S)
+#define CAFXG_X24(S) CAFXG_X16(S) CAFXG_X8(S)
 #define CAFXG_X32(S) CAFXG_X16(S) CAFXG_X16(S)
+#define CAFXG_X40(S) CAFXG_X32(S) CAFXG_X8(S)
+#define CAFXG_X48(S) CAFXG_X32(S) CAFXG_X16(S)
+#define CAFXG_X56(S) CAFXG_X48(S) CAFXG_X8(S)
+#define CAFXG_X64(S) CAFXG_X32(S) CAFXG_X32(S)
+
+// Expands BODY(CAFXG_Xk) for the compile-time step count K (one unrolled
+// PTX block of K steps).
+#define CAFXG_STEPS_SWITCH(K, BODY)                    \
+  if constexpr (K == 4) { BODY(CAFXG_X4); }            \
+  else if constexpr (K == 8) { BODY(CAFXG_X8); }       \
+  else if constexpr (K == 16) { BODY(CAFXG_X16); }     \
+  else if constexpr (K == 24) { BODY(CAFXG_X24); }     \
+  else if constexpr (K == 32) { BODY(CAFXG_X32); }     \
+  else if constexpr (K == 40) { BODY(CAFXG_X40); }     \
+  else if constexpr (K == 48) { BODY(CAFXG_X48); }     \
+  else if constexpr (K == 56) { BODY(CAFXG_X56); }     \
+  else { static_assert(K == 64, "unsupported step count"); BODY(CAFXG_X64); }
 
 #define CAFXG_F32_OPERANDS                                                     \
   : "+l"(zr[0]), "+l"(zi[0]), "+l"(zr2[0]), "+l"(zi2[0]), "+l"(zr[1]),         \
@@ -173,45 +192,31 @@ struct F32Slots {
 
   template <int kSteps, bool kExact>
   __device__ __forceinline__ void run(uint32_t (&n)[kSlots]) {
-    if constexpr (kSteps == 32 && !kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X32(CAFXG_F32_STEP2(CAFXG_F32_FAST))
-                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
-    else if constexpr (kSteps == 32 && kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X32(CAFXG_F32_STEP2(CAFXG_F32_EXACT))
-                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
-    else if constexpr (kSteps == 16 && !kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X16(CAFXG_F32_STEP2(CAFXG_F32_FAST))
-                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
-    else if constexpr (kSteps == 16 && kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X16(CAFXG_F32_STEP2(CAFXG_F32_EXACT))
-                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
-    else if constexpr (kSteps == 4 && !kExact)
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP2(CAFXG_F32_FAST))
-                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
-    else
-      asm volatile(CAFXG_F32_PROLOGUE CAFXG_X4(CAFXG_F32_STEP2(CAFXG_F32_EXACT))
-                       CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS);
+#define CAFXG_B_FAST(X) asm volatile(CAFXG_F32_PROLOGUE X(CAFXG_F32_STEP2(CAFXG_F32_FAST)) \
+                                         CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS)
+#define CAFXG_B_EXACT(X) asm volatile(CAFXG_F32_PROLOGUE X(CAFXG_F32_STEP2(CAFXG_F32_EXACT)) \
+                                          CAFXG_F32_EPILOGUE CAFXG_F32_OPERANDS)
+    if constexpr (kExact) {
+      CAFXG_STEPS_SWITCH(kSteps, CAFXG_B_EXACT)
+    } else {
+      CAFXG_STEPS_SWITCH(kSteps, CAFXG_B_FAST)
+    }
+#undef CAFXG_B_FAST
+#undef CAFXG_B_EXACT
   }
   template <int kSteps, bool kExact>
   __device__ __forceinline__ void run_free() {
-    if constexpr (kSteps == 32 && !kExact)
-      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X32(CAFXG_F32_FREE2(CAFXG_F32_FREE_FAST))
-                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
-    else if constexpr (kSteps == 32 && kExact)
-      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X32(CAFXG_F32_FREE2(CAFXG_F32_FREE_EXACT))
-                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
-    else if constexpr (kSteps == 16 && !kExact)
-      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X16(CAFXG_F32_FREE2(CAFXG_F32_FREE_FAST))
-                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
-    else if constexpr (kSteps == 16 && kExact)
-      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X16(CAFXG_F32_FREE2(CAFXG_F32_FREE_EXACT))
-                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
-    else if constexpr (!kExact)
-      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X4(CAFXG_F32_FREE2(CAFXG_F32_FREE_FAST))
-                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
-    else
-      asm volatile(CAFXG_F32_FREE_PROLOGUE CAFXG_X4(CAFXG_F32_FREE2(CAFXG_F32_FREE_EXACT))
-                       CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS);
+#define CAFXG_B_FAST(X) asm volatile(CAFXG_F32_FREE_PROLOGUE X(CAFXG_F32_FREE2(CAFXG_F32_FREE_FAST)) \
+                                         CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS)
+#define CAFXG_B_EXACT(X) asm volatile(CAFXG_F32_FREE_PROLOGUE X(CAFXG_F32_FREE2(CAFXG_F32_FREE_EXACT)) \
+                                          CAFXG_F32_FREE_EPILOGUE CAFXG_F32_FREE_OPERANDS)
+    if constexpr (kExact) {
+      CAFXG_STEPS_SWITCH(kSteps, CAFXG_B_EXACT)
+    } else {
+      CAFXG_STEPS_SWITCH(kSteps, CAFXG_B_FAST)
+    }
+#undef CAFXG_B_FAST
+#undef CAFXG_B_EXACT
   }
   // slot s lives in half (s & 1) of pair (s >> 1)
   __device__ __forceinline__ void start(int s, float fr, float fi) {
@@ -327,45 +332,31 @@ struct F64Slots {
 
   template <int kSteps, bool kExact>
   __device__ __forceinline__ void run(uint32_t (&n)[kSlots]) {
-    if constexpr (kSteps == 32 && !kExact)
-      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X32(CAFXG_F64_PAIR(
-          CAFXG_F64_STEP_FAST)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
-    else if constexpr (kSteps == 32 && kExact)
-      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X32(CAFXG_F64_PAIR(
-          CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
-    else if constexpr (kSteps == 16 && !kExact)
-      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X16(CAFXG_F64_PAIR(
-          CAFXG_F64_STEP_FAST)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
-    else if constexpr (kSteps == 16 && kExact)
-      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X16(CAFXG_F64_PAIR(
-          CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
-    else if constexpr (kSteps == 4 && !kExact)
-      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X4(CAFXG_F64_PAIR(
-          CAFXG_F64_STEP_FAST)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
-    else
-      asm volatile(CAFXG_F64_PROLOGUE CAFXG_X4(CAFXG_F64_PAIR(
-          CAFXG_F64_STEP_EXACT)) CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS);
+#define CAFXG_B_FAST(X) asm volatile(CAFXG_F64_PROLOGUE X(CAFXG_F64_PAIR(CAFXG_F64_STEP_FAST)) \
+                                         CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS)
+#define CAFXG_B_EXACT(X) asm volatile(CAFXG_F64_PROLOGUE X(CAFXG_F64_PAIR(CAFXG_F64_STEP_EXACT)) \
+                                          CAFXG_F64_EPILOGUE CAFXG_F64_OPERANDS)
+    if constexpr (kExact) {
+      CAFXG_STEPS_SWITCH(kSteps, CAFXG_B_EXACT)
+    } else {
+      CAFXG_STEPS_SWITCH(kSteps, CAFXG_B_FAST)
+    }
+#undef CAFXG_B_FAST
+#undef CAFXG_B_EXACT
   }
   template <int kSteps, bool kExact>
   __device__ __forceinline__ void run_free() {
-    if constexpr (kSteps == 32 && !kExact)
-      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X32(CAFXG_F64_FREE2(CAFXG_F64_FREE_FAST))
-                       "}" CAFXG_F64_FREE_OPERANDS);
-    else if constexpr (kSteps == 32 && kExact)
-      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X32(CAFXG_F64_FREE2(CAFXG_F64_FREE_EXACT))
-                       "}" CAFXG_F64_FREE_OPERANDS);
-    else if constexpr (kSteps == 16 && !kExact)
-      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X16(CAFXG_F64_FREE2(CAFXG_F64_FREE_FAST))
-                       "}" CAFXG_F64_FREE_OPERANDS);
-    else if constexpr (kSteps == 16 && kExact)
-      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X16(CAFXG_F64_FREE2(CAFXG_F64_FREE_EXACT))
-                       "}" CAFXG_F64_FREE_OPERANDS);
-    else if constexpr (!kExact)
-      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X4(CAFXG_F64_FREE2(CAFXG_F64_FREE_FAST))
-                       "}" CAFXG_F64_FREE_OPERANDS);
-    else
-      asm volatile(CAFXG_F64_FREE_PROLOGUE CAFXG_X4(CAFXG_F64_FREE2(CAFXG_F64_FREE_EXACT))
-                       "}" CAFXG_F64_FREE_OPERANDS);
+#define CAFXG_B_FAST(X) asm volatile(CAFXG_F64_FREE_PROLOGUE X(CAFXG_F64_FREE2(CAFXG_F64_FREE_FAST)) \
+                                         "}" CAFXG_F64_FREE_OPERANDS)
+#define CAFXG_B_EXACT(X) asm volatile(CAFXG_F64_FREE_PROLOGUE X(CAFXG_F64_FREE2(CAFXG_F64_FREE_EXACT)) \
+                                          "}" CAFXG_F64_FREE_OPERANDS)
+    if constexpr (kExact) {
+      CAFXG_STEPS_SWITCH(kSteps, CAFXG_B_EXACT)
+    } else {
+      CAFXG_STEPS_SWITCH(kSteps, CAFXG_B_FAST)
+    }
+#undef CAFXG_B_FAST
+#undef CAFXG_B_EXACT
   }
   __device__ __forceinline__ void start(int s, double xr, double xi) {
     if (s == 0) {
@@ -616,7 +607,7 @@ constexpr size_t deferred_smem_bytes() {
   return sizeof(ReplayQueue<Slots>) * (kMandelThreads / 32);
 }
 
-template <class Slots, int kSteps, bool kExact>
+template <class Slots, int kUnit, bool kExact>
 __device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
                                        uint32_t first, uint32_t count, uint32_t maxit) {
   constexpr int NS = Slots::kSlots;
@@ -639,7 +630,9 @@ __device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
     }
   }
   __syncwarp();  // entries consumed before later pushes overwrite them
-  rp.template run<kSteps, kExact>(rn);
+#pragma unroll 1
+  for (uint32_t r = 0; r < L.block_reps; ++r)
+    rp.template run<kUnit, kExact>(rn);
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     if (ro[s] != 0xffffffffu) {
@@ -649,7 +642,7 @@ __device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
   }
 }
 
-template <class Slots, int kSteps, bool kExact, bool kInlineCoords>
+template <class Slots, int kUnit, bool kExact, bool kInlineCoords>
 __global__ void __launch_bounds__(kMandelThreads, 2)
     mandel_deferred_kernel(const __grid_constant__ MLaunch L) {
   constexpr int NS = Slots::kSlots;
@@ -660,11 +653,15 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t maxit = L.max_iter;
+  // block length: kUnit unrolled steps x block_reps (chosen by the host so
+  // that max_iter is (nearly) a multiple of it: no steps past max_iter)
+  const uint32_t reps = L.block_reps;
+  const uint32_t block = kUnit * reps;
 
   Feeder<Slots, kInlineCoords> feed;
   Slots sl;
   sl.zero = L.zero;
-  uint32_t n[NS];  // steps completed (a multiple of kSteps), all unescaped
+  uint32_t n[NS];  // steps completed (a multiple of the block), all unescaped
   uint32_t o[NS];
   uint32_t live = 0;
   uint32_t queued = 0;  // warp-uniform queue length
@@ -682,13 +679,15 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
       szr[s] = sl.zr_of(s);
       szi[s] = sl.zi_of(s);
     }
-    sl.template run_free<kSteps, kExact>();
+#pragma unroll 1
+    for (uint32_t r = 0; r < reps; ++r)
+      sl.template run_free<kUnit, kExact>();
     const uint32_t esc = sl.escaped() & live;
     uint32_t done = esc;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       if ((live & ~esc) >> s & 1u) {
-        n[s] += kSteps;
+        n[s] += block;
         if (n[s] >= maxit) {
           L.out[o[s]] = maxit;
           done |= 1u << s;
@@ -720,42 +719,49 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
     if (queued >= kBatch) {
       __syncwarp();
       queued -= kBatch;
-      replay<Slots, kSteps, kExact>(L, q, queued, kBatch, maxit);
+      replay<Slots, kUnit, kExact>(L, q, queued, kBatch, maxit);
     }
   }
   if (queued) {
     __syncwarp();
-    replay<Slots, kSteps, kExact>(L, q, 0, queued, maxit);
+    replay<Slots, kUnit, kExact>(L, q, 0, queued, maxit);
   }
   retire_block(L);
 }
 
 template <class A, int kSteps, bool kExact>
-int launch_t(const MLaunch& L, int grid, bool deferred, cudaStream_t s) {
-  if (deferred) {
-    constexpr size_t smem = deferred_smem_bytes<A>();
-    if (L.inline_coords)
-      mandel_deferred_kernel<A, kSteps, kExact, true><<<grid, kMandelThreads, smem, s>>>(L);
-    else
-      mandel_deferred_kernel<A, kSteps, kExact, false><<<grid, kMandelThreads, smem, s>>>(L);
-  } else if (L.inline_coords) {
+int launch_t(const MLaunch& L, int grid, cudaStream_t s) {
+  if (L.inline_coords)
     mandel_kernel<A, kSteps, kExact, true><<<grid, kMandelThreads, 0, s>>>(L);
-  } else {
+  else
     mandel_kernel<A, kSteps, kExact, false><<<grid, kMandelThreads, 0, s>>>(L);
-  }
+  return (int)cudaGetLastError();
+}
+
+template <class A, int kUnit, bool kExact>
+int launch_deferred_t(const MLaunch& L, int grid, cudaStream_t s) {
+  constexpr size_t smem = deferred_smem_bytes<A>();
+  if (L.inline_coords)
+    mandel_deferred_kernel<A, kUnit, kExact, true><<<grid, kMandelThreads, smem, s>>>(L);
+  else
+    mandel_deferred_kernel<A, kUnit, kExact, false><<<grid, kMandelThreads, smem, s>>>(L);
   return (int)cudaGetLastError();
 }
 
 template <class A, int kSteps, bool kExact>
-int occ_t(bool deferred) {
+int occ_t() {
   int n = 0;
-  if (deferred)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &n, mandel_deferred_kernel<A, kSteps, kExact, false>, kMandelThreads,
-        deferred_smem_bytes<A>());
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &n, mandel_kernel<A, kSteps, kExact, false>, kMandelThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mandel_kernel<A, kSteps, kExact, false>,
+                                                kMandelThreads, 0);
+  return n;
+}
+
+template <class A, int kUnit, bool kExact>
+int occ_deferred_t() {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &n, mandel_deferred_kernel<A, kUnit, kExact, false>, kMandelThreads,
+      deferred_smem_bytes<A>());
   return n;
 }
 
@@ -766,6 +772,7 @@ static_assert(deferred_smem_bytes<F64Slots>() <= 48 * 1024, "replay queues excee
 
 #define CAFXG_MANDEL_K(FN, SL, K, ...)                                 \
   return exact ? FN<SL, K, true>(__VA_ARGS__) : FN<SL, K, false>(__VA_ARGS__)
+// checked kernel: ksteps 4 / 16 / 32 between refills
 #define CAFXG_MANDEL_DISPATCH(FN, ...)                                 \
   do {                                                                 \
     if (precision == 0) {                                              \
@@ -777,13 +784,40 @@ static_assert(deferred_smem_bytes<F64Slots>() <= 48 * 1024, "replay queues excee
     if (ksteps <= 16) CAFXG_MANDEL_K(FN, F64Slots, 16, __VA_ARGS__);   \
     CAFXG_MANDEL_K(FN, F64Slots, 32, __VA_ARGS__);                     \
   } while (0)
+// deferred kernel: unrolled unit of 8 steps x runtime reps, or one
+// fully unrolled 32-step block
+#define CAFXG_DEFERRED_UNITS(FN, SL, ...)                              \
+  do {                                                                 \
+    if (unit == 8) CAFXG_MANDEL_K(FN, SL, 8, __VA_ARGS__);             \
+    if (unit == 16) CAFXG_MANDEL_K(FN, SL, 16, __VA_ARGS__);           \
+    if (unit == 24) CAFXG_MANDEL_K(FN, SL, 24, __VA_ARGS__);           \
+    if (unit == 40) CAFXG_MANDEL_K(FN, SL, 40, __VA_ARGS__);           \
+    if (unit == 48) CAFXG_MANDEL_K(FN, SL, 48, __VA_ARGS__);           \
+    if (unit == 56) CAFXG_MANDEL_K(FN, SL, 56, __VA_ARGS__);           \
+    if (unit == 64) CAFXG_MANDEL_K(FN, SL, 64, __VA_ARGS__);           \
+    CAFXG_MANDEL_K(FN, SL, 32, __VA_ARGS__);                           \
+  } while (0)
+// deferred kernel: an unrolled unit of 16..48 steps (x block_reps, normally
+// 1), or 8-step units x runtime reps for other block lengths
+#define CAFXG_DEFERRED_DISPATCH(FN, ...)                               \
+  do {                                                                 \
+    if (precision == 0)                                                \
+      CAFXG_DEFERRED_UNITS(FN, F32Slots, __VA_ARGS__);                 \
+    CAFXG_DEFERRED_UNITS(FN, F64Slots, __VA_ARGS__);                   \
+  } while (0)
 
-int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,
+int mandel_launch(const MLaunch& L0, int precision, const MandelLaunchCfg& cfg,
                   void* stream) {
-  const int ksteps = cfg.ksteps;
   const bool exact = cfg.exact;
   cudaStream_t s = (cudaStream_t)stream;
-  CAFXG_MANDEL_DISPATCH(launch_t, L, cfg.grid, cfg.deferred, s);
+  if (cfg.deferred) {
+    const int unit = cfg.unit;
+    MLaunch L = L0;
+    L.block_reps = (uint32_t)cfg.reps;
+    CAFXG_DEFERRED_DISPATCH(launch_deferred_t, L, cfg.grid, s);
+  }
+  const int ksteps = cfg.ksteps;
+  CAFXG_MANDEL_DISPATCH(launch_t, L0, cfg.grid, s);
 }
 
 int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
@@ -800,8 +834,10 @@ int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
   return (int)cudaGetLastError();
 }
 
-int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact, bool deferred) {
-  CAFXG_MANDEL_DISPATCH(occ_t, deferred);
+int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact, bool deferred, int unit) {
+  if (deferred)
+    CAFXG_DEFERRED_DISPATCH(occ_deferred_t);
+  CAFXG_MANDEL_DISPATCH(occ_t);
 }
 
 int mandel_slots_per_thread(int precision) {

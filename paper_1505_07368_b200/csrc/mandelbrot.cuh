@@ -44,6 +44,7 @@ struct MLaunch {
   uint32_t* sched;      // [0] chunk cursor, [1] finished blocks (self-reset)
   float zero;           // always 0.0f; opaque to ptxas (see the escape block)
   uint32_t inline_coords;  // 1: tiles carry no coordinate tables (cx == cy == null)
+  uint32_t block_reps;  // deferred kernel: unrolled units per unchecked block
 };
 
 // Host launchers (mandelbrot.cu). precision: 0 = fp32, 1 = fp64.
@@ -55,16 +56,18 @@ struct MLaunch {
 // 2 - 2^-10 < |c| < 2 + 2^-10, see mandelbrot.cu).
 struct MandelLaunchCfg {
   int grid;
-  int ksteps;      // steps between refills
+  int ksteps;      // checked kernel: steps between refills (4 / 16 / 32)
   bool exact;
   bool deferred;
+  int unit = 8;    // deferred kernel: unrolled steps per unit (8 or 32) ...
+  int reps = 4;    // ... and units per unchecked block (block = unit x reps)
 };
 int mandel_launch(const MLaunch& L, int precision, const MandelLaunchCfg& cfg,
                   void* stream);
 // Prologue: fills every tile's cx/cy tables (grid.y = tile).
 int mandel_coords_launch(const MLaunch& L, int precision, uint32_t max_extent,
                          void* stream);
-int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact, bool deferred);
+int mandel_max_blocks_per_sm(int precision, int ksteps, bool exact, bool deferred, int unit);
 int mandel_slots_per_thread(int precision);
 
 }  // namespace cafxg

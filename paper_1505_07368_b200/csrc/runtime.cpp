@@ -235,7 +235,7 @@ struct Device {
   bool stop = false;
   std::thread completer;
   std::atomic<int> inflight{0};
-  int mandel_occ[2][3][2][2] = {};  // [precision][ksteps 4/16/32][exact][deferred]
+  int mandel_occ[2][8][2][2] = {};  // see mandel_cfg
   // pinned staging ring for descriptor uploads (a pageable cudaMemcpyAsync
   // may wait for earlier work on the stream, serialising host and device)
   std::mutex up_mu;
@@ -548,6 +548,49 @@ static bool deferred_enabled() {
   return on;
 }
 
+// Unchecked block length B of the deferred kernel. Modelled cost per pixel
+// that never escapes, relative to max_iter steps:
+//   ceil(max_iter / B) * B / max_iter * (1 + alpha / B) + gamma * B
+// (overshoot past max_iter; block-end test and refill, ~alpha steps' worth;
+// replays of escaped blocks grow with B). alpha = 7 (fp32) / 2 (fp64: the
+// steps cost twice as much) and gamma = 0.002 fit the block-length sweep
+// (DESIGN.md §3.1): cfg3 (fp32, max_iter 1000) runs 38.0 / 35.7 / 35.2 /
+// 34.9 / 35.0 ms at B = 32 / 40 / 48 / 56 / 64 and picks 56; the fp64
+// reference mode (max_iter 500) picks 24. Each B is one fully unrolled PTX
+// block (8-step units in a runtime loop were 5% slower at B = 32).
+// CAFXG_BLOCK=<B> forces a length (multiple of 8; 16..64 unrolled).
+static void pick_block(uint32_t max_iter, int precision, MandelLaunchCfg& c) {
+  static const int env = [] {
+    const char* e = getenv("CAFXG_BLOCK");
+    return e ? atoi(e) : 0;
+  }();
+  auto set = [&](uint32_t b) {
+    if (b >= 16 && b <= 64 && b % 8 == 0) {
+      c.unit = (int)b;
+      c.reps = 1;
+    } else {
+      c.unit = 8;
+      c.reps = (int)(b / 8);
+    }
+  };
+  if (env >= 8 && env % 8 == 0) {
+    set((uint32_t)env);
+    return;
+  }
+  const double alpha = precision ? 2.0 : 7.0, gamma = 0.002;
+  uint32_t best = 32;
+  double best_cost = 1e300;
+  for (uint32_t b = 16; b <= 64; b += 8) {
+    const double over = (double)((max_iter + b - 1) / b * b) / max_iter;
+    const double cost = over * (1.0 + alpha / b) + gamma * b;
+    if (cost < best_cost) {
+      best = b;
+      best_cost = cost;
+    }
+  }
+  set(best);
+}
+
 static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
                                   bool exact, bool safe, uint64_t pixels) {
   MandelLaunchCfg c;
@@ -560,10 +603,15 @@ static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
     c.ksteps = ks_env;
   c.exact = exact;
   c.deferred = safe && max_iter >= 256 && deferred_enabled();
-  int& occ = d->mandel_occ[precision][c.ksteps == 4 ? 0 : c.ksteps == 16 ? 1 : 2][exact]
-                          [c.deferred];
+  if (c.deferred)
+    pick_block(max_iter, precision, c);
+  // occupancy per kernel variant: [precision][checked ksteps 4/16/32 |
+  // deferred unit 8/32][exact][deferred]
+  const int vi = c.deferred ? c.unit / 8 - 1 : (c.ksteps == 4 ? 0 : c.ksteps == 16 ? 1 : 2);
+  int& occ = d->mandel_occ[precision][vi][exact][c.deferred];
   if (occ == 0)
-    occ = std::max(1, mandel_max_blocks_per_sm(precision, c.ksteps, exact, c.deferred));
+    occ = std::max(1, mandel_max_blocks_per_sm(precision, c.ksteps, exact, c.deferred,
+                                               c.unit));
   const uint64_t per_block = (uint64_t)kMandelThreads * mandel_slots_per_thread(precision);
   uint64_t want = (pixels + per_block - 1) / per_block;
   uint64_t full = (uint64_t)d->sms * occ;

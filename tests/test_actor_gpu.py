@@ -92,6 +92,44 @@ def test_request_burst_from_many_clients(ctx, pinned):
     a.release()
 
 
+def test_staging_ring_reuse_and_oversized_request(ctx):
+    """The dispatcher's per-device staging ring: a burst of more batches than
+    ring slots (slot reuse ordered by the copy-out events), one request above
+    the 16M-pixel batch cap (its slot grows), then small requests again."""
+    a = ctx.spawn("mandelbrot")
+    W, H = 4096, 4200  # 17.2M px > kMaxBatchPx
+    big = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, W, H, 24)
+    mids = [pkg.mandel_desc(-2.0 + 0.01 * k, 1.0, -1.0, 1.0, 2048, 2048, 24)
+            for k in range(20)]  # 4M px each: several per batch, > 8 batches
+    out_big = ctx.pinned_empty(W * H, np.uint32)
+    out_mid = [ctx.pinned_empty(2048 * 2048, np.uint32) for _ in mids]
+    rng = np.random.default_rng(17)
+    smalls = [storm_tile(rng) for _ in range(32)]
+    out_small = [np.zeros(4096, np.uint32) for _ in smalls]
+    futs = [a.request([(pkg.MandelDesc * 1)(d)], o) for d, o in zip(mids[:10], out_mid[:10])]
+    futs.append(a.request([(pkg.MandelDesc * 1)(big)], out_big))
+    futs += [a.request([(pkg.MandelDesc * 1)(d)], o) for d, o in zip(mids[10:], out_mid[10:])]
+    futs += [a.request([(pkg.MandelDesc * 1)(d)], o) for d, o in zip(smalls, out_small)]
+    for f in futs:
+        f.result(timeout=120)
+    for r0 in (0, 2099, H - 1):
+        ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, W, H, 24, fp64=False, centre=True,
+                          row0=r0, nrows=1)
+        assert np.array_equal(out_big.reshape(H, W)[r0], ref[0])
+    for d, o in zip(mids, out_mid):
+        for r0 in (0, 1023, 2047):
+            ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, 2048, 2048, 24, fp64=False, centre=True,
+                              row0=r0, nrows=1)
+            assert np.array_equal(o.reshape(2048, 2048)[r0], ref[0])
+    for d, o in zip(smalls, out_small):
+        ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, 64, 64, 256, fp64=True, centre=True)
+        assert np.array_equal(o.reshape(64, 64), ref)
+    ctx.pinned_free(out_big)
+    for o in out_mid:
+        ctx.pinned_free(o)
+    a.release()
+
+
 def test_multi_tile_request(ctx):
     a = ctx.spawn("mandelbrot")
     rng = np.random.default_rng(5)

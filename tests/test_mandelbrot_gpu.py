@@ -187,6 +187,34 @@ with pkg.Context(1) as c:
         assert np.array_equal(res["00"], res[k]), k
 
 
+def test_every_block_length_is_exact():
+    """The deferred kernel's unchecked block length (picked per launch from
+    max_iter) is forced through CAFXG_BLOCK to every
+    unrolled length 16..64 and to 8-step units x runtime reps (72); each
+    result equals the oracle, fp32 and fp64."""
+    cases = [(-0.75, -0.73, 0.10, 0.12, 300, 200, 1000, False),
+             (-0.7487, -0.7485, 0.0650, 0.0652, 160, 120, 2777, False),
+             (-1.5, 0.5, -1.0, 1.0, 240, 200, 500, True),
+             (-0.16, -0.14, 1.03, 1.05, 120, 100, 1234, True)]
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+cases = %r
+with pkg.Context(1) as c:
+    outs = [c.mandelbrot(pkg.mandel_desc(x0, x1, y0, y1, w, h, it, fp64=f))
+            for (x0, x1, y0, y1, w, h, it, f) in cases]
+np.save(sys.argv[1], np.concatenate(outs))
+""" % (ROOT, cases)
+    want = np.concatenate([oracle.tile(x0, x1, y0, y1, w, h, it, fp64=f, centre=True).ravel()
+                           for (x0, x1, y0, y1, w, h, it, f) in cases])
+    for b in (16, 24, 32, 40, 48, 56, 64, 72):
+        path = f"/tmp/cafxg_block_{b}.npy"
+        env = dict(os.environ, CAFXG_BLOCK=str(b))
+        subprocess.check_call([sys.executable, "-c", code, path], env=env)
+        assert np.array_equal(np.load(path), want), b
+
+
 def test_multi_tile_batch_and_offsets(ctx):
     tiles, refs, off = [], [], 0
     rng = np.random.default_rng(3)
