@@ -360,14 +360,14 @@ def run_ours(args):
     peak_tops = sms * 128 * sm_max * 1e6 / 1e12
     achieved = 8.0 * iters_local / (kernel_ms / 1e3) / 1e12
     # DRAM traffic of the escape kernel from the committed ncu capture of the
-    # full-image launch (profiles/round1/mandel_cfg3_deferred_full.txt:
-    # 1.020146 GB written + 10.927616 MB read), scaled to this rank's share
-    traffic = round((1.020146e9 + 10.927616e6) * npx / (W_IMG * H_IMG))
-    # The same capture: FMA pipe busy 85.5% of active cycles over 36.72 ms at
-    # 1.963 GHz = 1.17e12 executed FP32 lane-ops for 1.82e11 iterations, i.e.
-    # 6.41 executed lane-ops per iteration (6 in the unchecked step, the rest
-    # block-end tests and replays) against the algorithmic 8.
-    exec_ops_per_iter = 6.41
+    # full-image launch (profiles/round1/mandel_cfg3_b56_full.txt:
+    # 1.020756 GB written + 10.830336 MB read), scaled to this rank's share
+    traffic = round((1.020756e9 + 10.830336e6) * npx / (W_IMG * H_IMG))
+    # The same capture: FMA pipe busy 90.6% of active cycles over 34.85 ms at
+    # 1.964 GHz = 1.175e12 FMA-pipe lane-cycles for 1.82e11 iterations, i.e.
+    # 6.45 executed lane-ops per iteration (6 in the unchecked step, the rest
+    # block-end tests, refills and exact replays) against the algorithmic 8.
+    exec_ops_per_iter = 6.45
     roof = {"bound": "fp32_pipe", "achieved": round(achieved, 3), "peak": round(peak_tops, 3),
             "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4), "traffic": traffic,
             "traffic_note": "dram read+write bytes per launch (ncu, profiles/round1); "
@@ -378,10 +378,10 @@ def run_ours(args):
                           "(3 mul + 5 add, SURVEY §8d)",
             "frac_executed": round(achieved / peak_tops * exec_ops_per_iter / 8.0, 4),
             "frac_note": "frac counts the reference's 8 FP ops per iteration; the kernel "
-                         "executes 6 per iteration (escape test deferred to 32-step block "
-                         "ends, 2*zr*zi+ci as one FMA) plus block-end tests and exact "
-                         "replays, 6.41 lane-ops/iteration measured (ncu FMA pipe busy "
-                         "85.5%, profiles/round1/mandel_cfg3_deferred_full.txt); "
+                         "executes 6 per iteration (escape test deferred to the ends of "
+                         "56-step unchecked blocks, 2*zr*zi+ci as one FMA) plus block-end "
+                         "tests and exact replays, 6.45 lane-ops/iteration measured (ncu "
+                         "FMA pipe busy 90.6%, profiles/round1/mandel_cfg3_b56_full.txt); "
                          "frac_executed is the pipe fraction doing that executed work"}
     if clk.get("sm_mhz"):
         peak_clk = sms * 128 * clk["sm_mhz"] * 1e6 / 1e12
