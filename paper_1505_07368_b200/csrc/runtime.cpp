@@ -31,6 +31,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <shared_mutex>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -92,12 +93,10 @@ class PinnedPool {
     }
     std::lock_guard<std::mutex> g(mu_);
     live_[p] = cls;
-    ranges_[(uintptr_t)p] = cls;
-    // publish a new immutable snapshot for the lock-free contains(); older
-    // snapshots may still be read and are kept until the pool dies
-    auto* snap = new std::vector<std::pair<uintptr_t, size_t>>(ranges_.begin(), ranges_.end());
-    retired_.emplace_back(snap);
-    snap_.store(snap, std::memory_order_release);
+    {
+      std::unique_lock<std::shared_mutex> w(ranges_mu_);
+      ranges_[(uintptr_t)p] = cls;
+    }
     return p;
   }
 
@@ -111,23 +110,31 @@ class PinnedPool {
     return true;
   }
 
-  // [p, p+bytes) inside one pool buffer (no driver call, no lock: every
-  // client thread classifies its reply buffer here). Pool buffers stay
-  // pinned and device-mapped until the context closes, so a buffer that is
-  // currently on the free list still qualifies.
+  // [p, p+bytes) inside one pool buffer (no driver call). Every client
+  // thread classifies its reply buffer here, so the common case takes no lock
+  // at all: a thread-local cache of the last buffer hit (pool buffers stay
+  // pinned and device-mapped until the context closes, so a cached range
+  // never goes stale, and a buffer on the free list still qualifies);
+  // otherwise a shared (reader) lock on the range map.
   bool contains(const void* p, size_t bytes) const {
-    const auto* snap = snap_.load(std::memory_order_acquire);
-    if (!snap || snap->empty())
-      return false;
+    struct Hit {
+      uint64_t pool = 0;
+      uintptr_t base = 0;
+      size_t size = 0;
+    };
+    thread_local Hit hit;
     const uintptr_t a = (uintptr_t)p;
-    auto it = std::upper_bound(snap->begin(), snap->end(), a,
-                               [](uintptr_t v, const std::pair<uintptr_t, size_t>& e) {
-                                 return v < e.first;
-                               });
-    if (it == snap->begin())
+    if (hit.pool == id_ && a >= hit.base && a + bytes <= hit.base + hit.size)
+      return true;
+    std::shared_lock<std::shared_mutex> r(ranges_mu_);
+    auto it = ranges_.upper_bound(a);
+    if (it == ranges_.begin())
       return false;
     --it;
-    return a + bytes <= it->first + it->second;
+    if (a + bytes > it->first + it->second)
+      return false;
+    hit = Hit{id_, it->first, it->second};
+    return true;
   }
 
  private:
@@ -140,9 +147,12 @@ class PinnedPool {
   std::mutex mu_;
   std::unordered_map<void*, size_t> live_;
   std::map<size_t, std::vector<void*>> free_;
+  mutable std::shared_mutex ranges_mu_;
   std::map<uintptr_t, size_t> ranges_;  // every buffer ever allocated
-  std::atomic<const std::vector<std::pair<uintptr_t, size_t>>*> snap_{nullptr};
-  std::vector<std::unique_ptr<std::vector<std::pair<uintptr_t, size_t>>>> retired_;
+  // unique per pool instance (never reused), so a thread-local cache entry of
+  // a closed context can never match a later one
+  static inline std::atomic<uint64_t> next_id_{1};
+  const uint64_t id_ = next_id_.fetch_add(1);
 };
 
 // True when [p, p+bytes) is page-locked host memory the device can address
@@ -1036,13 +1046,20 @@ static bool sgemm_pipeline_eligible(const cafxg_sgemm_desc& g, uint32_t rows) {
          sgemm_tc_supported(128, g.N, g.K, g.K, g.N, g.N);
 }
 
+// hostB: when non-null, B (K x N, host) is uploaded here on the upload
+// stream, ahead of the A blocks, instead of by the caller into dB: the first A
+// block then follows B over PCIe without waiting for B's split.
 static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
                                  const float* A, const float* dB, float* C, uint32_t r0,
-                                 uint32_t r1) {
+                                 uint32_t r1, const float* hostB = nullptr) {
   const size_t N = g.N, K = g.K;
   const uint32_t rows = r1 - r0;
   uint32_t R = ((rows + 7) / 8 + 127) / 128 * 128;  // ~8 blocks of whole 128-row tiles
-  R = std::max<uint32_t>(R, 512);
+  static const uint32_t rmin = [] {  // CAFXG_SGEMM_RMIN: experiments only
+    const char* e = getenv("CAFXG_SGEMM_RMIN");
+    return e ? (uint32_t)atoi(e) : 512u;
+  }();
+  R = std::max<uint32_t>(R, rmin);
   float *Bh = nullptr, *Bl = nullptr, *Ah = nullptr, *Al = nullptr;
   float* dA[2] = {nullptr, nullptr};
   float* dC[2] = {nullptr, nullptr};
@@ -1055,11 +1072,17 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
     CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dA[b], (size_t)R * K * 4, cs));
     CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dC[b], (size_t)R * N * 4, cs));
   }
+  CAFXG_TRY(stream_after(d->h2d, cs));  // the buffers exist before uploads
+  if (hostB) {
+    CAFXG_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(dB), hostB, K * N * 4,
+                                   cudaMemcpyHostToDevice, d->h2d));
+    ctx->st_h2d += K * N * 4;
+    CAFXG_TRY(stream_after(cs, d->h2d));
+  }
   int e = sgemm_tc_split_b(dB, (int)N, (int)K, (int)N, Bh, Bl, cs);
   if (e != 0)
     return cuda_status((cudaError_t)e, "sgemm: B split");
   ctx->st_launches++;
-  CAFXG_TRY(stream_after(d->h2d, cs));  // the buffers exist before uploads
   std::vector<cudaEvent_t> ev_split, ev_gemm, ev_down;
   auto mk = [](std::vector<cudaEvent_t>& v) {
     cudaEvent_t ev;
@@ -1090,7 +1113,8 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
     e = sgemm_tc_split_a(dA[slot], (int)K, (int)m, (int)K, Ah, Al, cs);
     cudaEventRecord(mk(ev_split), cs);
     if (e == 0)
-      e = sgemm_tc_gemm(Ah, Al, Bh, Bl, dC[slot], (int)m, (int)N, (int)K, (int)N, cs);
+      e = sgemm_tc_gemm(Ah, Al, Bh, Bl, dC[slot], (int)m, (int)N, (int)K, (int)N, cs,
+                        sgemm_tc_splits((int)m, (int)N, (int)K, d->sms));
     if (e != 0)
       status = cuda_status((cudaError_t)e, "sgemm: 3xtf32 launch");
     ctx->st_launches += 2;
@@ -1152,6 +1176,7 @@ static int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
   for (size_t k = 0; k < use; ++k)
     locks.emplace_back(ctx->devs[k]->submit_mu);
   int status = CAFXG_OK;
+  const bool defer_b = use == 1 && g.M && g.ldb == g.N && sgemm_pipeline_eligible(g, g.M);
   for (size_t k = 0; k < use && status == CAFXG_OK; ++k) {
     Device* d = ctx->devs[k].get();
     cudaSetDevice(d->ordinal);
@@ -1159,6 +1184,8 @@ static int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
       status = cuda_status(cudaGetLastError(), "sgemm: device B allocation");
       break;
     }
+    if (defer_b)
+      continue;  // uploaded by sgemm_pipeline_device on the upload stream
     size_t k0 = use == 1 ? 0 : (size_t)g.K / use * k;
     size_t kn = use == 1 ? g.K : (size_t)g.K / use;
     if (kn && cudaMemcpyAsync(dB[k] + k0 * g.ldb, B + k0 * g.ldb, kn * g.ldb * 4,
@@ -1228,7 +1255,7 @@ static int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
     part.ldc = g.N;
     float *dA = nullptr, *dC = nullptr;
     if (s == CAFXG_OK && part.M && g.ldb == g.N && sgemm_pipeline_eligible(g, part.M)) {
-      s = sgemm_pipeline_device(ctx, d, g, A, dB[k], C, r0, r1);
+      s = sgemm_pipeline_device(ctx, d, g, A, dB[k], C, r0, r1, defer_b ? B : nullptr);
       cudaFreeAsync(dB[k], d->d2h);
       if (s != CAFXG_OK)
         push_completion(ctx, d, d->d2h, [join, s](int) { join->part_done(s); });

@@ -25,11 +25,9 @@ int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al
 int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl,
                      void* stream);
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl,
-                  float* C, int M, int N, int K, int ldc, void* stream, int splits = 1,
-                  float* work = nullptr);
-// split-K factor for small C grids and its workspace (splits * M * N floats)
+                  float* C, int M, int N, int K, int ldc, void* stream, int splits = 1);
+// split-K factor (thread-block cluster size, <= 8) for small C grids
 int sgemm_tc_splits(int M, int N, int K, int sms);
-size_t sgemm_tc_work_bytes(int M, int N, int K, int sms);
 
 // Device FNV-1a-64 over u32 cells hashed big-endian (fnv.cu).
 size_t fnv_scratch_bytes(uint64_t n, int sms);

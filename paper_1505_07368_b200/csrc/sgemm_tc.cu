@@ -49,6 +49,8 @@ constexpr uint32_t TMEM_COLS = 512;                       // 2 x 256-column accu
 // round-to-nearest, which keeps the error at the per-chunk level.
 constexpr int CHUNK_KB = 8;                               // k-blocks per chunk (128 K)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+static_assert(BM * BN * 4 <= STAGES * STAGE_BYTES, "split-K partial must fit the stages");
+constexpr int kMaxSplits = 8;  // portable cluster size
 
 // ---- PTX helpers -----------------------------------------------------------
 
@@ -133,6 +135,31 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// split-K partial tile (128 x 256 fp32) in shared memory, float4 granules:
+// row r, column granule c4 (0..63) XOR-swizzled by r % 8 so a warp storing
+// one granule of 32 consecutive rows hits 8 distinct 16-byte bank groups
+__device__ __forceinline__ int partial_index(int r, int c4) {
+  return r * (BN / 4) + (c4 ^ (r & 7));
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// 16-byte load from the shared memory of cluster CTA `rank` at the address
+// that `local` has in this CTA
+__device__ __forceinline__ float4 ld_cluster_f4(uint32_t local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote)
+               : "memory");
+  return v;
+}
+
 // ---- the GEMM kernel --------------------------------------------------------
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -140,9 +167,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         const __grid_constant__ CUtensorMap mAl,
                         const __grid_constant__ CUtensorMap mBh,
                         const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
-                        int M, int N, int K, int ldc, int splits, float* __restrict__ work) {
-  // split-K: CTA z of `splits` covers K range [z*K/splits, (z+1)*K/splits) and
-  // writes its partial tile to work + z*M*N (summed by splitk_reduce_kernel)
+                        int M, int N, int K, int ldc, int splits) {
+  // split-K: the `splits` CTAs of one C tile form a thread-block cluster; CTA
+  // z covers K range [z*K/splits, (z+1)*K/splits), parks its partial tile in
+  // its own shared memory, and after a cluster barrier each CTA sums 1/splits
+  // of the tile's rows over the peers' partials through distributed shared
+  // memory, in fixed z order (deterministic; no workspace, no extra launch)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -157,9 +187,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // grouped raster: GROUP_M consecutive M tiles share each N tile
   const int tiles_m = M / BM, tiles_n = N / BN;
   const int per_group = GROUP_M * tiles_n;
-  const int tiles = tiles_m * tiles_n;
-  const int kz = blockIdx.x / tiles;
-  const int bid = blockIdx.x % tiles;
+  const int kz = blockIdx.x % splits;   // == %cluster_ctarank (cluster = splits x 1 x 1)
+  const int bid = blockIdx.x / splits;
   const int first_m = (bid / per_group) * GROUP_M;
   const int gsize = min(GROUP_M, tiles_m - first_m);
   const int in_group = bid % per_group;
@@ -168,10 +197,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int ksplit = K / splits;
   const int k_base = kz * ksplit;
   const int nk = ksplit / BK;
-  if (splits > 1) {
-    C = work + (size_t)kz * M * N;
-    ldc = N;
-  }
 
   if (warp == 0 && lane == 0) {
     for (const CUtensorMap* m : {&mAh, &mAl, &mBh, &mBl})
@@ -267,37 +292,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&acc_empty[b]))
                      : "memory");
     }
-    float* crow = C + (size_t)(m0 + row) * ldc + n0 + half * 128;
+    if (splits == 1) {
+      float* crow = C + (size_t)(m0 + row) * ldc + n0 + half * 128;
 #pragma unroll
-    for (int j = 0; j < 128; j += 4)
-      *reinterpret_cast<float4*>(crow + j) =
-          make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+      for (int j = 0; j < 128; j += 4)
+        *reinterpret_cast<float4*>(crow + j) =
+            make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+    } else {
+      // partial tile into the (now idle) stage buffers: the last acc_full
+      // commit follows every MMA, so no TMA write or MMA read is pending
+      float4* part = reinterpret_cast<float4*>(smem);
+#pragma unroll
+      for (int j = 0; j < 128; j += 4)
+        part[partial_index(row, half * 32 + j / 4)] =
+            make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (splits > 1) {
+    cluster_sync();  // every partial of the cluster is written
+    const int rows = BM / splits;
+    const uint32_t mine = smem_u32(smem);
+    for (int i = threadIdx.x; i < rows * (BN / 4); i += TC_THREADS) {
+      const int r = kz * rows + i / (BN / 4), c4 = i % (BN / 4);
+      const uint32_t off = (uint32_t)partial_index(r, c4) * 16u;
+      float4 acc = ld_cluster_f4(mine + off, 0);
+      for (int z = 1; z < splits; ++z) {
+        const float4 v = ld_cluster_f4(mine + off, (uint32_t)z);
+        acc.x = __fadd_rn(acc.x, v.x);
+        acc.y = __fadd_rn(acc.y, v.y);
+        acc.z = __fadd_rn(acc.z, v.z);
+        acc.w = __fadd_rn(acc.w, v.w);
+      }
+      *reinterpret_cast<float4*>(C + (size_t)(m0 + r) * ldc + n0 + c4 * 4) = acc;
+    }
+    cluster_sync();  // the peers are done reading this CTA's partial
+  }
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
-}
-
-// C = sum of the split-K partials, in fixed order (deterministic)
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ work,
-                                                            int splits, int M, int N,
-                                                            float* __restrict__ C, int ldc) {
-  const size_t total = (size_t)M * N / 4;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x) {
-    float4 acc = reinterpret_cast<const float4*>(work)[i];
-    for (int z = 1; z < splits; ++z) {
-      float4 v = reinterpret_cast<const float4*>(work + (size_t)z * M * N)[i];
-      acc.x = __fadd_rn(acc.x, v.x);
-      acc.y = __fadd_rn(acc.y, v.y);
-      acc.z = __fadd_rn(acc.z, v.z);
-      acc.w = __fadd_rn(acc.w, v.w);
-    }
-    size_t e = i * 4, r = e / N, c = e % N;
-    *reinterpret_cast<float4*>(C + r * ldc + c) = acc;
-  }
 }
 
 // ---- hi/lo split ----------------------------------------------------------
@@ -339,6 +373,48 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float* __res
   __shared__ float th[32][33], tl[32][33];
   const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int j = ty; j < 32; j += 8) {
+    float h, l;
+    split_tf32(B[(size_t)(k0 + j) * ldb + n0 + tx], h, l);
+    th[j][tx] = h;
+    tl[j][tx] = l;
+  }
+  __syncthreads();
+  for (int j = ty; j < 32; j += 8) {
+    Bth[(size_t)(n0 + j) * K + k0 + tx] = th[tx][j];
+    Btl[(size_t)(n0 + j) * K + k0 + tx] = tl[tx][j];
+  }
+}
+
+// Both operands in one launch (device-API requests): blocks [0, nb_a) split
+// A's rows, the rest split + transpose 32 x 32 tiles of B.
+__global__ void __launch_bounds__(256) split_ab_kernel(const float* __restrict__ A, int lda,
+                                                       int M, int K, float* __restrict__ Ah,
+                                                       float* __restrict__ Al,
+                                                       const float* __restrict__ B, int ldb,
+                                                       int N, float* __restrict__ Bth,
+                                                       float* __restrict__ Btl, int nb_a) {
+  __shared__ float th[32][33], tl[32][33];
+  if ((int)blockIdx.x < nb_a) {
+    const size_t total = (size_t)M * K;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total / 4;
+         i += (size_t)nb_a * blockDim.x) {
+      size_t e = i * 4;
+      size_t r = e / K, c = e % K;
+      float4 v = *reinterpret_cast<const float4*>(A + r * lda + c);
+      float4 h, l;
+      split_tf32(v.x, h.x, l.x);
+      split_tf32(v.y, h.y, l.y);
+      split_tf32(v.z, h.z, l.z);
+      split_tf32(v.w, h.w, l.w);
+      *reinterpret_cast<float4*>(Ah + e) = h;
+      *reinterpret_cast<float4*>(Al + e) = l;
+    }
+    return;
+  }
+  const int t = (int)blockIdx.x - nb_a, tn = N / 32;
+  const int k0 = (t / tn) * 32, n0 = (t % tn) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int j = ty; j < 32; j += 8) {
     float h, l;
     split_tf32(B[(size_t)(k0 + j) * ldb + n0 + tx], h, l);
@@ -396,9 +472,9 @@ bool sgemm_tc_supported(int M, int N, int K, int lda, int ldb, int ldc) {
 }
 
 size_t sgemm_tc_scratch_bytes(int M, int N, int K) {
-  // hi/lo splits of A and B^T, plus the split-K workspace (148 SMs)
-  return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float) +
-         sgemm_tc_work_bytes(M, N, K, 148);
+  // hi/lo splits of A and B^T (split-K reduces through distributed shared
+  // memory and needs no workspace)
+  return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float);
 }
 
 int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al,
@@ -416,23 +492,19 @@ int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl
   return (int)cudaGetLastError();
 }
 
-// Split-K factor that fills the GPU when the C tile grid alone cannot (each
-// split keeps >= 8 k-blocks of 16 and a multiple of 32 in K).
+// Split-K factor (cluster size) for C grids too small to fill the GPU: the
+// largest power of two <= 8 that keeps the grid within one wave (one CTA per
+// SM) and every split >= 128 deep in K (one accumulator chunk).
 int sgemm_tc_splits(int M, int N, int K, int sms) {
   const int tiles = (M / BM) * (N / BN);
   int s = 1;
-  while (s < 8 && tiles * s * 2 <= 2 * sms && K % (32 * s * 2) == 0 && K / (s * 2) >= 128)
+  while (s < kMaxSplits && tiles * s * 2 <= sms && K % (16 * s * 2) == 0 && K / (s * 2) >= 128)
     s *= 2;
   return s;
 }
 
-size_t sgemm_tc_work_bytes(int M, int N, int K, int sms) {
-  int s = sgemm_tc_splits(M, N, K, sms);
-  return s > 1 ? (size_t)s * M * N * sizeof(float) : 0;
-}
-
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl, float* C,
-                  int M, int N, int K, int ldc, void* stream, int splits, float* work) {
+                  int M, int N, int K, int ldc, void* stream, int splits) {
   CUtensorMap mAh, mAl, mBh, mBl;
   if (!make_map(&mAh, Ah, M, K, BM) || !make_map(&mAl, Al, M, K, BM) ||
       !make_map(&mBh, Bh, N, K, BN) || !make_map(&mBl, Bl, N, K, BN))
@@ -448,35 +520,43 @@ int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float
       configured.fetch_or(1ull << dev);
     }
   }
-  if (splits < 1 || !work)
+  if (splits < 1 || splits > kMaxSplits || (splits & (splits - 1)) ||
+      K % (16 * splits) != 0)
     splits = 1;
-  int tiles = (M / BM) * (N / BN);
-  sgemm_3xtf32_kernel<<<tiles * splits, TC_THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
-      mAh, mAl, mBh, mBl, C, M, N, K, ldc, splits, work);
-  if (splits > 1) {
-    int grid = (int)std::min<size_t>(((size_t)M * N / 4 + 255) / 256, 148 * 8);
-    splitk_reduce_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(work, splits, M, N, C, ldc);
-  }
+  const int tiles = (M / BM) * (N / BN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(tiles * splits));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)splits;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel, mAh, mAl, mBh, mBl, C, M, N, K, ldc, splits);
   return (int)cudaGetLastError();
 }
 
 int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int K, int lda,
                     int ldb, int ldc, void* scratch, int sm_count, void* stream,
                     int* launches) {
-  (void)sm_count;
   float* Ah = static_cast<float*>(scratch);
   float* Al = Ah + (size_t)M * K;
   float* Bh = Al + (size_t)M * K;
   float* Bl = Bh + (size_t)N * K;
-  const int splits = sgemm_tc_splits(M, N, K, 148);  // as sgemm_tc_scratch_bytes
-  float* work = splits > 1 ? Bl + (size_t)N * K : nullptr;
-  int e = sgemm_tc_split_a(A, lda, M, K, Ah, Al, stream);
+  const int splits = sgemm_tc_splits(M, N, K, sm_count > 0 ? sm_count : 148);
+  const int nb_a = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 8);
+  const int nb_b = (N / 32) * (K / 32);
+  split_ab_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B, ldb,
+                                                                 N, Bh, Bl, nb_a);
+  int e = (int)cudaGetLastError();
   if (e == 0)
-    e = sgemm_tc_split_b(B, ldb, K, N, Bh, Bl, stream);
-  if (e == 0)
-    e = sgemm_tc_gemm(Ah, Al, Bh, Bl, C, M, N, K, ldc, stream, splits, work);
+    e = sgemm_tc_gemm(Ah, Al, Bh, Bl, C, M, N, K, ldc, stream, splits);
   if (launches)
-    *launches = splits > 1 ? 4 : 3;
+    *launches = 2;
   return e;
 }
 

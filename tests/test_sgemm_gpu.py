@@ -71,6 +71,31 @@ def test_sgemm_3xtf32(ctx, M, N, K):
     assert check(A, B, C) <= TOL
 
 
+@pytest.mark.parametrize("M,N,K,splits", [(128, 256, 1024, 8), (256, 512, 512, 4),
+                                          (512, 1024, 256, 2), (1024, 1024, 1024, 4),
+                                          (2048, 2048, 512, 1)])
+def test_sgemm_cluster_split_k(ctx, M, N, K, splits):
+    """Small C grids split K across a thread-block cluster of 2/4/8 CTAs that
+    reduce their partial tiles through distributed shared memory: within the
+    tolerance, and bit-identical from run to run (fixed summation order).
+    `splits` is the factor sgemm_tc_splits picks for the shape on 148 SMs."""
+    import torch
+    A = torch.from_numpy(oracle.fill_uniform(M * K, 31).reshape(M, K)).cuda()
+    B = torch.from_numpy(oracle.fill_uniform(K * N, 32).reshape(K, N)).cuda()
+    outs = []
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    for _ in range(2):
+        C = torch.full((M, N), float("nan"), device="cuda")
+        ctx.sgemm_device(M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream,
+                         mode=pkg.SGEMM_3XTF32)
+        torch.cuda.synchronize()
+        outs.append(C.cpu().numpy())
+    assert not np.isnan(outs[0]).any()
+    assert np.array_equal(outs[0], outs[1])
+    assert check(A.cpu().numpy(), B.cpu().numpy(), outs[0]) <= TOL
+
+
 @pytest.mark.parametrize("M,N,K,pad", [(3072, 512, 256, 0), (1280, 256, 512, 8)])
 def test_sgemm_pipelined_host_request(ctx, M, N, K, pad):
     """Host request >= 1024 rows: row-block pipeline (upload / 3xTF32 / download
