@@ -29,3 +29,32 @@ with pkg.Context(1) as ctx:
         print(f"n={n} e2e median {statistics.median(ts):.3f} ms  min {min(ts):.3f} ms", flush=True)
         for h in (hA, hB, hC):
             ctx.pinned_free(h)
+
+# host-side cost of the submit call itself (API calls, planning) vs the wait
+import ctypes as C  # noqa: E402
+with pkg.Context(1) as ctx:
+    L = pkg.lib()
+    for n in sizes:
+        hA, hB = ctx.pinned_empty((n, n), np.float32), ctx.pinned_empty((n, n), np.float32)
+        hC = ctx.pinned_empty((n, n), np.float32)
+        d = pkg.SgemmDesc()
+        d.M = d.N = d.K = n
+        d.lda = d.ldb = d.ldc = n
+        d.mode = pkg.SGEMM_AUTO
+        from paper_1505_07368_b200.cafxg import DONE_FN  # noqa: E402
+        noop = DONE_FN(lambda u, s: None)
+        sub, tot = [], []
+        for k in range(40):
+            t0 = time.perf_counter()
+            L.cafxg_sgemm_submit(ctx.handle, C.byref(d), hA.ctypes.data, hB.ctypes.data,
+                                 hC.ctypes.data, noop, None)
+            t1 = time.perf_counter()
+            ctx.sync()
+            t2 = time.perf_counter()
+            if k >= 5:
+                sub.append((t1 - t0) * 1e3)
+                tot.append((t2 - t0) * 1e3)
+        print(f"n={n} submit call {statistics.median(sub):.3f} ms, submit+sync "
+              f"{statistics.median(tot):.3f} ms", flush=True)
+        for h in (hA, hB, hC):
+            ctx.pinned_free(h)
