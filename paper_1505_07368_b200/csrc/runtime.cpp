@@ -1026,6 +1026,19 @@ static int ensure_nccl(cafxg_ctx* ctx) {
 }
 
 // Streams `b` waits for what `a` has enqueued so far.
+static double trace_now_ms() {
+  static const auto t0 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+static bool trace_on() {
+  static const bool on = [] {
+    const char* e = getenv("CAFXG_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 static int stream_after(cudaStream_t b, cudaStream_t a) {
   cudaEvent_t ev;
   CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1073,10 +1086,23 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
     CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dC[b], (size_t)R * N * 4, cs));
   }
   CAFXG_TRY(stream_after(d->h2d, cs));  // the buffers exist before uploads
+  // CAFXG_TRACE=1: device timeline of the request (uploads, GEMMs, downloads)
+  std::vector<std::pair<const char*, cudaEvent_t>> tev;
+  const double t_host0 = trace_now_ms();
+  auto tmark = [&](const char* what, cudaStream_t sm) {
+    if (!trace_on())
+      return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, sm);
+    tev.emplace_back(what, e);
+  };
+  tmark("start", d->h2d);
   if (hostB) {
     CAFXG_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(dB), hostB, K * N * 4,
                                    cudaMemcpyHostToDevice, d->h2d));
     ctx->st_h2d += K * N * 4;
+    tmark("B up", d->h2d);
     CAFXG_TRY(stream_after(cs, d->h2d));
   }
   int e = sgemm_tc_split_b(dB, (int)N, (int)K, (int)N, Bh, Bl, cs);
@@ -1107,6 +1133,7 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
                                              cudaMemcpyHostToDevice, d->h2d),
                            "sgemm: A upload");
     ctx->st_h2d += (size_t)m * K * 4;
+    tmark("A up", d->h2d);
     CAFXG_TRY(stream_after(cs, d->h2d));
     if (i >= 2)
       cudaStreamWaitEvent(cs, ev_down[i - 2], 0);  // C slot drained
@@ -1118,6 +1145,7 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
     if (e != 0)
       status = cuda_status((cudaError_t)e, "sgemm: 3xtf32 launch");
     ctx->st_launches += 2;
+    tmark("gemm", cs);
     cudaEventRecord(mk(ev_gemm), cs);
     cudaStreamWaitEvent(d->d2h, ev_gemm.back(), 0);
     if (status == CAFXG_OK)
@@ -1126,7 +1154,23 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
                                              cudaMemcpyDeviceToHost, d->d2h),
                            "sgemm: C download");
     ctx->st_d2h += (size_t)m * N * 4;
+    tmark("C down", d->d2h);
     cudaEventRecord(mk(ev_down), d->d2h);
+  }
+  if (!tev.empty()) {
+    const double t_host1 = trace_now_ms();
+    cudaEventSynchronize(tev.back().second);
+    const double t_seen = trace_now_ms();
+    fprintf(stderr, "cafxg sgemm trace: host enqueue %.3f ms, sync seen at %.3f ms; device:",
+            t_host1 - t_host0, t_seen - t_host0);
+    for (auto& [what, e] : tev) {
+      float t = 0;
+      cudaEventElapsedTime(&t, tev[0].second, e);
+      fprintf(stderr, " %s %.3f", what, t);
+    }
+    fprintf(stderr, "\n");
+    for (auto& pe : tev)
+      cudaEventDestroy(pe.second);
   }
   // everything is released on the download stream, which by now follows
   // every upload and kernel of this request
@@ -1375,19 +1419,6 @@ static void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* 
 // over every tile of every request into a device staging buffer, then one
 // scatter launch straight into the pinned reply buffers (or one D2H into a
 // pinned bounce buffer + host memcpy for pageable replies).
-static double trace_now_ms() {
-  static const auto t0 = std::chrono::steady_clock::now();
-  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-}
-
-static bool trace_on() {
-  static const bool on = [] {
-    const char* e = getenv("CAFXG_TRACE");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 static void callback_loop(cafxg_ctx* ctx) {
   while (true) {
     std::function<void()> job;
