@@ -492,13 +492,45 @@ int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl
   return (int)cudaGetLastError();
 }
 
+// How many clusters of `splits` CTAs of the GEMM kernel can be resident at
+// once (clusters are placed within one GPC / die, so this is less than
+// sms / splits: e.g. 8-CTA clusters do not all fit 148 SMs).
+static int max_active_clusters(int splits) {
+  static std::atomic<int> cache[kMaxSplits + 1];
+  int v = cache[splits].load();
+  if (v)
+    return v;
+  cudaFuncSetAttribute(sgemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       SMEM_BYTES);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(splits * 256));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)splits;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, sgemm_3xtf32_kernel, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 148 / splits;
+  }
+  cache[splits].store(n);
+  return n;
+}
+
 // Split-K factor (cluster size) for C grids too small to fill the GPU: the
-// largest power of two <= 8 that keeps the grid within one wave (one CTA per
-// SM) and every split >= 128 deep in K (one accumulator chunk).
+// largest power of two <= 8 whose clusters (one per C tile) are all resident
+// at once and that keeps every split >= 128 deep in K (one accumulator chunk).
 int sgemm_tc_splits(int M, int N, int K, int sms) {
+  (void)sms;
   const int tiles = (M / BM) * (N / BN);
   int s = 1;
-  while (s < kMaxSplits && tiles * s * 2 <= sms && K % (16 * s * 2) == 0 && K / (s * 2) >= 128)
+  while (s < kMaxSplits && tiles <= max_active_clusters(s * 2) && K % (16 * s * 2) == 0 &&
+         K / (s * 2) >= 128)
     s *= 2;
   return s;
 }
