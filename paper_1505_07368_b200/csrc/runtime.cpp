@@ -234,6 +234,10 @@ struct Device {
   int ordinal = 0;
   int sms = 0;
   cudaStream_t compute = nullptr, d2h = nullptr, h2d = nullptr;
+  // second compute stream: consecutive waves of a host request alternate
+  // between the two, so a wave's kernel fills the SMs the previous wave's
+  // tail leaves idle
+  cudaStream_t compute2 = nullptr;
   uint32_t* sched = nullptr;  // kSchedSlots x {cursor, finished}
   std::atomic<uint32_t> sched_next{0};
   std::mutex submit_mu;
@@ -774,6 +778,8 @@ static std::vector<std::vector<SubTile>> plan_mandel(
   return per;
 }
 
+static int stream_after(cudaStream_t b, cudaStream_t a);  // b waits for a's work so far
+
 // Submits one device's share: waves of sub-tiles, each a single launch into a
 // device staging buffer followed by the copy-out on the d2h stream, so the
 // PCIe transfer of wave w overlaps the compute of wave w+1.
@@ -805,7 +811,12 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
     return e && e[0] == '1';
   }();
   std::vector<std::array<cudaEvent_t, 3>> tev;
+  // waves alternate between the two compute streams (both ordered after the
+  // device's earlier work; compute is ordered after both at the end)
+  CAFXG_TRY(stream_after(d->compute2, d->compute));
+  uint32_t wave = 0;
   while (i < subs.size()) {
+    cudaStream_t ks = (wave++ & 1) ? d->compute2 : d->compute;
     // group a wave (same precision)
     size_t j = i;
     uint64_t px = 0;
@@ -817,7 +828,7 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
       ++j;
     }
     uint32_t* dout = nullptr;
-    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dout, px * 4, d->compute));
+    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dout, px * 4, ks));
     std::vector<MTile> mt(j - i);
     uint32_t chunks = 0, maxit = 0;
     uint64_t off = 0;
@@ -831,14 +842,14 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
       tev.push_back({});
       for (auto& e : tev.back())
         cudaEventCreate(&e);
-      cudaEventRecord(tev.back()[0], d->compute);
+      cudaEventRecord(tev.back()[0], ks);
     }
-    CAFXG_TRY(launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, d->compute));
+    CAFXG_TRY(launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks));
     if (trace)
-      cudaEventRecord(tev.back()[1], d->compute);
+      cudaEventRecord(tev.back()[1], ks);
     cudaEvent_t ev;
     CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    CAFXG_CUDA_TRY(cudaEventRecord(ev, d->compute));
+    CAFXG_CUDA_TRY(cudaEventRecord(ev, ks));
     CAFXG_CUDA_TRY(cudaStreamWaitEvent(d->d2h, ev, 0));
     cudaEventDestroy(ev);  // destruction is deferred until the event completes
     off = 0;
@@ -863,6 +874,7 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
     left -= px;
     i = j;
   }
+  CAFXG_TRY(stream_after(d->compute, d->compute2));
   if (trace && !tev.empty()) {
     cudaError_t se = cudaEventSynchronize(tev.back()[2]);
     for (size_t w = 0; w < tev.size(); ++w) {
@@ -1887,6 +1899,7 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
                     i, prop.major, prop.minor);
       d->sms = prop.multiProcessorCount;
       CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->compute, cudaStreamNonBlocking));
+      CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->compute2, cudaStreamNonBlocking));
       CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking));
       CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->h2d, cudaStreamNonBlocking));
       CAFXG_CUDA_TRY(cudaMalloc(&d->sched, kSchedSlots * 2 * sizeof(uint32_t)));
@@ -1975,6 +1988,8 @@ int cafxg_close(cafxg_ctx* ctx) {
     }
     cudaFree(d->sched);
     cudaStreamSynchronize(d->h2d);
+    cudaStreamSynchronize(d->compute2);
+    cudaStreamDestroy(d->compute2);
     cudaStreamDestroy(d->compute);
     cudaStreamDestroy(d->d2h);
     cudaStreamDestroy(d->h2d);
