@@ -657,6 +657,7 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
   // that max_iter is (nearly) a multiple of it: no steps past max_iter)
   const uint32_t reps = L.block_reps;
   const uint32_t block = kUnit * reps;
+  uint32_t* const out = L.out;
 
   Feeder<Slots, kInlineCoords> feed;
   Slots sl;
@@ -684,15 +685,17 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
       sl.template run_free<kUnit, kExact>();
     const uint32_t esc = sl.escaped() & live;
     uint32_t done = esc;
+    // branch-free per slot (predicated store): nested ifs here compiled to
+    // four BSSY/BRA regions that re-loaded max_iter and L.out from constant
+    // memory inside each, and the block end waited on those loads
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      if ((live & ~esc) >> s & 1u) {
-        n[s] += block;
-        if (n[s] >= maxit) {
-          L.out[o[s]] = maxit;
-          done |= 1u << s;
-        }
-      }
+      const bool act = ((live & ~esc) >> s) & 1u;
+      n[s] += act ? block : 0u;
+      const bool hit = act && n[s] >= maxit;
+      if (hit)
+        out[o[s]] = maxit;
+      done |= (uint32_t)hit << s;
     }
     if (__any_sync(kFull, esc != 0)) {
       uint32_t base = queued;
