@@ -499,6 +499,8 @@ struct Feeder {
         base += __popc(b[s]);
       }
       cur += min(want, avail);
+      if (want <= avail)
+        return;  // every free slot got a pixel (skips a round of ballots)
     }
   }
 };
