@@ -265,6 +265,11 @@ struct Device {
   size_t stage_cap[kMaxInflight] = {};
   cudaEvent_t stage_ev[kMaxInflight] = {};
   uint32_t stage_next = 0;
+  // reusable events for host request pipelines (caller holds submit_mu): an
+  // event may be re-recorded as soon as the waits on its last record are
+  // enqueued, so these never need to be destroyed per request
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t order_ev = nullptr;   // stream_after_pooled
   cudaEvent_t trace_ref = nullptr;  // CAFXG_TRACE time base
   double trace_ref_ms = 0;
 
@@ -1060,6 +1065,31 @@ static int stream_after(cudaStream_t b, cudaStream_t a) {
   return CAFXG_OK;
 }
 
+// The same with the device's reusable ordering event (caller holds
+// d->submit_mu): the wait captures the record, so the event is free again at
+// once.
+static int stream_after_pooled(Device* d, cudaStream_t b, cudaStream_t a) {
+  if (!d->order_ev)
+    CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&d->order_ev, cudaEventDisableTiming));
+  CAFXG_CUDA_TRY(cudaEventRecord(d->order_ev, a));
+  CAFXG_CUDA_TRY(cudaStreamWaitEvent(b, d->order_ev, 0));
+  return CAFXG_OK;
+}
+
+static cudaEvent_t pooled_event(Device* d) {
+  if (!d->ev_pool.empty()) {
+    cudaEvent_t e = d->ev_pool.back();
+    d->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+
 // Host-request pipeline for one device's C rows [r0, r1) with B already in
 // device memory (dB, K x N): B is split once (tf32 hi/lo, transposed), then
 // per block of R rows: H2D of A_i on the upload stream -> hi/lo split + 3xTF32
@@ -1097,7 +1127,7 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
     CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dA[b], (size_t)R * K * 4, cs));
     CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dC[b], (size_t)R * N * 4, cs));
   }
-  CAFXG_TRY(stream_after(d->h2d, cs));  // the buffers exist before uploads
+  CAFXG_TRY(stream_after_pooled(d, d->h2d, cs));  // the buffers exist before uploads
   // CAFXG_TRACE=1: device timeline of the request (uploads, GEMMs, downloads)
   std::vector<std::pair<const char*, cudaEvent_t>> tev;
   const double t_host0 = trace_now_ms();
@@ -1115,16 +1145,20 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
                                    cudaMemcpyHostToDevice, d->h2d));
     ctx->st_h2d += K * N * 4;
     tmark("B up", d->h2d);
-    CAFXG_TRY(stream_after(cs, d->h2d));
+    CAFXG_TRY(stream_after_pooled(d, cs, d->h2d));
   }
   int e = sgemm_tc_split_b(dB, (int)N, (int)K, (int)N, Bh, Bl, cs);
   if (e != 0)
     return cuda_status((cudaError_t)e, "sgemm: B split");
   ctx->st_launches++;
+  // tensor maps encoded once per request: every block reuses Ah/Al (R rows)
+  // and Bh/Bl
+  SgemmTcMaps maps;
+  if (int me = sgemm_tc_make_maps(Ah, Al, (int)R, Bh, Bl, (int)N, (int)K, &maps))
+    return cuda_status((cudaError_t)me, "sgemm: tensor maps");
   std::vector<cudaEvent_t> ev_split, ev_gemm, ev_down;
-  auto mk = [](std::vector<cudaEvent_t>& v) {
-    cudaEvent_t ev;
-    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  auto mk = [d](std::vector<cudaEvent_t>& v) {
+    cudaEvent_t ev = pooled_event(d);
     v.push_back(ev);
     return ev;
   };
@@ -1146,14 +1180,14 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
                            "sgemm: A upload");
     ctx->st_h2d += (size_t)m * K * 4;
     tmark("A up", d->h2d);
-    CAFXG_TRY(stream_after(cs, d->h2d));
+    CAFXG_TRY(stream_after_pooled(d, cs, d->h2d));
     if (i >= 2)
       cudaStreamWaitEvent(cs, ev_down[i - 2], 0);  // C slot drained
     e = sgemm_tc_split_a(dA[slot], (int)K, (int)m, (int)K, Ah, Al, cs);
     cudaEventRecord(mk(ev_split), cs);
     if (e == 0)
-      e = sgemm_tc_gemm(Ah, Al, Bh, Bl, dC[slot], (int)m, (int)N, (int)K, (int)N, cs,
-                        sgemm_tc_splits((int)m, (int)N, (int)K, d->sms));
+      e = sgemm_tc_gemm_maps(&maps, dC[slot], (int)m, (int)N, (int)K, (int)N, cs,
+                             sgemm_tc_splits((int)m, (int)N, (int)K, d->sms));
     if (e != 0)
       status = cuda_status((cudaError_t)e, "sgemm: 3xtf32 launch");
     ctx->st_launches += 2;
@@ -1186,12 +1220,14 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
   }
   // everything is released on the download stream, which by now follows
   // every upload and kernel of this request
-  CAFXG_TRY(stream_after(d->d2h, cs));
+  CAFXG_TRY(stream_after_pooled(d, d->d2h, cs));
   for (float* p : {Bh, Bl, Ah, Al, dA[0], dA[1], dC[0], dC[1]})
     cudaFreeAsync(p, d->d2h);
+  // every wait on these records is enqueued: back to the pool
   for (auto* v : {&ev_split, &ev_gemm, &ev_down})
     for (auto ev : *v)
-      cudaEventDestroy(ev);
+      if (ev)
+        d->ev_pool.push_back(ev);
   return status;
 }
 
@@ -1979,6 +2015,10 @@ int cafxg_close(cafxg_ctx* ctx) {
       cudaEventDestroy(ev);
     for (auto ev : d->up_ev)
       cudaEventDestroy(ev);
+    for (auto ev : d->ev_pool)
+      cudaEventDestroy(ev);
+    if (d->order_ev)
+      cudaEventDestroy(d->order_ev);
     cudaFreeHost(d->up_base);
     for (int i = 0; i < kMaxInflight; ++i) {
       if (d->stage[i])

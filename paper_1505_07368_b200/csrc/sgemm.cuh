@@ -26,6 +26,16 @@ int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl
                      void* stream);
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl,
                   float* C, int M, int N, int K, int ldc, void* stream, int splits = 1);
+// The four TMA tensor maps of a GEMM (A_hi, A_lo over a_rows rows; B_hi,
+// B_lo), encoded once and reused by launches over the same buffers: a row
+// block of m <= a_rows rows only touches rows below m.
+struct SgemmTcMaps {
+  alignas(64) unsigned char m[4][128];
+};
+int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
+                       const float* Bl, int N, int K, SgemmTcMaps* maps);
+int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
+                       void* stream, int splits);
 // split-K factor (thread-block cluster size, <= 8) for small C grids
 int sgemm_tc_splits(int M, int N, int K, int sms);
 

@@ -535,12 +535,19 @@ int sgemm_tc_splits(int M, int N, int K, int sms) {
   return s;
 }
 
-int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl, float* C,
-                  int M, int N, int K, int ldc, void* stream, int splits) {
-  CUtensorMap mAh, mAl, mBh, mBl;
-  if (!make_map(&mAh, Ah, M, K, BM) || !make_map(&mAl, Al, M, K, BM) ||
-      !make_map(&mBh, Bh, N, K, BN) || !make_map(&mBl, Bl, N, K, BN))
+int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
+                       const float* Bl, int N, int K, SgemmTcMaps* maps) {
+  static_assert(sizeof(CUtensorMap) <= sizeof(maps->m[0]), "tensor map storage");
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(maps->m);
+  if (!make_map(&m[0], Ah, a_rows, K, BM) || !make_map(&m[1], Al, a_rows, K, BM) ||
+      !make_map(&m[2], Bh, N, K, BN) || !make_map(&m[3], Bl, N, K, BN))
     return (int)cudaErrorInvalidValue;
+  return 0;
+}
+
+int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
+                       void* stream, int splits) {
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   {
     // once per device (the attribute is per-device state)
     static std::atomic<uint64_t> configured{0};
@@ -568,8 +575,17 @@ int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel, mAh, mAl, mBh, mBl, C, M, N, K, ldc, splits);
+  cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel, m[0], m[1], m[2], m[3], C, M, N, K, ldc,
+                     splits);
   return (int)cudaGetLastError();
+}
+
+int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl, float* C,
+                  int M, int N, int K, int ldc, void* stream, int splits) {
+  SgemmTcMaps maps;
+  if (int e = sgemm_tc_make_maps(Ah, Al, M, Bh, Bl, N, K, &maps))
+    return e;
+  return sgemm_tc_gemm_maps(&maps, C, M, N, K, ldc, stream, splits);
 }
 
 int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int K, int lda,
