@@ -155,7 +155,7 @@ def peaks():
 
 # ---- CPU baselines (test infrastructure: oracle) ---------------------------------------
 
-def cpu_cfg3_sample(target_s: float = 8.0):
+def cpu_cfg3_sample(target_s: float = 12.0):
     """Times the oracle restatement on a row sample of cfg3 with every host
     thread; returns (Giter/s, cores, description)."""
     from oracle import oracle
