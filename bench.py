@@ -360,14 +360,14 @@ def run_ours(args):
     peak_tops = sms * 128 * sm_max * 1e6 / 1e12
     achieved = 8.0 * iters_local / (kernel_ms / 1e3) / 1e12
     # DRAM traffic of the escape kernel from the committed ncu capture of the
-    # full-image launch (profiles/round1/mandel_cfg3_b56_full.txt:
-    # 1.020756 GB written + 10.830336 MB read), scaled to this rank's share
-    traffic = round((1.020756e9 + 10.830336e6) * npx / (W_IMG * H_IMG))
-    # The same capture: FMA pipe busy 90.6% of active cycles over 34.85 ms at
-    # 1.964 GHz = 1.175e12 FMA-pipe lane-cycles for 1.82e11 iterations, i.e.
-    # 6.45 executed lane-ops per iteration (6 in the unchecked step, the rest
+    # full-image launch (profiles/round1/mandel_cfg3_final_full.txt:
+    # 1.023211 GB written + 11.369216 MB read), scaled to this rank's share
+    traffic = round((1.023211e9 + 11.369216e6) * npx / (W_IMG * H_IMG))
+    # The same capture: FMA pipe busy 91.9% of active cycles over 34.44 ms at
+    # 1.963 GHz = 1.176e12 FMA-pipe lane-cycles for 1.82e11 iterations, i.e.
+    # 6.46 executed lane-ops per iteration (6 in the unchecked step, the rest
     # block-end tests, refills and exact replays) against the algorithmic 8.
-    exec_ops_per_iter = 6.45
+    exec_ops_per_iter = 6.46
     roof = {"bound": "fp32_pipe", "achieved": round(achieved, 3), "peak": round(peak_tops, 3),
             "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4), "traffic": traffic,
             "traffic_note": "dram read+write bytes per launch (ncu, profiles/round1); "
@@ -380,8 +380,8 @@ def run_ours(args):
             "frac_note": "frac counts the reference's 8 FP ops per iteration; the kernel "
                          "executes 6 per iteration (escape test deferred to the ends of "
                          "56-step unchecked blocks, 2*zr*zi+ci as one FMA) plus block-end "
-                         "tests and exact replays, 6.45 lane-ops/iteration measured (ncu "
-                         "FMA pipe busy 90.6%, profiles/round1/mandel_cfg3_b56_full.txt); "
+                         "tests and exact replays, 6.46 lane-ops/iteration measured (ncu "
+                         "FMA pipe busy 91.9%, profiles/round1/mandel_cfg3_final_full.txt); "
                          "frac_executed is the pipe fraction doing that executed work"}
     if clk.get("sm_mhz"):
         peak_clk = sms * 128 * clk["sm_mhz"] * 1e6 / 1e12
@@ -466,10 +466,12 @@ def run_secondary(ctx, args):
     it1 = float(o1.to(torch.int64).sum().item())
     h1 = ctx.pinned_empty(1920 * 1080, np.uint32)
     ctx.mandelbrot(d1, h1)
-    t0 = time.perf_counter()
-    for _ in range(20):
+    walls = []
+    for _ in range(30):
+        t0 = time.perf_counter()
         ctx.mandelbrot(d1, h1)
-    e2e = (time.perf_counter() - t0) / 20 * 1e3
+        walls.append(time.perf_counter() - t0)
+    e2e = statistics.median(walls) * 1e3
     ctx.pinned_free(h1)
     out["cfg1_mandelbrot_1920x1080_fp32"] = {
         "kernel_ms": round(ms, 4), "giter_s": round(it1 / ms / 1e6, 2),
@@ -493,11 +495,15 @@ def run_secondary(ctx, args):
         hA[...] = An
         hB[...] = Bn
         ctx.sgemm(hA, hB, hC)
-        e2e_reps = 5 if n <= 2048 else 2
-        t0 = time.perf_counter()
+        # median of per-call wall times (a 1024^3 call is ~0.3 ms, so single
+        # calls are noisy)
+        e2e_reps = 30 if n <= 2048 else 3
+        walls = []
         for _ in range(e2e_reps):
+            t0 = time.perf_counter()
             ctx.sgemm(hA, hB, hC)
-        e2e = (time.perf_counter() - t0) / e2e_reps * 1e3
+            walls.append(time.perf_counter() - t0)
+        e2e = statistics.median(walls) * 1e3
         for h in (hA, hB, hC):
             ctx.pinned_free(h)
         bf16 = float(peaks().get("bf16_tflops") or 1590.0)
