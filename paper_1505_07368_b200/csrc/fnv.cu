@@ -33,7 +33,7 @@ namespace {
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
 constexpr int kP1Threads = 32;   // one warp per segment: 32 threads x 8 low bytes
 constexpr int kSubSegs = 32;     // sub-segments per segment (pass 3: one warp)
-constexpr int kTile = 1024;      // cells staged in smem per round (pass 1)
+constexpr int kTile = 256;       // cells staged in smem per round (pass 1; 4 KB, 32 warps/SM)
 constexpr int kRecWords = 64;    // 256 low bytes = 64 packed words per record
 
 // Pass 1: per segment, the low byte after every sub-segment for all 256
@@ -48,7 +48,10 @@ __global__ void __launch_bounds__(kP1Threads)
     fnv_lowbyte_kernel(const uint32_t* __restrict__ cells, uint64_t n, uint64_t seg_cells,
                        uint64_t sub_cells, uint32_t* __restrict__ rec,
                        uint8_t* __restrict__ L) {
-  __shared__ uint32_t tile[kTile];
+  // each staged cell pre-expanded into its four steps' operands (byte b in
+  // both 16-bit slots, big-endian order): the inner loop reads them with one
+  // broadcast 16-byte load instead of a load and four byte permutes per lane
+  __shared__ uint4 tile[kTile];
   const uint64_t begin = (uint64_t)blockIdx.x * seg_cells;
   const uint64_t end = begin + seg_cells < n ? begin + seg_cells : n;
   const uint32_t tid = threadIdx.x;
@@ -62,28 +65,42 @@ __global__ void __launch_bounds__(kP1Threads)
     myrec[(size_t)j * kRecWords] = __byte_perm(r[0], r[1], 0x6420);
     myrec[(size_t)j * kRecWords + 1] = __byte_perm(r[2], r[3], 0x6420);
   };
+  auto step = [&](uint32_t bb) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      r[k] = ((r[k] ^ bb) & 0x00ff00ffu) * 179u;
+  };
   uint64_t next_rec = begin;  // cell index of the next sub-segment start
   uint32_t j = 0;
   for (uint64_t base = begin; base < end; base += kTile) {
     const uint32_t cnt = end - base < (uint64_t)kTile ? (uint32_t)(end - base) : kTile;
     __syncwarp();
-    for (uint32_t i = tid; i < cnt; i += kP1Threads)
-      tile[i] = __ldg(cells + base + i);
+    for (uint32_t i = tid; i < cnt; i += kP1Threads) {
+      const uint32_t x = __ldg(cells + base + i);
+      tile[i] = make_uint4(__byte_perm(x, 0, 0x4343), __byte_perm(x, 0, 0x4242),
+                           __byte_perm(x, 0, 0x4141), __byte_perm(x, 0, 0x4040));
+    }
     __syncwarp();
-    for (uint32_t i = 0; i < cnt; ++i) {
-      if (base + i == next_rec) {
-        record(j);
-        ++j;
-        next_rec += sub_cells;
+    uint32_t i = 0;
+    while (i < cnt) {
+      // run to the next sub-segment start (or the tile end) without tests
+      uint32_t stop = cnt;
+      if (next_rec < base + cnt) {
+        if (next_rec == base + i) {
+          record(j);
+          ++j;
+          next_rec += sub_cells;
+          continue;
+        }
+        stop = (uint32_t)(next_rec - base);
       }
-      const uint32_t x = tile[i];  // broadcast read
-#pragma unroll
-      for (int sh = 3; sh >= 0; --sh) {
-        // byte sh of x into both slots: selector picks x.byte[sh] / zero
-        const uint32_t bb = __byte_perm(x, 0, sh | (4 << 4) | (sh << 8) | (4 << 12));
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          r[k] = ((r[k] ^ bb) & 0x00ff00ffu) * 179u;
+#pragma unroll 4
+      for (; i < stop; ++i) {
+        const uint4 v = tile[i];  // broadcast read
+        step(v.x);
+        step(v.y);
+        step(v.z);
+        step(v.w);
       }
     }
   }
