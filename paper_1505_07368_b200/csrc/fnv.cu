@@ -47,19 +47,20 @@ constexpr int kRecWords = 64;    // 256 low bytes = 64 packed words per record
 __global__ void __launch_bounds__(kP1Threads)
     fnv_lowbyte_kernel(const uint32_t* __restrict__ cells, uint64_t n, uint64_t seg_cells,
                        uint64_t sub_cells, uint32_t* __restrict__ rec,
-                       uint8_t* __restrict__ L) {
+                       uint8_t* __restrict__ L, uint32_t seg0) {
+  const uint32_t seg = seg0 + blockIdx.x;
   // each staged cell pre-expanded into its four steps' operands (byte b in
   // both 16-bit slots, big-endian order): the inner loop reads them with one
   // broadcast 16-byte load instead of a load and four byte permutes per lane
   __shared__ uint4 tile[kTile];
-  const uint64_t begin = (uint64_t)blockIdx.x * seg_cells;
+  const uint64_t begin = (uint64_t)seg * seg_cells;
   const uint64_t end = begin + seg_cells < n ? begin + seg_cells : n;
   const uint32_t tid = threadIdx.x;
   uint32_t r[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     r[k] = (8 * tid + 2 * k) | ((8 * tid + 2 * k + 1) << 16);
-  uint32_t* myrec = rec + (size_t)blockIdx.x * kSubSegs * kRecWords + 2 * tid;
+  uint32_t* myrec = rec + (size_t)seg * kSubSegs * kRecWords + 2 * tid;
   auto record = [&](uint32_t j) {
     // low bytes of the slots, packed in incoming-value order
     myrec[(size_t)j * kRecWords] = __byte_perm(r[0], r[1], 0x6420);
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(kP1Threads)
   }
   for (; j < kSubSegs; ++j)  // empty trailing sub-segments start where we end
     record(j);
-  uint32_t* out = reinterpret_cast<uint32_t*>(L + (size_t)blockIdx.x * 256) + 2 * tid;
+  uint32_t* out = reinterpret_cast<uint32_t*>(L + (size_t)seg * 256) + 2 * tid;
   out[0] = __byte_perm(r[0], r[1], 0x6420);
   out[1] = __byte_perm(r[2], r[3], 0x6420);
 }
@@ -247,36 +248,76 @@ size_t fnv_scratch_bytes(uint64_t n, int sms) {
   return PC + rec + L + p.nseg + 1 + 64;
 }
 
-// Enqueues the device FNV of `n` cells onto `stream`; the 64-bit hash lands
-// in device memory `out`. Scratch: fnv_scratch_bytes(n, sms).
-int fnv_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out, void* scratch,
-               int sms, void* stream, int* launches) {
+namespace {
+struct FnvScratch {
+  uint64_t *SP, *SC;
+  uint32_t* rec;
+  uint8_t *L, *lin;
+};
+FnvScratch carve(const FnvPlan& p, void* scratch) {
+  FnvScratch x;
+  x.SP = static_cast<uint64_t*>(scratch);
+  x.SC = x.SP + p.nseg;
+  x.rec = reinterpret_cast<uint32_t*>(x.SC + p.nseg);
+  x.L = reinterpret_cast<uint8_t*>(x.rec + (size_t)p.nseg * kSubSegs * kRecWords);
+  x.lin = x.L + (size_t)p.nseg * 256;
+  return x;
+}
+}  // namespace
+
+void fnv_segments(uint64_t n, int sms, uint64_t* seg_cells, uint32_t* nseg) {
+  FnvPlan p = plan(n, sms);
+  *seg_cells = p.seg_cells;
+  *nseg = p.nseg;
+}
+
+int fnv_lowbyte_launch(const uint32_t* cells, uint64_t n, uint32_t seg_begin, uint32_t seg_count,
+                       void* scratch, int sms, void* stream) {
+  FnvPlan p = plan(n, sms);
+  if (seg_begin >= p.nseg || seg_count == 0)
+    return 0;
+  if (seg_count > p.nseg - seg_begin)
+    seg_count = p.nseg - seg_begin;
+  FnvScratch x = carve(p, scratch);
+  fnv_lowbyte_kernel<<<seg_count, kP1Threads, 0, (cudaStream_t)stream>>>(
+      cells, n, p.seg_cells, p.sub_cells, x.rec, x.L, seg_begin);
+  return (int)cudaGetLastError();
+}
+
+int fnv_finish_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out,
+                      void* scratch, int sms, void* stream, int* launches) {
   cudaStream_t st = (cudaStream_t)stream;
   FnvPlan p = plan(n, sms);
-  uint64_t* SP = static_cast<uint64_t*>(scratch);
-  uint64_t* SC = SP + p.nseg;
-  uint32_t* rec = reinterpret_cast<uint32_t*>(SC + p.nseg);
-  uint8_t* L = reinterpret_cast<uint8_t*>(rec + (size_t)p.nseg * kSubSegs * kRecWords);
-  uint8_t* lin = L + (size_t)p.nseg * 256;
+  FnvScratch x = carve(p, scratch);
   int k = 0;
-  if (p.nseg) {
-    fnv_lowbyte_kernel<<<p.nseg, kP1Threads, 0, st>>>(cells, n, p.seg_cells, p.sub_cells, rec,
-                                                       L);
-    ++k;
-  }
-  fnv_scan_kernel<<<1, 256, 0, st>>>(L, p.nseg, seed, lin);
+  fnv_scan_kernel<<<1, 256, 0, st>>>(x.L, p.nseg, seed, x.lin);
   ++k;
   if (p.nseg) {
     uint64_t threads = (uint64_t)p.nseg * kSubSegs;
     fnv_affine_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
-        cells, n, p.seg_cells, p.sub_cells, p.nseg, rec, lin, SP, SC);
+        cells, n, p.seg_cells, p.sub_cells, p.nseg, x.rec, x.lin, x.SP, x.SC);
     ++k;
   }
-  fnv_fold_kernel<<<1, 1, 0, st>>>(SP, SC, p.nseg, seed, lin, out);
+  fnv_fold_kernel<<<1, 1, 0, st>>>(x.SP, x.SC, p.nseg, seed, x.lin, out);
   ++k;
   if (launches)
     *launches = k;
   return (int)cudaGetLastError();
+}
+
+// Enqueues the device FNV of `n` cells onto `stream`; the 64-bit hash lands
+// in device memory `out`. Scratch: fnv_scratch_bytes(n, sms).
+int fnv_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out, void* scratch,
+               int sms, void* stream, int* launches) {
+  FnvPlan p = plan(n, sms);
+  int e = fnv_lowbyte_launch(cells, n, 0, p.nseg, scratch, sms, stream);
+  if (e)
+    return e;
+  int k = 0;
+  e = fnv_finish_launch(cells, n, seed, out, scratch, sms, stream, &k);
+  if (launches)
+    *launches = k + (p.nseg ? 1 : 0);
+  return e;
 }
 
 }  // namespace cafxg

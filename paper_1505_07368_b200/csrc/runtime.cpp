@@ -2376,9 +2376,12 @@ int cafxg_run_mandelbrot(cafxg_ctx* ctx, uint32_t size, uint32_t max_iter, uint6
   std::vector<uint32_t> r0(G + 1);
   for (size_t g = 0; g <= G; ++g)
     r0[g] = (uint32_t)((uint64_t)size * g / G);
-  // pass 1: image + FNV tables of each block with seed 0 placeholder; the
-  // chaining needs the previous block's hash, so blocks are hashed in order
-  // below (the walk is cheap; the tables are the work).
+  // Per device: its block of rows in one escape launch, then the seed-
+  // independent FNV pass 1 (per-segment low-byte tables, the bulk of the
+  // hash) -- in parallel on every device. Then the cheap seeded passes run
+  // device after device, each block seeded with the previous block's hash
+  // (FNV is sequential). Overlapping pass 1 with the image on one device
+  // was tried and is slower.
   std::vector<void*> scratch(G, nullptr);
   for (size_t g = 0; g < G; ++g) {
     Device* d = ctx->devs[g].get();
@@ -2402,15 +2405,22 @@ int cafxg_run_mandelbrot(cafxg_ctx* ctx, uint32_t size, uint32_t max_iter, uint6
     fill_mtile(m, t, 0, 0);
     CAFXG_TRY(launch_mandel(ctx, d, img[g], {m}, tile_chunks(t.nrows, t.ncols), CAFXG_FP64,
                             max_iter, use_exact(ctx, t), n, d->compute));
+    uint64_t seg_cells = 0;
+    uint32_t nseg = 0;
+    fnv_segments(n, d->sms, &seg_cells, &nseg);
+    int e = fnv_lowbyte_launch(img[g], n, 0, nseg, scratch[g], d->sms, d->compute);
+    if (e != 0)
+      return cuda_status((cudaError_t)e, "fnv pass-1 launch");
+    ctx->st_launches++;
   }
-  // pass 2: hash the blocks in row order, each seeded with the previous hash
+  // the seeded passes, block after block
   uint64_t h = 0xcbf29ce484222325ull;
   for (size_t g = 0; g < G; ++g) {
     Device* d = ctx->devs[g].get();
     cudaSetDevice(d->ordinal);
     uint64_t n = (uint64_t)(r0[g + 1] - r0[g]) * size;
     int launches = 0;
-    int e = fnv_launch(img[g], n, h, dh[g], scratch[g], d->sms, d->compute, &launches);
+    int e = fnv_finish_launch(img[g], n, h, dh[g], scratch[g], d->sms, d->compute, &launches);
     if (e != 0)
       return cuda_status((cudaError_t)e, "fnv launch");
     ctx->st_launches += launches;

@@ -43,5 +43,13 @@ int sgemm_tc_splits(int M, int N, int K, int sms);
 size_t fnv_scratch_bytes(uint64_t n, int sms);
 int fnv_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out,
                void* scratch, int sms, void* stream, int* launches);
+// The same in two parts, so the seed-independent pass 1 (per-segment
+// low-byte tables, the bulk of the work) can run on segments as soon as
+// their cells exist: segments are fnv_segments() cells long.
+void fnv_segments(uint64_t n, int sms, uint64_t* seg_cells, uint32_t* nseg);
+int fnv_lowbyte_launch(const uint32_t* cells, uint64_t n, uint32_t seg_begin,
+                       uint32_t seg_count, void* scratch, int sms, void* stream);
+int fnv_finish_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t* out,
+                      void* scratch, int sms, void* stream, int* launches);
 
 }  // namespace cafxg
