@@ -10,27 +10,52 @@
 namespace cafxg {
 namespace {
 
-__global__ void __launch_bounds__(1024) copy_segments_kernel(const CopySeg* segs,
-                                                            uint32_t n) {
-  for (uint32_t s = blockIdx.x; s < n; s += gridDim.x) {
-    const CopySeg g = segs[s];
-    const uintptr_t a = (uintptr_t)g.src | (uintptr_t)g.dst | (uintptr_t)g.bytes;
-    if ((a & 15u) == 0) {
-      const uint4* src = (const uint4*)g.src;
-      uint4* dst = (uint4*)g.dst;
-      const uint64_t n16 = g.bytes >> 4;
-      for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x)
-        dst[i] = __ldg(src + i);
-    } else {
-      const uint8_t* src = (const uint8_t*)g.src;
-      uint8_t* dst = (uint8_t*)g.dst;
-      for (uint64_t i = threadIdx.x; i < g.bytes; i += blockDim.x)
-        dst[i] = src[i];
-    }
+__device__ __forceinline__ void copy_segment(const CopySeg& g) {
+  const uintptr_t a = (uintptr_t)g.src | (uintptr_t)g.dst | (uintptr_t)g.bytes;
+  if ((a & 15u) == 0) {
+    const uint4* src = (const uint4*)g.src;
+    uint4* dst = (uint4*)g.dst;
+    const uint64_t n16 = g.bytes >> 4;
+    for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x)
+      dst[i] = __ldg(src + i);
+  } else {
+    const uint8_t* src = (const uint8_t*)g.src;
+    uint8_t* dst = (uint8_t*)g.dst;
+    for (uint64_t i = threadIdx.x; i < g.bytes; i += blockDim.x)
+      dst[i] = src[i];
   }
 }
 
+__global__ void __launch_bounds__(1024) copy_segments_kernel(const CopySeg* segs,
+                                                            uint32_t n) {
+  for (uint32_t s = blockIdx.x; s < n; s += gridDim.x)
+    copy_segment(segs[s]);
+}
+
+struct InlineSegs {
+  CopySeg s[kInlineSegs];
+};
+
+__global__ void __launch_bounds__(1024) copy_segments_inline_kernel(
+    const __grid_constant__ InlineSegs segs, uint32_t n) {
+  for (uint32_t s = blockIdx.x; s < n; s += gridDim.x)
+    copy_segment(segs.s[s]);
+}
+
 }  // namespace
+
+int copy_segments_inline_launch(const CopySeg* segs_host, uint32_t n, void* stream) {
+  if (n == 0)
+    return 0;
+  if (n > kInlineSegs)
+    return (int)cudaErrorInvalidValue;
+  InlineSegs p;
+  for (uint32_t i = 0; i < n; ++i)
+    p.s[i] = segs_host[i];
+  uint32_t grid = n < 16 ? n : 16;
+  copy_segments_inline_kernel<<<grid, 1024, 0, (cudaStream_t)stream>>>(p, n);
+  return (int)cudaGetLastError();
+}
 
 int copy_segments_launch(const CopySeg* segs_dev, uint32_t n, void* stream) {
   if (n == 0)

@@ -1685,7 +1685,8 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   // the reply segment table goes up on the compute stream: an upload-ring
   // slot recorded on the copy stream would only free up behind every queued
   // copy-out, and reusing it would block the dispatcher
-  if (status == CAFXG_OK && px && all_pinned) {
+  const bool inline_segs = segs.size() <= kInlineSegs;
+  if (status == CAFXG_OK && px && all_pinned && !inline_segs) {
     size_t sb = segs.size() * sizeof(CopySeg);
     status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, d->compute), "segs alloc");
     if (status == CAFXG_OK)
@@ -1696,19 +1697,13 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   // the compute stream instead was slower even for closed-loop trickles,
   // 144 -> 218 ms, because it serialises copy-out and the next kernel)
   cudaStream_t cs = d->d2h;
-  if (status == CAFXG_OK && px) {
-    cudaEvent_t ev;
-    status = cuda_status(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-    if (status == CAFXG_OK) {
-      cudaEventRecord(ev, d->compute);
-      cudaStreamWaitEvent(d->d2h, ev, 0);
-      cudaEventDestroy(ev);
-    }
-  }
+  if (status == CAFXG_OK && px)
+    status = stream_after_pooled(d, d->d2h, d->compute);
   if (status == CAFXG_OK && px) {
     if (all_pinned) {
       {
-        int e = copy_segments_launch(dsegs, (uint32_t)segs.size(), cs);
+        int e = inline_segs ? copy_segments_inline_launch(segs.data(), (uint32_t)segs.size(), cs)
+                            : copy_segments_launch(dsegs, (uint32_t)segs.size(), cs);
         status = cuda_status((cudaError_t)e, "reply scatter launch");
         ctx->st_launches++;
       }
