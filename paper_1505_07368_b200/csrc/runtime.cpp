@@ -1875,6 +1875,9 @@ static void wake_dispatcher(cafxg_ctx* ctx) {
 // C ABI
 // =====================================================================================
 
+// No C++ exception crosses the ABI: functions that allocate on the host are
+// function-try-blocks that turn std::bad_alloc and friends into an error
+// status (config_error) with the message in cafxg_last_error().
 extern "C" {
 
 int cafxg_abi_version(void) { return CAFXG_ABI_VERSION; }
@@ -1973,7 +1976,7 @@ int cafxg_sync(cafxg_ctx* ctx) {
   return CAFXG_OK;
 }
 
-int cafxg_close(cafxg_ctx* ctx) {
+int cafxg_close(cafxg_ctx* ctx) try {
   if (!ctx)
     return CAFXG_OK;
   {
@@ -2034,17 +2037,25 @@ int cafxg_close(cafxg_ctx* ctx) {
       ctx->nccl.CommDestroy(c);
   delete ctx;
   return CAFXG_OK;
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_close: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_close: unknown exception");
 }
 
 int cafxg_device_count(const cafxg_ctx* ctx) { return ctx ? (int)ctx->devs.size() : 0; }
 
-int cafxg_host_alloc(cafxg_ctx* ctx, size_t bytes, void** ptr) {
+int cafxg_host_alloc(cafxg_ctx* ctx, size_t bytes, void** ptr) try {
   if (!ctx || !ptr)
     return fail(CAFXG_E_CONFIG, "host_alloc: null argument");
   *ptr = ctx->pinned.alloc(bytes ? bytes : 1);
   if (!*ptr)
     return fail(CAFXG_E_OUT_OF_RANGE, "host_alloc: cudaHostAlloc of %zu bytes failed", bytes);
   return CAFXG_OK;
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_host_alloc: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_host_alloc: unknown exception");
 }
 
 int cafxg_host_free(cafxg_ctx* ctx, void* ptr) {
@@ -2056,11 +2067,15 @@ int cafxg_host_free(cafxg_ctx* ctx, void* ptr) {
                                : fail(CAFXG_E_CONFIG, "host_free: pointer not from host_alloc");
 }
 
-int cafxg_host_register(cafxg_ctx* ctx, void* ptr, size_t bytes) {
+int cafxg_host_register(cafxg_ctx* ctx, void* ptr, size_t bytes) try {
   if (!ctx || !ptr || !bytes)
     return fail(CAFXG_E_CONFIG, "host_register: bad argument");
   CAFXG_CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
   return CAFXG_OK;
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_host_register: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_host_register: unknown exception");
 }
 
 int cafxg_host_unregister(cafxg_ctx* ctx, void* ptr) {
@@ -2106,12 +2121,16 @@ struct Waiter {
 }  // namespace
 
 int cafxg_mandelbrot(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles, size_t n,
-                     uint32_t* host_out) {
+                     uint32_t* host_out) try {
   Waiter w;
   int s = cafxg_mandelbrot_submit(ctx, tiles, n, host_out, &Waiter::cb, &w);
   if (s != CAFXG_OK)
     return s;
   return w.wait();
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_mandelbrot: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_mandelbrot: unknown exception");
 }
 
 int cafxg_mandelbrot_device(cafxg_ctx* ctx, int device, const cafxg_mandel_desc* tiles,
@@ -2170,16 +2189,20 @@ int cafxg_sgemm_submit(cafxg_ctx* ctx, const cafxg_sgemm_desc* d, const float* A
 }
 
 int cafxg_sgemm(cafxg_ctx* ctx, const cafxg_sgemm_desc* d, const float* A, const float* B,
-                float* C) {
+                float* C) try {
   Waiter w;
   int s = cafxg_sgemm_submit(ctx, d, A, B, C, &Waiter::cb, &w);
   if (s != CAFXG_OK)
     return s;
   return w.wait();
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_sgemm: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_sgemm: unknown exception");
 }
 
 int cafxg_sgemm_device(cafxg_ctx* ctx, int device, const cafxg_sgemm_desc* desc,
-                       const float* A, const float* B, float* C, void* stream) {
+                       const float* A, const float* B, float* C, void* stream) try {
   if (!ctx || !desc || device < 0 || device >= (int)ctx->devs.size())
     return fail(CAFXG_E_CONFIG, "sgemm_device: bad argument");
   cafxg_sgemm_desc g = *desc;
@@ -2187,12 +2210,16 @@ int cafxg_sgemm_device(cafxg_ctx* ctx, int device, const cafxg_sgemm_desc* desc,
   Device* d = ctx->devs[device].get();
   cudaSetDevice(d->ordinal);
   return sgemm_on_device(ctx, d, g, A, B, C, stream ? (cudaStream_t)stream : d->compute);
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_sgemm_device: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_sgemm_device: unknown exception");
 }
 
 // ---- actors --------------------------------------------------------------------
 
 int cafxg_spawn(cafxg_ctx* ctx, const char* kernel_name, const uint64_t* dims, size_t ndims,
-                cafxg_actor** out) {
+                cafxg_actor** out) try {
   if (!ctx || !kernel_name || !out)
     return fail(CAFXG_E_CONFIG, "spawn: null argument");
   *out = nullptr;
@@ -2216,6 +2243,10 @@ int cafxg_spawn(cafxg_ctx* ctx, const char* kernel_name, const uint64_t* dims, s
     a->dims[i] = dims[i];
   *out = a;
   return CAFXG_OK;
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_spawn: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_spawn: unknown exception");
 }
 
 static int actor_check(cafxg_actor* a, const void* const* in, const size_t* in_bytes,
@@ -2263,7 +2294,7 @@ size_t cafxg_actor_reply_bytes(cafxg_actor* a, const void* const* in, const size
 
 int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in, const size_t* in_bytes,
                         size_t n_in, void* out, size_t out_bytes, cafxg_done_fn done,
-                        void* user) {
+                        void* user) try {
   size_t rb = 0;
   CAFXG_TRY(actor_check(a, in, in_bytes, n_in, &rb));
   if (!a->alive.load())
@@ -2311,6 +2342,10 @@ int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in, const size_t* in_
   if (head == nullptr)  // empty -> non-empty: the dispatcher may sleep
     wake_dispatcher(ctx);
   return CAFXG_OK;
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_actor_enqueue: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_actor_enqueue: unknown exception");
 }
 
 int cafxg_actor_quit(cafxg_actor* a) {
@@ -2331,7 +2366,7 @@ int cafxg_actor_release(cafxg_actor* a) {
 }
 
 int cafxg_fnv1a_u32_device(cafxg_ctx* ctx, int device, const uint32_t* cells, uint64_t n,
-                           uint64_t seed, uint64_t* hash, void* stream) {
+                           uint64_t seed, uint64_t* hash, void* stream) try {
   if (!ctx || !hash || device < 0 || device >= (int)ctx->devs.size() || (n && !cells))
     return fail(CAFXG_E_CONFIG, "fnv1a_u32_device: bad argument");
   Device* d = ctx->devs[device].get();
@@ -2351,6 +2386,10 @@ int cafxg_fnv1a_u32_device(cafxg_ctx* ctx, int device, const uint32_t* cells, ui
   CAFXG_CUDA_TRY(cudaFreeAsync(dhash, s));
   CAFXG_CUDA_TRY(cudaStreamSynchronize(s));
   return CAFXG_OK;
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_fnv1a_u32_device: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_fnv1a_u32_device: unknown exception");
 }
 
 // run_mandelbrot(size, max_iter) (bench.cpp:481-505) on the context's devices:
@@ -2360,7 +2399,7 @@ int cafxg_fnv1a_u32_device(cafxg_ctx* ctx, int device, const uint32_t* cells, ui
 // chained on the host in row order: the checksum is the reference's
 // collector hash (bench.cpp:329-331) without moving the image off the GPUs.
 int cafxg_run_mandelbrot(cafxg_ctx* ctx, uint32_t size, uint32_t max_iter, uint64_t* checksum,
-                         double* wall_ms) {
+                         double* wall_ms) try {
   if (!ctx || !checksum || size == 0)
     return fail(CAFXG_E_CONFIG, "run_mandelbrot: bad argument");
   auto t0 = std::chrono::steady_clock::now();
@@ -2435,6 +2474,10 @@ int cafxg_run_mandelbrot(cafxg_ctx* ctx, uint32_t size, uint32_t max_iter, uint6
     *wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
                    .count();
   return CAFXG_OK;
+} catch (const std::exception& ex) {
+  return fail(CAFXG_E_CONFIG, "cafxg_run_mandelbrot: %s", ex.what());
+} catch (...) {
+  return fail(CAFXG_E_CONFIG, "cafxg_run_mandelbrot: unknown exception");
 }
 
 int cafxg_get_stats(cafxg_ctx* ctx, cafxg_stats* out) {
