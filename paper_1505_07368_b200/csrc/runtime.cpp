@@ -1231,6 +1231,154 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
   return status;
 }
 
+// Large single-device host requests: a 2D wavefront over C blocks. A's row
+// blocks and B's column blocks go up interleaved (A0, B0, A1, B1, ...); each
+// block is split (tf32 hi/lo; B^T) as it lands, and every C block (i, j)
+// whose A_i and B_j are both resident is multiplied at once and downloaded
+// on the copy stream. The row-block pipeline needs all of B before its first
+// GEMM (1 GiB, ~20 ms over PCIe at 16384^3); here compute follows the
+// uploads one block behind, so the request approaches the 2 GiB upload time.
+static bool sgemm_tiled2d_eligible(const cafxg_sgemm_desc& g) {
+  static const bool on = [] {
+    const char* e = getenv("CAFXG_SGEMM_2D");
+    return !(e && e[0] == '0');
+  }();
+  return on && g.mode != CAFXG_SGEMM_FFMA && g.M >= 8192 && g.N >= 8192 && g.M % 128 == 0 &&
+         g.N % 256 == 0 && sgemm_tc_supported(128, 256, g.K, g.K, g.N, g.N);
+}
+
+static int sgemm_tiled2d_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
+                                const float* A, const float* B, float* C) {
+  const size_t M = g.M, N = g.N, K = g.K;
+  static const uint32_t div = [] {  // blocks per dimension (CAFXG_SGEMM_2D_DIV)
+    const char* e = getenv("CAFXG_SGEMM_2D_DIV");
+    const int v = e ? atoi(e) : 0;
+    return v >= 2 && v <= 64 ? (uint32_t)v : 8u;
+  }();
+  const uint32_t Mb = (uint32_t)((M / div + 127) / 128 * 128);
+  const uint32_t Nb = (uint32_t)((N / div + 255) / 256 * 256);
+  const uint32_t nbm = (uint32_t)((M + Mb - 1) / Mb), nbn = (uint32_t)((N + Nb - 1) / Nb);
+  cudaStream_t cs = d->compute;
+  float *dA = nullptr, *dB = nullptr, *Ah = nullptr, *Al = nullptr, *Bh = nullptr,
+        *Bl = nullptr, *dC = nullptr;
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dA, M * K * 4, cs));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dB, K * N * 4, cs));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Ah, M * K * 4, cs));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Al, M * K * 4, cs));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Bh, N * K * 4, cs));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Bl, N * K * 4, cs));
+  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dC, M * N * 4, cs));
+  SgemmTcMaps maps;  // whole Ah/Al and Bh/Bl; blocks address rows by offset
+  if (int me = sgemm_tc_make_maps(Ah, Al, (int)M, Bh, Bl, (int)N, (int)K, &maps))
+    return cuda_status((cudaError_t)me, "sgemm: tensor maps");
+  CAFXG_TRY(stream_after_pooled(d, d->h2d, cs));  // buffers exist before uploads
+  // CAFXG_TRACE=1: completion times of uploads, GEMM blocks and downloads
+  std::vector<std::pair<char, cudaEvent_t>> tev;
+  auto tmark = [&](char what, cudaStream_t sm) {
+    if (!trace_on())
+      return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, sm);
+    tev.emplace_back(what, e);
+  };
+  tmark('S', d->h2d);
+  std::vector<cudaEvent_t> evs;
+  auto ev_on = [&](cudaStream_t sm) {
+    cudaEvent_t e = pooled_event(d);
+    cudaEventRecord(e, sm);
+    evs.push_back(e);
+    return e;
+  };
+  int status = CAFXG_OK;
+  uint32_t na = 0, nb = 0;  // A row blocks / B column blocks resident
+  auto gemm_block = [&](uint32_t i, uint32_t j) {
+    const uint32_t m0 = i * Mb, n0 = j * Nb;
+    const uint32_t mi = (uint32_t)std::min<size_t>(Mb, M - m0);
+    const uint32_t nj = (uint32_t)std::min<size_t>(Nb, N - n0);
+    float* cblk = dC + (size_t)m0 * N + n0;
+    int e = sgemm_tc_gemm_maps(&maps, cblk, (int)mi, (int)nj, (int)K, (int)N, cs,
+                               sgemm_tc_splits((int)mi, (int)nj, (int)K, d->sms), (int)m0,
+                               (int)n0);
+    ctx->st_launches++;
+    tmark('G', cs);
+    if (e != 0)
+      return cuda_status((cudaError_t)e, "sgemm: 3xtf32 block launch");
+    cudaStreamWaitEvent(d->d2h, ev_on(cs), 0);
+    ctx->st_d2h += (size_t)mi * nj * 4;
+    const int st = cuda_status(cudaMemcpy2DAsync(C + (size_t)m0 * g.ldc + n0, (size_t)g.ldc * 4,
+                                                 cblk, N * 4, (size_t)nj * 4, mi,
+                                                 cudaMemcpyDeviceToHost, d->d2h),
+                               "sgemm: C block download");
+    tmark('D', d->d2h);
+    return st;
+  };
+  for (uint32_t t = 0; t < std::max(nbm, nbn) && status == CAFXG_OK; ++t) {
+    if (t < nbm) {  // A row block t
+      const uint32_t m0 = t * Mb, mi = (uint32_t)std::min<size_t>(Mb, M - m0);
+      status = cuda_status(cudaMemcpy2DAsync(dA + (size_t)m0 * K, K * 4, A + (size_t)m0 * g.lda,
+                                             (size_t)g.lda * 4, K * 4, mi,
+                                             cudaMemcpyHostToDevice, d->h2d),
+                           "sgemm: A block upload");
+      ctx->st_h2d += (size_t)mi * K * 4;
+      tmark('A', d->h2d);
+      if (status != CAFXG_OK)
+        break;
+      cudaStreamWaitEvent(cs, ev_on(d->h2d), 0);
+      int e = sgemm_tc_split_a(dA + (size_t)m0 * K, (int)K, (int)mi, (int)K, Ah + (size_t)m0 * K,
+                               Al + (size_t)m0 * K, cs);
+      ctx->st_launches++;
+      if (e != 0) {
+        status = cuda_status((cudaError_t)e, "sgemm: A split");
+        break;
+      }
+      ++na;
+      for (uint32_t j = 0; j < nb && status == CAFXG_OK; ++j)
+        status = gemm_block(t, j);
+    }
+    if (t < nbn && status == CAFXG_OK) {  // B column block t
+      const uint32_t n0 = t * Nb, nj = (uint32_t)std::min<size_t>(Nb, N - n0);
+      status = cuda_status(cudaMemcpy2DAsync(dB + n0, N * 4, B + n0, (size_t)g.ldb * 4,
+                                             (size_t)nj * 4, K, cudaMemcpyHostToDevice, d->h2d),
+                           "sgemm: B block upload");
+      ctx->st_h2d += K * nj * 4;
+      tmark('B', d->h2d);
+      if (status != CAFXG_OK)
+        break;
+      cudaStreamWaitEvent(cs, ev_on(d->h2d), 0);
+      int e = sgemm_tc_split_b(dB + n0, (int)N, (int)K, (int)nj, Bh + (size_t)n0 * K,
+                               Bl + (size_t)n0 * K, cs);
+      ctx->st_launches++;
+      if (e != 0) {
+        status = cuda_status((cudaError_t)e, "sgemm: B split");
+        break;
+      }
+      ++nb;
+      for (uint32_t i = 0; i < na && status == CAFXG_OK; ++i)
+        status = gemm_block(i, t);
+    }
+  }
+  if (!tev.empty()) {
+    cudaEventSynchronize(tev.back().second);
+    fprintf(stderr, "cafxg sgemm 2d trace (ms):");
+    for (auto& [w, e] : tev) {
+      float t = 0;
+      cudaEventElapsedTime(&t, tev[0].second, e);
+      fprintf(stderr, " %c%.2f", w, t);
+    }
+    fprintf(stderr, "\n");
+    for (auto& pe : tev)
+      cudaEventDestroy(pe.second);
+  }
+  CAFXG_TRY(stream_after_pooled(d, d->d2h, cs));
+  for (float* p : {dA, dB, Ah, Al, Bh, Bl, dC})
+    cudaFreeAsync(p, d->d2h);
+  for (auto e : evs)
+    if (e)
+      d->ev_pool.push_back(e);
+  return status;
+}
+
 // Host-to-host sgemm. One device: H2D A,B -> GEMM -> D2H C. G devices: A is
 // split into row blocks; each device uploads 1/G of B's rows and an NCCL
 // all-gather over NVLink completes B everywhere; each device returns its C
@@ -1260,6 +1408,20 @@ static int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
   join->user = user;
   join->remaining = (int)use;
   ctx->st_requests++;
+  if (use == 1 && sgemm_tiled2d_eligible(g)) {
+    Device* d = ctx->devs[0].get();
+    std::lock_guard<std::mutex> lk(d->submit_mu);
+    cudaSetDevice(d->ordinal);
+    int s = sgemm_tiled2d_device(ctx, d, g, A, B, C);
+    if (s != CAFXG_OK) {
+      // queued work may still read the host buffers: report after it
+      push_completion(ctx, d, d->d2h, [join, s](int) { join->part_done(s); });
+      return CAFXG_OK;
+    }
+    if (push_completion(ctx, d, d->d2h, [join](int st) { join->part_done(st); }) != CAFXG_OK)
+      join->part_done(CAFXG_E_DOWN);
+    return CAFXG_OK;
+  }
   const size_t bytesB = (size_t)g.K * g.ldb * 4;
   const uint32_t rows_per = (uint32_t)((g.M + use - 1) / use);
   // allocation + upload of B slices on every used device

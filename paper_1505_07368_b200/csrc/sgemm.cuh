@@ -34,8 +34,10 @@ struct SgemmTcMaps {
 };
 int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
                        const float* Bl, int N, int K, SgemmTcMaps* maps);
+// a_row0 / b_row0: this GEMM's first row inside the mapped A / B^T (block
+// (i, j) of a larger product whose maps were encoded once)
 int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
-                       void* stream, int splits);
+                       void* stream, int splits, int a_row0 = 0, int b_row0 = 0);
 // split-K factor (thread-block cluster size, <= 8) for small C grids
 int sgemm_tc_splits(int M, int N, int K, int sms);
 

@@ -167,7 +167,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         const __grid_constant__ CUtensorMap mAl,
                         const __grid_constant__ CUtensorMap mBh,
                         const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
-                        int M, int N, int K, int ldc, int splits) {
+                        int M, int N, int K, int ldc, int splits, int a_row0,
+                        int b_row0) {
+  // a_row0 / b_row0: first row of this GEMM's A / B^T block inside the
+  // matrices the tensor maps describe (a sub-block of a larger product)
   // split-K: the `splits` CTAs of one C tile form a thread-block cluster; CTA
   // z covers K range [z*K/splits, (z+1)*K/splits), parks its partial tile in
   // its own shared memory, and after a cluster barrier each CTA sums 1/splits
@@ -232,10 +235,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint8_t* st = smem + s * STAGE_BYTES;
       mbar_expect_tx(&full[s], STAGE_BYTES);
       const int kx = k_base + kb * BK;
-      tma_load_2d(st, &mAh, &full[s], kx, m0);
-      tma_load_2d(st + A_TILE, &mAl, &full[s], kx, m0);
-      tma_load_2d(st + 2 * A_TILE, &mBh, &full[s], kx, n0);
-      tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], kx, n0);
+      tma_load_2d(st, &mAh, &full[s], kx, a_row0 + m0);
+      tma_load_2d(st + A_TILE, &mAl, &full[s], kx, a_row0 + m0);
+      tma_load_2d(st + 2 * A_TILE, &mBh, &full[s], kx, b_row0 + n0);
+      tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], kx, b_row0 + n0);
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer ----
@@ -546,7 +549,7 @@ int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float
 }
 
 int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
-                       void* stream, int splits) {
+                       void* stream, int splits, int a_row0, int b_row0) {
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   {
     // once per device (the attribute is per-device state)
@@ -576,7 +579,7 @@ int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel, m[0], m[1], m[2], m[3], C, M, N, K, ldc,
-                     splits);
+                     splits, a_row0, b_row0);
   return (int)cudaGetLastError();
 }
 

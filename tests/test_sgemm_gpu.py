@@ -112,6 +112,23 @@ def test_sgemm_pipelined_host_request(ctx, M, N, K, pad):
         assert np.isnan(Cbig[:, N:]).all()   # the padding is never written
 
 
+@pytest.mark.parametrize("M,N,K,pad", [(8192, 8192, 256, 0), (8320, 8448, 128, 8)])
+def test_sgemm_2d_wavefront_host_request(ctx, M, N, K, pad):
+    """Large host request: A row blocks and B column blocks uploaded
+    interleaved, every C block multiplied once both operands are resident
+    and downloaded by itself; padded leading dimensions of A, B and C."""
+    Abig = oracle.fill_uniform(M * (K + pad), 41).reshape(M, K + pad)
+    Bbig = oracle.fill_uniform(K * (N + pad), 42).reshape(K, N + pad)
+    A, B = Abig[:, :K], Bbig[:, :N]
+    Cbig = np.full((M, N + pad), np.nan, dtype=np.float32)
+    C = Cbig[:, :N]
+    ctx.sgemm(A, B, C)
+    assert not np.isnan(C).any()
+    assert check(np.ascontiguousarray(A), np.ascontiguousarray(B), C) <= TOL
+    if pad:
+        assert np.isnan(Cbig[:, N:]).all()
+
+
 def test_sgemm_3xtf32_rejects_unsupported_shape(ctx):
     A = np.zeros((100, 64), np.float32)
     B = np.zeros((64, 256), np.float32)
