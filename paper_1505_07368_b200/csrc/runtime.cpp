@@ -613,7 +613,8 @@ static void pick_block(uint32_t max_iter, int precision, MandelLaunchCfg& c) {
 static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
                                   bool exact, bool safe, uint64_t pixels) {
   MandelLaunchCfg c;
-  c.ksteps = max_iter >= 512 ? 32 : max_iter >= 128 ? 16 : 4;
+  // checked kernel: steps between votes (cfg1, max_iter 100: 16 steps 0.065 ms, 4 steps 0.074)
+  c.ksteps = max_iter >= 512 ? 32 : max_iter >= 64 ? 16 : 4;
   static const int ks_env = [] {  // CAFXG_KSTEPS=4|16|32: experiments only
     const char* e = getenv("CAFXG_KSTEPS");
     return e ? atoi(e) : 0;
