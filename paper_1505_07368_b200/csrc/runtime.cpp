@@ -759,8 +759,12 @@ static std::vector<std::vector<SubTile>> plan_mandel(
   uint64_t total = 0;
   for (size_t i = 0; i < n; ++i)
     total += (uint64_t)tiles[i].nrows * tiles[i].ncols;
-  // band size: ~1M pixels when the request is large enough to share
-  const uint64_t band_px = (ndev > 1 || total > (64ull << 20)) ? (1ull << 20) : UINT64_MAX;
+  // band size: ~1M pixels when the request is large enough to share; a
+  // single-device request of 1M..64M pixels goes in two halves, so the first
+  // half's copy-out overlaps the second half's kernel (cfg1: 2M pixels)
+  const uint64_t band_px = (ndev > 1 || total > (64ull << 20)) ? (1ull << 20)
+                           : total >= (1ull << 20)           ? (total + 1) / 2
+                                                            : UINT64_MAX;
   size_t next = 0;
   for (size_t i = 0; i < n; ++i) {
     const cafxg_mandel_desc& t = tiles[i];
@@ -811,6 +815,8 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
   // pixels still to schedule: waves shrink geometrically towards the end so
   // the copy-out left exposed after the last kernel is small
   uint64_t left = dev_px_total;
+  // smallest wave: 4M pixels (launch overhead), 1M for small requests
+  const uint64_t min_wave = dev_px_total >= (64ull << 20) ? (4ull << 20) : (1ull << 20);
   // CAFXG_TRACE=1: per-wave device timeline on stderr (debug aid)
   static const bool trace = [] {
     const char* e = getenv("CAFXG_TRACE");
@@ -827,7 +833,7 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
     size_t j = i;
     uint64_t px = 0;
     int prec = subs[i].d.precision;
-    const uint64_t cap = std::max<uint64_t>(std::min<uint64_t>(wave_px, left / 4), 4ull << 20);
+    const uint64_t cap = std::max<uint64_t>(std::min<uint64_t>(wave_px, left / 4), min_wave);
     while (j < subs.size() && subs[j].d.precision == prec &&
            (px == 0 || px + subs[j].pixels <= cap)) {
       px += subs[j].pixels;
