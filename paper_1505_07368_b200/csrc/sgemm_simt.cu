@@ -67,12 +67,15 @@ __global__ void __launch_bounds__(NT, 2)
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 
-  float acc[8][8];
+  // accumulators as packed pairs (columns 2p, 2p+1 of row i): the inner
+  // product is issued as FFMA2 (two FMAs per lane per instruction), which
+  // halves the issue slots the FMAs take next to the shared-memory loads
+  uint64_t acc2[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      acc[i][j] = 0.0f;
+    for (int j = 0; j < 4; ++j)
+      acc2[i][j] = 0ull;
 
   float ra[8], rb[8];
   const int ar = threadIdx.x >> 2, ac = (threadIdx.x & 3) * 4;
@@ -103,20 +106,26 @@ __global__ void __launch_bounds__(NT, 2)
     }
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
-      float a[8], b[8];
-      float4 a0 = *reinterpret_cast<const float4*>(&As[cur][k][ty * 4]);
-      float4 a1 = *reinterpret_cast<const float4*>(&As[cur][k][ty * 4 + 64]);
-      float4 b0 = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * 4]);
-      float4 b1 = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * 4 + 64]);
+      float a[8];
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[cur][k][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[cur][k][ty * 4 + 64]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * 4 + 64]);
       a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
       a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
-      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
-      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+      uint64_t b2[4];
+      asm("mov.b64 %0, {%1, %2};" : "=l"(b2[0]) : "f"(b0.x), "f"(b0.y));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(b2[1]) : "f"(b0.z), "f"(b0.w));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(b2[2]) : "f"(b1.x), "f"(b1.y));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(b2[3]) : "f"(b1.z), "f"(b1.w));
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 8; ++i) {
+        uint64_t a2;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(a2) : "f"(a[i]));
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j)
+          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[i][j]) : "l"(a2), "l"(b2[j]));
+      }
     }
     if (kt + 1 < nk) {
       stash(cur ^ 1);
@@ -124,6 +133,12 @@ __global__ void __launch_bounds__(NT, 2)
     }
   }
 
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[i][2 * j]), "=f"(acc[i][2 * j + 1]) : "l"(acc2[i][j]));
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     int gm = m0 + ty * 4 + (i & 3) + (i >> 2) * 64;
