@@ -799,7 +799,11 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
                                 bool exact, Join* join) {
   cudaSetDevice(d->ordinal);
   std::lock_guard<std::mutex> g(d->submit_mu);
-  const uint64_t wave_px = 16ull << 20;
+  static const uint64_t wave_px = [] {  // CAFXG_WAVE_MPX: experiments only
+    const char* e = getenv("CAFXG_WAVE_MPX");
+    const int v = e ? atoi(e) : 0;
+    return (v > 0 ? (uint64_t)v : 32ull) << 20;
+  }();
   uint32_t* staging = nullptr;  // pinned bounce buffer for pageable outputs
   uint64_t dev_px_total = 0;
   for (auto& s : subs)
@@ -816,7 +820,12 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
   // the copy-out left exposed after the last kernel is small
   uint64_t left = dev_px_total;
   // smallest wave: 4M pixels (launch overhead), 1M for small requests
-  const uint64_t min_wave = dev_px_total >= (64ull << 20) ? (4ull << 20) : (1ull << 20);
+  static const uint64_t big_min = [] {  // CAFXG_MIN_WAVE_MPX: experiments only
+    const char* e = getenv("CAFXG_MIN_WAVE_MPX");
+    const int v = e ? atoi(e) : 0;
+    return (v > 0 ? (uint64_t)v : 2ull) << 20;
+  }();
+  const uint64_t min_wave = dev_px_total >= (64ull << 20) ? big_min : (1ull << 20);
   // CAFXG_TRACE=1: per-wave device timeline on stderr (debug aid)
   static const bool trace = [] {
     const char* e = getenv("CAFXG_TRACE");
