@@ -760,11 +760,12 @@ static std::vector<std::vector<SubTile>> plan_mandel(
   for (size_t i = 0; i < n; ++i)
     total += (uint64_t)tiles[i].nrows * tiles[i].ncols;
   // band size: ~1M pixels when the request is large enough to share; a
-  // single-device request of 1M..64M pixels goes in two halves, so the first
-  // half's copy-out overlaps the second half's kernel (cfg1: 2M pixels)
+  // single-device request of 1M..64M pixels goes in ~8 bands of >= 1M (two
+  // for cfg1's 2M pixels), so copy-outs overlap the later bands' kernels
+  // (a rank's 1/8 share of cfg3 is 32M pixels)
   const uint64_t band_px = (ndev > 1 || total > (64ull << 20)) ? (1ull << 20)
-                           : total >= (1ull << 20)           ? (total + 1) / 2
-                                                            : UINT64_MAX;
+                           : total >= (1ull << 20) ? std::max<uint64_t>((total + 7) / 8, 1ull << 20)
+                                                   : UINT64_MAX;
   size_t next = 0;
   for (size_t i = 0; i < n; ++i) {
     const cafxg_mandel_desc& t = tiles[i];
