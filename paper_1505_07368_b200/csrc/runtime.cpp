@@ -270,6 +270,10 @@ struct Device {
   // enqueued, so these never need to be destroyed per request
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t order_ev = nullptr;   // stream_after_pooled
+  // grow-only workspace of the host sgemm row-block pipeline (caller holds
+  // submit_mu; each request orders itself after the previous one's use)
+  float* sgemm_ws = nullptr;
+  size_t sgemm_ws_bytes = 0;
   cudaEvent_t trace_ref = nullptr;  // CAFXG_TRACE time base
   double trace_ref_ms = 0;
 
@@ -1136,15 +1140,38 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
   float* dA[2] = {nullptr, nullptr};
   float* dC[2] = {nullptr, nullptr};
   cudaStream_t cs = d->compute;
-  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Bh, N * K * 4, cs));
-  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Bl, N * K * 4, cs));
-  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Ah, (size_t)R * K * 4, cs));
-  CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Al, (size_t)R * K * 4, cs));
-  for (int b = 0; b < 2; ++b) {
-    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dA[b], (size_t)R * K * 4, cs));
-    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dC[b], (size_t)R * N * 4, cs));
+  // buffers carved from the device's grow-only workspace (a stream-ordered
+  // allocation and free per buffer and request cost more host time than the
+  // GEMMs of a 1024^3 request); 256-byte aligned pieces
+  {
+    const size_t pieces[8] = {N * K, N * K, (size_t)R * K, (size_t)R * K, (size_t)R * K,
+                              (size_t)R * K, (size_t)R * N, (size_t)R * N};
+    size_t need = 0;
+    for (size_t p : pieces)
+      need += (p * 4 + 255) / 256 * 256;
+    if (d->sgemm_ws_bytes < need) {
+      if (d->sgemm_ws) {
+        cudaStreamSynchronize(d->h2d);
+        cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(d->d2h);
+        cudaFree(d->sgemm_ws);
+        d->sgemm_ws = nullptr;
+        d->sgemm_ws_bytes = 0;
+      }
+      CAFXG_CUDA_TRY(cudaMalloc((void**)&d->sgemm_ws, need));
+      d->sgemm_ws_bytes = need;
+    }
+    float** dst[8] = {&Bh, &Bl, &Ah, &Al, &dA[0], &dA[1], &dC[0], &dC[1]};
+    uint8_t* base = reinterpret_cast<uint8_t*>(d->sgemm_ws);
+    for (int i = 0; i < 8; ++i) {
+      *dst[i] = reinterpret_cast<float*>(base);
+      base += (pieces[i] * 4 + 255) / 256 * 256;
+    }
   }
-  CAFXG_TRY(stream_after_pooled(d, d->h2d, cs));  // the buffers exist before uploads
+  // the previous request's kernels and downloads are done with the workspace
+  // before this one's uploads and kernels touch it
+  CAFXG_TRY(stream_after_pooled(d, cs, d->d2h));
+  CAFXG_TRY(stream_after_pooled(d, d->h2d, cs));
   // CAFXG_TRACE=1: device timeline of the request (uploads, GEMMs, downloads)
   std::vector<std::pair<const char*, cudaEvent_t>> tev;
   const double t_host0 = trace_now_ms();
@@ -1238,8 +1265,6 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
   // everything is released on the download stream, which by now follows
   // every upload and kernel of this request
   CAFXG_TRY(stream_after_pooled(d, d->d2h, cs));
-  for (float* p : {Bh, Bl, Ah, Al, dA[0], dA[1], dC[0], dC[1]})
-    cudaFreeAsync(p, d->d2h);
   // every wait on these records is enqueued: back to the pool
   for (auto* v : {&ev_split, &ev_gemm, &ev_down})
     for (auto ev : *v)
@@ -2194,6 +2219,8 @@ int cafxg_close(cafxg_ctx* ctx) try {
       cudaEventDestroy(ev);
     for (auto ev : d->ev_pool)
       cudaEventDestroy(ev);
+    if (d->sgemm_ws)
+      cudaFree(d->sgemm_ws);
     if (d->order_ev)
       cudaEventDestroy(d->order_ev);
     cudaFreeHost(d->up_base);
