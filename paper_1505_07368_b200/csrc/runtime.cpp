@@ -764,11 +764,16 @@ static std::vector<std::vector<SubTile>> plan_mandel(
   for (size_t i = 0; i < n; ++i)
     total += (uint64_t)tiles[i].nrows * tiles[i].ncols;
   // band size: ~1M pixels when the request is large enough to share; a
-  // single-device request of 1M..64M pixels goes in ~8 bands of >= 1M (two
+  // single-device request of 1M..64M pixels goes in ~8 bands of >= 512K (four
   // for cfg1's 2M pixels), so copy-outs overlap the later bands' kernels
   // (a rank's 1/8 share of cfg3 is 32M pixels)
+  static const uint64_t band_min = [] {  // CAFXG_BAND_MIN_KPX: experiments only
+    const char* e = getenv("CAFXG_BAND_MIN_KPX");
+    const int v = e ? atoi(e) : 0;
+    return (v > 0 ? (uint64_t)v : 512ull) << 10;
+  }();
   const uint64_t band_px = (ndev > 1 || total > (64ull << 20)) ? (1ull << 20)
-                           : total >= (1ull << 20) ? std::max<uint64_t>((total + 7) / 8, 1ull << 20)
+                           : total >= (1ull << 20) ? std::max<uint64_t>((total + 7) / 8, band_min)
                                                    : UINT64_MAX;
   size_t next = 0;
   for (size_t i = 0; i < n; ++i) {
@@ -824,13 +829,18 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
   // pixels still to schedule: waves shrink geometrically towards the end so
   // the copy-out left exposed after the last kernel is small
   uint64_t left = dev_px_total;
-  // smallest wave: 4M pixels (launch overhead), 1M for small requests
+  // smallest wave: 2M pixels (launch overhead), 512K for small requests
   static const uint64_t big_min = [] {  // CAFXG_MIN_WAVE_MPX: experiments only
     const char* e = getenv("CAFXG_MIN_WAVE_MPX");
     const int v = e ? atoi(e) : 0;
     return (v > 0 ? (uint64_t)v : 2ull) << 20;
   }();
-  const uint64_t min_wave = dev_px_total >= (64ull << 20) ? big_min : (1ull << 20);
+  static const uint64_t small_min = [] {  // CAFXG_SMALL_WAVE_KPX: experiments only
+    const char* e = getenv("CAFXG_SMALL_WAVE_KPX");
+    const int v = e ? atoi(e) : 0;
+    return (v > 0 ? (uint64_t)v : 512ull) << 10;
+  }();
+  const uint64_t min_wave = dev_px_total >= (64ull << 20) ? big_min : small_min;
   // CAFXG_TRACE=1: per-wave device timeline on stderr (debug aid)
   static const bool trace = [] {
     const char* e = getenv("CAFXG_TRACE");
