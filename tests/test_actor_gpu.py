@@ -156,6 +156,83 @@ def test_matrix_multiply_actor(ctx):
     a.release()
 
 
+def test_mixed_clients_two_actors(ctx):
+    """8 client threads send an interleaved random mix to a Mandelbrot actor
+    (fp32 / fp64, storm tiles and multi-tile images, pinned and pageable
+    replies) and two matrix_multiply actors (256 and 1024) at once; every
+    reply is checked. Exercises the dispatcher's batching across kinds and
+    precisions, the staging ring and the sgemm host paths concurrently."""
+    mb = ctx.spawn("mandelbrot")
+    mm = {256: ctx.spawn("matrix_multiply", (256, 256)),
+          1024: ctx.spawn("matrix_multiply", (1024, 1024))}
+    mats = {n: (oracle.fill_uniform(n * n, 50 + n), oracle.fill_uniform(n * n, 60 + n))
+            for n in mm}
+    errors, checks = [], []
+    lock = threading.Lock()
+
+    def client(c):
+        rng = np.random.default_rng(300 + c)
+        try:
+            pend = []
+            for i in range(24):
+                kind = int(rng.integers(0, 6))
+                if kind <= 2:    # one storm tile
+                    d = storm_tile(rng, it=int(rng.choice([100, 256, 700])))
+                    d.precision = pkg.FP64 if kind == 0 else pkg.FP32
+                    out = ctx.pinned_empty(4096, np.uint32) if i & 1 else np.zeros(4096, np.uint32)
+                    pend.append(("tile", d, out, mb.request([(pkg.MandelDesc * 1)(d)], out)))
+                elif kind <= 4:  # a small image in two tiles
+                    w, h = int(rng.integers(40, 200)), int(rng.integers(2, 60))
+                    it = int(rng.choice([50, 300]))
+                    t0 = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, w, h, it, row0=0, nrows=h // 2)
+                    t1 = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, w, h, it, row0=h // 2,
+                                         nrows=h - h // 2)
+                    out = np.zeros(w * h, np.uint32)
+                    pend.append(("image", (w, h, it), out,
+                                 mb.request([(pkg.MandelDesc * 2)(t0, t1)], out)))
+                else:            # matrix_multiply
+                    n = 256 if rng.integers(0, 2) else 1024
+                    A, B = mats[n]
+                    out = np.zeros(n * n, np.float32)
+                    pend.append(("mm", n, out, mm[n].request([A, B], out)))
+            for kind, arg, out, fut in pend:
+                fut.result(timeout=120)
+                with lock:
+                    checks.append((kind, arg, out))
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=client, args=(c,)) for c in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
+    assert len(checks) == 8 * 24
+    for kind, arg, out in checks:
+        if kind == "tile":
+            d = arg
+            ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, 64, 64, d.max_iter,
+                              fp64=d.precision == pkg.FP64, centre=True)
+            assert np.array_equal(out.reshape(64, 64), ref)
+        elif kind == "image":
+            w, h, it = arg
+            ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, w, h, it, fp64=False, centre=True)
+            assert np.array_equal(out.reshape(h, w), ref)
+        else:
+            n = arg
+            A, B = mats[n]
+            rows = np.arange(0, n, n // 8, dtype=np.uint32)
+            R = oracle.sgemm_ref_rows(A.reshape(n, n), B.reshape(n, n), rows, n, n)
+            assert oracle.sgemm_rel_err(out.reshape(n, n), R, rows, n) <= 1e-5
+    for kind, _, o in checks:
+        if kind == "tile":
+            ctx.pinned_free(o)   # no-op for the pageable ones
+    mb.release()
+    for a in mm.values():
+        a.release()
+
+
 def test_interface_errors(ctx):
     with pytest.raises(pkg.CafxgError) as e:
         ctx.spawn("no_such_kernel")
