@@ -1308,7 +1308,16 @@ static int sgemm_tiled2d_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_des
     return v >= 2 && v <= 64 ? (uint32_t)v : 8u;
   }();
   const uint32_t Mb = (uint32_t)((M / div + 127) / 128 * 128);
-  const uint32_t Nb = (uint32_t)((N / div + 255) / 256 * 256);
+  // column blocks sized so a block's C tiles (128 x 256 each, one CTA per
+  // tile) come close to one full wave of SMs: 2048 x 2304 blocks are 144
+  // tiles on 148 SMs where 2048 x 2048 were 128
+  uint32_t Nb = (uint32_t)((N / div + 255) / 256 * 256);
+  {
+    const uint32_t rows_t = Mb / 128;
+    uint32_t cols_t = std::max<uint32_t>(1, (uint32_t)d->sms / std::max<uint32_t>(1, rows_t));
+    if (cols_t * 256 >= Nb && cols_t * 256 < 2 * Nb)
+      Nb = std::min<uint32_t>(cols_t * 256, (uint32_t)N);
+  }
   const uint32_t nbm = (uint32_t)((M + Mb - 1) / Mb), nbn = (uint32_t)((N + Nb - 1) / Nb);
   cudaStream_t cs = d->compute;
   float *dA = nullptr, *dB = nullptr, *Ah = nullptr, *Al = nullptr, *Bh = nullptr,
