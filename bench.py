@@ -43,6 +43,8 @@ MAX_ITER = 1000
 REGION = (-0.75, -0.73, 0.10, 0.12)
 BAND_ROWS = 64
 METRIC = "Mandelbrot Giter/s (BASELINE cfg3: 16384^2 fp32 max_iter=1000 zoom)"
+WORKLOAD = ("cfg3: one 16384x16384 fp32 Mandelbrot request, max_iter=1000, "
+            "x[-0.75,-0.73] y[0.10,0.12], pixel centres")
 
 
 def parse():
@@ -156,13 +158,24 @@ def peaks():
 # ---- CPU baselines (test infrastructure: oracle) ---------------------------------------
 
 def cpu_cfg3_sample(target_s: float = 12.0):
-    """Times the oracle restatement on a row sample of cfg3 with every host
-    thread; returns (Giter/s, cores, description)."""
+    """Times the reference's CPU path on a row sample of cfg3 with every host
+    thread; returns (Giter/s, cores, kind, description). kind "reference":
+    the unmodified reference's own escape loop (cafx::bench::mandelbrot_cell,
+    bench.cpp:367, compiled from its sources into oracle/_ref) over cfg3's
+    region at pixel centres -- in fp64, the only precision the reference has;
+    kind "port": the oracle restatement in fp32 when oracle/_ref is absent."""
+    import ctypes
     from oracle import oracle
     threads = os.cpu_count() or 1
     x0, x1, y0, y1 = REGION
+    R = oracle.ref()
 
     def run(stride):
+        if R is not None:
+            sec = ctypes.c_double()
+            iters = R.ref_region_iters_mt(x0, x1, y0, y1, W_IMG, H_IMG, MAX_ITER, stride,
+                                          threads, ctypes.byref(sec))
+            return float(iters), sec.value
         t0 = time.perf_counter()
         out = oracle.tile(x0, x1, y0, y1, W_IMG, H_IMG, MAX_ITER, fp64=False, centre=True,
                           threads=threads, sample_stride=stride)
@@ -175,10 +188,17 @@ def cpu_cfg3_sample(target_s: float = 12.0):
     rows = max(16, min(H_IMG, int(target_s * rate / per_row)))
     stride = max(1, H_IMG // rows)
     iters, dt = run(stride)
-    return iters / dt / 1e9, threads, (
-        f"oracle port (cafx_oracle.c, -O3 -ffp-contract=off), every {stride}th row of cfg3 "
-        f"({H_IMG // stride} rows x {W_IMG} px, {iters:.3g} iterations in {dt:.2f} s), "
-        f"{threads} threads, rows dealt cyclically")
+    if R is not None:
+        kind = "reference"
+        what = ("the unmodified reference's mandelbrot_cell (bench.cpp:367, oracle/_ref, "
+                "compiled from its sources with its own flags) in fp64 -- the reference has "
+                "no fp32 path -- over cfg3's region at pixel centres")
+    else:
+        kind = "port"
+        what = "oracle port (cafx_oracle.c, -O3 -ffp-contract=off) in fp32"
+    return iters / dt / 1e9, threads, kind, (
+        f"{what}, every {stride}th row of cfg3 ({H_IMG // stride} rows x {W_IMG} px, "
+        f"{iters:.3g} iterations in {dt:.2f} s), {threads} threads, rows dealt cyclically")
 
 
 def reference_paper_scale():
@@ -203,40 +223,55 @@ def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
+    import ctypes
     from oracle import oracle
     threads = os.cpu_count() or 1
     x0, x1, y0, y1 = REGION
-    # size the per-step sample to ~4 s of CPU work
-    t0 = time.perf_counter()
-    probe = oracle.tile(x0, x1, y0, y1, W_IMG, H_IMG, MAX_ITER, fp64=False, centre=True,
-                        threads=threads, sample_stride=1024)
-    rate = float(probe[::1024].sum()) / (time.perf_counter() - t0)
-    per_row = float(probe[::1024].sum()) / (H_IMG // 1024)
-    stride = max(1, H_IMG // max(16, min(H_IMG, int(4.0 * rate / per_row))))
-    times, iters = [], 0.0
-    for k in range(args.warmup + args.steps):
+    R = oracle.ref()
+
+    # the reference's own escape loop (mandelbrot_cell, bench.cpp:367, from
+    # oracle/_ref) over cfg3's region in fp64 (it has no fp32 path); the
+    # oracle port in fp32 only when the reference could not be compiled
+    def run(stride):
+        if R is not None:
+            sec = ctypes.c_double()
+            it = R.ref_region_iters_mt(x0, x1, y0, y1, W_IMG, H_IMG, MAX_ITER, stride, threads,
+                                       ctypes.byref(sec))
+            return float(it), sec.value
         t0 = time.perf_counter()
         out = oracle.tile(x0, x1, y0, y1, W_IMG, H_IMG, MAX_ITER, fp64=False, centre=True,
                           threads=threads, sample_stride=stride)
-        dt = time.perf_counter() - t0
+        return float(out[::stride].sum(dtype="uint64")), time.perf_counter() - t0
+
+    # size the per-step sample to ~4 s of CPU work
+    it, dt = run(1024)
+    rate, per_row = it / dt, it / (H_IMG // 1024)
+    stride = max(1, H_IMG // max(16, min(H_IMG, int(4.0 * rate / per_row))))
+    times, iters = [], 0.0
+    for k in range(args.warmup + args.steps):
+        it, dt = run(stride)
         if k >= args.warmup:
             times.append(dt)
-            iters = float(out[::stride].sum(dtype="uint64"))
+            iters = it
     step_s = statistics.mean(times)
     value = iters / step_s / 1e9
+    kind = "reference" if R is not None else "port"
     sample = (f"every {stride}th row of cfg3 ({H_IMG // stride} rows x {W_IMG} px, "
               f"{iters:.3g} iterations per step)")
+    note = ("the unmodified reference's mandelbrot_cell (bench.cpp:367, oracle/_ref) in fp64 "
+            "-- the reference has no fp32 path and hard-codes [-1.5,0.5]x[-1,1] in "
+            "mandelbrot_row (bench.cpp:384-386), so its escape loop is driven over cfg3's "
+            "pixel centres directly" if R is not None else
+            "oracle port in fp32 (oracle/_ref not built)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Giter/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(step_s * 1e3, 2), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (deterministic plane grid)",
-        "config": {"workload": "cfg3 16384x16384 fp32 max_iter=1000 x[-0.75,-0.73] "
-                               "y[0.10,0.12] pixel centres", "sample": sample},
+        "vs_baseline": None, "dtype": "f64" if R is not None else "f32",
+        "data": "synthetic (deterministic plane grid)",
+        "config": {"workload": WORKLOAD, "sample": sample},
         "cpu_baseline": {"value": round(value, 4), "unit": "Giter/s", "cores": threads,
-                         "kind": "port", "sample": sample + "; the reference hard-codes "
-                         "fp64 and [-1.5,0.5]x[-1,1] (bench.cpp:384-386), so its own "
-                         "code cannot run this config; paper-scale run below"},
+                         "kind": kind, "sample": sample + "; " + note},
         "e2e": {"value": round(value, 4), "unit": "Giter/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -393,8 +428,8 @@ def run_ours(args):
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        v, cores, desc = cpu_cfg3_sample()
-        cpu = {"value": round(v, 4), "unit": "Giter/s", "cores": cores, "kind": "port",
+        v, cores, kind, desc = cpu_cfg3_sample()
+        cpu = {"value": round(v, 4), "unit": "Giter/s", "cores": cores, "kind": kind,
                "sample": desc}
 
     if rank == 0:
@@ -403,8 +438,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (deterministic plane grid, BASELINE cfg3)",
-            "config": {"workload": "cfg3: one 16384x16384 fp32 Mandelbrot request, "
-                                   "max_iter=1000, x[-0.75,-0.73] y[0.10,0.12], pixel centres",
+            "config": {"workload": WORKLOAD,
                        "sharding": f"cyclic {BAND_ROWS}-row bands over {world} rank(s)",
                        "iterations_per_step": iters_total,
                        "l2": "256 MiB L2 flush between steps (untimed); output >= 128 MiB/rank",

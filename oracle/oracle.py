@@ -84,6 +84,10 @@ def ref():
         R.ref_run_mandelbrot.restype = C.c_uint64
         R.ref_run_mandelbrot.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32,
                                          C.POINTER(C.c_double)]
+        R.ref_region_iters_mt.restype = C.c_uint64
+        R.ref_region_iters_mt.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double,
+                                          C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, C.POINTER(C.c_double)]
         _ref = R
     return _ref
 

@@ -115,3 +115,18 @@ def test_sgemm_reference_rows():
     C = np.zeros((48, 56), dtype=np.float32)
     oracle.sgemm_f32(A, B, C, 56, 40, 0, 48, block=8, threads=3)
     assert oracle.sgemm_rel_err(C, R, rows, 56) < 1e-6
+
+
+@pytest.mark.skipif(oracle.ref() is None, reason="oracle/_ref not built (no /root/reference)")
+def test_reference_region_driver_matches_oracle():
+    """bench.py's CPU baseline drives the reference's own mandelbrot_cell over
+    a region at pixel centres (ref_region_iters_mt, oracle/ref_shim.cpp): its
+    iteration sum equals the fp64 oracle's on the same sampled rows."""
+    import ctypes as C
+    R = oracle.ref()
+    for (x0, x1, y0, y1, w, h, it, stride) in [(-0.75, -0.73, 0.10, 0.12, 97, 64, 300, 5),
+                                               (-2.0, 1.0, -1.0, 1.0, 120, 90, 100, 1)]:
+        sec = C.c_double()
+        got = R.ref_region_iters_mt(x0, x1, y0, y1, w, h, it, stride, 3, C.byref(sec))
+        ref = oracle.tile(x0, x1, y0, y1, w, h, it, fp64=True, centre=True)
+        assert got == int(ref[::stride].sum(dtype=np.uint64))
