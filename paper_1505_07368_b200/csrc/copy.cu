@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.hpp"
 
@@ -44,6 +45,18 @@ __global__ void __launch_bounds__(1024) copy_segments_inline_kernel(
 
 }  // namespace
 
+// CTAs of a scatter launch: a few wide CTAs already saturate PCIe writes and
+// leave the other SMs to the next batch's escape kernel (CAFXG_SCATTER_CTAS
+// overrides, experiments only)
+static uint32_t scatter_ctas(uint32_t n) {
+  static const uint32_t cap = [] {
+    const char* e = getenv("CAFXG_SCATTER_CTAS");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? (uint32_t)v : 16u;
+  }();
+  return n < cap ? n : cap;
+}
+
 int copy_segments_inline_launch(const CopySeg* segs_host, uint32_t n, void* stream) {
   if (n == 0)
     return 0;
@@ -52,7 +65,7 @@ int copy_segments_inline_launch(const CopySeg* segs_host, uint32_t n, void* stre
   InlineSegs p;
   for (uint32_t i = 0; i < n; ++i)
     p.s[i] = segs_host[i];
-  uint32_t grid = n < 16 ? n : 16;
+  uint32_t grid = scatter_ctas(n);
   copy_segments_inline_kernel<<<grid, 1024, 0, (cudaStream_t)stream>>>(p, n);
   return (int)cudaGetLastError();
 }
@@ -63,7 +76,7 @@ int copy_segments_launch(const CopySeg* segs_dev, uint32_t n, void* stream) {
   // A few wide CTAs already saturate PCIe writes (~53 GB/s measured with
   // 16 x 1024 threads); leaving the other SMs free lets the next batch's
   // escape kernel run concurrently on the compute stream.
-  uint32_t grid = n < 16 ? n : 16;
+  uint32_t grid = scatter_ctas(n);
   copy_segments_kernel<<<grid, 1024, 0, (cudaStream_t)stream>>>(segs_dev, n);
   return (int)cudaGetLastError();
 }
