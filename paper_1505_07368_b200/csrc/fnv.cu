@@ -37,8 +37,8 @@ constexpr int kTile = 256;       // cells staged in smem per round (pass 1; 4 KB
 constexpr int kRecWords = 64;    // 256 low bytes = 64 packed words per record
 
 // Pass 1: per segment, the low byte after every sub-segment for all 256
-// incoming low bytes. Thread t tracks incoming values 8t..8t+7 in four
-// registers, two 16-bit slots each (value in bits 0-7 / 16-23): one step is
+// incoming low bytes (128 tracked, see below), two per register in 16-bit
+// slots (value in bits 0-7 / 16-23): one step is
 // r = ((r ^ b) & 0x00ff00ff) * 179 -- one LOP3 and one IMAD per two lanes
 // (179 * 255 < 2^16, so the slots never interfere; the next step's mask
 // drops the product's high byte). rec[(seg * kSubSegs + j) * 64 + w] holds
@@ -56,19 +56,26 @@ __global__ void __launch_bounds__(kP1Threads)
   const uint64_t begin = (uint64_t)seg * seg_cells;
   const uint64_t end = begin + seg_cells < n ? begin + seg_cells : n;
   const uint32_t tid = threadIdx.x;
-  uint32_t r[4];
+  // Only incoming low bytes 0..127 are tracked: every step is "bit j flips
+  // with input bit j, plus a function of the lower bits" (XOR with a byte,
+  // multiplication by an odd constant), and so is any composition of steps;
+  // hence out(v + 128) = out(v) ^ 128 and the other half of every record and
+  // table is the tracked half with the top bit flipped. Lane t tracks values
+  // 4t..4t+3 in two registers (two 16-bit slots each).
+  uint32_t r[2];
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
-    r[k] = (8 * tid + 2 * k) | ((8 * tid + 2 * k + 1) << 16);
-  uint32_t* myrec = rec + (size_t)seg * kSubSegs * kRecWords + 2 * tid;
+  for (int k = 0; k < 2; ++k)
+    r[k] = (4 * tid + 2 * k) | ((4 * tid + 2 * k + 1) << 16);
+  uint32_t* myrec = rec + (size_t)seg * kSubSegs * kRecWords + tid;
   auto record = [&](uint32_t j) {
     // low bytes of the slots, packed in incoming-value order
-    myrec[(size_t)j * kRecWords] = __byte_perm(r[0], r[1], 0x6420);
-    myrec[(size_t)j * kRecWords + 1] = __byte_perm(r[2], r[3], 0x6420);
+    const uint32_t w = __byte_perm(r[0], r[1], 0x6420);
+    myrec[(size_t)j * kRecWords] = w;
+    myrec[(size_t)j * kRecWords + 32] = w ^ 0x80808080u;
   };
   auto step = [&](uint32_t bb) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 2; ++k)
       r[k] = ((r[k] ^ bb) & 0x00ff00ffu) * 179u;
   };
   uint64_t next_rec = begin;  // cell index of the next sub-segment start
@@ -107,9 +114,10 @@ __global__ void __launch_bounds__(kP1Threads)
   }
   for (; j < kSubSegs; ++j)  // empty trailing sub-segments start where we end
     record(j);
-  uint32_t* out = reinterpret_cast<uint32_t*>(L + (size_t)seg * 256) + 2 * tid;
-  out[0] = __byte_perm(r[0], r[1], 0x6420);
-  out[1] = __byte_perm(r[2], r[3], 0x6420);
+  uint32_t* out = reinterpret_cast<uint32_t*>(L + (size_t)seg * 256) + tid;
+  const uint32_t w = __byte_perm(r[0], r[1], 0x6420);
+  out[0] = w;
+  out[32] = w ^ 0x80808080u;
 }
 
 // Pass 2: the real incoming low byte of every segment, and the final one.
