@@ -121,29 +121,56 @@ __global__ void __launch_bounds__(kP1Threads)
 }
 
 // Pass 2: the real incoming low byte of every segment, and the final one.
-// One CTA: the tables are staged through shared memory 32 segments at a time
-// so the single walking thread chases pointers in smem, not L2.
-__global__ void __launch_bounds__(256)
-    fnv_scan_kernel(const uint8_t* __restrict__ L, uint32_t nseg, uint64_t seed,
-                    uint8_t* __restrict__ lin) {
-  __shared__ uint32_t tab[32 * 64];
-  uint32_t l = (uint32_t)(seed & 255u);
-  for (uint32_t s0 = 0; s0 < nseg; s0 += 32) {
-    const uint32_t cnt = nseg - s0 < 32 ? nseg - s0 : 32;
-    __syncthreads();
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(L + (size_t)s0 * 256);
-    for (uint32_t i = threadIdx.x; i < cnt * 64; i += blockDim.x)
-      tab[i] = src[i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint8_t* t = reinterpret_cast<const uint8_t*>(tab);
-      for (uint32_t k = 0; k < cnt; ++k) {
-        lin[s0 + k] = (uint8_t)l;
-        l = t[k * 256 + l];
-      }
-    }
+// Segment maps compose, so the walk is two-level: (a) one warp per group of
+// kGroup segments composes the group's tables into one; (b) one thread walks
+// the group tables from the seed; (c) one thread per group walks its own
+// segments from the group's incoming byte.
+constexpr uint32_t kGroup = 64;
+
+__global__ void __launch_bounds__(32)
+    fnv_group_tables_kernel(const uint8_t* __restrict__ L, uint32_t nseg,
+                            uint8_t* __restrict__ GT) {
+  const uint32_t g = blockIdx.x, lane = threadIdx.x;
+  const uint32_t s0 = g * kGroup, s1 = min(nseg, s0 + kGroup);
+  uint32_t v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    v[i] = lane * 8 + i;  // T = identity on the lane's 8 values
+  for (uint32_t k = s0; k < s1; ++k) {
+    const uint8_t* t = L + (size_t)k * 256;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = __ldg(t + v[i]);
   }
-  if (threadIdx.x == 0)
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    GT[(size_t)g * 256 + lane * 8 + i] = (uint8_t)v[i];
+}
+
+__global__ void fnv_group_walk_kernel(const uint8_t* __restrict__ GT, uint32_t ngroups,
+                                      uint64_t seed, uint8_t* __restrict__ gin) {
+  uint32_t l = (uint32_t)(seed & 255u);
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    gin[g] = (uint8_t)l;
+    l = GT[(size_t)g * 256 + l];
+  }
+  gin[ngroups] = (uint8_t)l;
+}
+
+__global__ void __launch_bounds__(256)
+    fnv_segment_walk_kernel(const uint8_t* __restrict__ L, uint32_t nseg,
+                            const uint8_t* __restrict__ gin, uint8_t* __restrict__ lin) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t ngroups = (nseg + kGroup - 1) / kGroup;
+  if (g >= ngroups)
+    return;
+  uint32_t l = gin[g];
+  const uint32_t s0 = g * kGroup, s1 = min(nseg, s0 + kGroup);
+  for (uint32_t k = s0; k < s1; ++k) {
+    lin[k] = (uint8_t)l;
+    l = __ldg(L + (size_t)k * 256 + l);
+  }
+  if (s1 == nseg)
     lin[nseg] = (uint8_t)l;
 }
 
@@ -209,14 +236,35 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Fold: u = u * P_s + C_s over the segments in order.
-__global__ void fnv_fold_kernel(const uint64_t* __restrict__ SP, const uint64_t* __restrict__ SC,
-                                uint32_t nseg, uint64_t seed, const uint8_t* __restrict__ lin,
-                                uint64_t* out) {
+// Fold: u = u * P_s + C_s over the segments in order, two-level like the
+// walk: one thread composes each group's maps ((P1,C1) then (P2,C2) =
+// (P1 P2, C1 P2 + C2)), one thread folds the groups from the seed.
+__global__ void __launch_bounds__(256)
+    fnv_group_affine_kernel(const uint64_t* __restrict__ SP, const uint64_t* __restrict__ SC,
+                            uint32_t nseg, uint64_t* __restrict__ GP,
+                            uint64_t* __restrict__ GC) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t ngroups = (nseg + kGroup - 1) / kGroup;
+  if (g >= ngroups)
+    return;
+  uint64_t P = 1, C = 0;
+  const uint32_t s0 = g * kGroup, s1 = min(nseg, s0 + kGroup);
+  for (uint32_t k = s0; k < s1; ++k) {
+    const uint64_t p2 = SP[k];
+    C = C * p2 + SC[k];
+    P = P * p2;
+  }
+  GP[g] = P;
+  GC[g] = C;
+}
+
+__global__ void fnv_fold_kernel(const uint64_t* __restrict__ GP, const uint64_t* __restrict__ GC,
+                                uint32_t ngroups, uint64_t seed,
+                                const uint8_t* __restrict__ last_low, uint64_t* out) {
   uint64_t u = seed >> 8;
-  for (uint32_t s = 0; s < nseg; ++s)
-    u = u * SP[s] + SC[s];
-  *out = (u << 8) | lin[nseg];
+  for (uint32_t g = 0; g < ngroups; ++g)
+    u = u * GP[g] + GC[g];
+  *out = (u << 8) | *last_low;
 }
 
 uint64_t pow_mod64(uint64_t b, uint64_t e) {
@@ -250,25 +298,33 @@ FnvPlan plan(uint64_t n, int sms) {
 
 size_t fnv_scratch_bytes(uint64_t n, int sms) {
   FnvPlan p = plan(n, sms);
+  const size_t ng = (p.nseg + kGroup - 1) / kGroup;
   size_t rec = (size_t)p.nseg * kSubSegs * kRecWords * sizeof(uint32_t);
   size_t L = (size_t)p.nseg * 256;
   size_t PC = (size_t)p.nseg * 2 * sizeof(uint64_t);
-  return PC + rec + L + p.nseg + 1 + 64;
+  size_t groups = ng * 2 * sizeof(uint64_t) + ng * 256 + ng + 1;
+  return PC + rec + L + p.nseg + 1 + groups + 256;
 }
 
 namespace {
 struct FnvScratch {
-  uint64_t *SP, *SC;
+  uint64_t *SP, *SC, *GP, *GC;
   uint32_t* rec;
-  uint8_t *L, *lin;
+  uint8_t *L, *lin, *GT, *gin;
+  uint32_t ngroups;
 };
 FnvScratch carve(const FnvPlan& p, void* scratch) {
   FnvScratch x;
+  x.ngroups = (p.nseg + kGroup - 1) / kGroup;
   x.SP = static_cast<uint64_t*>(scratch);
   x.SC = x.SP + p.nseg;
-  x.rec = reinterpret_cast<uint32_t*>(x.SC + p.nseg);
+  x.GP = x.SC + p.nseg;
+  x.GC = x.GP + x.ngroups;
+  x.rec = reinterpret_cast<uint32_t*>(x.GC + x.ngroups);
   x.L = reinterpret_cast<uint8_t*>(x.rec + (size_t)p.nseg * kSubSegs * kRecWords);
   x.lin = x.L + (size_t)p.nseg * 256;
+  x.GT = x.lin + p.nseg + 1;
+  x.gin = x.GT + (size_t)x.ngroups * 256;
   return x;
 }
 }  // namespace
@@ -298,15 +354,20 @@ int fnv_finish_launch(const uint32_t* cells, uint64_t n, uint64_t seed, uint64_t
   FnvPlan p = plan(n, sms);
   FnvScratch x = carve(p, scratch);
   int k = 0;
-  fnv_scan_kernel<<<1, 256, 0, st>>>(x.L, p.nseg, seed, x.lin);
-  ++k;
+  const uint32_t ng = x.ngroups;
   if (p.nseg) {
+    fnv_group_tables_kernel<<<ng, 32, 0, st>>>(x.L, p.nseg, x.GT);
+    fnv_group_walk_kernel<<<1, 1, 0, st>>>(x.GT, ng, seed, x.gin);
+    fnv_segment_walk_kernel<<<(ng + 255) / 256, 256, 0, st>>>(x.L, p.nseg, x.gin, x.lin);
     uint64_t threads = (uint64_t)p.nseg * kSubSegs;
     fnv_affine_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
         cells, n, p.seg_cells, p.sub_cells, p.nseg, x.rec, x.lin, x.SP, x.SC);
-    ++k;
+    fnv_group_affine_kernel<<<(ng + 255) / 256, 256, 0, st>>>(x.SP, x.SC, p.nseg, x.GP, x.GC);
+    k += 5;
+  } else {
+    cudaMemsetAsync(x.lin, (int)(seed & 255u), 1, st);  // no cells: low byte = seed's
   }
-  fnv_fold_kernel<<<1, 1, 0, st>>>(x.SP, x.SC, p.nseg, seed, x.lin, out);
+  fnv_fold_kernel<<<1, 1, 0, st>>>(x.GP, x.GC, ng, seed, x.lin + p.nseg, out);
   ++k;
   if (launches)
     *launches = k;
