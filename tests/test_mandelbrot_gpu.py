@@ -341,3 +341,46 @@ def test_concurrent_host_requests(ctx):
     for t in th:
         t.join()
     assert not errors
+
+
+def test_randomised_requests_fuzz(ctx):
+    """96 seeded random requests across every kernel variant: sizes from 1
+    pixel to 300x300 (and sub-tiles of larger images), max_iter from 0 to
+    3000 (checked kernel below 256 and near |c| = 2, deferred above, every
+    block length the picker can choose), fp32 / fp64, corner / centre
+    sampling, regions from the whole plane to deep zooms; several tiles per
+    request with gaps in the output. Every pixel against the oracle."""
+    rng = np.random.default_rng(int(os.environ.get("CAFXG_FUZZ_SEED", "2025")))
+    cases = int(os.environ.get("CAFXG_FUZZ_CASES", "96"))
+    pixels = 0
+    for case in range(cases):
+        fp64 = bool(rng.integers(0, 2))
+        centre = bool(rng.integers(0, 2))
+        it = int(rng.choice([0, 1, 2, 7, 63, 64, 100, 255, 256, 300, 500, 777, 1000, 1499,
+                             3000]))
+        span = float(10 ** rng.uniform(-7, 0.6))
+        x0 = float(rng.uniform(-2.3, 0.6))
+        y0 = float(rng.uniform(-1.3, 1.0))
+        W, H = int(rng.integers(1, 400)), int(rng.integers(1, 300))
+        x1, y1 = x0 + span, y0 + span * H / W
+        ntiles = int(rng.integers(1, 4))
+        tiles, refs, off = [], [], 0
+        for _ in range(ntiles):
+            r0 = int(rng.integers(0, H))
+            nr = int(rng.integers(1, H - r0 + 1))
+            c0 = int(rng.integers(0, W))
+            nc = int(rng.integers(1, W - c0 + 1))
+            off += int(rng.integers(0, 5))          # gap in the output
+            tiles.append(pkg.mandel_desc(x0, x1, y0, y1, W, H, it, fp64=fp64, centre=centre,
+                                         row0=r0, nrows=nr, col0=c0, ncols=nc,
+                                         out_offset=off))
+            refs.append((off, oracle.tile(x0, x1, y0, y1, W, H, it, fp64=fp64, centre=centre,
+                                          row0=r0, nrows=nr, col0=c0, ncols=nc)))
+            off += nr * nc
+        out = np.full(off, 0xDEADBEEF, dtype=np.uint32)
+        ctx.mandelbrot(tiles, out)
+        for (o, ref) in refs:
+            got = out[o:o + ref.size].reshape(ref.shape)
+            assert np.array_equal(got, ref), (case, x0, x1, y0, y1, W, H, it, fp64, centre)
+            pixels += ref.size
+    print(f"fuzz: {cases} requests, {pixels} pixels checked")
