@@ -1,6 +1,8 @@
 """GPU parity for the matrix_multiply kernels: sampled rows against the
 fp64-accumulated check, normwise max_j|dC| / max_j|R| <= 1e-5 (BASELINE.json
 config 2/5 tolerance)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -135,3 +137,29 @@ def test_sgemm_3xtf32_rejects_unsupported_shape(ctx):
     with pytest.raises(pkg.CafxgError) as e:
         ctx.sgemm(A, B, mode=pkg.SGEMM_3XTF32)
     assert e.value.code == 8
+
+
+def test_sgemm_randomised_shapes(ctx):
+    """Seeded random shapes, modes and leading dimensions: tcgen05-eligible
+    shapes (multiples of 128 / 256 / 32) and odd ones (FFMA), host arrays
+    with padded rows; every result within the fp32 tolerance."""
+    rng = np.random.default_rng(int(os.environ.get("CAFXG_FUZZ_SEED", "11")))
+    for case in range(int(os.environ.get("CAFXG_FUZZ_CASES", "40"))):
+        if rng.integers(0, 2):
+            M, N, K = (int(rng.integers(1, 9)) * 128, int(rng.integers(1, 5)) * 256,
+                       int(rng.integers(1, 33)) * 32)
+        else:
+            M, N, K = (int(rng.integers(1, 700)), int(rng.integers(1, 700)),
+                       int(rng.integers(1, 700)))
+        mode = int(rng.choice([pkg.SGEMM_AUTO, pkg.SGEMM_FFMA]))
+        pa, pb, pc = (int(rng.integers(0, 9)) for _ in range(3))
+        A = oracle.fill_uniform(M * (K + pa), 100 + case).reshape(M, K + pa)[:, :K]
+        B = oracle.fill_uniform(K * (N + pb), 200 + case).reshape(K, N + pb)[:, :N]
+        Cbig = np.full((M, N + pc), np.nan, dtype=np.float32)
+        C = Cbig[:, :N]
+        ctx.sgemm(A, B, C, mode=mode)
+        assert not np.isnan(C).any(), (case, M, N, K, mode)
+        assert check(np.ascontiguousarray(A), np.ascontiguousarray(B), C) <= TOL, \
+            (case, M, N, K, mode)
+        if pc:
+            assert np.isnan(Cbig[:, N:]).all()
