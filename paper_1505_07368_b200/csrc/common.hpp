@@ -57,7 +57,7 @@ struct CopySeg {
 int copy_segments_launch(const CopySeg* segs_dev, uint32_t n, void* stream);
 // Small batches pass their segment table by value in the kernel parameters
 // (no allocation, upload or free per batch).
-constexpr uint32_t kInlineSegs = 256;  // 6 KB of parameters
+constexpr uint32_t kInlineSegs = 32;  // 768 B of parameters (launch cost grows with them)
 int copy_segments_inline_launch(const CopySeg* segs_host, uint32_t n, void* stream);
 
 }  // namespace cafxg

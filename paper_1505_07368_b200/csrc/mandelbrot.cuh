@@ -7,7 +7,7 @@ namespace cafxg {
 
 // One tile of a batch, as the kernel sees it. Built on the host from
 // cafxg_mandel_desc (include/cafxg.h). Tiles are split into chunks of
-// kChunk pixels; chunks never straddle tiles, and chunk_begin is the global
+// chunk_px pixels; chunks never straddle tiles, and chunk_begin is the global
 // index of the tile's first chunk (ascending across the batch).
 struct MTile {
   double x0, xspan, y0, yspan;  // xspan = x1 - x0, yspan = y1 - y0 (fp64)
@@ -17,7 +17,7 @@ struct MTile {
   uint32_t nrows, ncols;
   uint32_t max_iter;
   uint32_t chunk_begin;
-  uint32_t chunks_per_row;      // ceil(ncols / kChunk); chunks never straddle rows
+  uint32_t chunks_per_row;      // ceil(ncols / chunk_px); chunks never straddle rows
   uint32_t out_off;             // tile's first count in MLaunch::out (row-major,
                                 // pitch ncols); launch total < 2^32 elements
   // Coordinate tables (filled by the prologue kernel): cx[ncols] real parts
@@ -28,10 +28,11 @@ struct MTile {
 };
 
 constexpr int kInlineTiles = 32;   // tiles passed by value in the params (< 4 KB)
-// Pixels per work chunk: one refill generation of a warp (32 lanes x 4
-// slots), so when the cursor runs dry no warp still holds unstarted pixels
-// (512-pixel chunks left ~0.2 ms tails per launch).
-constexpr uint32_t kChunk = 128;
+// Pixels per work chunk: one refill generation of a warp (32 lanes x 4 fp32
+// or 2 fp64 slots), so when the cursor runs dry no warp still holds unstarted
+// pixels (512-pixel chunks left ~0.2 ms tails per launch), and a small batch
+// spreads over as many warps as it has slot-fulls of pixels.
+constexpr uint32_t chunk_px(int precision) { return precision ? 64u : 128u; }
 constexpr int kMandelThreads = 256;
 
 struct MLaunch {

@@ -299,6 +299,7 @@ struct cafxg_ctx {
   // statistics
   std::atomic<uint64_t> st_requests{0}, st_batches{0}, st_launches{0},
       st_h2d{0}, st_d2h{0}, st_max_batch{0};
+  std::atomic<uint64_t> st_batch_ns{0};  // dispatcher time spent submitting batches
   // actor dispatcher
   std::atomic<Request*> inbox{nullptr};
   std::mutex disp_mu;
@@ -515,10 +516,11 @@ struct SubTile {
   uint64_t pixels;
 };
 
-// Work chunks of a tile: rows x ceil(ncols / kChunk) (chunks never straddle
-// rows, see mandel_kernel).
-static uint32_t tile_chunks(uint32_t nrows, uint32_t ncols) {
-  return nrows * ((ncols + kChunk - 1) / kChunk);
+// Work chunks of a tile: rows x ceil(ncols / chunk) (chunks never straddle
+// rows, see mandel_kernel); a chunk is one refill generation of a warp.
+static uint32_t tile_chunks(uint32_t nrows, uint32_t ncols, uint32_t precision) {
+  const uint32_t c = chunk_px((int)precision);
+  return nrows * ((ncols + c - 1) / c);
 }
 
 static void fill_mtile(MTile& m, const cafxg_mandel_desc& d, uint64_t out_off,
@@ -536,7 +538,7 @@ static void fill_mtile(MTile& m, const cafxg_mandel_desc& d, uint64_t out_off,
   m.ncols = d.ncols;
   m.max_iter = d.max_iter;
   m.chunk_begin = chunk_begin;
-  m.chunks_per_row = (d.ncols + kChunk - 1) / kChunk;
+  m.chunks_per_row = (d.ncols + chunk_px((int)d.precision) - 1) / chunk_px((int)d.precision);
   m.out_off = (uint32_t)out_off;
 }
 
@@ -709,7 +711,7 @@ static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
   uint64_t pixels = 0;
   for (auto& t : tiles) {
     t.chunk_begin = chunks;
-    chunks += tile_chunks(t.nrows, t.ncols);
+    chunks += tile_chunks(t.nrows, t.ncols, (uint32_t)precision);
     pixels += (uint64_t)t.nrows * t.ncols;
     max_extent = std::max(max_extent, t.ncols + t.nrows);
   }
@@ -870,7 +872,7 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
     uint64_t off = 0;
     for (size_t k = i; k < j; ++k) {
       fill_mtile(mt[k - i], subs[k].d, off, chunks);
-      chunks += tile_chunks(subs[k].d.nrows, subs[k].d.ncols);
+      chunks += tile_chunks(subs[k].d.nrows, subs[k].d.ncols, subs[k].d.precision);
       maxit = std::max(maxit, subs[k].d.max_iter);
       off += subs[k].pixels;
     }
@@ -1824,6 +1826,11 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     t_last_error = err;
   };
   const uint32_t slot = d->stage_next++ % kMaxInflight;
+  // consecutive batches alternate between the two compute streams: a small
+  // batch's kernel is latency-bound (fp64 storm tiles: ~16 us for 256
+  // dependent iterations on a fraction of the SMs), so batches in flight
+  // overlap instead of queueing behind each other
+  cudaStream_t ks = (slot & 1) ? d->compute2 : d->compute;
   if (!d->stage[0]) {
     // first batch on this device: the whole ring at the batch cap, so later
     // batches never allocate (one request above the cap still grows its slot)
@@ -1844,6 +1851,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
       // growth (warm-up): the old buffer may still feed an earlier batch
       if (d->stage[slot]) {
         cudaStreamSynchronize(d->compute);
+        cudaStreamSynchronize(d->compute2);
         cudaStreamSynchronize(d->d2h);
         cudaFree(d->stage[slot]);
         d->stage[slot] = nullptr;
@@ -1865,7 +1873,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     }
     // the copy-out of the batch that used this slot before must be done
     // reading it (recorded on the copy stream; a no-op the first time)
-    cudaStreamWaitEvent(d->compute, d->stage_ev[slot], 0);
+    cudaStreamWaitEvent(ks, d->stage_ev[slot], 0);
     dout = reinterpret_cast<uint32_t*>(d->stage[slot]);
   }
   std::vector<MTile> mt;
@@ -1881,7 +1889,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
       fill_mtile(m, t, off, chunks);
       mt.push_back(m);
       uint64_t tp = (uint64_t)t.nrows * t.ncols;
-      chunks += tile_chunks(t.nrows, t.ncols);
+      chunks += tile_chunks(t.nrows, t.ncols, t.precision);
       off += tp;
     }
     segs.push_back(CopySeg{dout + roff, r->out, (off - roff) * 4});
@@ -1893,17 +1901,17 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   if (trace_on()) {
     if (!d->trace_ref) {
       cudaEventCreate(&d->trace_ref);
-      cudaEventRecord(d->trace_ref, d->compute);
+      cudaEventRecord(d->trace_ref, ks);
       cudaEventSynchronize(d->trace_ref);
       d->trace_ref_ms = trace_now_ms();
     }
     for (auto& e : tev)
       cudaEventCreate(&e);
-    cudaEventRecord(tev[0], d->compute);
+    cudaEventRecord(tev[0], ks);
   }
-  status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, d->compute);
+  status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks);
   if (tev[0])
-    cudaEventRecord(tev[1], d->compute);
+    cudaEventRecord(tev[1], ks);
   const double t_launched = trace_now_ms();
   // the reply segment table goes up on the compute stream: an upload-ring
   // slot recorded on the copy stream would only free up behind every queued
@@ -1911,9 +1919,9 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   const bool inline_segs = segs.size() <= kInlineSegs;
   if (status == CAFXG_OK && px && all_pinned && !inline_segs) {
     size_t sb = segs.size() * sizeof(CopySeg);
-    status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, d->compute), "segs alloc");
+    status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, ks), "segs alloc");
     if (status == CAFXG_OK)
-      status = upload(d, dsegs, segs.data(), sb, d->compute);
+      status = upload(d, dsegs, segs.data(), sb, ks);
   }
   // the reply copy-out runs on the copy stream so it overlaps the next
   // batch's compute (a storm moves 16 KiB per request over PCIe; copying on
@@ -1921,7 +1929,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   // 144 -> 218 ms, because it serialises copy-out and the next kernel)
   cudaStream_t cs = d->d2h;
   if (status == CAFXG_OK && px)
-    status = stream_after_pooled(d, d->d2h, d->compute);
+    status = stream_after_pooled(d, d->d2h, ks);
   if (status == CAFXG_OK && px) {
     if (all_pinned) {
       {
@@ -2079,7 +2087,11 @@ static void dispatcher_loop(cafxg_ctx* ctx) {
       if (trace_on())
         fprintf(stderr, "cafxg dispatch %.3f ms: batch %zu, %zu queued behind, inflight %d\n",
                 trace_now_ms(), batch.size(), queue.size(), (int)d->inflight.load());
+      const auto b0 = std::chrono::steady_clock::now();
       run_mandel_batch(ctx, d, std::move(batch));
+      ctx->st_batch_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                              std::chrono::steady_clock::now() - b0)
+                              .count();
     }
   }
 }
@@ -2202,6 +2214,10 @@ int cafxg_sync(cafxg_ctx* ctx) {
 int cafxg_close(cafxg_ctx* ctx) try {
   if (!ctx)
     return CAFXG_OK;
+  if ((trace_on() || getenv("CAFXG_STATS")) && ctx->st_batches.load())
+    fprintf(stderr, "cafxg: %llu batches, dispatcher submit time %.3f ms (%.2f us/batch)\n",
+            (unsigned long long)ctx->st_batches.load(), ctx->st_batch_ns.load() / 1e6,
+            ctx->st_batch_ns.load() / 1e3 / ctx->st_batches.load());
   {
     std::lock_guard<std::mutex> lk(ctx->disp_mu);
     ctx->disp_stop = true;
@@ -2390,7 +2406,7 @@ int cafxg_mandelbrot_device(cafxg_ctx* ctx, int device, const cafxg_mandel_desc*
       MTile m;
       fill_mtile(m, tiles[i], tiles[i].out_offset - lo, chunks);
       mt.push_back(m);
-      chunks += tile_chunks(tiles[i].nrows, tiles[i].ncols);
+      chunks += tile_chunks(tiles[i].nrows, tiles[i].ncols, tiles[i].precision);
       maxit = std::max(maxit, tiles[i].max_iter);
       px += tp;
     }
@@ -2662,7 +2678,7 @@ int cafxg_run_mandelbrot(cafxg_ctx* ctx, uint32_t size, uint32_t max_iter, uint6
     CAFXG_TRY(validate_mandel(t));
     MTile m;
     fill_mtile(m, t, 0, 0);
-    CAFXG_TRY(launch_mandel(ctx, d, img[g], {m}, tile_chunks(t.nrows, t.ncols), CAFXG_FP64,
+    CAFXG_TRY(launch_mandel(ctx, d, img[g], {m}, tile_chunks(t.nrows, t.ncols, CAFXG_FP64), CAFXG_FP64,
                             max_iter, use_exact(ctx, t), n, d->compute));
     uint64_t seg_cells = 0;
     uint32_t nseg = 0;

@@ -32,6 +32,8 @@ WORK = {
     "deep_fp32_4096_it5000": [pkg.mandel_desc(-0.7487, -0.7485, 0.0650, 0.0652, 4096, 4096,
                                               5000)],
     "storm_fp64_4096x64sq_it256": storm(4096, 256),
+    "storm_fp64_16x64sq_it256": storm(16, 256),
+    "storm_fp64_64x64sq_it256": storm(64, 256),
     "cfg1_fp32_1920x1080_it100": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)],
 }
 
@@ -43,7 +45,7 @@ with pkg.Context(1) as ctx:
         npx = sum(t.nrows * t.ncols for t in tiles)
         out = torch.empty(npx, dtype=torch.int32, device="cuda")
         ts = []
-        for k in range(7):
+        for k in range(22):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             a.record(s)
