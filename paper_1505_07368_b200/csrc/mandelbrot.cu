@@ -468,7 +468,7 @@ struct Feeder {
         uint32_t cpr = T->chunks_per_row;
         uint32_t crow = local / cpr;
         uint32_t ncols = T->ncols;
-        constexpr uint32_t kChunk = 32u * NS;  // == chunk_px(precision)
+        constexpr uint32_t kChunk = kChunkPx;
         cur = (local - crow * cpr) * kChunk;
         cend = min(cur + kChunk, ncols);
         if constexpr (kInlineCoords) {
@@ -771,8 +771,6 @@ int occ_deferred_t() {
   return n;
 }
 
-static_assert(chunk_px(0) == 32u * F32Slots::kSlots && chunk_px(1) == 32u * F64Slots::kSlots,
-              "a work chunk is one refill generation of a warp");
 static_assert(deferred_smem_bytes<F32Slots>() <= 48 * 1024, "replay queues exceed 48 KB");
 static_assert(deferred_smem_bytes<F64Slots>() <= 48 * 1024, "replay queues exceed 48 KB");
 

@@ -28,11 +28,13 @@ struct MTile {
 };
 
 constexpr int kInlineTiles = 32;   // tiles passed by value in the params (< 4 KB)
-// Pixels per work chunk: one refill generation of a warp (32 lanes x 4 fp32
-// or 2 fp64 slots), so when the cursor runs dry no warp still holds unstarted
-// pixels (512-pixel chunks left ~0.2 ms tails per launch), and a small batch
-// spreads over as many warps as it has slot-fulls of pixels.
-constexpr uint32_t chunk_px(int precision) { return precision ? 64u : 128u; }
+// Pixels per work chunk: one refill generation of a warp in fp32 (32 lanes x
+// 4 slots), so when the cursor runs dry no warp still holds unstarted pixels
+// (512-pixel chunks left ~0.2 ms tails per launch). fp64 warps have 2 slots
+// per lane; 64-pixel chunks for them measured slower (fp64 reference mode
+// 21.65 -> 21.9 ms, more cursor traffic) and no faster for small batches.
+constexpr uint32_t kChunkPx = 128;
+constexpr uint32_t chunk_px(int /*precision*/) { return kChunkPx; }
 constexpr int kMandelThreads = 256;
 
 struct MLaunch {
