@@ -568,7 +568,8 @@ def run_secondary(ctx, args):
                      "reference on the 8-core build container"}
 
     out["cfg4_request_storm"] = run_storm(ctx)
-    out["cfg4_request_storm_closed_loop"] = run_storm(ctx, closed_loop=True)
+    out["cfg4_request_storm_closed_loop"] = run_storm(ctx, closed_loop="scheduled")
+    out["cfg4_request_storm_closed_loop_os_threads"] = run_storm(ctx, closed_loop=True)
     return out
 
 
@@ -577,7 +578,10 @@ def run_storm(ctx, clients=64, per=1600, seed=2024, closed_loop=False):
     actors, paper_1505_07368_b200/tools/storm_client.cpp) x 1600 requests, each
     a 64x64 fp64 tile (pitch 1/512, max_iter 256) at a seeded offset, replies in
     pinned buffers. Open loop = async sends with sender-directed replies;
-    closed loop = one outstanding request per client (sync_send)."""
+    closed loop = one outstanding request per client (sync_send); with
+    closed_loop="scheduled" the clients run as actors on hardware_concurrency
+    worker threads (the cafx scheduler model) instead of one blocked OS thread
+    each."""
     import ctypes as C
 
     import numpy as np
@@ -598,16 +602,17 @@ def run_storm(ctx, clients=64, per=1600, seed=2024, closed_loop=False):
     S.cafxg_storm_run.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint32,
                                   C.c_uint32, C.c_int, C.POINTER(C.c_double),
                                   C.POINTER(C.c_uint32)]
+    mode = 2 if closed_loop == "scheduled" else 1 if closed_loop else 0
     actor = ctx.spawn("mandelbrot")
     # warm-up: one full untimed storm of the same shape (staging ring, request
     # allocator arenas, pinned reply pages, first launches)
     wms, errs = C.c_double(), C.c_uint32()
     S.cafxg_storm_run(actor.handle, descs, replies.ctypes.data, 16384, clients, per,
-                      1 if closed_loop else 0, C.byref(wms), C.byref(errs))
+                      mode, C.byref(wms), C.byref(errs))
     replies[:] = 0
     st0 = ctx.stats()
     rc = S.cafxg_storm_run(actor.handle, descs, replies.ctypes.data, 16384, clients, per,
-                           1 if closed_loop else 0, C.byref(wms), C.byref(errs))
+                           mode, C.byref(wms), C.byref(errs))
     st1 = ctx.stats()
     dt = wms.value / 1e3
     iters = float(replies.sum(dtype=np.uint64))
@@ -619,8 +624,10 @@ def run_storm(ctx, clients=64, per=1600, seed=2024, closed_loop=False):
         bad += int(not np.array_equal(replies[int(k)].reshape(64, 64), ref))
     actor.release()
     ctx.pinned_free(replies)
-    return {"mode": "closed loop (1 outstanding/client)" if closed_loop else
-            "open loop (async sends)", "requests": total, "clients": clients,
+    names = ["open loop (async sends)", "closed loop (1 outstanding/client, one OS thread each)",
+             "closed loop (1 outstanding/client, clients as actors on %d worker threads)"
+             % (os.cpu_count() or 1)]
+    return {"mode": names[mode], "requests": total, "clients": clients,
             "status": rc, "wall_ms": round(wms.value, 2),
             "requests_per_s": round(total / dt, 1), "giter_s": round(iters / dt / 1e9, 2),
             "batches": int(st1.batches - st0.batches), "max_batch": int(st1.max_batch),

@@ -211,6 +211,7 @@ typedef struct {
   uint64_t kernel_launches;/* kernels launched by the backend */
   uint64_t h2d_bytes, d2h_bytes;
   uint64_t max_batch;      /* largest batch seen */
+  uint64_t direct_batches; /* batches whose escape kernel wrote the replies itself */
 } cafxg_stats;
 int cafxg_get_stats(cafxg_ctx* ctx, cafxg_stats* out);
 

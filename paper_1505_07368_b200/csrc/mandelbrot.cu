@@ -431,8 +431,9 @@ __global__ void __launch_bounds__(256)
 // coordinate is chunk state held in registers: the row's imaginary part, the
 // column table and the output row base. refill() hands the next pixels to
 // the lane slots that are free (bit s of `live` clear).
-template <class Slots, bool kInlineCoords>
+template <class Slots, int kMode>
 struct Feeder {
+  static constexpr bool kInlineCoords = kMode >= 1;
   using Cd = typename Slots::C;
   static constexpr int NS = Slots::kSlots;
   uint32_t cur = 0, cend = 0, orow = 0;
@@ -463,7 +464,8 @@ struct Feeder {
           exhausted = true;
           return;
         }
-        const MTile* T = tile_ptr(L, find_tile(L, c));
+        const uint32_t ti = find_tile(L, c);
+        const MTile* T = tile_ptr(L, ti);
         uint32_t local = c - T->chunk_begin;
         uint32_t cpr = T->chunks_per_row;
         uint32_t crow = local / cpr;
@@ -479,6 +481,8 @@ struct Feeder {
           ci_row = __ldg(static_cast<const Cd*>(T->cy) + crow);
         }
         orow = T->out_off + crow * ncols;
+        if constexpr (kMode == 2)
+          orow |= ti << kDirectShift;
         continue;
       }
       const uint32_t avail = cend - cur;
@@ -506,6 +510,70 @@ struct Feeder {
   }
 };
 
+// ---- direct reply -------------------------------------------------------------
+// Small batches (MLaunch::direct) skip the separate reply-scatter launch. Each
+// warp counts the pixels it finishes per tile in shared memory (no fences on
+// the per-round path); when the warp exits, it publishes its counts with one
+// fence and one global atomic per tile it touched, and the warp whose count
+// completes a tile copies the tile from the staging buffer (L2-resident, just
+// written) to its pinned host reply, 8 x 16-byte loads in flight per lane.
+// Ordering: stores -> __threadfence -> count (release); count ->
+// __threadfence -> __ldcg of the tile (acquire).
+__device__ __forceinline__ uint32_t* direct_counts() {
+  __shared__ uint32_t cnt[kMandelThreads / 32][kInlineTiles];
+  return cnt[threadIdx.x >> 5];
+}
+
+__device__ __forceinline__ void direct_begin() {
+  direct_counts()[threadIdx.x & 31u] = 0;  // kInlineTiles == 32
+  __syncwarp();
+}
+
+__device__ __forceinline__ void direct_count(uint32_t o, bool fin) {
+  if (fin)
+    atomicAdd(&direct_counts()[o >> kDirectShift], 1u);
+}
+
+__device__ __forceinline__ void direct_finish(const MLaunch& L) {
+  const uint32_t lane = threadIdx.x & 31u;
+  __syncwarp();
+  const uint32_t mine = direct_counts()[lane];
+  __threadfence();
+  bool complete = false;
+  if (mine) {
+    const MTile& T = L.inl[lane];
+    complete = atomicAdd(&L.tile_done[lane], mine) + mine == T.nrows * T.ncols;
+  }
+  uint32_t fins = __ballot_sync(kFull, complete);
+  if (fins)
+    __threadfence();
+  while (fins) {
+    const uint32_t t = (uint32_t)(__ffs(fins) - 1);
+    fins &= fins - 1;
+    const MTile& T = L.inl[t];
+    const uint32_t nv = T.nrows * T.ncols / 4;
+    const uint4* from = reinterpret_cast<const uint4*>(L.out + T.out_off);
+    uint4* to = reinterpret_cast<uint4*>(T.reply);
+    for (uint32_t i0 = 0; i0 < nv; i0 += 32 * 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t i = i0 + k * 32 + lane;
+        if (i < nv)
+          v[k] = __ldcg(from + i);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t i = i0 + k * 32 + lane;
+        if (i < nv)
+          to[i] = v[k];
+      }
+    }
+    if (lane == t)
+      L.tile_done[t] = 0;  // ready for the next launch on this staging slot
+  }
+}
+
 // Self-resetting scheduler: the last block to finish zeroes the cursor so
 // the slot can serve the next launch without a memset.
 __device__ __forceinline__ void retire_block(const MLaunch& L) {
@@ -526,17 +594,21 @@ __device__ __forceinline__ void retire_block(const MLaunch& L) {
 // with two independent FP2 chains in fp32; fp64 is bound by the FP64 pipe.
 // Used where the deferred kernel's precondition does not hold (tiles that
 // reach |c| ~ 2) and for small max_iter.
-// kInlineCoords: coordinates computed at pixel start (batches of small tiles)
-// instead of loaded from the tables of coords_kernel (big tiles).
-template <class Slots, int kSteps, bool kExact, bool kInlineCoords>
-__global__ void __launch_bounds__(kMandelThreads, 4)
+// kMode 0: coordinates loaded from the tables of coords_kernel (big tiles);
+// 1: computed at pixel start (batches of small tiles); 2: as 1, plus the
+// direct reply (MLaunch::direct; 2 CTAs per SM so the copy path has
+// registers).
+template <class Slots, int kSteps, bool kExact, int kMode>
+__global__ void __launch_bounds__(kMandelThreads, kMode == 2 ? 2 : 4)
     mandel_kernel(const __grid_constant__ MLaunch L) {
+  constexpr bool kDirect = kMode == 2;
   constexpr int NS = Slots::kSlots;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t maxit = L.max_iter;  // uniform per launch
+  constexpr uint32_t omask = kDirect ? (1u << kDirectShift) - 1u : 0xffffffffu;
 
-  Feeder<Slots, kInlineCoords> feed;
+  Feeder<Slots, kMode> feed;
   Slots sl;
   sl.zero = L.zero;
   uint32_t n[NS];   // iterations completed without escape; bit 31 = escaped
@@ -548,6 +620,8 @@ __global__ void __launch_bounds__(kMandelThreads, 4)
     o[s] = 0;
   }
 
+  if constexpr (kDirect)
+    direct_begin();
   feed.refill(L, sl, n, o, live, lt_mask);
   while (__any_sync(kFull, live != 0)) {
     sl.template run<kSteps, kExact>(n);
@@ -562,13 +636,20 @@ __global__ void __launch_bounds__(kMandelThreads, 4)
       for (int s = 0; s < NS; ++s) {
         if (done >> s & 1u) {
           uint32_t c = (int32_t)n[s] < 0 ? (n[s] & 0x7fffffffu) + 1u : n[s];
-          L.out[o[s]] = min(c, maxit);
+          L.out[o[s] & omask] = min(c, maxit);
         }
+      }
+      if constexpr (kDirect) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          direct_count(o[s], done >> s & 1u);
       }
       live &= ~done;
       feed.refill(L, sl, n, o, live, lt_mask);
     }
   }
+  if constexpr (kDirect)
+    direct_finish(L);
   retire_block(L);
 }
 
@@ -610,7 +691,7 @@ constexpr size_t deferred_smem_bytes() {
   return sizeof(ReplayQueue<Slots>) * (kMandelThreads / 32);
 }
 
-template <class Slots, int kUnit, bool kExact>
+template <class Slots, int kUnit, bool kExact, bool kDirect>
 __device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
                                        uint32_t first, uint32_t count, uint32_t maxit) {
   constexpr int NS = Slots::kSlots;
@@ -636,18 +717,25 @@ __device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
 #pragma unroll 1
   for (uint32_t r = 0; r < L.block_reps; ++r)
     rp.template run<kUnit, kExact>(rn);
+  constexpr uint32_t omask = kDirect ? (1u << kDirectShift) - 1u : 0xffffffffu;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     if (ro[s] != 0xffffffffu) {
       uint32_t c = (int32_t)rn[s] < 0 ? (rn[s] & 0x7fffffffu) + 1u : rn[s];
-      L.out[ro[s]] = min(c, maxit);
+      L.out[ro[s] & omask] = min(c, maxit);
     }
+  }
+  if constexpr (kDirect) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      direct_count(ro[s], ro[s] != 0xffffffffu);
   }
 }
 
-template <class Slots, int kUnit, bool kExact, bool kInlineCoords>
+template <class Slots, int kUnit, bool kExact, int kMode>
 __global__ void __launch_bounds__(kMandelThreads, 2)
     mandel_deferred_kernel(const __grid_constant__ MLaunch L) {
+  constexpr bool kDirect = kMode == 2;
   constexpr int NS = Slots::kSlots;
   constexpr uint32_t kBatch = 32 * NS;
   using Cd = typename Slots::C;
@@ -661,8 +749,9 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
   const uint32_t reps = L.block_reps;
   const uint32_t block = kUnit * reps;
   uint32_t* const out = L.out;
+  constexpr uint32_t omask = kDirect ? (1u << kDirectShift) - 1u : 0xffffffffu;
 
-  Feeder<Slots, kInlineCoords> feed;
+  Feeder<Slots, kMode> feed;
   Slots sl;
   sl.zero = L.zero;
   uint32_t n[NS];  // steps completed (a multiple of the block), all unescaped
@@ -675,6 +764,8 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
     o[s] = 0;
   }
 
+  if constexpr (kDirect)
+    direct_begin();
   feed.refill(L, sl, n, o, live, lt_mask);
   while (__any_sync(kFull, live != 0)) {
     Cd szr[NS], szi[NS];
@@ -697,7 +788,7 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
       n[s] += act ? block : 0u;
       const bool hit = act && n[s] >= maxit;
       if (hit)
-        out[o[s]] = maxit;
+        out[o[s] & omask] = maxit;
       done |= (uint32_t)hit << s;
     }
     if (__any_sync(kFull, esc != 0)) {
@@ -719,45 +810,64 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
       queued = base;
     }
     if (__any_sync(kFull, done != 0)) {
+      if constexpr (kDirect) {  // block-end finishes (escapes finish in replay)
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          direct_count(o[s], (done & ~esc) >> s & 1u);
+      }
       live &= ~done;
       feed.refill(L, sl, n, o, live, lt_mask);
     }
     if (queued >= kBatch) {
       __syncwarp();
       queued -= kBatch;
-      replay<Slots, kUnit, kExact>(L, q, queued, kBatch, maxit);
+      replay<Slots, kUnit, kExact, kDirect>(L, q, queued, kBatch, maxit);
     }
   }
   if (queued) {
     __syncwarp();
-    replay<Slots, kUnit, kExact>(L, q, 0, queued, maxit);
+    replay<Slots, kUnit, kExact, kDirect>(L, q, 0, queued, maxit);
   }
+  if constexpr (kDirect)
+    direct_finish(L);
   retire_block(L);
 }
 
 template <class A, int kSteps, bool kExact>
 int launch_t(const MLaunch& L, int grid, cudaStream_t s) {
-  if (L.inline_coords)
-    mandel_kernel<A, kSteps, kExact, true><<<grid, kMandelThreads, 0, s>>>(L);
+  if (L.direct)
+    mandel_kernel<A, kSteps, kExact, 2><<<grid, kMandelThreads, 0, s>>>(L);
+  else if (L.inline_coords)
+    mandel_kernel<A, kSteps, kExact, 1><<<grid, kMandelThreads, 0, s>>>(L);
   else
-    mandel_kernel<A, kSteps, kExact, false><<<grid, kMandelThreads, 0, s>>>(L);
+    mandel_kernel<A, kSteps, kExact, 0><<<grid, kMandelThreads, 0, s>>>(L);
   return (int)cudaGetLastError();
 }
 
 template <class A, int kUnit, bool kExact>
 int launch_deferred_t(const MLaunch& L, int grid, cudaStream_t s) {
   constexpr size_t smem = deferred_smem_bytes<A>();
-  if (L.inline_coords)
-    mandel_deferred_kernel<A, kUnit, kExact, true><<<grid, kMandelThreads, smem, s>>>(L);
+  if (L.direct) {
+    // the direct-reply counters (static shared memory) push the fp32 kernel
+    // past the 48 KB that needs no opt-in
+    static const cudaError_t opt = cudaFuncSetAttribute(
+        mandel_deferred_kernel<A, kUnit, kExact, 2>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (opt != cudaSuccess)
+      return (int)opt;
+    mandel_deferred_kernel<A, kUnit, kExact, 2><<<grid, kMandelThreads, smem, s>>>(L);
+  }
+  else if (L.inline_coords)
+    mandel_deferred_kernel<A, kUnit, kExact, 1><<<grid, kMandelThreads, smem, s>>>(L);
   else
-    mandel_deferred_kernel<A, kUnit, kExact, false><<<grid, kMandelThreads, smem, s>>>(L);
+    mandel_deferred_kernel<A, kUnit, kExact, 0><<<grid, kMandelThreads, smem, s>>>(L);
   return (int)cudaGetLastError();
 }
 
 template <class A, int kSteps, bool kExact>
 int occ_t() {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mandel_kernel<A, kSteps, kExact, false>,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mandel_kernel<A, kSteps, kExact, 0>,
                                                 kMandelThreads, 0);
   return n;
 }
@@ -766,7 +876,7 @@ template <class A, int kUnit, bool kExact>
 int occ_deferred_t() {
   int n = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &n, mandel_deferred_kernel<A, kUnit, kExact, false>, kMandelThreads,
+      &n, mandel_deferred_kernel<A, kUnit, kExact, 0>, kMandelThreads,
       deferred_smem_bytes<A>());
   return n;
 }

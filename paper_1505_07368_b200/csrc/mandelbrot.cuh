@@ -25,6 +25,10 @@ struct MTile {
   // the request precision (float or double).
   void* cx;
   void* cy;
+  // Direct reply (MLaunch::direct): the tile's reply buffer, device-mapped
+  // pinned host memory, 16-byte aligned; the kernel copies the finished tile
+  // there itself.
+  uint32_t* reply;
 };
 
 constexpr int kInlineTiles = 32;   // tiles passed by value in the params (< 4 KB)
@@ -48,7 +52,15 @@ struct MLaunch {
   float zero;           // always 0.0f; opaque to ptxas (see the escape block)
   uint32_t inline_coords;  // 1: tiles carry no coordinate tables (cx == cy == null)
   uint32_t block_reps;  // deferred kernel: unrolled units per unchecked block
+  // Direct reply: n <= kInlineTiles tiles, each a multiple of 4 pixels at a
+  // 4-pixel-aligned out_off, batch < 2^kDirectShift pixels. Output offsets then
+  // carry the tile index in their top bits; tile_done[t] counts the tile's
+  // finished pixels (zero at launch, reset by the warp that copies the tile).
+  uint32_t direct;
+  uint32_t* tile_done;
 };
+static_assert(sizeof(MLaunch) <= 4096, "MLaunch is passed by value");
+constexpr int kDirectShift = 26;
 
 // Host launchers (mandelbrot.cu). precision: 0 = fp32, 1 = fp64.
 // `exact` selects the 8-op escape step; the default 7-op step folds

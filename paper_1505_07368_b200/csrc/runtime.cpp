@@ -225,6 +225,12 @@ constexpr uint32_t kSchedSlots = 1024;
 // kernel of the next and the pipeline drains quickly after the last request.
 constexpr int kMaxInflight = 8;
 constexpr int kSoftInflight = 4;
+// Staging slot tail: the direct-reply tile counters (kInlineTiles u32).
+constexpr size_t kStageTail = 256;
+// Direct reply: per-tile limit (one warp copies the finished tile: 16 KiB
+// storm tiles take 32 rounds of 16-byte stores; a 1M-pixel band would stall
+// its warp for milliseconds).
+constexpr uint64_t kDirectTilePx = 64u << 10;
 constexpr uint64_t kInlineCopyPx = 256u << 10;  // copy-out on the compute stream below  // beyond this only when a full batch is queued
 constexpr uint64_t kMaxBatchPx = 16ull << 20;
 constexpr int kUpSlots = 16;
@@ -264,6 +270,7 @@ struct Device {
   uint8_t* stage[kMaxInflight] = {};
   size_t stage_cap[kMaxInflight] = {};
   cudaEvent_t stage_ev[kMaxInflight] = {};
+  bool stage_on_copy[kMaxInflight] = {};  // last user recorded stage_ev on d2h
   uint32_t stage_next = 0;
   // reusable events for host request pipelines (caller holds submit_mu): an
   // event may be re-recorded as soon as the waits on its last record are
@@ -300,6 +307,8 @@ struct cafxg_ctx {
   std::atomic<uint64_t> st_requests{0}, st_batches{0}, st_launches{0},
       st_h2d{0}, st_d2h{0}, st_max_batch{0};
   std::atomic<uint64_t> st_batch_ns{0};  // dispatcher time spent submitting batches
+  std::atomic<uint64_t> st_direct{0};    // batches replied by the escape kernel itself
+  std::atomic<uint64_t> st_phase_ns[6] = {};  // run_mandel_batch phases (CAFXG_STATS)
   // actor dispatcher
   std::atomic<Request*> inbox{nullptr};
   std::mutex disp_mu;
@@ -540,6 +549,8 @@ static void fill_mtile(MTile& m, const cafxg_mandel_desc& d, uint64_t out_off,
   m.chunk_begin = chunk_begin;
   m.chunks_per_row = (d.ncols + chunk_px((int)d.precision) - 1) / chunk_px((int)d.precision);
   m.out_off = (uint32_t)out_off;
+  m.cx = m.cy = nullptr;
+  m.reply = nullptr;
 }
 
 // Precondition of the deferred escape test (mandel_deferred_kernel): the
@@ -562,6 +573,15 @@ static bool deferred_safe(const MTile& t) {
                                  std::max(std::fabs(ya), std::fabs(yb)));
   const double eta = std::ldexp(1.0, -10), pad = 1e-6;  // pad: fp32 rounding of c
   return rmax < 2.0 - eta - pad || rmin > 2.0 + eta + pad;
+}
+
+// CAFXG_DIRECT_REPLY=0 keeps every batch on the reply-scatter launch
+static bool direct_reply_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CAFXG_DIRECT_REPLY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // CAFXG_DEFERRED=0 forces the per-step-checked kernel everywhere
@@ -651,12 +671,14 @@ static MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
 // inline capacity are uploaded first.
 static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                                std::vector<MTile>& tiles, int precision, bool exact,
-                               cudaStream_t stream, bool coords_only, bool skip_coords);
+                               cudaStream_t stream, bool coords_only, bool skip_coords,
+                               uint32_t* direct_counters = nullptr);
 
 static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                          const std::vector<MTile>& tiles_in, uint32_t total_chunks,
                          int precision, uint32_t max_iter, bool exact,
-                         uint64_t pixels, cudaStream_t stream) {
+                         uint64_t pixels, cudaStream_t stream,
+                         uint32_t* direct_counters = nullptr) {
   (void)max_iter;
   (void)pixels;
   if (total_chunks == 0)
@@ -697,7 +719,10 @@ static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
     for (auto& t : tiles)
       if (t.max_iter == it)
         grp.push_back(t);
-    CAFXG_TRY(launch_mandel_group(ctx, d, out_base, grp, precision, exact, stream, false, true));
+    if (direct_counters && its.size() != 1)
+      return fail(CAFXG_E_CONFIG, "internal: direct reply across max_iter groups");
+    CAFXG_TRY(launch_mandel_group(ctx, d, out_base, grp, precision, exact, stream, false, true,
+                                  direct_counters));
   }
   if (coords)
     CAFXG_CUDA_TRY(cudaFreeAsync(coords, stream));
@@ -706,7 +731,8 @@ static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
 
 static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                                std::vector<MTile>& tiles, int precision, bool exact,
-                               cudaStream_t stream, bool coords_only, bool skip_coords) {
+                               cudaStream_t stream, bool coords_only, bool skip_coords,
+                               uint32_t* direct_counters) {
   uint32_t chunks = 0, max_extent = 0;
   uint64_t pixels = 0;
   for (auto& t : tiles) {
@@ -725,6 +751,13 @@ static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
   L.sched = d->next_sched();
   L.zero = 0.0f;
   L.inline_coords = tiles[0].cx == nullptr;
+  if (direct_counters) {
+    // run_mandel_batch checked the same conditions and skips the reply copy
+    if (tiles.size() > (size_t)kInlineTiles || !L.inline_coords)
+      return fail(CAFXG_E_CONFIG, "internal: direct reply on an ineligible batch");
+    L.direct = 1;
+    L.tile_done = direct_counters;
+  }
   MTile* dev_tiles = nullptr;
   if (tiles.size() <= (size_t)kInlineTiles) {
     for (size_t i = 0; i < tiles.size(); ++i)
@@ -747,7 +780,11 @@ static int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
     for (auto& t : tiles)
       safe = safe && deferred_safe(t);
     MandelLaunchCfg cfg = mandel_cfg(d, precision, L.max_iter, exact, safe, pixels);
+    const auto l0 = std::chrono::steady_clock::now();
     int e = mandel_launch(L, precision, cfg, stream);
+    ctx->st_phase_ns[5] += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                               std::chrono::steady_clock::now() - l0)
+                               .count();
     if (e != 0)
       return cuda_status((cudaError_t)e, "mandelbrot launch");
     ctx->st_launches++;
@@ -1797,8 +1834,20 @@ static void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* 
   ctx->cb_cv.notify_all();
 }
 
+static inline uint64_t now_ns() {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
 static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> batch) {
   const double t_begin = trace_now_ms();
+  uint64_t ph = now_ns();
+  auto phase = [&](int i) {
+    const uint64_t t = now_ns();
+    ctx->st_phase_ns[i] += t - ph;
+    ph = t;
+  };
   cudaSetDevice(d->ordinal);
   std::lock_guard<std::mutex> g(d->submit_mu);
   const double t_lock = trace_now_ms();
@@ -1831,12 +1880,27 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   // dependent iterations on a fraction of the SMs), so batches in flight
   // overlap instead of queueing behind each other
   cudaStream_t ks = (slot & 1) ? d->compute2 : d->compute;
+  // Direct reply (mandel_kernel / mandel_deferred_kernel copy each finished
+  // tile to its pinned reply themselves): small batches whose replies are all
+  // device-mapped pinned memory. Saves the reply-scatter launch and the
+  // copy-stream ordering on the dispatcher, and the launch gap on the device.
+  bool direct = all_pinned && direct_reply_enabled() && ntiles <= (size_t)kInlineTiles &&
+                px < (1ull << kDirectShift);
+  for (Request* r : batch) {
+    direct = direct && r->max_iter == maxit && (reinterpret_cast<uintptr_t>(r->out) & 15) == 0;
+    for (uint32_t k = 0; direct && k < r->ntiles; ++k) {
+      const cafxg_mandel_desc& t = r->tile(k);
+      const uint64_t tp = (uint64_t)t.nrows * t.ncols;
+      direct = tp % 4 == 0 && tp <= kDirectTilePx;
+    }
+  }
   if (!d->stage[0]) {
     // first batch on this device: the whole ring at the batch cap, so later
     // batches never allocate (one request above the cap still grows its slot)
     for (int i = 0; i < kMaxInflight; ++i) {
-      const size_t cap = kMaxBatchPx * 4 + 16;
-      if (cudaMalloc((void**)&d->stage[i], cap) == cudaSuccess) {
+      const size_t cap = kMaxBatchPx * 4 + kStageTail;
+      if (cudaMalloc((void**)&d->stage[i], cap) == cudaSuccess &&
+          cudaMemset(d->stage[i] + cap - kStageTail, 0, kStageTail) == cudaSuccess) {
         d->stage_cap[i] = cap;
       } else {
         cudaGetLastError();
@@ -1846,7 +1910,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     }
   }
   {
-    const size_t need = px * 4 + 16;
+    const size_t need = px * 4 + kStageTail;
     if (d->stage_cap[slot] < need) {
       // growth (warm-up): the old buffer may still feed an earlier batch
       if (d->stage[slot]) {
@@ -1857,8 +1921,9 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
         d->stage[slot] = nullptr;
         d->stage_cap[slot] = 0;
       }
-      size_t cap = std::max<size_t>(need, kMaxBatchPx * 4 + 16);
-      if (cudaMalloc((void**)&d->stage[slot], cap) != cudaSuccess) {
+      size_t cap = std::max<size_t>(need, kMaxBatchPx * 4 + kStageTail);
+      if (cudaMalloc((void**)&d->stage[slot], cap) != cudaSuccess ||
+          cudaMemset(d->stage[slot] + cap - kStageTail, 0, kStageTail) != cudaSuccess) {
         d->stage[slot] = nullptr;
         fail_all(cuda_status(cudaGetLastError(), "batch staging allocation"));
         return;
@@ -1872,8 +1937,12 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
       return;
     }
     // the copy-out of the batch that used this slot before must be done
-    // reading it (recorded on the copy stream; a no-op the first time)
-    cudaStreamWaitEvent(ks, d->stage_ev[slot], 0);
+    // reading it (recorded on the copy stream). A slot always runs on the
+    // same compute stream (kMaxInflight is even), so after a direct-reply
+    // batch the order is implied.
+    if (d->stage_on_copy[slot])
+      cudaStreamWaitEvent(ks, d->stage_ev[slot], 0);
+    d->stage_on_copy[slot] = !direct;
     dout = reinterpret_cast<uint32_t*>(d->stage[slot]);
   }
   std::vector<MTile> mt;
@@ -1887,6 +1956,8 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
       const cafxg_mandel_desc& t = r->tile(k);
       MTile m;
       fill_mtile(m, t, off, chunks);
+      if (direct)
+        m.reply = static_cast<uint32_t*>(r->out) + (off - roff);
       mt.push_back(m);
       uint64_t tp = (uint64_t)t.nrows * t.ncols;
       chunks += tile_chunks(t.nrows, t.ncols, t.precision);
@@ -1895,6 +1966,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     segs.push_back(CopySeg{dout + roff, r->out, (off - roff) * 4});
   }
   const double t_built = trace_now_ms();
+  phase(0);
   // CAFXG_TRACE: device-side timestamps of this batch (kernel start/end,
   // copy-out end), reported against a per-device reference event
   cudaEvent_t tev[3] = {};
@@ -1909,7 +1981,13 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
       cudaEventCreate(&e);
     cudaEventRecord(tev[0], ks);
   }
-  status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks);
+  uint32_t* counters =
+      direct ? reinterpret_cast<uint32_t*>(d->stage[slot] + d->stage_cap[slot] - kStageTail)
+             : nullptr;
+  status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks, counters);
+  if (direct)
+    ctx->st_direct++;
+  phase(1);
   if (tev[0])
     cudaEventRecord(tev[1], ks);
   const double t_launched = trace_now_ms();
@@ -1917,7 +1995,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   // slot recorded on the copy stream would only free up behind every queued
   // copy-out, and reusing it would block the dispatcher
   const bool inline_segs = segs.size() <= kInlineSegs;
-  if (status == CAFXG_OK && px && all_pinned && !inline_segs) {
+  if (status == CAFXG_OK && px && all_pinned && !inline_segs && !direct) {
     size_t sb = segs.size() * sizeof(CopySeg);
     status = cuda_status(cudaMallocAsync((void**)&dsegs, sb, ks), "segs alloc");
     if (status == CAFXG_OK)
@@ -1927,10 +2005,11 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
   // batch's compute (a storm moves 16 KiB per request over PCIe; copying on
   // the compute stream instead was slower even for closed-loop trickles,
   // 144 -> 218 ms, because it serialises copy-out and the next kernel)
-  cudaStream_t cs = d->d2h;
-  if (status == CAFXG_OK && px)
+  cudaStream_t cs = direct ? ks : d->d2h;
+  if (status == CAFXG_OK && px && !direct)
     status = stream_after_pooled(d, d->d2h, ks);
-  if (status == CAFXG_OK && px) {
+  phase(2);
+  if (status == CAFXG_OK && px && !direct) {
     if (all_pinned) {
       {
         int e = inline_segs ? copy_segments_inline_launch(segs.data(), (uint32_t)segs.size(), cs)
@@ -1948,9 +2027,11 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
     }
     ctx->st_d2h += px * 4;
   }
+  phase(3);
   if (dsegs)
     cudaFreeAsync(dsegs, cs);
-  cudaEventRecord(d->stage_ev[slot], cs);  // slot free once the copy-out is done
+  if (!direct)
+    cudaEventRecord(d->stage_ev[slot], cs);  // slot free once the copy-out is done
   if (tev[0])
     cudaEventRecord(tev[2], cs);
   ctx->st_batches++;
@@ -1988,6 +2069,7 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
                               d->trace_ref_ms + g[2]);
                     }
                   });
+  phase(4);
 }
 
 static Device* pick_device(cafxg_ctx* ctx) {
@@ -2010,9 +2092,14 @@ static void dispatcher_loop(cafxg_ctx* ctx) {
   // A trickle of requests (closed-loop clients) coalesces while kSoftInflight
   // batches run; a backlog of at least one full batch (open-loop bursts) may
   // fill the pipeline up to kMaxInflight.
+  static const int soft = [] {  // CAFXG_SOFT_INFLIGHT: experiments only
+    const char* e = getenv("CAFXG_SOFT_INFLIGHT");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 && v <= kMaxInflight ? v : kSoftInflight;
+  }();
   auto may_dispatch = [&](const Device* d) {
     const int n = d->inflight.load();
-    return n < kSoftInflight || (n < kMaxInflight && queued_px >= kMaxBatchPx);
+    return n < soft || (n < kMaxInflight && queued_px >= kMaxBatchPx);
   };
   while (true) {
     {
@@ -2218,6 +2305,16 @@ int cafxg_close(cafxg_ctx* ctx) try {
     fprintf(stderr, "cafxg: %llu batches, dispatcher submit time %.3f ms (%.2f us/batch)\n",
             (unsigned long long)ctx->st_batches.load(), ctx->st_batch_ns.load() / 1e6,
             ctx->st_batch_ns.load() / 1e3 / ctx->st_batches.load());
+  if ((trace_on() || getenv("CAFXG_STATS")) && ctx->st_batches.load())
+    fprintf(stderr, "cafxg:   %llu batches replied by the escape kernel (direct)\n",
+            (unsigned long long)ctx->st_direct.load());
+  if ((trace_on() || getenv("CAFXG_STATS")) && ctx->st_batches.load()) {
+    const char* nm[6] = {"build", "kernel launch", "copy-stream order", "reply launch",
+                         "record+completion", "(of which the escape-kernel launch call)"};
+    for (int i = 0; i < 6; ++i)
+      fprintf(stderr, "cafxg:   %s %.2f us/batch\n", nm[i],
+              ctx->st_phase_ns[i].load() / 1e3 / ctx->st_batches.load());
+  }
   {
     std::lock_guard<std::mutex> lk(ctx->disp_mu);
     ctx->disp_stop = true;
@@ -2730,6 +2827,7 @@ int cafxg_get_stats(cafxg_ctx* ctx, cafxg_stats* out) {
   out->h2d_bytes = ctx->st_h2d.load();
   out->d2h_bytes = ctx->st_d2h.load();
   out->max_batch = ctx->st_max_batch.load();
+  out->direct_batches = ctx->st_direct.load();
   return CAFXG_OK;
 }
 

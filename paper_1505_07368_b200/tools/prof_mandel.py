@@ -1,6 +1,6 @@
 """Small driver for ncu captures of the escape kernel: one warm-up and one
 profiled launch of a BASELINE config through cafxg_mandelbrot_device.
-    python paper_1505_07368_b200/tools/prof_mandel.py cfg3|cfg1|storm64|ref4096
+    python paper_1505_07368_b200/tools/prof_mandel.py cfg3|cfg1|storm64|storm16|ref4096
 """
 import os
 import sys
@@ -17,9 +17,9 @@ elif which == "cfg1":
     tiles = [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)]
 elif which == "ref4096":
     tiles = [pkg.reference_desc(4096, 500)]
-else:  # 64 storm tiles in one launch
+else:  # storm64 / storm16: that many storm tiles in one launch
     tiles = []
-    for k in range(64):
+    for k in range(int(which[5:] or 64)):
         x0, y0 = -2.0 + (k * 23 % 1472) / 512, -1.0 + (k * 37 % 960) / 512
         tiles.append(pkg.mandel_desc(x0, x0 + 0.125, y0, y0 + 0.125, 64, 64, 256, fp64=True,
                                      out_offset=k * 4096))

@@ -130,6 +130,79 @@ def test_staging_ring_reuse_and_oversized_request(ctx):
     a.release()
 
 
+def _tile_ref(d):
+    return oracle.tile(d.x0, d.x1, d.y0, d.y1, d.ncols, d.nrows, d.max_iter,
+                       fp64=bool(d.precision), centre=bool(d.sampling))
+
+
+def test_direct_reply_small_batches(ctx):
+    """Small batches into pinned replies skip the reply-scatter launch: the
+    escape kernel counts finished pixels per tile and the warp completing a
+    tile copies it to the reply (checked kernel, deferred kernel and its
+    replays; fp32 and fp64; multi-tile requests). Tiles whose pixel count is
+    not a multiple of 4 keep the scatter launch. Every reply exact."""
+    a = ctx.spawn("mandelbrot")
+    rng = np.random.default_rng(5)
+    cases = [
+        [storm_tile(rng)],                                                  # fp64, checked
+        [pkg.mandel_desc(-0.30, -0.20, 0.60, 0.70, 64, 48, 300, fp64=True)],  # fp64 deferred
+        [pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 96, 80, 1000)],          # fp32 deferred
+        [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 128, 64, 100)],              # fp32 checked
+        [storm_tile(rng), storm_tile(rng), storm_tile(rng)],                # multi-tile
+        [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 33, 7, 200)],                # 231 px: scatter
+    ]
+    before = ctx.stats()
+    for rep in range(3):
+        for tiles in cases:
+            descs = (pkg.MandelDesc * len(tiles))(*tiles)
+            npx = sum(t.nrows * t.ncols for t in tiles)
+            out = ctx.pinned_empty(npx, np.uint32)
+            out[:] = 0xdeadbeef
+            a.request([descs], out).result(timeout=60)
+            off = 0
+            for t in tiles:
+                n = t.nrows * t.ncols
+                assert np.array_equal(out[off:off + n].reshape(t.nrows, t.ncols), _tile_ref(t))
+                off += n
+            ctx.pinned_free(out)
+    after = ctx.stats()
+    assert after.direct_batches - before.direct_batches >= 3 * 5
+    a.release()
+
+
+def test_direct_reply_concurrent_clients(ctx):
+    """Closed-loop clients (one outstanding request each): batches of several
+    requests replied by the kernel, staging slots and their tile counters
+    reused across both compute streams; every reply exact."""
+    a = ctx.spawn("mandelbrot")
+    clients, per = 12, 25
+    rng = np.random.default_rng(17)
+    descs = [[storm_tile(rng) for _ in range(per)] for _ in range(clients)]
+    refs = [[_tile_ref(d) for d in row] for row in descs]
+    errors = []
+    before = ctx.stats()
+
+    def client(c):
+        try:
+            out = ctx.pinned_empty(4096, np.uint32)
+            for i in range(per):
+                out[:] = 0
+                a.request([(pkg.MandelDesc * 1)(descs[c][i])], out).result(timeout=60)
+                if not np.array_equal(out.reshape(64, 64), refs[c][i]):
+                    errors.append((c, i))
+            ctx.pinned_free(out)
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+    th = [threading.Thread(target=client, args=(c,)) for c in range(clients)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
+    assert ctx.stats().direct_batches > before.direct_batches
+    a.release()
+
+
 def test_multi_tile_request(ctx):
     a = ctx.spawn("mandelbrot")
     rng = np.random.default_rng(5)
