@@ -24,6 +24,17 @@ with pkg.Context(1) as ctx:
                                                              fp64=True))], outs[k])
             for k in range(64)]
     [f.result(60) for f in futs]
+    # direct replies (one small request per batch): checked kernel, deferred
+    # kernel with replays (fp32 and fp64), a multi-tile request
+    for tiles in [[pkg.mandel_desc(-2.0, -1.875, -0.0625, 0.0625, 64, 64, 256, fp64=True)],
+                  [pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 96, 80, 1000)],
+                  [pkg.mandel_desc(-0.30, -0.20, 0.60, 0.70, 64, 48, 300, fp64=True)],
+                  [pkg.mandel_desc(-1.0 + k / 8, -0.875 + k / 8, 0.0, 0.125, 64, 64, 256,
+                                   fp64=True) for k in range(3)]]:
+        out = ctx.pinned_empty(sum(t.nrows * t.ncols for t in tiles), np.uint32)
+        a.request([(pkg.MandelDesc * len(tiles))(*tiles)], out).result(60)
+        ctx.pinned_free(out)
+    assert ctx.stats().direct_batches >= 4
     a.release()
     # sgemm: FFMA, 3xTF32 direct, pipelined host request; device FNV; run_mandelbrot
     for M, N, K, mode in [(100, 77, 33, pkg.SGEMM_FFMA), (256, 256, 64, pkg.SGEMM_3XTF32),
