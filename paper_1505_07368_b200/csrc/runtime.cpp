@@ -1334,7 +1334,13 @@ static bool sgemm_tiled2d_eligible(const cafxg_sgemm_desc& g) {
     const char* e = getenv("CAFXG_SGEMM_2D");
     return !(e && e[0] == '0');
   }();
-  return on && g.mode != CAFXG_SGEMM_FFMA && g.M >= 8192 && g.N >= 8192 && g.M % 128 == 0 &&
+  static const uint32_t min_dim = [] {  // CAFXG_SGEMM_2D_MIN: experiments only
+    const char* e = getenv("CAFXG_SGEMM_2D_MIN");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? (uint32_t)v : 8192u;
+  }();
+  return on && g.mode != CAFXG_SGEMM_FFMA && g.M >= min_dim && g.N >= min_dim &&
+         g.M % 128 == 0 &&
          g.N % 256 == 0 && sgemm_tc_supported(128, 256, g.K, g.K, g.N, g.N);
 }
 
