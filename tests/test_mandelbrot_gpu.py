@@ -317,6 +317,30 @@ def test_run_mandelbrot_on_device(ctx, golden, size, it):
     assert ms > 0
 
 
+def test_run_mandelbrot_csv_contract(golden, tmp_path):
+    """tools/bench_csv.py appends rows in the reference harness's CSV schema
+    (header of append_csv, bench.cpp:515-516), so GPU and reference runs share
+    one file; the checksum column is the reference's."""
+    import csv
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "bench_csv", os.path.join(os.path.dirname(pkg.__file__), "tools", "bench_csv.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    out = tmp_path / "runs.csv"
+    for _ in range(2):  # the second call appends without a second header
+        mod.main(["--size", "256", "--iter", "100", "--runs", "2", "--csv", str(out)])
+    rows = list(csv.reader(open(out)))
+    assert rows[0] == ["benchmark", "param_string", "workers", "run_index", "wall_clock_ms",
+                       "peak_rss_bytes", "checksum"]
+    want = [g for g in golden["run_mandelbrot"] if g["size"] == 256 and g["max_iter"] == 100]
+    assert len(rows) == 5 and all(len(r) == 7 for r in rows)
+    for r in rows[1:]:
+        assert r[0] == "mandelbrot-gpu" and r[1].startswith("size=256;iter=100;devices=")
+        assert int(r[6]) == int(want[0]["checksum"]) and float(r[4]) > 0
+
+
 def test_concurrent_host_requests(ctx):
     """Several host threads submitting to one context at once (the C ABI is
     thread-safe; ctypes releases the GIL for the blocking call)."""
