@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "sgemm.cuh"
@@ -225,6 +226,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: everything above (barrier init, TMEM
+  // allocation, tensor-map prefetch) overlaps the tail of the operand split;
+  // no global memory is touched before the split grid has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
@@ -366,6 +371,7 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const float* __restrict
     *reinterpret_cast<float4*>(Ah + e) = h;
     *reinterpret_cast<float4*>(Al + e) = l;
   }
+  asm volatile("griddepcontrol.launch_dependents;");
 }
 
 // B (K x N, ldb) -> Bth, Btl (N x K packed): 32x32 tiles through smem
@@ -387,6 +393,7 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float* __res
     Bth[(size_t)(n0 + j) * K + k0 + tx] = th[tx][j];
     Btl[(size_t)(n0 + j) * K + k0 + tx] = tl[tx][j];
   }
+  asm volatile("griddepcontrol.launch_dependents;");
 }
 
 // Both operands in one launch (device-API requests): blocks [0, nb_a) split
@@ -399,20 +406,22 @@ __global__ void __launch_bounds__(256) split_ab_kernel(const float* __restrict__
                                                        float* __restrict__ Btl, int nb_a) {
   __shared__ float th[32][33], tl[32][33];
   if ((int)blockIdx.x < nb_a) {
-    const size_t total = (size_t)M * K;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total / 4;
-         i += (size_t)nb_a * blockDim.x) {
-      size_t e = i * 4;
-      size_t r = e / K, c = e % K;
-      float4 v = *reinterpret_cast<const float4*>(A + r * lda + c);
+    // rows of A in float4 steps; 32-bit index math (sgemm_tc_launch checks
+    // M * K / 4 < 2^32)
+    const uint32_t k4 = (uint32_t)K / 4, total = (uint32_t)M * k4;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (uint32_t)nb_a * blockDim.x) {
+      const uint32_t r = i / k4, c = (i - r * k4) * 4;
+      float4 v = *reinterpret_cast<const float4*>(A + (size_t)r * lda + c);
       float4 h, l;
       split_tf32(v.x, h.x, l.x);
       split_tf32(v.y, h.y, l.y);
       split_tf32(v.z, h.z, l.z);
       split_tf32(v.w, h.w, l.w);
-      *reinterpret_cast<float4*>(Ah + e) = h;
-      *reinterpret_cast<float4*>(Al + e) = l;
+      *reinterpret_cast<float4*>(Ah + (size_t)i * 4) = h;
+      *reinterpret_cast<float4*>(Al + (size_t)i * 4) = l;
     }
+    asm volatile("griddepcontrol.launch_dependents;");
     return;
   }
   const int t = (int)blockIdx.x - nb_a, tn = N / 32;
@@ -429,6 +438,7 @@ __global__ void __launch_bounds__(256) split_ab_kernel(const float* __restrict__
     Bth[(size_t)(n0 + j) * K + k0 + tx] = th[tx][j];
     Btl[(size_t)(n0 + j) * K + k0 + tx] = tl[tx][j];
   }
+  asm volatile("griddepcontrol.launch_dependents;");
 }
 
 // ---- tensor maps (driver entry point fetched through the runtime) ---------
@@ -548,6 +558,15 @@ int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float
   return 0;
 }
 
+// CAFXG_SGEMM_PDL=0 launches the GEMM without programmatic dependent launch
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CAFXG_SGEMM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
                        void* stream, int splits, int a_row0, int b_row0) {
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
@@ -571,13 +590,17 @@ int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, i
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)splits;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // programmatic dependent launch (the kernel waits with griddepcontrol.wait
+  // before touching global memory, so any predecessor is safe)
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel, m[0], m[1], m[2], m[3], C, M, N, K, ldc,
                      splits, a_row0, b_row0);
   return (int)cudaGetLastError();
@@ -598,6 +621,8 @@ int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int 
   float* Al = Ah + (size_t)M * K;
   float* Bh = Al + (size_t)M * K;
   float* Bl = Bh + (size_t)N * K;
+  if ((size_t)M * K / 4 >= (1ull << 32))
+    return (int)cudaErrorInvalidValue;
   const int splits = sgemm_tc_splits(M, N, K, sm_count > 0 ? sm_count : 148);
   const int nb_a = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 8);
   const int nb_b = (N / 32) * (K / 32);
