@@ -231,6 +231,11 @@ constexpr size_t kStageTail = 256;
 // storm tiles take 32 rounds of 16-byte stores; a 1M-pixel band would stall
 // its warp for milliseconds).
 constexpr uint64_t kDirectTilePx = 64u << 10;
+// Launches of at most this many pixels compute coordinates inline (one fp64
+// divide per pixel start) instead of through a coordinate-table launch and
+// its allocation: for cfg1's 512K-pixel first wave the table path cost ~8 us
+// of host issue time before the escape kernel could start.
+constexpr uint64_t kInlineCoordsPx = 4u << 20;
 constexpr uint64_t kInlineCopyPx = 256u << 10;  // copy-out on the compute stream below  // beyond this only when a full batch is queued
 constexpr uint64_t kMaxBatchPx = 16ull << 20;
 constexpr int kUpSlots = 16;
@@ -338,6 +343,12 @@ struct cafxg_ctx {
 };
 
 namespace cafxg {
+
+// Host clock for CAFXG_TRACE timelines (ms since first use).
+static double trace_now_ms() {
+  static const auto t0 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
 
 static void note_max_batch(cafxg_ctx* ctx, uint64_t n) {
   uint64_t cur = ctx->st_max_batch.load();
@@ -680,16 +691,17 @@ static int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                          uint64_t pixels, cudaStream_t stream,
                          uint32_t* direct_counters = nullptr) {
   (void)max_iter;
-  (void)pixels;
   if (total_chunks == 0)
     return CAFXG_OK;
   // coordinate tables (one column and one row table per tile) pay off for
   // big tiles; batches of small tiles (request storms) compute coordinates
   // inline in the escape kernel and save the table launch
   std::vector<MTile> tiles = tiles_in;
-  bool small = true;
+  // (and so do launches of few pixels in all: kInlineCoordsPx)
+  bool small_tiles = true;
   for (auto& t : tiles)
-    small = small && (uint64_t)t.ncols * t.nrows <= (64u << 10);
+    small_tiles = small_tiles && (uint64_t)t.ncols * t.nrows <= (64u << 10);
+  const bool small = small_tiles || pixels <= kInlineCoordsPx;
   uint8_t* coords = nullptr;
   if (!small) {
     const size_t esz = precision ? sizeof(double) : sizeof(float);
@@ -838,6 +850,7 @@ static std::vector<std::vector<SubTile>> plan_mandel(
 }
 
 static int stream_after(cudaStream_t b, cudaStream_t a);  // b waits for a's work so far
+static int stream_after_pooled(Device* d, cudaStream_t b, cudaStream_t a);
 
 // Submits one device's share: waves of sub-tiles, each a single launch into a
 // device staging buffer followed by the copy-out on the d2h stream, so the
@@ -880,23 +893,42 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
     return (v > 0 ? (uint64_t)v : 512ull) << 10;
   }();
   const uint64_t min_wave = dev_px_total >= (64ull << 20) ? big_min : small_min;
+  // Small, shallow requests (<= 4M pixels, max_iter <= 256: cfg1) are bound by
+  // the copy-out, not the kernel: one small first wave starts the copy engine
+  // early and everything else goes in a second wave whose contiguous bands
+  // leave in one copy (2 MB copies ran at ~45 GB/s, the link does ~55).
+  // CAFXG_SMALL_PLAN=0: the geometric waves everywhere (experiments).
+  static const bool small_plan_on = [] {
+    const char* e = getenv("CAFXG_SMALL_PLAN");
+    return !(e && e[0] == '0');
+  }();
+  uint32_t req_maxit = 0;
+  for (auto& sb : subs)
+    req_maxit = std::max(req_maxit, sb.d.max_iter);
+  const bool two_waves = small_plan_on && dev_px_total <= (4ull << 20) && req_maxit <= 256;
   // CAFXG_TRACE=1: per-wave device timeline on stderr (debug aid)
   static const bool trace = [] {
     const char* e = getenv("CAFXG_TRACE");
     return e && e[0] == '1';
   }();
   std::vector<std::array<cudaEvent_t, 3>> tev;
+  std::vector<double> thost;  // host clock at each wave's start / after its launches
+  const double t_entry = trace_now_ms();
   // waves alternate between the two compute streams (both ordered after the
   // device's earlier work; compute is ordered after both at the end)
   CAFXG_TRY(stream_after(d->compute2, d->compute));
   uint32_t wave = 0;
   while (i < subs.size()) {
-    cudaStream_t ks = (wave++ & 1) ? d->compute2 : d->compute;
+    // (the two-wave plan keeps one stream: the first wave then runs alone and
+    // its copy starts sooner)
+    cudaStream_t ks = ((wave++ & 1) && !two_waves) ? d->compute2 : d->compute;
     // group a wave (same precision)
     size_t j = i;
     uint64_t px = 0;
     int prec = subs[i].d.precision;
-    const uint64_t cap = std::max<uint64_t>(std::min<uint64_t>(wave_px, left / 4), min_wave);
+    const uint64_t cap =
+        two_waves ? (wave == 1 ? min_wave : UINT64_MAX)
+                  : std::max<uint64_t>(std::min<uint64_t>(wave_px, left / 4), min_wave);
     while (j < subs.size() && subs[j].d.precision == prec &&
            (px == 0 || px + subs[j].pixels <= cap)) {
       px += subs[j].pixels;
@@ -918,19 +950,31 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
       for (auto& e : tev.back())
         cudaEventCreate(&e);
       cudaEventRecord(tev.back()[0], ks);
+      thost.push_back(trace_now_ms());
     }
     CAFXG_TRY(launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks));
     if (trace)
+      thost.push_back(trace_now_ms());
+    if (trace)
       cudaEventRecord(tev.back()[1], ks);
-    cudaEvent_t ev;
-    CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    CAFXG_CUDA_TRY(cudaEventRecord(ev, ks));
-    CAFXG_CUDA_TRY(cudaStreamWaitEvent(d->d2h, ev, 0));
-    cudaEventDestroy(ev);  // destruction is deferred until the event completes
+    CAFXG_TRY(stream_after_pooled(d, d->d2h, ks));
     off = 0;
+    // copies of consecutive sub-tiles that are contiguous on both sides
+    // (row bands of one tile into a pinned image; any run into the staging
+    // buffer) go out as one cudaMemcpyAsync
+    uint32_t* run_dst = nullptr;
+    uint64_t run_src = 0, run_px = 0;
+    auto flush_run = [&]() -> int {
+      if (run_px) {
+        CAFXG_CUDA_TRY(cudaMemcpyAsync(run_dst, dout + run_src, run_px * 4,
+                                       cudaMemcpyDeviceToHost, d->d2h));
+        ctx->st_d2h += run_px * 4;
+      }
+      run_px = 0;
+      return CAFXG_OK;
+    };
     for (size_t k = i; k < j; ++k) {
-      uint64_t bytes = subs[k].pixels * 4;
-      void* dst;
+      uint32_t* dst;
       if (out_pinned) {
         dst = host_out + subs[k].d.out_offset;
       } else {
@@ -938,11 +982,16 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
         scat.push_back({staged, subs[k].d.out_offset, subs[k].pixels});
         staged += subs[k].pixels;
       }
-      CAFXG_CUDA_TRY(cudaMemcpyAsync(dst, dout + off, bytes,
-                                     cudaMemcpyDeviceToHost, d->d2h));
-      ctx->st_d2h += bytes;
+      if (run_px && dst != run_dst + run_px)
+        CAFXG_TRY(flush_run());
+      if (!run_px) {
+        run_dst = dst;
+        run_src = off;
+      }
+      run_px += subs[k].pixels;
       off += subs[k].pixels;
     }
+    CAFXG_TRY(flush_run());
     CAFXG_CUDA_TRY(cudaFreeAsync(dout, d->d2h));
     if (trace)
       cudaEventRecord(tev.back()[2], d->d2h);
@@ -962,6 +1011,9 @@ static int submit_mandel_device(cafxg_ctx* ctx, Device* d,
       fprintf(stderr, "cafxg trace wave %zu: kernel %.3f..%.3f ms, copy done %.3f ms\n", w, a, b,
               c);
     }
+    for (size_t w = 0; w + 1 < thost.size(); w += 2)
+      fprintf(stderr, "cafxg trace host: wave %zu issued %.3f..%.3f ms after entry\n", w / 2,
+              thost[w] - t_entry, thost[w + 1] - t_entry);
     for (auto& w : tev)
       for (auto& e : w)
         cudaEventDestroy(e);
@@ -1112,11 +1164,6 @@ static int ensure_nccl(cafxg_ctx* ctx) {
   return CAFXG_OK;
 }
 
-// Streams `b` waits for what `a` has enqueued so far.
-static double trace_now_ms() {
-  static const auto t0 = std::chrono::steady_clock::now();
-  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-}
 
 static bool trace_on() {
   static const bool on = [] {
