@@ -714,9 +714,13 @@ __device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
     }
   }
   __syncwarp();  // entries consumed before later pushes overwrite them
+  if constexpr (kUnit == 8) {
 #pragma unroll 1
-  for (uint32_t r = 0; r < L.block_reps; ++r)
+    for (uint32_t r = 0; r < L.block_reps; ++r)
+      rp.template run<kUnit, kExact>(rn);
+  } else {
     rp.template run<kUnit, kExact>(rn);
+  }
   constexpr uint32_t omask = kDirect ? (1u << kDirectShift) - 1u : 0xffffffffu;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
@@ -774,23 +778,35 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
       szr[s] = sl.zr_of(s);
       szi[s] = sl.zi_of(s);
     }
+    if constexpr (kUnit == 8) {
 #pragma unroll 1
-    for (uint32_t r = 0; r < reps; ++r)
+      for (uint32_t r = 0; r < reps; ++r)
+        sl.template run_free<kUnit, kExact>();
+    } else {
+      // fully unrolled block (the host sets block_reps = 1): no runtime loop,
+      // which also spared ptxas a second copy of the block-start save
       sl.template run_free<kUnit, kExact>();
+    }
     const uint32_t esc = sl.escaped() & live;
     uint32_t done = esc;
-    // branch-free per slot (predicated store): nested ifs here compiled to
-    // four BSSY/BRA regions that re-loaded max_iter and L.out from constant
-    // memory inside each, and the block end waited on those loads
+    // counts first, then one rarely-taken branch for the stores (a pixel
+    // reaches max_iter once in its lifetime): a store per slot compiled to
+    // one BSSY region per slot, each re-loading max_iter and L.out
+    const uint32_t blk = kUnit == 8 ? block : (uint32_t)kUnit;
+    uint32_t hitm = 0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const bool act = ((live & ~esc) >> s) & 1u;
-      n[s] += act ? block : 0u;
-      const bool hit = act && n[s] >= maxit;
-      if (hit)
-        out[o[s] & omask] = maxit;
-      done |= (uint32_t)hit << s;
+      n[s] += act ? blk : 0u;
+      hitm |= (uint32_t)(act && n[s] >= maxit) << s;
     }
+    if (hitm) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if (hitm >> s & 1u)
+          out[o[s] & omask] = maxit;
+    }
+    done |= hitm;
     if (__any_sync(kFull, esc != 0)) {
       uint32_t base = queued;
 #pragma unroll
