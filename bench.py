@@ -395,14 +395,14 @@ def run_ours(args):
     peak_tops = sms * 128 * sm_max * 1e6 / 1e12
     achieved = 8.0 * iters_local / (kernel_ms / 1e3) / 1e12
     # DRAM traffic of the escape kernel from the committed ncu capture of the
-    # full-image launch (profiles/round1/mandel_cfg3_final_full.txt:
-    # 1.023211 GB written + 11.369216 MB read), scaled to this rank's share
-    traffic = round((1.023211e9 + 11.369216e6) * npx / (W_IMG * H_IMG))
-    # The same capture: FMA pipe busy 91.9% of active cycles over 34.44 ms at
-    # 1.963 GHz = 1.176e12 FMA-pipe lane-cycles for 1.82e11 iterations, i.e.
-    # 6.46 executed lane-ops per iteration (6 in the unchecked step, the rest
+    # full-image launch (profiles/round1/mandel_cfg3_v20_full.txt:
+    # 1.021409 GB written + 10.748672 MB read), scaled to this rank's share
+    traffic = round((1.021409e9 + 10.748672e6) * npx / (W_IMG * H_IMG))
+    # The same capture: FMA pipe busy 92.5% of active cycles over 33.97 ms at
+    # 1.962 GHz = 1.170e12 FMA-pipe lane-cycles for 1.82e11 iterations, i.e.
+    # 6.42 executed lane-ops per iteration (6 in the unchecked step, the rest
     # block-end tests, refills and exact replays) against the algorithmic 8.
-    exec_ops_per_iter = 6.46
+    exec_ops_per_iter = 6.42
     roof = {"bound": "fp32_pipe", "achieved": round(achieved, 3), "peak": round(peak_tops, 3),
             "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4), "traffic": traffic,
             "traffic_note": "dram read+write bytes per launch (ncu, profiles/round1); "
@@ -415,8 +415,8 @@ def run_ours(args):
             "frac_note": "frac counts the reference's 8 FP ops per iteration; the kernel "
                          "executes 6 per iteration (escape test deferred to the ends of "
                          "56-step unchecked blocks, 2*zr*zi+ci as one FMA) plus block-end "
-                         "tests and exact replays, 6.46 lane-ops/iteration measured (ncu "
-                         "FMA pipe busy 91.9%, profiles/round1/mandel_cfg3_final_full.txt); "
+                         "tests and exact replays, 6.42 lane-ops/iteration measured (ncu "
+                         "FMA pipe busy 92.5%, profiles/round1/mandel_cfg3_v20_full.txt); "
                          "frac_executed is the pipe fraction doing that executed work"}
     if clk.get("sm_mhz"):
         peak_clk = sms * 128 * clk["sm_mhz"] * 1e6 / 1e12

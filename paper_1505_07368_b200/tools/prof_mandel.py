@@ -1,6 +1,6 @@
 """Small driver for ncu captures of the escape kernel: one warm-up and one
 profiled launch of a BASELINE config through cafxg_mandelbrot_device.
-    python paper_1505_07368_b200/tools/prof_mandel.py cfg3|cfg1|storm64|storm16|ref4096
+    python paper_1505_07368_b200/tools/prof_mandel.py cfg3|cfg1|storm64|storm16|ref4096|ref16000
 """
 import os
 import sys
@@ -17,6 +17,8 @@ elif which == "cfg1":
     tiles = [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)]
 elif which == "ref4096":
     tiles = [pkg.reference_desc(4096, 500)]
+elif which == "ref16000":
+    tiles = [pkg.reference_desc(16000, 500)]
 else:  # storm64 / storm16: that many storm tiles in one launch
     tiles = []
     for k in range(int(which[5:] or 64)):
