@@ -1778,10 +1778,7 @@ static void finish_request(Request* r, int status, bool account = true) {
 static void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* bounce,
                          int status);
 
-// One batch of Mandelbrot requests (same precision) on one device: one launch
-// over every tile of every request into a device staging buffer, then one
-// scatter launch straight into the pinned reply buffers (or one D2H into a
-// pinned bounce buffer + host memcpy for pageable replies).
+// Callback thread: runs reply jobs (slices of large batches, copy pieces).
 static void callback_loop(cafxg_ctx* ctx) {
   while (true) {
     std::function<void()> job;
@@ -1893,6 +1890,11 @@ static inline uint64_t now_ns() {
       .count();
 }
 
+// One batch of Mandelbrot requests (same precision) on one device: one launch
+// over every tile of every request into a device staging slot; small batches
+// into pinned replies are then copied out by that kernel itself (direct
+// reply), others by one scatter launch straight into the pinned reply buffers
+// (or one D2H into a pinned bounce buffer + host memcpy for pageable replies).
 static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> batch) {
   const double t_begin = trace_now_ms();
   uint64_t ph = now_ns();
