@@ -2040,8 +2040,10 @@ static void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> ba
       direct ? reinterpret_cast<uint32_t*>(d->stage[slot] + d->stage_cap[slot] - kStageTail)
              : nullptr;
   status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks, counters);
-  if (direct)
+  if (direct) {
     ctx->st_direct++;
+    ctx->st_d2h += px * 4;  // written to the replies by the kernel
+  }
   phase(1);
   if (tev[0])
     cudaEventRecord(tev[1], ks);
