@@ -152,10 +152,12 @@ def test_direct_reply_small_batches(ctx):
         [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 33, 7, 200)],                # 231 px: scatter
     ]
     before = ctx.stats()
+    reply_bytes = 0
     for rep in range(3):
         for tiles in cases:
             descs = (pkg.MandelDesc * len(tiles))(*tiles)
             npx = sum(t.nrows * t.ncols for t in tiles)
+            reply_bytes += npx * 4
             out = ctx.pinned_empty(npx, np.uint32)
             out[:] = 0xdeadbeef
             a.request([descs], out).result(timeout=60)
@@ -167,6 +169,7 @@ def test_direct_reply_small_batches(ctx):
             ctx.pinned_free(out)
     after = ctx.stats()
     assert after.direct_batches - before.direct_batches >= 3 * 5
+    assert after.d2h_bytes - before.d2h_bytes == reply_bytes  # direct replies counted too
     a.release()
 
 
