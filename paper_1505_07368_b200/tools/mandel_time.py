@@ -35,6 +35,11 @@ WORK = {
     "storm_fp64_16x64sq_it256": storm(16, 256),
     "storm_fp64_64x64sq_it256": storm(64, 256),
     "cfg1_fp32_1920x1080_it100": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)],
+    "cfg3reg_fp32_4096_it3000": [pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 4096, 4096, 3000)],
+    "deep_fp32_4096_it2000": [pkg.mandel_desc(-0.7487, -0.7485, 0.0650, 0.0652, 4096, 4096,
+                                              2000)],
+    "seahorse_fp64_4096_it2000": [pkg.mandel_desc(-0.76, -0.74, 0.09, 0.11, 4096, 4096, 2000,
+                                                  fp64=True)],
 }
 
 only = sys.argv[1:] or list(WORK)
