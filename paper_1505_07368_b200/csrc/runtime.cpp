@@ -1227,9 +1227,12 @@ static int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_de
   const size_t N = g.N, K = g.K;
   const uint32_t rows = r1 - r0;
   uint32_t R = ((rows + 7) / 8 + 127) / 128 * 128;  // ~8 blocks of whole 128-row tiles
-  static const uint32_t rmin = [] {  // CAFXG_SGEMM_RMIN: experiments only
+  // minimum block height (CAFXG_SGEMM_RMIN: experiments only): 256 since the
+  // GEMM launch follows the split with PDL (e2e 1024^3 0.275 -> 0.272 ms
+  // median, 2048^3 0.906 -> 0.869 ms; 128 lost at 1024^3)
+  static const uint32_t rmin = [] {
     const char* e = getenv("CAFXG_SGEMM_RMIN");
-    return e ? (uint32_t)atoi(e) : 512u;
+    return e ? (uint32_t)atoi(e) : 256u;
   }();
   R = std::max<uint32_t>(R, rmin);
   float *Bh = nullptr, *Bl = nullptr, *Ah = nullptr, *Al = nullptr;
