@@ -1,5 +1,5 @@
 // Device-side descriptors shared by the Mandelbrot kernels and the host
-// dispatcher (runtime.cpp).
+// runtime (rt_mandel.cpp, rt_actor.cpp).
 #pragma once
 #include <cstdint>
 
