@@ -232,6 +232,18 @@ class Context:
         _check(lib().cafxg_open(device_mask, C.byref(h)), "cafxg_open")
         self.handle = h.value
         self._pinned = {}
+        # async submits: what a pending submit needs alive (descriptor array,
+        # output array, callback), keyed by a token popped when it completes;
+        # one CFUNCTYPE object serves every submit and lives with the context
+        self._sub_keep = {}
+        self._sub_lock = threading.Lock()
+        self._sub_next = 0
+        self._sub_cb = DONE_FN(self._sub_done)
+
+    def _sub_done(self, user, status):
+        with self._sub_lock:
+            done, _ = self._sub_keep.pop(user)
+        done(status)
 
     # -- lifetime
     def close(self) -> None:
@@ -291,12 +303,21 @@ class Context:
     def mandelbrot_submit(self, tiles, out: np.ndarray, done) -> None:
         """`done(status)` runs on a backend completion thread."""
         arr, n = _desc_array(tiles)
-        cb = DONE_FN(lambda user, st: done(st))
-        keep = (arr, cb, out)
-        self._keep_cb = getattr(self, "_keep_cb", [])
-        self._keep_cb.append(keep)
-        _check(lib().cafxg_mandelbrot_submit(self.handle, arr, n, out.ctypes.data, cb, None),
-               "mandelbrot_submit")
+        with self._sub_lock:
+            self._sub_next += 1
+            token = self._sub_next
+            self._sub_keep[token] = (done, (arr, out))
+        code = lib().cafxg_mandelbrot_submit(self.handle, arr, n, out.ctypes.data,
+                                             self._sub_cb, token)
+        if code != OK:
+            with self._sub_lock:
+                self._sub_keep.pop(token, None)
+        _check(code, "mandelbrot_submit")
+
+    def pending_submits(self) -> int:
+        """Async submits whose callback has not run yet."""
+        with self._sub_lock:
+            return len(self._sub_keep)
 
     def mandelbrot_device(self, tiles, dev_ptr: int, stream: int = 0, device: int = 0) -> None:
         arr, n = _desc_array(tiles)

@@ -243,7 +243,9 @@ void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> batch) {
     for (uint32_t k = 0; direct && k < r->ntiles; ++k) {
       const cafxg_mandel_desc& t = r->tile(k);
       const uint64_t tp = (uint64_t)t.nrows * t.ncols;
-      direct = tp % 4 == 0 && tp <= kDirectTilePx;
+      // one launch (one max_iter group) covers a direct batch: a request
+      // whose tiles differ in max_iter takes the scatter path
+      direct = tp % 4 == 0 && tp <= kDirectTilePx && t.max_iter == maxit;
     }
   }
   if (!d->stage[0]) {
@@ -252,7 +254,10 @@ void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> batch) {
     for (int i = 0; i < kMaxInflight; ++i) {
       const size_t cap = kMaxBatchPx * 4 + kStageTail;
       if (cudaMalloc((void**)&d->stage[i], cap) == cudaSuccess &&
-          cudaMemset(d->stage[i] + cap - kStageTail, 0, kStageTail) == cudaSuccess) {
+          cudaMemset(d->stage[i] + cap - kStageTail, 0, kStageTail) == cudaSuccess &&
+          // the legacy stream's memset is not ordered before the non-blocking
+          // compute streams: wait for it
+          cudaStreamSynchronize(0) == cudaSuccess) {
         d->stage_cap[i] = cap;
       } else {
         cudaGetLastError();
@@ -275,7 +280,8 @@ void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> batch) {
       }
       size_t cap = std::max<size_t>(need, kMaxBatchPx * 4 + kStageTail);
       if (cudaMalloc((void**)&d->stage[slot], cap) != cudaSuccess ||
-          cudaMemset(d->stage[slot] + cap - kStageTail, 0, kStageTail) != cudaSuccess) {
+          cudaMemset(d->stage[slot] + cap - kStageTail, 0, kStageTail) != cudaSuccess ||
+          cudaStreamSynchronize(0) != cudaSuccess) {
         d->stage[slot] = nullptr;
         fail_all(cuda_status(cudaGetLastError(), "batch staging allocation"));
         return;

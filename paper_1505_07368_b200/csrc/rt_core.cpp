@@ -284,6 +284,8 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
       CAFXG_CUDA_TRY(cudaStreamCreateWithFlags(&d->h2d, cudaStreamNonBlocking));
       CAFXG_CUDA_TRY(cudaMalloc(&d->sched, kSchedSlots * 2 * sizeof(uint32_t)));
       CAFXG_CUDA_TRY(cudaMemset(d->sched, 0, kSchedSlots * 2 * sizeof(uint32_t)));
+      // complete before any launch on the non-blocking streams reads a cursor
+      CAFXG_CUDA_TRY(cudaStreamSynchronize(0));
       CAFXG_CUDA_TRY(cudaHostAlloc((void**)&d->up_base, kUpSlots * kUpSlotBytes,
                                    cudaHostAllocPortable));
       for (auto& ev : d->up_ev)
@@ -387,6 +389,9 @@ int cafxg_close(cafxg_ctx* ctx) try {
         cudaEventDestroy(d->stage_ev[i]);
     }
     cudaFree(d->sched);
+    for (auto ev : d->sched_ev)
+      if (ev)
+        cudaEventDestroy(ev);
     cudaStreamSynchronize(d->h2d);
     cudaStreamSynchronize(d->compute2);
     cudaStreamDestroy(d->compute2);

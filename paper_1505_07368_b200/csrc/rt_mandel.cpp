@@ -295,7 +295,6 @@ int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
   L.total_chunks = chunks;
   L.max_iter = tiles[0].max_iter;
   L.out = out_base;
-  L.sched = d->next_sched();
   L.zero = 0.0f;
   L.inline_coords = tiles[0].cx == nullptr;
   if (direct_counters) {
@@ -327,8 +326,14 @@ int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
     for (auto& t : tiles)
       safe = safe && deferred_safe(t);
     MandelLaunchCfg cfg = mandel_cfg(d, precision, L.max_iter, exact, safe, pixels);
+    // a scheduler slot of the ring, reused only after the launch that held it
+    // kSchedSlots launches ago finished (launches on different streams --
+    // user streams of cafxg_mandelbrot_device included -- may run at once)
+    const uint32_t slot = d->sched_acquire(stream);
+    L.sched = d->sched + 2 * slot;
     const auto l0 = std::chrono::steady_clock::now();
     int e = mandel_launch(L, precision, cfg, stream);
+    d->sched_release(slot, stream);
     ctx->st_phase_ns[5] += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
                                std::chrono::steady_clock::now() - l0)
                                .count();
@@ -451,89 +456,134 @@ int submit_mandel_device(cafxg_ctx* ctx, Device* d,
   const double t_entry = trace_now_ms();
   // waves alternate between the two compute streams (both ordered after the
   // device's earlier work; compute is ordered after both at the end)
-  CAFXG_TRY(stream_after(d->compute2, d->compute));
-  uint32_t wave = 0;
-  while (i < subs.size()) {
-    // (the two-wave plan keeps one stream: the first wave then runs alone and
-    // its copy starts sooner)
-    cudaStream_t ks = ((wave++ & 1) && !two_waves) ? d->compute2 : d->compute;
-    // group a wave (same precision)
-    size_t j = i;
-    uint64_t px = 0;
-    int prec = subs[i].d.precision;
-    const uint64_t cap =
-        two_waves ? (wave == 1 ? min_wave : UINT64_MAX)
-                  : std::max<uint64_t>(std::min<uint64_t>(wave_px, left / 4), min_wave);
-    while (j < subs.size() && subs[j].d.precision == prec &&
-           (px == 0 || px + subs[j].pixels <= cap)) {
-      px += subs[j].pixels;
-      ++j;
-    }
-    uint32_t* dout = nullptr;
-    CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dout, px * 4, ks));
-    std::vector<MTile> mt(j - i);
-    uint32_t chunks = 0, maxit = 0;
-    uint64_t off = 0;
-    for (size_t k = i; k < j; ++k) {
-      fill_mtile(mt[k - i], subs[k].d, off, chunks);
-      chunks += tile_chunks(subs[k].d.nrows, subs[k].d.ncols, subs[k].d.precision);
-      maxit = std::max(maxit, subs[k].d.max_iter);
-      off += subs[k].pixels;
-    }
-    if (trace) {
-      tev.push_back({});
-      for (auto& e : tev.back())
-        cudaEventCreate(&e);
-      cudaEventRecord(tev.back()[0], ks);
-      thost.push_back(trace_now_ms());
-    }
-    CAFXG_TRY(launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks));
-    if (trace)
-      thost.push_back(trace_now_ms());
-    if (trace)
-      cudaEventRecord(tev.back()[1], ks);
-    CAFXG_TRY(stream_after_pooled(d, d->d2h, ks));
-    off = 0;
-    // copies of consecutive sub-tiles that are contiguous on both sides
-    // (row bands of one tile into a pinned image; any run into the staging
-    // buffer) go out as one cudaMemcpyAsync
-    uint32_t* run_dst = nullptr;
-    uint64_t run_src = 0, run_px = 0;
-    auto flush_run = [&]() -> int {
-      if (run_px) {
-        CAFXG_CUDA_TRY(cudaMemcpyAsync(run_dst, dout + run_src, run_px * 4,
-                                       cudaMemcpyDeviceToHost, d->d2h));
-        ctx->st_d2h += run_px * 4;
+  uint32_t* dout_live = nullptr;  // the current wave's buffer until its free is queued
+  // the waves; a failure part-way leaves earlier waves' copies queued, so it
+  // is reported through the completion thread behind them (below)
+  auto issue_waves = [&]() -> int {
+    CAFXG_TRY(stream_after(d->compute2, d->compute));
+    uint32_t wave = 0;
+    while (i < subs.size()) {
+      // (the two-wave plan keeps one stream: the first wave then runs alone and
+      // its copy starts sooner)
+      cudaStream_t ks = ((wave++ & 1) && !two_waves) ? d->compute2 : d->compute;
+      // group a wave (same precision)
+      size_t j = i;
+      uint64_t px = 0;
+      int prec = subs[i].d.precision;
+      const uint64_t cap =
+          two_waves ? (wave == 1 ? min_wave : UINT64_MAX)
+                    : std::max<uint64_t>(std::min<uint64_t>(wave_px, left / 4), min_wave);
+      while (j < subs.size() && subs[j].d.precision == prec &&
+             (px == 0 || px + subs[j].pixels <= cap)) {
+        px += subs[j].pixels;
+        ++j;
       }
-      run_px = 0;
-      return CAFXG_OK;
-    };
-    for (size_t k = i; k < j; ++k) {
-      uint32_t* dst;
-      if (out_pinned) {
-        dst = host_out + subs[k].d.out_offset;
-      } else {
-        dst = staging + staged;
-        scat.push_back({staged, subs[k].d.out_offset, subs[k].pixels});
-        staged += subs[k].pixels;
+      uint32_t* dout = nullptr;
+      CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dout, px * 4, ks));
+      dout_live = dout;
+      // CAFXG_FAIL_WAVE=<w>: wave w fails after its buffer exists (tests the
+      // part-way failure path; never set in production)
+      static const int fail_wave = [] {
+        const char* e = getenv("CAFXG_FAIL_WAVE");
+        return e ? atoi(e) : -1;
+      }();
+      if ((int)wave - 1 == fail_wave)
+        return fail(CAFXG_E_DOWN, "mandelbrot: injected failure of wave %d", fail_wave);
+      std::vector<MTile> mt(j - i);
+      uint32_t chunks = 0, maxit = 0;
+      uint64_t off = 0;
+      for (size_t k = i; k < j; ++k) {
+        fill_mtile(mt[k - i], subs[k].d, off, chunks);
+        chunks += tile_chunks(subs[k].d.nrows, subs[k].d.ncols, subs[k].d.precision);
+        maxit = std::max(maxit, subs[k].d.max_iter);
+        off += subs[k].pixels;
       }
-      if (run_px && dst != run_dst + run_px)
-        CAFXG_TRY(flush_run());
-      if (!run_px) {
-        run_dst = dst;
-        run_src = off;
+      if (trace) {
+        tev.push_back({});
+        for (auto& e : tev.back())
+          cudaEventCreate(&e);
+        cudaEventRecord(tev.back()[0], ks);
+        thost.push_back(trace_now_ms());
       }
-      run_px += subs[k].pixels;
-      off += subs[k].pixels;
+      CAFXG_TRY(launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks));
+      if (trace)
+        thost.push_back(trace_now_ms());
+      if (trace)
+        cudaEventRecord(tev.back()[1], ks);
+      CAFXG_TRY(stream_after_pooled(d, d->d2h, ks));
+      off = 0;
+      // copies of consecutive sub-tiles that are contiguous on both sides
+      // (row bands of one tile into a pinned image; any run into the staging
+      // buffer) go out as one cudaMemcpyAsync
+      uint32_t* run_dst = nullptr;
+      uint64_t run_src = 0, run_px = 0;
+      auto flush_run = [&]() -> int {
+        if (run_px) {
+          CAFXG_CUDA_TRY(cudaMemcpyAsync(run_dst, dout + run_src, run_px * 4,
+                                         cudaMemcpyDeviceToHost, d->d2h));
+          ctx->st_d2h += run_px * 4;
+        }
+        run_px = 0;
+        return CAFXG_OK;
+      };
+      for (size_t k = i; k < j; ++k) {
+        uint32_t* dst;
+        if (out_pinned) {
+          dst = host_out + subs[k].d.out_offset;
+        } else {
+          dst = staging + staged;
+          scat.push_back({staged, subs[k].d.out_offset, subs[k].pixels});
+          staged += subs[k].pixels;
+        }
+        if (run_px && dst != run_dst + run_px)
+          CAFXG_TRY(flush_run());
+        if (!run_px) {
+          run_dst = dst;
+          run_src = off;
+        }
+        run_px += subs[k].pixels;
+        off += subs[k].pixels;
+      }
+      CAFXG_TRY(flush_run());
+      dout_live = nullptr;
+      CAFXG_CUDA_TRY(cudaFreeAsync(dout, d->d2h));
+      if (trace)
+        cudaEventRecord(tev.back()[2], d->d2h);
+      left -= px;
+      i = j;
     }
-    CAFXG_TRY(flush_run());
-    CAFXG_CUDA_TRY(cudaFreeAsync(dout, d->d2h));
-    if (trace)
-      cudaEventRecord(tev.back()[2], d->d2h);
-    left -= px;
-    i = j;
+    CAFXG_TRY(stream_after(d->compute, d->compute2));
+    return CAFXG_OK;
+  };
+  const int issued = issue_waves();
+  if (issued != CAFXG_OK) {
+    // the caller's buffer may still be the target of queued
+    // copies, so `done` must not fire before they drain. The copy stream is
+    // ordered after both compute streams (best effort: on a dead device these
+    // fail too, and the completion thread then sees the error), the live wave
+    // buffer is freed there, and the staging buffer in the completion.
+    std::string err = t_last_error;
+    stream_after(d->d2h, d->compute);
+    stream_after(d->d2h, d->compute2);
+    if (dout_live)
+      cudaFreeAsync(dout_live, d->d2h);
+    cudaGetLastError();
+    const int ps = push_completion(ctx, d, d->d2h, [ctx, staging, join, issued, err](int) {
+      if (staging)
+        ctx->pinned.free(staging);
+      set_last_error("%s", err.c_str());
+      join->part_done(issued);
+    });
+    if (ps != CAFXG_OK) {
+      // not even an event could be recorded: wait here for what is queued
+      cudaStreamSynchronize(d->d2h);
+      if (staging)
+        ctx->pinned.free(staging);
+      set_last_error("%s", err.c_str());
+      join->part_done(issued);
+    }
+    return CAFXG_OK;
   }
-  CAFXG_TRY(stream_after(d->compute, d->compute2));
   if (trace && !tev.empty()) {
     cudaError_t se = cudaEventSynchronize(tev.back()[2]);
     for (size_t w = 0; w < tev.size(); ++w) {

@@ -247,9 +247,27 @@ struct Device {
   cudaEvent_t trace_ref = nullptr;  // CAFXG_TRACE time base
   double trace_ref_ms = 0;
 
-  uint32_t* next_sched() {
-    uint32_t i = sched_next.fetch_add(1, std::memory_order_relaxed) % kSchedSlots;
-    return sched + 2 * i;
+  // Self-resetting scheduler slots: slot i is free again once the launch that
+  // last used it has finished; sched_acquire orders `stream` after that launch
+  // (two launches 1024 slots apart on different streams would
+  // otherwise share one cursor).
+  std::mutex sched_mu;
+  cudaEvent_t sched_ev[kSchedSlots] = {};
+  uint32_t sched_acquire(cudaStream_t stream) {
+    const uint32_t i = sched_next.fetch_add(1, std::memory_order_relaxed) % kSchedSlots;
+    std::lock_guard<std::mutex> g(sched_mu);
+    if (sched_ev[i])
+      cudaStreamWaitEvent(stream, sched_ev[i], 0);
+    return i;
+  }
+  void sched_release(uint32_t i, cudaStream_t stream) {
+    std::lock_guard<std::mutex> g(sched_mu);
+    if (!sched_ev[i] && cudaEventCreateWithFlags(&sched_ev[i], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      sched_ev[i] = nullptr;
+      return;
+    }
+    cudaEventRecord(sched_ev[i], stream);
   }
 };
 

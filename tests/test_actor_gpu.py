@@ -206,6 +206,32 @@ def test_direct_reply_concurrent_clients(ctx):
     a.release()
 
 
+def test_direct_reply_mixed_max_iter_request(ctx):
+    """A small pinned request whose tiles differ in max_iter, batched together
+    with storm tiles from other clients: it must take the scatter path (one
+    launch per max_iter group) and neither it nor its batch mates may fail
+    (it used to pass the direct-reply check and fail the batch)."""
+    a = ctx.spawn("mandelbrot")
+    rng = np.random.default_rng(23)
+    mixed = [storm_tile(rng, it=256), storm_tile(rng, it=100)]
+    storms = [[storm_tile(rng)] for _ in range(24)]
+    for rep in range(4):
+        futs, outs = [], []
+        for tiles in storms[:12] + [mixed] + storms[12:]:
+            out = ctx.pinned_empty(4096 * len(tiles), np.uint32)
+            out[:] = 0xdeadbeef
+            futs.append(a.request([(pkg.MandelDesc * len(tiles))(*tiles)], out))
+            outs.append((tiles, out))
+        for f in futs:
+            f.result(timeout=60)
+        for tiles, out in outs:
+            for k, t in enumerate(tiles):
+                assert np.array_equal(out[k * 4096:(k + 1) * 4096].reshape(64, 64),
+                                      _tile_ref(t))
+            ctx.pinned_free(out)
+    a.release()
+
+
 def test_multi_tile_request(ctx):
     a = ctx.spawn("mandelbrot")
     rng = np.random.default_rng(5)

@@ -111,6 +111,49 @@ def test_tiny_imaginary_rows_use_exact_step(ctx):
         assert np.array_equal(out, ref)
 
 
+def test_failure_after_queued_waves_reports_behind_them():
+    """A wave failing after earlier waves' copies were queued (CAFXG_FAIL_WAVE
+    injects it) reports through the completion thread behind those copies:
+    when `done` fires with the error, the first wave's rows have landed in the
+    caller's buffer (`done` used to fire at once, while DMA could
+    still write the buffer)."""
+    code = r"""
+import sys, threading, numpy as np
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 4096, 4096, 200)
+with pkg.Context(1) as c:
+    out = c.pinned_empty(4096 * 4096, np.uint32)
+    out[:] = 0xdeadbeef
+    seen = {}
+    ev = threading.Event()
+    def done(st):
+        seen["st"] = st
+        seen["first"] = out[:1024 * 4096].copy()
+        ev.set()
+    c.mandelbrot_submit(d, out, done)
+    assert ev.wait(60)
+    assert seen["st"] == 14, seen["st"]
+    first = seen["first"].reshape(1024, 4096)
+    for r in (0, 511, 1023):
+        ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 4096, 4096, 200, fp64=False, centre=True,
+                          row0=r, nrows=1)
+        assert np.array_equal(first[r], ref[0]), r
+    c.sync()
+    assert c.pending_submits() == 0
+    # the context stays usable
+    small = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 64, 64, 50)
+    ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 64, 64, 50, fp64=False, centre=True)
+    assert np.array_equal(c.mandelbrot(small).reshape(64, 64), ref)
+print("ok")
+""" % ROOT
+    env = dict(os.environ, CAFXG_FAIL_WAVE="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
 def test_exact_and_fast_steps_agree():
     """The 7-op (fma-folded) and the 8-op step give identical counts."""
     code = r"""
@@ -267,6 +310,7 @@ def test_device_api_with_torch(ctx):
 
 def test_async_submit_callback_runs_off_thread(ctx):
     import threading
+    import time
     d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 300, 300, 100)
     out = np.zeros(300 * 300, dtype=np.uint32)
     seen = {}
@@ -281,6 +325,12 @@ def test_async_submit_callback_runs_off_thread(ctx):
     assert seen["status"] == 0 and seen["thread"] != threading.get_ident()
     ref = oracle.tile(-2.0, 1.0, -1.0, 1.0, 300, 300, 100, fp64=False, centre=True)
     assert np.array_equal(out.reshape(300, 300), ref)
+    # what the submit kept alive is released once its callback ran
+    for _ in range(100):
+        if ctx.pending_submits() == 0:
+            break
+        time.sleep(0.01)
+    assert ctx.pending_submits() == 0
 
 
 def test_bad_requests_fail_synchronously(ctx):
