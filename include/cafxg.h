@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define CAFXG_ABI_VERSION 1
+#define CAFXG_ABI_VERSION 2  /* 2: cafxg_stats grew nccl_collectives, devices_used */
 
 /* ---- status codes: numeric values of cafx::errc (error.hpp:11-29) --------- */
 enum {
@@ -212,6 +212,8 @@ typedef struct {
   uint64_t h2d_bytes, d2h_bytes;
   uint64_t max_batch;      /* largest batch seen */
   uint64_t direct_batches; /* batches whose escape kernel wrote the replies itself */
+  uint64_t nccl_collectives; /* NCCL collectives issued (multi-device B all-gather) */
+  uint64_t devices_used;   /* bit i set: context device i has run a kernel */
 } cafxg_stats;
 int cafxg_get_stats(cafxg_ctx* ctx, cafxg_stats* out);
 

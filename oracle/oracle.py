@@ -88,6 +88,9 @@ def ref():
         R.ref_region_iters_mt.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double,
                                           C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                           C.c_uint32, C.POINTER(C.c_double)]
+        R.ref_tiles_mt.restype = C.c_uint64
+        R.ref_tiles_mt.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint32,
+                                   C.POINTER(C.c_double)]
         _ref = R
     return _ref
 
@@ -125,6 +128,24 @@ def tile(x0, x1, y0, y1, width, height, max_iter, fp64, centre,
     threads = threads or os.cpu_count() or 1
     lib().oracle_mandelbrot_tile_mt(C.byref(t), _ptr(out), threads, sample_stride)
     return out
+
+
+def ref_tiles(descs, n: int, threads=None):
+    """The unmodified reference's mandelbrot_cell (fp64) over every pixel of
+    `n` tile records laid out as cafxg_mandel_desc (a ctypes array or a buffer
+    address): (packed counts, total iterations, seconds). None without
+    oracle/_ref."""
+    R = ref()
+    if R is None:
+        return None
+    addr = descs if isinstance(descs, int) else C.addressof(descs)
+    rec = (C.c_uint32 * (20 * n)).from_address(addr)
+    dims = np.frombuffer(rec, dtype=np.uint32).reshape(n, 20)
+    npx = int((dims[:, 11].astype(np.uint64) * dims[:, 13].astype(np.uint64)).sum())
+    out = np.empty(npx, dtype=np.uint32)
+    sec = C.c_double()
+    it = R.ref_tiles_mt(addr, n, _ptr(out), threads or os.cpu_count() or 1, C.byref(sec))
+    return out, int(it), sec.value
 
 
 def fnv1a_u32(cells: np.ndarray, h: int = FNV_SEED) -> int:

@@ -521,6 +521,28 @@ void dispatcher_loop(cafxg_ctx* ctx) {
         ctx->st_requests--;  // counted by finish_request
         break;
       }
+      if (r->pixels >= kLargeActorPx) {
+        // a large request is not batched: it takes the host-request path --
+        // 1M-pixel row bands dealt cyclically over every device of the
+        // context, waves whose copy-out overlaps the next wave's kernel --
+        // with the reply buffer as the output (its tiles are packed in order,
+        // cafxg_actor_enqueue recomputed their offsets)
+        if (!batch.empty())
+          break;
+        queue.pop_front();
+        queued_px -= r->pixels;
+        std::vector<cafxg_mandel_desc> tiles(r->ntiles);
+        for (uint32_t k = 0; k < r->ntiles; ++k)
+          tiles[k] = r->tile(k);
+        int s = mandel_submit_impl(
+            ctx, tiles.data(), tiles.size(), static_cast<uint32_t*>(r->out),
+            [](void* u, int st) { finish_request((Request*)u, st); }, r);
+        if (s != CAFXG_OK)
+          push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); });
+        else
+          ctx->st_requests--;  // counted by finish_request
+        break;
+      }
       if (!batch.empty() &&
           (r->precision != batch[0]->precision ||
            px + r->pixels > kMaxBatchPx))

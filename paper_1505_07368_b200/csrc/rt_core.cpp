@@ -271,6 +271,7 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
     for (int i : ords) {
       auto d = std::make_unique<Device>();
       d->ordinal = i;
+      d->index = (int)ctx->devs.size();
       CAFXG_CUDA_TRY(cudaSetDevice(i));
       cudaDeviceProp prop{};
       CAFXG_CUDA_TRY(cudaGetDeviceProperties(&prop, i));
@@ -462,6 +463,8 @@ int cafxg_get_stats(cafxg_ctx* ctx, cafxg_stats* out) {
   out->d2h_bytes = ctx->st_d2h.load();
   out->max_batch = ctx->st_max_batch.load();
   out->direct_batches = ctx->st_direct.load();
+  out->nccl_collectives = ctx->st_nccl.load();
+  out->devices_used = ctx->st_dev_used.load();
   return CAFXG_OK;
 }
 

@@ -340,6 +340,7 @@ int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
     if (e != 0)
       return cuda_status((cudaError_t)e, "mandelbrot launch");
     ctx->st_launches++;
+    mark_used(ctx, d);
   }
   if (dev_tiles)
     CAFXG_CUDA_TRY(cudaFreeAsync(dev_tiles, stream));

@@ -51,6 +51,7 @@ int sgemm_on_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     int e = sgemm_tc_launch(A, B, C, g.M, g.N, g.K, g.lda, g.ldb, g.ldc, scratch,
                             d->sms, stream, &launches);
     ctx->st_launches += launches;
+    mark_used(ctx, d);
     CAFXG_CUDA_TRY(cudaFreeAsync(scratch, stream));
     if (e != 0)
       return cuda_status((cudaError_t)e, "sgemm 3xtf32 launch");
@@ -60,7 +61,16 @@ int sgemm_on_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
   if (e != 0)
     return cuda_status((cudaError_t)e, "sgemm simt launch");
   ctx->st_launches++;
+  mark_used(ctx, d);
   return CAFXG_OK;
+}
+
+static bool nccl_selftest() {
+  static const bool on = [] {
+    const char* e = getenv("CAFXG_NCCL_SELFTEST");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 int ensure_nccl(cafxg_ctx* ctx) {
@@ -214,6 +224,7 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     if (e != 0)
       status = cuda_status((cudaError_t)e, "sgemm: 3xtf32 launch");
     ctx->st_launches += 2;
+    mark_used(ctx, d);
     tmark("gemm", cs);
     cudaEventRecord(mk(ev_gemm), cs);
     cudaStreamWaitEvent(d->d2h, ev_gemm.back(), 0);
@@ -337,6 +348,7 @@ int sgemm_tiled2d_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
                                sgemm_tc_splits((int)mi, (int)nj, (int)K, d->sms), (int)m0,
                                (int)n0);
     ctx->st_launches++;
+    mark_used(ctx, d);
     tmark('G', cs);
     if (e != 0)
       return cuda_status((cudaError_t)e, "sgemm: 3xtf32 block launch");
@@ -438,13 +450,19 @@ int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
     // loadable) the slices are replicated by peer copies on the copy engines
     nccl = ensure_nccl(ctx) == CAFXG_OK;
     clear_last_error();
+  } else if (G == 1 && nccl_selftest()) {
+    // CAFXG_NCCL_SELFTEST=1: a one-device context runs B through the same
+    // NCCL calls (a one-rank communicator, in-place all-gather), so the NCCL
+    // branch is exercised on a one-GPU box; failing to set it up is an error
+    CAFXG_TRY(ensure_nccl(ctx));
+    nccl = true;
   }
   Join* join = new Join;
   join->done = done;
   join->user = user;
   join->remaining = (int)use;
   ctx->st_requests++;
-  if (use == 1 && sgemm_tiled2d_eligible(g)) {
+  if (use == 1 && !nccl && sgemm_tiled2d_eligible(g)) {
     Device* d = ctx->devs[0].get();
     std::lock_guard<std::mutex> lk(d->submit_mu);
     cudaSetDevice(d->ordinal);
@@ -466,7 +484,8 @@ int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
   for (size_t k = 0; k < use; ++k)
     locks.emplace_back(ctx->devs[k]->submit_mu);
   int status = CAFXG_OK;
-  const bool defer_b = use == 1 && g.M && g.ldb == g.N && sgemm_pipeline_eligible(g, g.M);
+  const bool defer_b =
+      use == 1 && !nccl && g.M && g.ldb == g.N && sgemm_pipeline_eligible(g, g.M);
   for (size_t k = 0; k < use && status == CAFXG_OK; ++k) {
     Device* d = ctx->devs[k].get();
     cudaSetDevice(d->ordinal);
@@ -523,7 +542,7 @@ int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
         if (ev)
           cudaEventDestroy(ev);
   }
-  if (status == CAFXG_OK && use > 1 && nccl) {
+  if (status == CAFXG_OK && nccl) {
     ctx->nccl.GroupStart();
     for (size_t k = 0; k < use; ++k) {
       size_t cnt = (size_t)g.K / use * g.ldb;
@@ -532,6 +551,8 @@ int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
     }
     if (ctx->nccl.GroupEnd() != ncclSuccess)
       status = fail(CAFXG_E_DOWN, "sgemm: NCCL all-gather of B failed");
+    else
+      ctx->st_nccl += use;
   }
   for (size_t k = 0; k < use; ++k) {
     Device* d = ctx->devs[k].get();

@@ -196,11 +196,15 @@ constexpr uint64_t kDirectTilePx = 64u << 10;
 constexpr uint64_t kInlineCoordsPx = 4u << 20;
 constexpr uint64_t kInlineCopyPx = 256u << 10;  // copy-out on the compute stream below  // beyond this only when a full batch is queued
 constexpr uint64_t kMaxBatchPx = 16ull << 20;
+// Actor requests of at least this many pixels are not batched: they go the
+// host-request way (row bands over every device, overlapped waves).
+constexpr uint64_t kLargeActorPx = 1ull << 20;
 constexpr int kUpSlots = 16;
 constexpr size_t kUpSlotBytes = 2u << 20;
 
 struct Device {
   int ordinal = 0;
+  int index = 0;  // position in the context's device list
   int sms = 0;
   cudaStream_t compute = nullptr, d2h = nullptr, h2d = nullptr;
   // second compute stream: consecutive waves of a host request alternate
@@ -289,6 +293,8 @@ struct cafxg_ctx {
       st_h2d{0}, st_d2h{0}, st_max_batch{0};
   std::atomic<uint64_t> st_batch_ns{0};  // dispatcher time spent submitting batches
   std::atomic<uint64_t> st_direct{0};    // batches replied by the escape kernel itself
+  std::atomic<uint64_t> st_nccl{0};      // NCCL collectives issued (B all-gathers)
+  std::atomic<uint64_t> st_dev_used{0};  // bit i: context device i ran a kernel
   std::atomic<uint64_t> st_phase_ns[6] = {};  // run_mandel_batch phases (CAFXG_STATS)
   // actor dispatcher
   std::atomic<Request*> inbox{nullptr};
@@ -348,6 +354,11 @@ struct SubTile {
   cafxg_mandel_desc d;  // row0/nrows narrowed; out_offset = host offset
   uint64_t pixels;
 };
+
+// records that context device `d` has run a kernel (cafxg_stats::devices_used)
+inline void mark_used(cafxg_ctx* ctx, const Device* d) {
+  ctx->st_dev_used.fetch_or(1ull << (d->index & 63), std::memory_order_relaxed);
+}
 
 // ---- rt_core.cpp ----
 double trace_now_ms();

@@ -128,3 +128,94 @@ def test_matrix_multiply_actor_over_devices(vctx):
     R = oracle.sgemm_ref_rows(A.reshape(size, size), B.reshape(size, size), rows, size, size)
     assert oracle.sgemm_rel_err(C.reshape(size, size), R, rows, size) <= 1e-5
     a.release()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_large_actor_request_split_over_devices(vctx, pinned):
+    """One compute-actor request of >= 1M pixels leaves the batching path and
+    is served by every device of the context: cyclic row bands, overlapped
+    waves, the reply assembled in the actor's reply buffer; bit-exact, and
+    every device ran a kernel (actor requests used one device)."""
+    os.environ["CAFXG_VIRTUAL_DEVICES"] = str(V)
+    try:
+        c = pkg.Context(device_mask=1)   # fresh: devices_used starts at 0
+    finally:
+        del os.environ["CAFXG_VIRTUAL_DEVICES"]
+    with c:
+        a = c.spawn("mandelbrot")
+        d = pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 1536, 1024, 600)
+        out = c.pinned_empty(1536 * 1024, np.uint32) if pinned else \
+            np.zeros(1536 * 1024, np.uint32)
+        out[:] = 0xdeadbeef
+        a.request([(pkg.MandelDesc * 1)(d)], out).result(timeout=120)
+        st = c.stats()
+        ref = oracle.tile(d.x0, d.x1, d.y0, d.y1, 1536, 1024, 600, fp64=False, centre=True)
+        assert np.array_equal(out.reshape(1024, 1536), ref)
+        assert st.devices_used == (1 << V) - 1
+        assert st.batches == 0  # not a dispatcher batch
+        assert st.requests == 1
+        if pinned:
+            c.pinned_free(out)
+        a.release()
+
+
+def test_sgemm_nccl_branch_one_rank():
+    """CAFXG_NCCL_SELFTEST=1: a one-device context sends B through the NCCL
+    calls of the multi-device path (libnccl dlopen, ncclCommInitAll, grouped
+    in-place all-gather with one rank), so the branch runs on a one-GPU box;
+    the product stays within 1e-5 and one collective was issued."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+M = N = K = 2048
+A = oracle.fill_uniform(M * K, 51).reshape(M, K)
+B = oracle.fill_uniform(K * N, 52).reshape(K, N)
+with pkg.Context(1) as c:
+    C = c.sgemm(A, B)
+    st = c.stats()
+rows = np.arange(0, M, 97, dtype=np.uint32)
+R = oracle.sgemm_ref_rows(A, B, rows, N, K)
+err = oracle.sgemm_rel_err(C, R, rows, N)
+assert st.nccl_collectives >= 1, st.nccl_collectives
+assert err <= 1e-5, err
+print("ok", st.nccl_collectives, err)
+""" % root
+    env = dict(os.environ, CAFXG_NCCL_SELFTEST="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
+
+
+def _gpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs (the NCCL all-gather over NVLink)")
+def test_two_gpu_context_nccl_and_bands():
+    """A context over the first two real GPUs: sgemm row blocks with B
+    replicated by the NCCL all-gather over NVLink, and cfg3-style cyclic
+    bands of one Mandelbrot request on both devices; both against the
+    oracle."""
+    with pkg.Context(device_mask=0b11) as c:
+        assert c.device_count == 2
+        M = N = K = 4096
+        A = oracle.fill_uniform(M * K, 61).reshape(M, K)
+        B = oracle.fill_uniform(K * N, 62).reshape(K, N)
+        before = c.stats()
+        C = c.sgemm(A, B)
+        after = c.stats()
+        assert after.nccl_collectives - before.nccl_collectives == 2
+        rows = np.arange(0, M, 127, dtype=np.uint32)
+        R = oracle.sgemm_ref_rows(A, B, rows, N, K)
+        assert oracle.sgemm_rel_err(C, R, rows, N) <= 1e-5
+        d = pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 2048, 2048, 1000)
+        out = c.mandelbrot(d).reshape(2048, 2048)
+        ref = oracle.tile(-0.75, -0.73, 0.10, 0.12, 2048, 2048, 1000, fp64=False, centre=True)
+        assert np.array_equal(out, ref)
+        assert c.stats().devices_used == 0b11
