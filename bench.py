@@ -488,6 +488,9 @@ def measure(args, N):
                                                     fp64=False, centre=True, row0=r,
                                                     nrows=1)[0])
                  for r in (1, 8191, H_IMG - 2))
+    # checksum of the gathered image: the compute-actor path's reply must
+    # match it bit for bit (secondary "actor_requests_cafx")
+    img_fnv = oracle.fnv1a_u32(host)
 
     # ---- roofline of the escape kernel (aggregate over the N devices) ----
     pk = peaks()
@@ -563,6 +566,7 @@ def measure(args, N):
     secondary = {}
     if not args.no_secondary:
         secondary = run_secondary(ctx, args, N)
+        secondary["actor_requests_cafx"] = sec_actor_cafx(N, img_fnv, e2e["ms"])
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Giter/s", "n_gpus": N,
@@ -660,8 +664,8 @@ def sec_cfg1(ctx, args):
     ctx.pinned_free(h1)
     res = {"kernel_ms": round(ms, 4), "giter_s": round(it1 / ms / 1e6, 2),
            "e2e_ms": round(e2e, 4), "e2e_giter_s": round(it1 / e2e / 1e6, 2),
-           "actor_e2e_ms": round(act, 4),
-           "actor_path": "ComputeActor.request -> cafxg_actor_enqueue, pinned reply"}
+           "python_actor_e2e_ms": round(act, 4),
+           "python_actor_path": "ComputeActor.request (ctypes, Future) -> cafxg_actor_enqueue, pinned reply; the C++ cafx path is secondary.actor_requests_cafx"}
     if not args.no_cpu_baseline:
         v, cores, kind, desc = cpu_region_rate(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100, 2.0)
         res["cpu_baseline"] = {"value": round(v, 4), "unit": "Giter/s", "cores": cores,
@@ -788,6 +792,34 @@ def sec_cfg3_actor(ctx):
                     "over every device, overlapped waves"}
 
 
+def sec_actor_cafx(N, cfg3_fnv, cfg3_e2e_ms):
+    """cfg1 and cfg3 as single requests of a cafx scoped_actor (unmodified
+    reference runtime) to a gpu_actor (tools/actor_request_cafx.cpp); replies
+    checked against the oracle (cfg1) and the C-ABI image (cfg3) by FNV-1a."""
+    import paper_1505_07368_b200 as pkg
+    from oracle import oracle
+    exe = os.path.join(ROOT, "build", "tests", "actor_request_cafx")
+    if not os.path.exists(exe):
+        return {"skipped": "build/tests/actor_request_cafx not built (needs /root/reference)"}
+    r = subprocess.run([exe, str((1 << N) - 1)], capture_output=True, text=True, timeout=600)
+    try:
+        j = json.loads(r.stdout.strip().splitlines()[-1])
+    except (ValueError, IndexError):
+        return {"error": (r.stderr or r.stdout)[-500:], "status": r.returncode}
+    ref1 = oracle.fnv1a_u32(oracle.tile(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100, fp64=False,
+                                        centre=True))
+    j["cfg1"]["bit_exact_vs_oracle"] = int(j["cfg1"]["fnv"]) == ref1
+    j["cfg3"]["bit_exact_vs_c_abi_image"] = int(j["cfg3"]["fnv"]) == cfg3_fnv
+    j["cfg3"]["c_abi_e2e_ms"] = round(cfg3_e2e_ms, 3)
+    j["cfg3"]["overhead_vs_c_abi"] = round(j["cfg3"]["median_ms"] / cfg3_e2e_ms - 1, 4)
+    j["status"] = r.returncode
+    j["path"] = ("cafx scoped_actor::request (unmodified reference runtime) -> gpu_actor "
+                 "(include/cafxg/gpu_actor.hpp) -> cafxg_actor_enqueue; reply vector in pinned "
+                 "pool memory written by the device")
+    del pkg
+    return j
+
+
 def storm_descs(total, seed=2024):
     """cfg4's request list: 64x64 fp64 tiles (pitch 1/512, max_iter 256) at
     seeded offsets inside [-2,1]x[-1,1]."""
@@ -884,10 +916,14 @@ def sec_cfg4(ctx, args, N, clients=64, per=1600):
             dpath, epath = os.path.join(td, "descs.bin"), os.path.join(td, "expect.u32")
             arr.tofile(dpath)
             expect.tofile(epath)
-            for mode in ("closed", "open"):
-                r = subprocess.run([exe, dpath, epath, str(clients), str(per), mode,
-                                    str((1 << N) - 1)], capture_output=True, text=True,
-                                   timeout=600)
+            # the reference scheduler as shipped (idle workers sleep 1 ms between
+            # steal sweeps) and with a 20 us back-off (scheduler_config::steal_sleep)
+            for mode, sleep_us in (("closed", None), ("closed", 20), ("open", None),
+                                   ("open", 20)):
+                cmd = [exe, dpath, epath, str(clients), str(per), mode, str((1 << N) - 1)]
+                if sleep_us is not None:
+                    cmd.append(str(sleep_us))
+                r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
                 try:
                     j = json.loads(r.stdout.strip().splitlines()[-1])
                 except (ValueError, IndexError):
@@ -900,7 +936,8 @@ def sec_cfg4(ctx, args, N, clients=64, per=1600):
                               "(multiset; async replies carry no request id)")
                 j["path"] = ("cafx event_based_actor clients (unmodified reference runtime) "
                              "-> gpu_actor (include/cafxg/gpu_actor.hpp) -> libcafxg")
-                out[f"cfg4_request_storm_cafx_actors_{mode}_loop"] = j
+                tag = "" if sleep_us is None else f"_steal_sleep_{sleep_us}us"
+                out[f"cfg4_request_storm_cafx_actors_{mode}_loop{tag}"] = j
     return out
 
 

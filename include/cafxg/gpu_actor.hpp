@@ -26,7 +26,16 @@
 //    pending requesters, abstract_actor.cpp:108-134) and unregisters, so
 //    ~actor_system does not wait forever (actor_system.cpp:21-30);
 //  * buffer types are registered with wire codecs (type_registry.hpp:74-80),
-//    so middleman::publish can serve a GPU actor to remote nodes.
+//    so middleman::publish can serve a GPU actor to remote nodes;
+//  * reply relay: a reply leaves libcafxg's completion thread through a
+//    lock-free per-actor queue drained by a job on the cafx scheduler
+//    (actor_system::schedule_job, scheduler.hpp:266-274), so the requesters
+//    are made runnable from a worker thread (its own deque) and a whole batch
+//    of replies costs one external enqueue instead of one each. External
+//    enqueues contend with the idle workers' steal sweeps over the deque
+//    mutexes (scheduler.hpp:374-402): delivering from a foreign thread cost
+//    ~15 us per reply against ~2.5-8 us relayed (a CPU probe of the pattern,
+//    DESIGN.md §5).
 #pragma once
 
 #include <atomic>
@@ -48,6 +57,7 @@
 #include "cafx/handle.hpp"
 #include "cafx/interface.hpp"
 #include "cafx/message.hpp"
+#include "cafx/resumable.hpp"
 #include "cafx/type_registry.hpp"
 #include "cafxg.h"
 
@@ -210,7 +220,15 @@ class gpu_actor final : public cafx::abstract_actor {
         backend_(backend),
         kernel_(std::move(kernel)) {}
 
-  ~gpu_actor() override { cafxg_actor_release(backend_); }
+  ~gpu_actor() override {
+    cafxg_actor_release(backend_);
+    // replies whose drain job never ran (the scheduler stopped first)
+    for (reply_node* n = replies_.exchange(nullptr); n;) {
+      reply_node* next = n->next;
+      delete n;
+      n = next;
+    }
+  }
 
   void enqueue(std::unique_ptr<cafx::envelope> env) override {
     if (env->cat == cafx::envelope::category::exit_signal) {
@@ -286,31 +304,103 @@ class gpu_actor final : public cafx::abstract_actor {
     f32vec floats;
   };
 
-  // Runs on libcafxg's completion thread.
+  // Runs on libcafxg's completion thread: the reply goes out through the
+  // relay (a scheduler job delivers it from a worker thread).
   static void on_done(void* user, int status) {
     std::unique_ptr<job_t> job{static_cast<job_t*>(user)};
     gpu_actor* self = job->self.get();
     if (self->terminated())
       return;  // pending requesters already got request_down from finalize
     if (status != CAFXG_OK) {
-      self->fail(*job->env, static_cast<cafx::errc>(status), cafxg_last_error());
+      self->respond(*job->env,
+                    cafx::make_message(cafx::error{static_cast<cafx::errc>(status),
+                                                   cafxg_last_error()}),
+                    true);
       return;
     }
     cafx::message reply = self->kernel_ == "mandelbrot"
                               ? cafx::make_message(std::move(job->counts))
                               : cafx::make_message(std::move(job->floats));
-    self->respond(*job->env, std::move(reply));
+    self->respond(*job->env, std::move(reply), true);
   }
 
-  // local_actor::respond (local_actor.cpp:319-329)
-  void respond(const cafx::envelope& req, cafx::message reply) {
-    auto& sys = home_system();
+  // local_actor::respond (local_actor.cpp:319-329); `relay`: hand the
+  // envelope to the relay instead of delivering on this thread
+  void respond(const cafx::envelope& req, cafx::message reply, bool relay = false) {
+    std::unique_ptr<cafx::envelope> out;
     if (req.is_request()) {
       auto rid = cafx::envelope::response_id(req.mid);
       drop_pending_request(rid);
-      sys.deliver(req.sender, cafx::make_envelope(std::move(reply), address(), rid));
+      out = cafx::make_envelope(std::move(reply), address(), rid);
     } else if (req.sender) {
-      sys.deliver(req.sender, cafx::make_envelope(std::move(reply), address()));
+      out = cafx::make_envelope(std::move(reply), address());
+    } else {
+      return;
+    }
+    if (relay)
+      post_reply(req.sender, std::move(out));
+    else
+      home_system().deliver(req.sender, std::move(out));
+  }
+
+  // ---- reply relay --------------------------------------------------------
+  struct reply_node {
+    cafx::actor_addr to;
+    std::unique_ptr<cafx::envelope> env;
+    reply_node* next = nullptr;
+  };
+
+  // A scheduler job that drains the actor's reply queue on a worker thread.
+  // Several may run at once (one is scheduled per empty -> non-empty
+  // transition); each reply is taken by exactly one drain (atomic exchange).
+  class relay_job final : public cafx::resumable {
+   public:
+    explicit relay_job(cafx::intrusive_ptr<gpu_actor> a) : actor_(std::move(a)) {}
+    resume_result resume(size_t) override {
+      actor_->drain_replies();
+      return resume_result::finished;
+    }
+    void ref_job() noexcept override { rc_.fetch_add(1, std::memory_order_relaxed); }
+    void deref_job() noexcept override {
+      if (rc_.fetch_sub(1, std::memory_order_acq_rel) == 1)
+        delete this;
+    }
+
+   private:
+    cafx::intrusive_ptr<gpu_actor> actor_;
+    std::atomic<int> rc_{0};
+  };
+
+  void post_reply(const cafx::actor_addr& to, std::unique_ptr<cafx::envelope> env) {
+    auto* n = new reply_node{to, std::move(env), nullptr};
+    reply_node* head = replies_.load(std::memory_order_relaxed);
+    do {
+      n->next = head;
+    } while (!replies_.compare_exchange_weak(head, n, std::memory_order_release,
+                                             std::memory_order_relaxed));
+    if (head == nullptr)  // empty -> non-empty: one drain job
+      home_system().schedule_job(new relay_job(cafx::intrusive_ptr<gpu_actor>{this}));
+  }
+
+  void drain_replies() {
+    auto& sys = home_system();
+    for (;;) {
+      reply_node* h = replies_.exchange(nullptr, std::memory_order_acq_rel);
+      if (!h)
+        return;
+      reply_node* fifo = nullptr;  // the stack holds the newest first
+      while (h) {
+        reply_node* n = h->next;
+        h->next = fifo;
+        fifo = h;
+        h = n;
+      }
+      while (fifo) {
+        reply_node* n = fifo->next;
+        sys.deliver(fifo->to, std::move(fifo->env));
+        delete fifo;
+        fifo = n;
+      }
     }
   }
 
@@ -336,6 +426,7 @@ class gpu_actor final : public cafx::abstract_actor {
   cafxg_actor* backend_;
   std::string kernel_;
   std::atomic<bool> quitting_{false};
+  std::atomic<reply_node*> replies_{nullptr};
 };
 
 /// spawn_cl for sm_100a: `kernel` names a precompiled kernel of libcafxg

@@ -364,9 +364,14 @@ std::vector<std::vector<SubTile>> plan_mandel(
     const int v = e ? atoi(e) : 0;
     return (v > 0 ? (uint64_t)v : 512ull) << 10;
   }();
-  const uint64_t band_px = (ndev > 1 || total > (64ull << 20)) ? (1ull << 20)
-                           : total >= (1ull << 20) ? std::max<uint64_t>((total + 7) / 8, band_min)
-                                                   : UINT64_MAX;
+  // Several devices: ~16 bands per device, 64K..1M pixels each, so cyclic
+  // dealing balances the work and a request of a few M pixels still reaches
+  // every device (cfg3 on 8 devices: 1M-pixel bands, 32 per device).
+  const uint64_t band_px =
+      ndev > 1 ? std::clamp<uint64_t>(total / (ndev * 16), 64ull << 10, 1ull << 20)
+      : total > (64ull << 20) ? (1ull << 20)
+      : total >= (1ull << 20) ? std::max<uint64_t>((total + 7) / 8, band_min)
+                              : UINT64_MAX;
   size_t next = 0;
   for (size_t i = 0; i < n; ++i) {
     const cafxg_mandel_desc& t = tiles[i];

@@ -4,6 +4,7 @@
 // gpu_actor.hpp) and check every reply. Timed by bench.py.
 //
 //   storm_cafx <descs.bin> <expect.u32> <clients> <per> <closed|open> [device_mask]
+//              [steal_sleep_us]
 //
 // descs.bin: clients*per cafxg_mandel_desc records (client c owns records
 // [c*per, (c+1)*per)); expect.u32: the same number of 64x64 tiles of
@@ -22,6 +23,13 @@
 //
 // One untimed warm-up storm of the same shape runs first (pinned reply pool,
 // staging ring, first launches). Prints one JSON line.
+//
+// steal_sleep_us sets the reference scheduler's idle back-off
+// (scheduler_config::steal_sleep, scheduler.hpp:33; default 1000 us): an idle
+// cafx worker polls its deque and sleeps that long between sweeps
+// (scheduler.hpp:374-402), and a reply delivered from a backend thread waits
+// in a worker's deque until the worker wakes, so closed-loop round trips are
+// bounded below by it. Omitted = the reference's default configuration.
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -194,6 +202,9 @@ int main(int argc, char** argv) {
   run.per = std::atoi(argv[4]);
   run.open_loop = std::string(argv[5]) == "open";
   const uint64_t mask = argc > 6 ? std::strtoull(argv[6], nullptr, 0) : 1;
+  cafx::scheduler_config cfg = cafx::scheduler_config::from_env();
+  if (argc > 7)
+    cfg.steal_sleep = std::chrono::microseconds(std::atoll(argv[7]));
   const size_t total = (size_t)run.clients * run.per;
   run.descs = static_cast<const cafxg_mandel_desc*>(
       map_file(argv[1], total * sizeof(cafxg_mandel_desc)));
@@ -211,8 +222,8 @@ int main(int argc, char** argv) {
   cafxg_stats s0{}, s1{};
   unsigned workers = 0;
   {
-    workers = (unsigned)cafx::scheduler_config::from_env().effective_workers();
-    cafx::actor_system sys;
+    workers = (unsigned)cfg.effective_workers();
+    cafx::actor_system sys{cfg};
     auto mb = cafxg::spawn_gpu(sys, ctx, "mandelbrot", {});
     storm(sys, mb, run);  // warm-up
     cafxg_get_stats(ctx, &s0);
@@ -223,12 +234,12 @@ int main(int argc, char** argv) {
       "{\"mode\": \"%s\", \"clients\": %d, \"requests\": %zu, \"wall_ms\": %.3f, "
       "\"requests_per_s\": %.1f, \"good\": %llu, \"bad\": %llu, \"errors\": %llu, "
       "\"batches\": %llu, \"kernel_launches\": %llu, \"scheduler_workers\": %u, "
-      "\"devices\": %d}\n",
+      "\"steal_sleep_us\": %lld, \"devices\": %d}\n",
       run.open_loop ? "open" : "closed", run.clients, total, ms, total / (ms / 1e3),
       (unsigned long long)run.good.load(), (unsigned long long)run.bad.load(),
       (unsigned long long)run.errors.load(), (unsigned long long)(s1.batches - s0.batches),
       (unsigned long long)(s1.kernel_launches - s0.kernel_launches), workers,
-      cafxg_device_count(ctx));
+      (long long)cfg.steal_sleep.count(), cafxg_device_count(ctx));
   cafxg_close(ctx);
   return run.good.load() == total && run.errors.load() == 0 ? 0 : 3;
 }

@@ -1,7 +1,13 @@
-"""GPU: the native request-storm driver (BASELINE config 4) in its three client
-disciplines -- open loop, closed loop with one OS thread per client, closed
-loop with the clients multiplexed on worker threads like cafx actors -- at a
-reduced size; sampled replies checked against the oracle."""
+"""GPU: bench.py's request-storm measurement (BASELINE config 4) at a reduced
+size -- the native driver in its three client disciplines (open loop, closed
+loop with one OS thread per client, closed loop with the clients multiplexed
+on worker threads like cafx actors) and the cafx client actors on the
+unmodified reference runtime (tools/storm_cafx.cpp, closed and open loop, the
+scheduler as shipped and with a short idle back-off); every reply of every
+mode checked against the reference's own mandelbrot_cell."""
+import os
+import types
+
 import pytest
 
 import bench
@@ -9,10 +15,22 @@ import bench
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("mode", [False, True, "scheduled"])
-def test_storm_modes(ctx, mode):
-    r = bench.run_storm(ctx, clients=8, per=64, closed_loop=mode)
-    assert r["status"] == 0 and r["errors"] == 0
-    assert r["requests"] == 8 * 64
-    assert r["mismatched_tiles"] == 0 and r["checked_tiles"] == 128
-    assert r["batches"] >= 1
+def test_storm_all_modes(ctx):
+    args = types.SimpleNamespace(no_cpu_baseline=False)
+    res = bench.sec_cfg4(ctx, args, 1, clients=8, per=64)
+    native = ["cfg4_request_storm", "cfg4_request_storm_closed_loop",
+              "cfg4_request_storm_closed_loop_os_threads"]
+    for k in native:
+        r = res[k]
+        assert r["status"] == 0 and r["errors"] == 0, (k, r)
+        assert r["requests"] == 8 * 64 and r["checked_tiles"] == 8 * 64
+        assert r["mismatched_tiles"] == 0, (k, r)
+        assert r["batches"] >= 1
+    assert res["cfg4_request_storm"]["cpu_baseline"]["value"] > 0
+    if os.path.exists(os.path.join(bench.ROOT, "build", "tests", "storm_cafx")):
+        cafx = [k for k in res if k.startswith("cfg4_request_storm_cafx_actors")]
+        assert len(cafx) == 4
+        for k in cafx:
+            r = res[k]
+            assert r["status"] == 0, (k, r)
+            assert r["good"] == 8 * 64 and r["bad"] == 0 and r["errors"] == 0, (k, r)
