@@ -1,5 +1,6 @@
-"""Device-API 3xTF32 sgemm timing (CUDA events on the launching stream, split +
-GEMM launches), n^3 for each n given; median and min of 10 after 3 warm-ups.
+"""Device-API 3xTF32 sgemm timing (CUDA events on the launching stream; one
+fused launch per GEMM), n^3 for each n given; median and min of 10 after 3
+warm-ups, plus a sampled-row error check.
     python paper_1505_07368_b200/tools/sgemm_time.py 1024 16384
 """
 import json
@@ -7,15 +8,20 @@ import os
 import statistics
 import sys
 
+import numpy as np
 import torch
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", ".."))
 import paper_1505_07368_b200 as pkg  # noqa: E402
+from oracle import oracle  # noqa: E402
 
 with pkg.Context(1) as ctx:
     for n in [int(x) for x in sys.argv[1:]] or [1024]:
-        A = torch.rand(n, n, device="cuda")
-        B = torch.rand(n, n, device="cuda")
+        A_h = oracle.fill_uniform(n * n, 1).reshape(n, n)
+        B_h = oracle.fill_uniform(n * n, 2).reshape(n, n)
+        A, B = torch.from_numpy(A_h).cuda(), torch.from_numpy(B_h).cuda()
+        if os.environ.get("TRANSPOSE_B"):  # experiments: B handed over as B^T (K-major)
+            B = B.t().contiguous()
         C = torch.empty(n, n, device="cuda")
         s = torch.cuda.Stream()
         ts = []
@@ -29,8 +35,12 @@ with pkg.Context(1) as ctx:
             torch.cuda.synchronize()
             if k >= 3:
                 ts.append(a.elapsed_time(b))
-        print(json.dumps({"n": n, "pdl": os.environ.get("CAFXG_SGEMM_PDL", "1"),
+        rows = np.arange(0, n, max(1, n // 16), dtype=np.uint32)
+        R = oracle.sgemm_ref_rows(A_h, B_h, rows, n, n)
+        err = oracle.sgemm_rel_err(C.cpu().numpy(), R, rows, n)
+        print(json.dumps({"n": n, "bn": os.environ.get("CAFXG_SGEMM_BN", "auto"),
                           "median_ms": round(statistics.median(ts), 4),
                           "min_ms": round(min(ts), 4),
-                          "tflops_median": round(2 * n ** 3 / statistics.median(ts) / 1e9, 1)}))
+                          "tflops_median": round(2 * n ** 3 / statistics.median(ts) / 1e9, 1),
+                          "err": err}), flush=True)
         del A, B, C

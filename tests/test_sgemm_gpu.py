@@ -131,6 +131,40 @@ def test_sgemm_2d_wavefront_host_request(ctx, M, N, K, pad):
         assert np.isnan(Cbig[:, N:]).all()
 
 
+@pytest.mark.parametrize("M,N,K,pad", [(256, 512, 512, 4), (384, 256, 288, 8)])
+def test_sgemm_3xtf32_leading_dims(ctx, M, N, K, pad):
+    """The tensor-core path with the caller's row pitches: padded lda / ldb /
+    ldc (16-byte multiples); the padding of C is never written."""
+    Abig = oracle.fill_uniform(M * (K + pad), 13).reshape(M, K + pad)
+    Bbig = oracle.fill_uniform(K * (N + pad), 14).reshape(K, N + pad)
+    A, B = Abig[:, :K], Bbig[:, :N]
+    Cbig = np.full((M, N + pad), np.nan, dtype=np.float32)
+    C = Cbig[:, :N]
+    ctx.sgemm(A, B, C, mode=pkg.SGEMM_3XTF32)
+    assert not np.isnan(C).any()
+    assert check(np.ascontiguousarray(A), np.ascontiguousarray(B), C) <= TOL
+    assert np.isnan(Cbig[:, N:]).all()
+
+
+def test_sgemm_3xtf32_k16384(ctx):
+    """cfg5's depth: K = 16384 (the deepest accumulation; the tensor core's
+    truncating accumulation is bounded by 128-K chunk sums), a 1024 x 256 C
+    block, 64 sampled rows against the fp64-accumulated check."""
+    import torch
+    M, N, K = 1024, 256, 16384
+    A_h = oracle.fill_uniform(M * K, 71).reshape(M, K)
+    B_h = oracle.fill_uniform(K * N, 72).reshape(K, N)
+    A, B = torch.from_numpy(A_h).cuda(), torch.from_numpy(B_h).cuda()
+    C = torch.empty(M, N, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    ctx.sgemm_device(M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream,
+                     mode=pkg.SGEMM_3XTF32)
+    torch.cuda.synchronize()
+    err = check(A_h, B_h, C.cpu().numpy(), nrows=64, seed=3)
+    assert err <= TOL, err
+
+
 def test_sgemm_3xtf32_rejects_unsupported_shape(ctx):
     A = np.zeros((100, 64), np.float32)
     B = np.zeros((64, 256), np.float32)
