@@ -153,7 +153,7 @@ typedef struct {
   uint32_t M, N, K;
   uint32_t lda, ldb, ldc; /* 0 = packed (K, N, N) */
   uint32_t mode;          /* CAFXG_SGEMM_* */
-  uint32_t reserved;
+  uint32_t splits;        /* 3xTF32 split-K cluster size 1/2/4/8; 0 = chosen per shape */
 } cafxg_sgemm_desc;
 
 /* Host-to-host request. With >1 device, A is split into row blocks per
@@ -187,6 +187,39 @@ int cafxg_sgemm_device(cafxg_ctx* ctx, int device, const cafxg_sgemm_desc* d,
  * local_actor.cpp:319-329). */
 int cafxg_spawn(cafxg_ctx* ctx, const char* kernel_name, const uint64_t* dims,
                 size_t ndims, cafxg_actor** out);
+
+/* The kernel's signature normalised the way spawn_cl takes it (PAPER.md:
+ * 357-361: a result type instead of the trailing output parameter), as text:
+ *   "matrix_multiply" -> "f32*(f32*,f32*)"    spawn_cl<float*(float*,float*)>
+ *   "mandelbrot"      -> "u32*(mandel_desc*)" spawn_cl<uint32_t*(cafxg_mandel_desc*)>
+ * (f32 = float, u32 = uint32_t, mandel_desc = cafxg_mandel_desc). Writes it
+ * NUL-terminated into buf (cap bytes); CAFXG_E_UNKNOWN_TYPE for unknown
+ * kernels, CAFXG_E_OUT_OF_RANGE if cap is too small. */
+int cafxg_kernel_signature(const char* kernel_name, char* buf, size_t cap);
+
+/* spawn_cl's tuning overload: launch-shape hints stored with the actor and
+ * applied to every request it serves (the OpenCL nd_range / work-group
+ * arguments have no meaning for these kernels; these are their knobs).
+ * Zero fields keep the backend's choice. */
+typedef struct {
+  uint32_t block_steps;  /* mandelbrot: escape-test interval of the deferred
+                            kernel, 16..64 and a multiple of 8 (steps run
+                            unchecked between tests); 0 = cost model */
+  uint32_t max_ctas;     /* mandelbrot: cap on the CTAs of a launch (shares
+                            the GPU with other work); 0 = every SM at full
+                            occupancy */
+  uint32_t sgemm_mode;   /* matrix_multiply: CAFXG_SGEMM_* */
+  uint32_t sgemm_splits; /* matrix_multiply: split-K cluster size 1/2/4/8 */
+  uint32_t reserved[4];  /* must be 0 */
+} cafxg_tuning;
+
+/* cafxg_spawn with the spawn_cl template signature checked against the
+ * kernel's (`signature` may be NULL: unchecked; a mismatch fails with
+ * CAFXG_E_INTERFACE_MISMATCH before any actor exists) and optional tuning
+ * (NULL = defaults; out-of-range values fail with CAFXG_E_CONFIG). */
+int cafxg_spawn_ex(cafxg_ctx* ctx, const char* kernel_name, const char* signature,
+                   const uint64_t* dims, size_t ndims, const cafxg_tuning* tuning,
+                   cafxg_actor** out);
 /* Enqueues one request. in[i]/in_bytes[i] are the request's input buffers;
  * the reply is written to out/out_bytes before `done(user, status)` runs.
  * Buffers must stay valid until then. Size checks happen here (returning the

@@ -12,6 +12,20 @@
 //   auto mb = cafxg::spawn_gpu(sys, ctx, "mandelbrot", {});
 //   //    request (cafxg::mandel_tiles) -> reply u32vec
 //
+// and the spawn_cl surface itself:
+//   auto mm = cafxg::spawn_cl<float*(float*, float*)>(sys, ctx, "matrix_multiply",
+//                                                     {size, size});
+//   //    typed handle (f32vec, f32vec) -> (f32vec); the template signature is
+//   //    checked against the kernel's (cafxg_kernel_signature)
+//   cafxg::spawn_cl<uint32_t*(cafxg_mandel_desc*)>(sys, ctx, "mandelbrot", {},
+//                                                  cafxg::tuning().block_steps(40));
+//   //    tuning overload: launch-shape hints for every request
+//   cafxg::spawn_cl<uint32_t*(cafxg_mandel_desc*)>(sys, ctx, "mandelbrot", {},
+//       cafx::behavior{[](uint32_t size, uint32_t it) { return mandel_tiles{...}; }},
+//       cafx::behavior{[](const u32vec& counts) { return checksum(counts); }});
+//   //    data-transformation overload: the actor's interface is
+//   //    (uint32, uint32) -> (uint64), the kernel signature stays hidden
+//
 // What it implements, against the reference runtime:
 //  * `enqueue` (abstract_actor.hpp:36) may be called from any thread; it
 //    decodes the request and hands it to cafxg_actor_enqueue (never blocks on
@@ -51,6 +65,7 @@
 
 #include "cafx/abstract_actor.hpp"
 #include "cafx/actor_system.hpp"
+#include "cafx/behavior.hpp"
 #include "cafx/detail/wire.hpp"
 #include "cafx/envelope.hpp"
 #include "cafx/error.hpp"
@@ -211,14 +226,22 @@ inline void register_types(cafx::type_registry& reg = cafx::type_registry::globa
     reg.add<mandel_tiles>("cafxg.mandel_tiles", codec::enc_tiles, codec::dec_tiles);
 }
 
-/// A cafx actor whose behaviour is one sm_100a kernel.
+/// A cafx actor whose behaviour is one sm_100a kernel, optionally behind a
+/// data transformation (spawn_cl's transformation overload): `map_args`
+/// turns a request into the kernel's input message, `map_result` turns the
+/// kernel's output into the reply. Both are ordinary cafx behaviors, so the
+/// transformation is written in the reference's own pattern DSL and its
+/// interface derived from it (derive_interface, behavior.hpp:528-532).
 class gpu_actor final : public cafx::abstract_actor {
  public:
-  gpu_actor(cafx::actor_system& sys, cafxg_ctx* ctx, cafxg_actor* backend, std::string kernel)
+  gpu_actor(cafx::actor_system& sys, cafxg_ctx* ctx, cafxg_actor* backend, std::string kernel,
+            cafx::behavior map_args = {}, cafx::behavior map_result = {})
       : cafx::abstract_actor(&sys, cafx::actor_addr{sys.node(), sys.next_actor_id()}),
         ctx_(ctx),
         backend_(backend),
-        kernel_(std::move(kernel)) {}
+        kernel_(std::move(kernel)),
+        map_args_(std::move(map_args)),
+        map_result_(std::move(map_result)) {}
 
   ~gpu_actor() override {
     cafxg_actor_release(backend_);
@@ -241,7 +264,23 @@ class gpu_actor final : public cafx::abstract_actor {
     }
     auto job = std::make_unique<job_t>();
     job->self = cafx::intrusive_ptr<gpu_actor>{this};
-    const cafx::message& msg = env->content;
+    // the kernel's input message: the request itself, or what map_args makes
+    // of it (kept in the job: the buffers handed to the backend live in it)
+    job->input = env->content;
+    if (map_args_.defined()) {
+      cafx::message req = env->content;
+      cafx::match_outcome out;
+      try {
+        out = cafx::match(map_args_, req);
+      } catch (const cafx::failure& f) {
+        return fail(*env, f.code(), f.what());
+      }
+      if (!out.matched || !out.response)
+        return fail(*env, cafx::errc::type_mismatch,
+                    "request matches no case of the compute actor's data transformation");
+      job->input = std::move(*out.response);
+    }
+    const cafx::message& msg = job->input;
     const void* in[2] = {nullptr, nullptr};
     size_t in_bytes[2] = {0, 0};
     size_t n_in = 0;
@@ -300,12 +339,14 @@ class gpu_actor final : public cafx::abstract_actor {
   struct job_t {
     cafx::intrusive_ptr<gpu_actor> self;
     std::unique_ptr<cafx::envelope> env;
+    cafx::message input;
     u32vec counts;
     f32vec floats;
   };
 
   // Runs on libcafxg's completion thread: the reply goes out through the
-  // relay (a scheduler job delivers it from a worker thread).
+  // relay (a scheduler job delivers it -- and applies map_result -- on a
+  // worker thread).
   static void on_done(void* user, int status) {
     std::unique_ptr<job_t> job{static_cast<job_t*>(user)};
     gpu_actor* self = job->self.get();
@@ -315,39 +356,46 @@ class gpu_actor final : public cafx::abstract_actor {
       self->respond(*job->env,
                     cafx::make_message(cafx::error{static_cast<cafx::errc>(status),
                                                    cafxg_last_error()}),
-                    true);
+                    true, false);
       return;
     }
     cafx::message reply = self->kernel_ == "mandelbrot"
                               ? cafx::make_message(std::move(job->counts))
                               : cafx::make_message(std::move(job->floats));
-    self->respond(*job->env, std::move(reply), true);
+    self->respond(*job->env, std::move(reply), true, self->map_result_.defined());
   }
 
-  // local_actor::respond (local_actor.cpp:319-329); `relay`: hand the
-  // envelope to the relay instead of delivering on this thread
-  void respond(const cafx::envelope& req, cafx::message reply, bool relay = false) {
-    std::unique_ptr<cafx::envelope> out;
+  // local_actor::respond (local_actor.cpp:319-329). `relay`: hand the reply
+  // to the relay instead of delivering on this thread; `post`: the relay
+  // passes it through map_result first.
+  void respond(const cafx::envelope& req, cafx::message reply, bool relay = false,
+               bool post = false) {
+    uint64_t rid = 0;
     if (req.is_request()) {
-      auto rid = cafx::envelope::response_id(req.mid);
+      rid = cafx::envelope::response_id(req.mid);
       drop_pending_request(rid);
-      out = cafx::make_envelope(std::move(reply), address(), rid);
-    } else if (req.sender) {
-      out = cafx::make_envelope(std::move(reply), address());
-    } else {
+    } else if (!req.sender) {
       return;
     }
-    if (relay)
-      post_reply(req.sender, std::move(out));
-    else
-      home_system().deliver(req.sender, std::move(out));
+    if (relay) {
+      post_reply(new reply_node{req.sender, rid, std::move(reply), post, nullptr});
+      return;
+    }
+    home_system().deliver(req.sender, rid ? cafx::make_envelope(std::move(reply), address(), rid)
+                                          : cafx::make_envelope(std::move(reply), address()));
+  }
+
+  void fail(const cafx::envelope& req, cafx::errc code, const std::string& what) {
+    respond(req, cafx::make_message(cafx::error{code, what}));
   }
 
   // ---- reply relay --------------------------------------------------------
   struct reply_node {
     cafx::actor_addr to;
-    std::unique_ptr<cafx::envelope> env;
-    reply_node* next = nullptr;
+    uint64_t rid;          // response id, 0 for an async reply
+    cafx::message msg;
+    bool post;             // apply map_result before delivery
+    reply_node* next;
   };
 
   // A scheduler job that drains the actor's reply queue on a worker thread.
@@ -371,8 +419,7 @@ class gpu_actor final : public cafx::abstract_actor {
     std::atomic<int> rc_{0};
   };
 
-  void post_reply(const cafx::actor_addr& to, std::unique_ptr<cafx::envelope> env) {
-    auto* n = new reply_node{to, std::move(env), nullptr};
+  void post_reply(reply_node* n) {
     reply_node* head = replies_.load(std::memory_order_relaxed);
     do {
       n->next = head;
@@ -380,6 +427,19 @@ class gpu_actor final : public cafx::abstract_actor {
                                              std::memory_order_relaxed));
     if (head == nullptr)  // empty -> non-empty: one drain job
       home_system().schedule_job(new relay_job(cafx::intrusive_ptr<gpu_actor>{this}));
+  }
+
+  // map_result of a kernel reply; a reply it does not match becomes an error
+  cafx::message transform_result(cafx::message m) {
+    try {
+      auto out = cafx::match(map_result_, m);
+      if (out.matched && out.response)
+        return std::move(*out.response);
+      return cafx::make_message(cafx::error{cafx::errc::type_mismatch,
+                                            "kernel result matches no case of map_result"});
+    } catch (const cafx::failure& f) {
+      return cafx::make_message(cafx::error{f.code(), f.what()});
+    }
   }
 
   void drain_replies() {
@@ -397,15 +457,14 @@ class gpu_actor final : public cafx::abstract_actor {
       }
       while (fifo) {
         reply_node* n = fifo->next;
-        sys.deliver(fifo->to, std::move(fifo->env));
+        cafx::message m = fifo->post ? transform_result(std::move(fifo->msg))
+                                     : std::move(fifo->msg);
+        sys.deliver(fifo->to, fifo->rid ? cafx::make_envelope(std::move(m), address(), fifo->rid)
+                                        : cafx::make_envelope(std::move(m), address()));
         delete fifo;
         fifo = n;
       }
     }
-  }
-
-  void fail(const cafx::envelope& req, cafx::errc code, const std::string& what) {
-    respond(req, cafx::make_message(cafx::error{code, what}));
   }
 
   void on_exit(const cafx::envelope& env) {
@@ -425,9 +484,84 @@ class gpu_actor final : public cafx::abstract_actor {
   cafxg_ctx* ctx_;
   cafxg_actor* backend_;
   std::string kernel_;
+  cafx::behavior map_args_, map_result_;
   std::atomic<bool> quitting_{false};
   std::atomic<reply_node*> replies_{nullptr};
 };
+
+// ---- spawn_cl ----------------------------------------------------------------
+
+/// Element type of a kernel buffer parameter -> the message payload type that
+/// carries it and its token in the normalised signature text.
+template <class T>
+struct buffer_traits;
+template <>
+struct buffer_traits<float> {
+  using type = f32vec;
+  static constexpr const char* token = "f32*";
+};
+template <>
+struct buffer_traits<uint32_t> {
+  using type = u32vec;
+  static constexpr const char* token = "u32*";
+};
+template <>
+struct buffer_traits<cafxg_mandel_desc> {
+  using type = mandel_tiles;
+  static constexpr const char* token = "mandel_desc*";
+};
+
+/// spawn_cl's template argument `Out*(In*...)`: the
+/// kernel signature normalised to a result type instead of the trailing
+/// output parameter.
+template <class Sig>
+struct kernel_sig;
+template <class R, class... Ts>
+struct kernel_sig<R*(Ts*...)> {
+  static std::string text() {
+    std::string s = std::string(buffer_traits<std::remove_cv_t<R>>::token) + "(";
+    bool first = true;
+    ((s += (first ? "" : ","), s += buffer_traits<std::remove_cv_t<Ts>>::token, first = false),
+     ...);
+    return s + ")";
+  }
+  // the typed rule (In buffers...) -> (Out buffer)
+  static cafx::rule rule(const cafx::type_registry& reg) {
+    cafx::rule r;
+    r.inputs = {cafx::type_spec::of(reg.id_of<typename buffer_traits<std::remove_cv_t<Ts>>::type>())...};
+    r.outputs = {cafx::type_spec::of(reg.id_of<typename buffer_traits<std::remove_cv_t<R>>::type>())};
+    return r;
+  }
+  // payload types of the kernel input message / of the kernel output
+  static std::vector<cafx::type_spec> input_specs(const cafx::type_registry& reg) {
+    return rule(reg).inputs;
+  }
+};
+
+namespace detail {
+
+inline cafxg_actor* spawn_backend(cafxg_ctx* ctx, const std::string& kernel, const char* sig,
+                                  std::initializer_list<uint64_t> dims,
+                                  const cafxg_tuning* tuning) {
+  register_types();
+  std::vector<uint64_t> d(dims);
+  cafxg_actor* h = nullptr;
+  int s = cafxg_spawn_ex(ctx, kernel.c_str(), sig, d.data(), d.size(), tuning, &h);
+  if (s != CAFXG_OK)
+    throw cafx::failure{static_cast<cafx::errc>(s), cafxg_last_error()};
+  return h;
+}
+
+inline cafx::actor make_handle(cafx::actor_system& sys, cafxg_ctx* ctx, cafxg_actor* h,
+                               const std::string& kernel, cafx::behavior map_args = {},
+                               cafx::behavior map_result = {}) {
+  auto ptr = cafx::make_counted<gpu_actor>(sys, ctx, h, kernel, std::move(map_args),
+                                           std::move(map_result));
+  sys.register_actor(cafx::abstract_actor_ptr{ptr.get()});
+  return cafx::actor{cafx::abstract_actor_ptr{ptr.get()}};
+}
+
+}  // namespace detail
 
 /// spawn_cl for sm_100a: `kernel` names a precompiled kernel of libcafxg
 /// ("mandelbrot", "matrix_multiply"); `dims` are the spawn_cl dimensions.
@@ -435,15 +569,8 @@ class gpu_actor final : public cafx::abstract_actor {
 inline cafx::actor spawn_gpu(cafx::actor_system& sys, cafxg_ctx* ctx,
                              const std::string& kernel,
                              std::initializer_list<uint64_t> dims) {
-  register_types();
-  std::vector<uint64_t> d(dims);
-  cafxg_actor* h = nullptr;
-  int s = cafxg_spawn(ctx, kernel.c_str(), d.data(), d.size(), &h);
-  if (s != CAFXG_OK)
-    throw cafx::failure{static_cast<cafx::errc>(s), cafxg_last_error()};
-  auto ptr = cafx::make_counted<gpu_actor>(sys, ctx, h, kernel);
-  sys.register_actor(cafx::abstract_actor_ptr{ptr.get()});
-  return cafx::actor{cafx::abstract_actor_ptr{ptr.get()}};
+  cafxg_actor* h = detail::spawn_backend(ctx, kernel, nullptr, dims, nullptr);
+  return detail::make_handle(sys, ctx, h, kernel);
 }
 
 /// Typed variant: one rule (inputs) -> (output), checked by typed sends
@@ -464,6 +591,79 @@ inline cafx::typed_actor spawn_gpu_typed(cafx::actor_system& sys, cafxg_ctx* ctx
   }
   return cafx::typed_actor{cafx::abstract_actor_ptr{h.ptr()},
                            cafx::messaging_interface{r}};
+}
+
+/// spawn_cl's tuning overload: launch-shape hints for every request of the
+/// actor (include/cafxg.h, cafxg_tuning). Zero fields keep the defaults.
+struct tuning : cafxg_tuning {
+  tuning() : cafxg_tuning{} {}
+  tuning& block_steps(uint32_t v) { cafxg_tuning::block_steps = v; return *this; }
+  tuning& max_ctas(uint32_t v) { cafxg_tuning::max_ctas = v; return *this; }
+  tuning& sgemm_mode(uint32_t v) { cafxg_tuning::sgemm_mode = v; return *this; }
+  tuning& sgemm_splits(uint32_t v) { cafxg_tuning::sgemm_splits = v; return *this; }
+};
+
+/// spawn_cl<Out*(In*...)>(sys, ctx, kernel, dims[, tuning]) -- PAPER.md:
+/// 357-361 with the OpenCL source replaced by a precompiled sm_100a kernel.
+/// The template signature is checked against the kernel's registered one
+/// (cafxg_kernel_signature) before anything is spawned: a mismatch throws
+/// failure{interface_mismatch}. Returns a typed handle whose one rule is
+/// (In buffers...) -> (Out buffer), e.g. spawn_cl<float*(float*, float*)>
+/// -> (f32vec, f32vec) -> (f32vec).
+template <class Sig>
+cafx::typed_actor spawn_cl(cafx::actor_system& sys, cafxg_ctx* ctx, const std::string& kernel,
+                           std::initializer_list<uint64_t> dims, const tuning& t = tuning{}) {
+  register_types();
+  const std::string sig = kernel_sig<Sig>::text();
+  cafxg_actor* h = detail::spawn_backend(ctx, kernel, sig.c_str(), dims, &t);
+  auto a = detail::make_handle(sys, ctx, h, kernel);
+  return cafx::typed_actor{cafx::abstract_actor_ptr{a.ptr()},
+                           cafx::messaging_interface{
+                               kernel_sig<Sig>::rule(cafx::type_registry::global())}};
+}
+
+/// spawn_cl's data-transformation overload: the actor shows other actors an
+/// interface of its own instead of the kernel signature. `map_args` maps a
+/// request to the kernel's input message (each of its cases must produce
+/// exactly Sig's input buffers), `map_result` maps the kernel's output buffer
+/// to the reply (its one case takes Sig's output buffer). The typed handle's
+/// rules are map_args' inputs -> map_result's outputs; a request matching no
+/// case of map_args is answered with error{type_mismatch}. Both behaviors
+/// must be typable (no catch-all), else failure{interface_mismatch}.
+template <class Sig>
+cafx::typed_actor spawn_cl(cafx::actor_system& sys, cafxg_ctx* ctx, const std::string& kernel,
+                           std::initializer_list<uint64_t> dims, cafx::behavior map_args,
+                           cafx::behavior map_result, const tuning& t = tuning{}) {
+  register_types();
+  auto& reg = cafx::type_registry::global();
+  const cafx::rule krule = kernel_sig<Sig>::rule(reg);
+  auto in_if = cafx::derive_interface(map_args);
+  auto out_if = cafx::derive_interface(map_result);
+  if (!in_if || !out_if || in_if->empty() || out_if->size() != 1)
+    throw cafx::failure{cafx::errc::interface_mismatch,
+                        "spawn_cl: map_args / map_result must be typable behaviors "
+                        "(map_result with exactly one case)"};
+  const cafx::rule& post = out_if->rules().front();
+  if (post.inputs != krule.outputs)
+    throw cafx::failure{cafx::errc::interface_mismatch,
+                        "spawn_cl: map_result must take the kernel's output " +
+                            kernel_sig<Sig>::text()};
+  std::vector<cafx::rule> rules;
+  for (const cafx::rule& pre : in_if->rules()) {
+    if (pre.outputs != krule.inputs)
+      throw cafx::failure{cafx::errc::interface_mismatch,
+                          "spawn_cl: every map_args case must produce the kernel's inputs " +
+                              kernel_sig<Sig>::text() + ", got " + cafx::to_string(pre)};
+    cafx::rule r;
+    r.inputs = pre.inputs;
+    r.outputs = post.outputs;
+    rules.push_back(std::move(r));
+  }
+  const std::string sig = kernel_sig<Sig>::text();
+  cafxg_actor* h = detail::spawn_backend(ctx, kernel, sig.c_str(), dims, &t);
+  auto a = detail::make_handle(sys, ctx, h, kernel, std::move(map_args), std::move(map_result));
+  return cafx::typed_actor{cafx::abstract_actor_ptr{a.ptr()},
+                           cafx::messaging_interface{std::move(rules)}};
 }
 
 }  // namespace cafxg

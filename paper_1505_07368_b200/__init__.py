@@ -6,12 +6,12 @@ the ctypes binding (``cafxg``) used by the tests and bench.py.
 """
 from .cafxg import (  # noqa: F401
     CENTRE, CORNER, FP32, FP64, SGEMM_3XTF32, SGEMM_AUTO, SGEMM_FFMA,
-    CafxgError, ComputeActor, Context, MandelDesc, SgemmDesc, lib, mandel_desc,
-    reference_desc, tile_pixels,
+    CafxgError, ComputeActor, Context, MandelDesc, SgemmDesc, Tuning, kernel_signature, lib,
+    mandel_desc, reference_desc, tile_pixels,
 )
 
 __all__ = [
     "CENTRE", "CORNER", "FP32", "FP64", "SGEMM_3XTF32", "SGEMM_AUTO", "SGEMM_FFMA",
-    "CafxgError", "ComputeActor", "Context", "MandelDesc", "SgemmDesc", "lib",
-    "mandel_desc", "reference_desc", "tile_pixels",
+    "CafxgError", "ComputeActor", "Context", "MandelDesc", "SgemmDesc", "Tuning",
+    "kernel_signature", "lib", "mandel_desc", "reference_desc", "tile_pixels",
 ]

@@ -39,7 +39,8 @@ EXPORTS = [
     "cafxg_mandelbrot_submit", "cafxg_mandelbrot", "cafxg_mandelbrot_device",
     "cafxg_fnv1a_u32_device", "cafxg_run_mandelbrot",
     "cafxg_sgemm_submit", "cafxg_sgemm", "cafxg_sgemm_device",
-    "cafxg_spawn", "cafxg_actor_enqueue", "cafxg_actor_reply_bytes",
+    "cafxg_spawn", "cafxg_spawn_ex", "cafxg_kernel_signature",
+    "cafxg_actor_enqueue", "cafxg_actor_reply_bytes",
     "cafxg_actor_quit", "cafxg_actor_release", "cafxg_get_stats",
 ]
 
@@ -66,7 +67,15 @@ class MandelDesc(C.Structure):
 class SgemmDesc(C.Structure):
     _fields_ = [("M", C.c_uint32), ("N", C.c_uint32), ("K", C.c_uint32),
                 ("lda", C.c_uint32), ("ldb", C.c_uint32), ("ldc", C.c_uint32),
-                ("mode", C.c_uint32), ("reserved", C.c_uint32)]
+                ("mode", C.c_uint32), ("splits", C.c_uint32)]
+
+
+class Tuning(C.Structure):
+    """spawn_cl's tuning overload (cafxg_tuning): zero fields keep the
+    backend's choice."""
+    _fields_ = [("block_steps", C.c_uint32), ("max_ctas", C.c_uint32),
+                ("sgemm_mode", C.c_uint32), ("sgemm_splits", C.c_uint32),
+                ("reserved", C.c_uint32 * 4)]
 
 
 class Stats(C.Structure):
@@ -112,6 +121,9 @@ def lib() -> C.CDLL:
         L.cafxg_sgemm.argtypes = [vp, C.POINTER(SgemmDesc), vp, vp, vp]
         L.cafxg_sgemm_device.argtypes = [vp, i, C.POINTER(SgemmDesc), vp, vp, vp, vp]
         L.cafxg_spawn.argtypes = [vp, C.c_char_p, C.POINTER(u64), sz, C.POINTER(vp)]
+        L.cafxg_spawn_ex.argtypes = [vp, C.c_char_p, C.c_char_p, C.POINTER(u64), sz,
+                                     C.POINTER(Tuning), C.POINTER(vp)]
+        L.cafxg_kernel_signature.argtypes = [C.c_char_p, C.c_char_p, sz]
         L.cafxg_actor_enqueue.argtypes = [vp, C.POINTER(vp), C.POINTER(sz), sz, vp, sz,
                                           DONE_FN, vp]
         L.cafxg_actor_reply_bytes.restype = sz
@@ -142,6 +154,13 @@ def mandel_desc(x0, x1, y0, y1, width, height, max_iter, fp64=False, centre=True
                       height - row0 if nrows is None else nrows, col0,
                       width - col0 if ncols is None else ncols, max_iter,
                       FP64 if fp64 else FP32, CENTRE if centre else CORNER, 0, out_offset)
+
+
+def kernel_signature(kernel: str) -> str:
+    """The kernel's normalised spawn_cl signature, e.g. "f32*(f32*,f32*)"."""
+    buf = C.create_string_buffer(128)
+    _check(lib().cafxg_kernel_signature(kernel.encode(), buf, 128), "kernel_signature")
+    return buf.value.decode()
 
 
 def reference_desc(size: int, max_iter: int) -> MandelDesc:
@@ -341,27 +360,34 @@ class Context:
 
     # -- sgemm
     def sgemm(self, A: np.ndarray, B: np.ndarray, C_: np.ndarray | None = None,
-              mode: int = SGEMM_AUTO) -> np.ndarray:
+              mode: int = SGEMM_AUTO, splits: int = 0) -> np.ndarray:
         M, K = A.shape
         K2, N = B.shape
         assert K == K2
         if C_ is None:
             C_ = np.empty((M, N), dtype=np.float32)
-        d = SgemmDesc(M, N, K, A.strides[0] // 4, B.strides[0] // 4, C_.strides[0] // 4, mode, 0)
+        d = SgemmDesc(M, N, K, A.strides[0] // 4, B.strides[0] // 4, C_.strides[0] // 4, mode,
+                      splits)
         _check(lib().cafxg_sgemm(self.handle, C.byref(d), A.ctypes.data, B.ctypes.data,
                                  C_.ctypes.data), "sgemm")
         return C_
 
     def sgemm_device(self, M, N, K, dA, dB, dC, stream=0, mode=SGEMM_AUTO, device=0,
-                     lda=0, ldb=0, ldc=0) -> None:
-        d = SgemmDesc(M, N, K, lda, ldb, ldc, mode, 0)
+                     lda=0, ldb=0, ldc=0, splits=0) -> None:
+        d = SgemmDesc(M, N, K, lda, ldb, ldc, mode, splits)
         _check(lib().cafxg_sgemm_device(self.handle, device, C.byref(d), dA, dB, dC,
                                         stream or None), "sgemm_device")
 
     # -- spawn_cl facade
-    def spawn(self, kernel: str, dims=()) -> ComputeActor:
+    def spawn(self, kernel: str, dims=(), signature: str | None = None,
+              tuning: Tuning | None = None) -> ComputeActor:
+        """spawn_cl: `signature` (e.g. "f32*(f32*,f32*)") is checked against
+        the kernel's; `tuning` holds launch-shape hints for its requests."""
         n = len(dims)
         d = (C.c_uint64 * max(n, 1))(*dims)
         h = C.c_void_p()
-        _check(lib().cafxg_spawn(self.handle, kernel.encode(), d, n, C.byref(h)), "spawn")
+        _check(lib().cafxg_spawn_ex(self.handle, kernel.encode(),
+                                    signature.encode() if signature else None, d, n,
+                                    C.byref(tuning) if tuning is not None else None,
+                                    C.byref(h)), "spawn")
         return ComputeActor(self, h.value, kernel)

@@ -20,7 +20,15 @@ struct cafxg_actor {
   std::atomic<bool> alive{true};
   std::atomic<int> refs{1};
   std::atomic<uint64_t> pending{0};
+  cafxg_tuning tune{};  // spawn_cl tuning overload (zeros: backend defaults)
 };
+
+namespace cafxg {
+// requests of actors spawned with different tuning never share a launch
+static bool same_tuning(const cafxg_actor* a, const cafxg_actor* b) {
+  return a == b || std::memcmp(&a->tune, &b->tune, sizeof(cafxg_tuning)) == 0;
+}
+}  // namespace cafxg
 
 struct Request {
   const cafxg_mandel_desc& tile(size_t i) const { return i == 0 ? tile0 : more[i - 1]; }
@@ -342,7 +350,8 @@ void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> batch) {
   uint32_t* counters =
       direct ? reinterpret_cast<uint32_t*>(d->stage[slot] + d->stage_cap[slot] - kStageTail)
              : nullptr;
-  status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks, counters);
+  status = launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks, counters,
+                         &batch[0]->actor->tune);
   if (direct) {
     ctx->st_direct++;
     ctx->st_d2h += px * 4;  // written to the replies by the kernel
@@ -512,7 +521,8 @@ void dispatcher_loop(cafxg_ctx* ctx) {
         queue.pop_front();
         cafxg_sgemm_desc g{};
         g.M = g.N = g.K = (uint32_t)r->actor->dims[0];
-        g.mode = CAFXG_SGEMM_AUTO;
+        g.mode = r->actor->tune.sgemm_mode;
+        g.splits = r->actor->tune.sgemm_splits;
         int s = sgemm_submit_impl(
             ctx, &g, r->a, r->b, (float*)r->out,
             [](void* u, int st) { finish_request((Request*)u, st); }, r);
@@ -536,7 +546,7 @@ void dispatcher_loop(cafxg_ctx* ctx) {
           tiles[k] = r->tile(k);
         int s = mandel_submit_impl(
             ctx, tiles.data(), tiles.size(), static_cast<uint32_t*>(r->out),
-            [](void* u, int st) { finish_request((Request*)u, st); }, r);
+            [](void* u, int st) { finish_request((Request*)u, st); }, r, &r->actor->tune);
         if (s != CAFXG_OK)
           push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); });
         else
@@ -544,7 +554,7 @@ void dispatcher_loop(cafxg_ctx* ctx) {
         break;
       }
       if (!batch.empty() &&
-          (r->precision != batch[0]->precision ||
+          (r->precision != batch[0]->precision || !same_tuning(r->actor, batch[0]->actor) ||
            px + r->pixels > kMaxBatchPx))
         break;
       queue.pop_front();
@@ -581,22 +591,75 @@ extern "C" {
 
 // ---- actors --------------------------------------------------------------------
 
-int cafxg_spawn(cafxg_ctx* ctx, const char* kernel_name, const uint64_t* dims, size_t ndims,
-                cafxg_actor** out) try {
+// The kernels' signatures, normalised like spawn_cl's template argument
+// (PAPER.md:357-361): result type first, then the inputs.
+static const char* kernel_signature(Kernel k) {
+  return k == Kernel::matrix_multiply ? "f32*(f32*,f32*)" : "u32*(mandel_desc*)";
+}
+
+static int kernel_by_name(const char* name, Kernel* k) {
+  if (!std::strcmp(name, "mandelbrot"))
+    *k = Kernel::mandelbrot;
+  else if (!std::strcmp(name, "matrix_multiply"))
+    *k = Kernel::matrix_multiply;
+  else
+    return fail(CAFXG_E_UNKNOWN_TYPE, "spawn: no kernel named '%s'", name);
+  return CAFXG_OK;
+}
+
+int cafxg_kernel_signature(const char* kernel_name, char* buf, size_t cap) {
+  if (!kernel_name || !buf)
+    return fail(CAFXG_E_CONFIG, "kernel_signature: null argument");
+  Kernel k;
+  CAFXG_TRY(kernel_by_name(kernel_name, &k));
+  const char* sig = kernel_signature(k);
+  if (std::strlen(sig) + 1 > cap)
+    return fail(CAFXG_E_OUT_OF_RANGE, "kernel_signature: buffer of %zu bytes too small", cap);
+  std::memcpy(buf, sig, std::strlen(sig) + 1);
+  return CAFXG_OK;
+}
+
+static int validate_tuning(Kernel k, const cafxg_tuning& t) {
+  for (uint32_t r : t.reserved)
+    if (r)
+      return fail(CAFXG_E_CONFIG, "tuning: reserved fields must be 0");
+  if (k == Kernel::mandelbrot) {
+    if (t.block_steps && (t.block_steps < 16 || t.block_steps > 64 || t.block_steps % 8))
+      return fail(CAFXG_E_CONFIG, "tuning: block_steps must be 16..64 and a multiple of 8");
+    if (t.sgemm_mode || t.sgemm_splits)
+      return fail(CAFXG_E_CONFIG, "tuning: sgemm fields on a mandelbrot actor");
+  } else {
+    if (t.sgemm_mode > CAFXG_SGEMM_3XTF32)
+      return fail(CAFXG_E_CONFIG, "tuning: bad sgemm_mode");
+    if (t.sgemm_splits > 8 || (t.sgemm_splits & (t.sgemm_splits - 1)))
+      return fail(CAFXG_E_CONFIG, "tuning: sgemm_splits must be 0, 1, 2, 4 or 8");
+    if (t.block_steps || t.max_ctas)
+      return fail(CAFXG_E_CONFIG, "tuning: mandelbrot fields on a matrix_multiply actor");
+  }
+  return CAFXG_OK;
+}
+
+int cafxg_spawn_ex(cafxg_ctx* ctx, const char* kernel_name, const char* signature,
+                   const uint64_t* dims, size_t ndims, const cafxg_tuning* tuning,
+                   cafxg_actor** out) try {
   if (!ctx || !kernel_name || !out)
     return fail(CAFXG_E_CONFIG, "spawn: null argument");
   *out = nullptr;
   Kernel k;
-  if (!std::strcmp(kernel_name, "mandelbrot")) {
-    k = Kernel::mandelbrot;
-  } else if (!std::strcmp(kernel_name, "matrix_multiply")) {
-    k = Kernel::matrix_multiply;
+  CAFXG_TRY(kernel_by_name(kernel_name, &k));
+  if (signature && std::strcmp(signature, kernel_signature(k)) != 0)
+    return fail(CAFXG_E_INTERFACE_MISMATCH, "spawn_cl: signature %s does not match kernel %s %s",
+                signature, kernel_name, kernel_signature(k));
+  if (k == Kernel::matrix_multiply) {
     // spawn_cl<float*(float*,float*)>(src, "matrix_multiply", {size, size})
     if (ndims != 2 || !dims || dims[0] == 0 || dims[0] != dims[1] || dims[0] > (1u << 16))
       return fail(CAFXG_E_INTERFACE_MISMATCH,
                   "spawn: matrix_multiply takes dims {size, size}");
-  } else {
-    return fail(CAFXG_E_UNKNOWN_TYPE, "spawn: no kernel named '%s'", kernel_name);
+  }
+  cafxg_tuning t{};
+  if (tuning) {
+    CAFXG_TRY(validate_tuning(k, *tuning));
+    t = *tuning;
   }
   auto* a = new cafxg_actor;
   a->ctx = ctx;
@@ -604,12 +667,18 @@ int cafxg_spawn(cafxg_ctx* ctx, const char* kernel_name, const uint64_t* dims, s
   a->ndims = std::min<size_t>(ndims, 3);
   for (size_t i = 0; i < a->ndims; ++i)
     a->dims[i] = dims[i];
+  a->tune = t;
   *out = a;
   return CAFXG_OK;
 } catch (const std::exception& ex) {
-  return fail(CAFXG_E_CONFIG, "cafxg_spawn: %s", ex.what());
+  return fail(CAFXG_E_CONFIG, "cafxg_spawn_ex: %s", ex.what());
 } catch (...) {
-  return fail(CAFXG_E_CONFIG, "cafxg_spawn: unknown exception");
+  return fail(CAFXG_E_CONFIG, "cafxg_spawn_ex: unknown exception");
+}
+
+int cafxg_spawn(cafxg_ctx* ctx, const char* kernel_name, const uint64_t* dims, size_t ndims,
+                cafxg_actor** out) {
+  return cafxg_spawn_ex(ctx, kernel_name, nullptr, dims, ndims, nullptr, out);
 }
 
 int actor_check(cafxg_actor* a, const void* const* in, const size_t* in_bytes,

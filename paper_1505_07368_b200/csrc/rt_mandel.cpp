@@ -183,7 +183,8 @@ void pick_block(uint32_t max_iter, int precision, MandelLaunchCfg& c) {
 }
 
 MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
-                                  bool exact, bool safe, uint64_t pixels) {
+                                  bool exact, bool safe, uint64_t pixels,
+                                  const cafxg_tuning* tune) {
   MandelLaunchCfg c;
   // checked kernel: steps between votes (cfg1, max_iter 100: 16 steps 0.065 ms, 4 steps 0.074)
   c.ksteps = max_iter >= 512 ? 32 : max_iter >= 64 ? 16 : 4;
@@ -195,8 +196,13 @@ MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
     c.ksteps = ks_env;
   c.exact = exact;
   c.deferred = safe && max_iter >= 256 && deferred_enabled();
-  if (c.deferred)
+  if (c.deferred) {
     pick_block(max_iter, precision, c);
+    if (tune && tune->block_steps) {  // spawn_cl tuning (validated at spawn)
+      c.unit = (int)tune->block_steps;
+      c.reps = 1;
+    }
+  }
   // occupancy per kernel variant: [precision][checked ksteps 4/16/32 |
   // deferred unit 8/32][exact][deferred]
   const int vi = c.deferred ? c.unit / 8 - 1 : (c.ksteps == 4 ? 0 : c.ksteps == 16 ? 1 : 2);
@@ -208,6 +214,8 @@ MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
   uint64_t want = (pixels + per_block - 1) / per_block;
   uint64_t full = (uint64_t)d->sms * occ;
   c.grid = (int)std::max<uint64_t>(1, std::min(want, full));
+  if (tune && tune->max_ctas)
+    c.grid = std::min(c.grid, (int)tune->max_ctas);
   return c;
 }
 
@@ -218,13 +226,14 @@ MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
 int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                                std::vector<MTile>& tiles, int precision, bool exact,
                                cudaStream_t stream, bool coords_only, bool skip_coords,
-                               uint32_t* direct_counters = nullptr);
+                               uint32_t* direct_counters = nullptr,
+                               const cafxg_tuning* tune = nullptr);
 
 int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                          const std::vector<MTile>& tiles_in, uint32_t total_chunks,
                          int precision, uint32_t max_iter, bool exact,
                          uint64_t pixels, cudaStream_t stream,
-                         uint32_t* direct_counters) {
+                         uint32_t* direct_counters, const cafxg_tuning* tune) {
   (void)max_iter;
   if (total_chunks == 0)
     return CAFXG_OK;
@@ -269,7 +278,7 @@ int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
     if (direct_counters && its.size() != 1)
       return fail(CAFXG_E_CONFIG, "internal: direct reply across max_iter groups");
     CAFXG_TRY(launch_mandel_group(ctx, d, out_base, grp, precision, exact, stream, false, true,
-                                  direct_counters));
+                                  direct_counters, tune));
   }
   if (coords)
     CAFXG_CUDA_TRY(cudaFreeAsync(coords, stream));
@@ -279,7 +288,7 @@ int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
 int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                                std::vector<MTile>& tiles, int precision, bool exact,
                                cudaStream_t stream, bool coords_only, bool skip_coords,
-                               uint32_t* direct_counters) {
+                               uint32_t* direct_counters, const cafxg_tuning* tune) {
   uint32_t chunks = 0, max_extent = 0;
   uint64_t pixels = 0;
   for (auto& t : tiles) {
@@ -325,7 +334,7 @@ int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
     bool safe = true;
     for (auto& t : tiles)
       safe = safe && deferred_safe(t);
-    MandelLaunchCfg cfg = mandel_cfg(d, precision, L.max_iter, exact, safe, pixels);
+    MandelLaunchCfg cfg = mandel_cfg(d, precision, L.max_iter, exact, safe, pixels, tune);
     // a scheduler slot of the ring, reused only after the launch that held it
     // kSchedSlots launches ago finished (launches on different streams --
     // user streams of cafxg_mandelbrot_device included -- may run at once)
@@ -404,7 +413,7 @@ int stream_after_pooled(Device* d, cudaStream_t b, cudaStream_t a);
 int submit_mandel_device(cafxg_ctx* ctx, Device* d,
                                 const std::vector<SubTile>& subs,
                                 uint32_t* host_out, bool out_pinned,
-                                bool exact, Join* join) {
+                                bool exact, Join* join, const cafxg_tuning* tune) {
   cudaSetDevice(d->ordinal);
   std::lock_guard<std::mutex> g(d->submit_mu);
   static const uint64_t wave_px = [] {  // CAFXG_WAVE_MPX: experiments only
@@ -511,7 +520,8 @@ int submit_mandel_device(cafxg_ctx* ctx, Device* d,
         cudaEventRecord(tev.back()[0], ks);
         thost.push_back(trace_now_ms());
       }
-      CAFXG_TRY(launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks));
+      CAFXG_TRY(launch_mandel(ctx, d, dout, mt, chunks, prec, maxit, exact, px, ks, nullptr,
+                              tune));
       if (trace)
         thost.push_back(trace_now_ms());
       if (trace)
@@ -624,7 +634,7 @@ int submit_mandel_device(cafxg_ctx* ctx, Device* d,
 
 int mandel_submit_impl(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles,
                               size_t n, uint32_t* host_out, cafxg_done_fn done,
-                              void* user) {
+                              void* user, const cafxg_tuning* tune) {
   if (!ctx || (n && !tiles) || (n && !host_out))
     return fail(CAFXG_E_CONFIG, "mandelbrot_submit: null argument");
   uint64_t out_elems = 0;
@@ -658,7 +668,7 @@ int mandel_submit_impl(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles,
     if (plan[k].empty())
       continue;
     int s = submit_mandel_device(ctx, ctx->devs[k].get(), plan[k], host_out,
-                                 pinned, exact, join);
+                                 pinned, exact, join, tune);
     if (s != CAFXG_OK) {
       // parts already submitted still report through the join
       std::string err = t_last_error;

@@ -15,6 +15,8 @@ int validate_sgemm(cafxg_sgemm_desc& d) {
     return fail(CAFXG_E_OUT_OF_RANGE, "sgemm: leading dimension below extent");
   if (d.mode > CAFXG_SGEMM_3XTF32)
     return fail(CAFXG_E_CONFIG, "sgemm: bad mode");
+  if (d.splits > 8 || (d.splits & (d.splits - 1)))
+    return fail(CAFXG_E_CONFIG, "sgemm: splits must be 0, 1, 2, 4 or 8");
   if (d.M > (1u << 30) || d.N > (1u << 30) || d.K > (1u << 30))
     return fail(CAFXG_E_OUT_OF_RANGE, "sgemm: dimension too large");
   return CAFXG_OK;
@@ -49,7 +51,7 @@ int sgemm_on_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     CAFXG_CUDA_TRY(cudaMallocAsync(&scratch, sb, stream));
     int launches = 0;
     int e = sgemm_tc_launch(A, B, C, g.M, g.N, g.K, g.lda, g.ldb, g.ldc, scratch,
-                            d->sms, stream, &launches);
+                            d->sms, stream, &launches, (int)g.splits);
     ctx->st_launches += launches;
     mark_used(ctx, d);
     CAFXG_CUDA_TRY(cudaFreeAsync(scratch, stream));
@@ -220,7 +222,8 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     cudaEventRecord(mk(ev_split), cs);
     if (e == 0)
       e = sgemm_tc_gemm_maps(&maps, dC[slot], (int)m, (int)N, (int)K, (int)N, cs,
-                             sgemm_tc_splits((int)m, (int)N, (int)K, d->sms));
+                             g.splits ? (int)g.splits
+                                      : sgemm_tc_splits((int)m, (int)N, (int)K, d->sms));
     if (e != 0)
       status = cuda_status((cudaError_t)e, "sgemm: 3xtf32 launch");
     ctx->st_launches += 2;
@@ -345,8 +348,9 @@ int sgemm_tiled2d_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     const uint32_t nj = (uint32_t)std::min<size_t>(Nb, N - n0);
     float* cblk = dC + (size_t)m0 * N + n0;
     int e = sgemm_tc_gemm_maps(&maps, cblk, (int)mi, (int)nj, (int)K, (int)N, cs,
-                               sgemm_tc_splits((int)mi, (int)nj, (int)K, d->sms), (int)m0,
-                               (int)n0);
+                               g.splits ? (int)g.splits
+                                        : sgemm_tc_splits((int)mi, (int)nj, (int)K, d->sms),
+                               (int)m0, (int)n0);
     ctx->st_launches++;
     mark_used(ctx, d);
     tmark('G', cs);

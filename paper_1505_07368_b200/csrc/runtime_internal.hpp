@@ -397,10 +397,12 @@ int launch_mandel(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
                   const std::vector<MTile>& tiles_in, uint32_t total_chunks,
                   int precision, uint32_t max_iter, bool exact,
                   uint64_t pixels, cudaStream_t stream,
-                  uint32_t* direct_counters = nullptr);
+                  uint32_t* direct_counters = nullptr,
+                  const cafxg_tuning* tune = nullptr);
 std::vector<std::vector<SubTile>> plan_mandel(const cafxg_mandel_desc* tiles, size_t n, size_t ndev);
 int mandel_submit_impl(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles, size_t n,
-                       uint32_t* host_out, cafxg_done_fn done, void* user);
+                       uint32_t* host_out, cafxg_done_fn done, void* user,
+                       const cafxg_tuning* tune = nullptr);
 
 // ---- rt_sgemm.cpp ----
 int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc, const float* A,

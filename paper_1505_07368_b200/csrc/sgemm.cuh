@@ -14,9 +14,10 @@ int sgemm_simt_launch(const float* A, const float* B, float* C, int M, int N,
 // (sgemm_tc_scratch_bytes).
 bool sgemm_tc_supported(int M, int N, int K, int lda, int ldb, int ldc);
 size_t sgemm_tc_scratch_bytes(int M, int N, int K);
+// splits: split-K cluster size (1/2/4/8), 0 = sgemm_tc_splits' choice
 int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N,
                     int K, int lda, int ldb, int ldc, void* scratch,
-                    int sm_count, void* stream, int* launches);
+                    int sm_count, void* stream, int* launches, int splits = 0);
 // The three stages separately (pipelined host requests): tf32 hi/lo split of
 // an A row block (M x K, packed out), split + transpose of B (to N x K), and
 // the GEMM on split operands.

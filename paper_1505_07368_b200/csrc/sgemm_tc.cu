@@ -616,14 +616,15 @@ int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float
 
 int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int K, int lda,
                     int ldb, int ldc, void* scratch, int sm_count, void* stream,
-                    int* launches) {
+                    int* launches, int splits_req) {
   float* Ah = static_cast<float*>(scratch);
   float* Al = Ah + (size_t)M * K;
   float* Bh = Al + (size_t)M * K;
   float* Bl = Bh + (size_t)N * K;
   if ((size_t)M * K / 4 >= (1ull << 32))
     return (int)cudaErrorInvalidValue;
-  const int splits = sgemm_tc_splits(M, N, K, sm_count > 0 ? sm_count : 148);
+  const int splits =
+      splits_req > 0 ? splits_req : sgemm_tc_splits(M, N, K, sm_count > 0 ? sm_count : 148);
   const int nb_a = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 8);
   const int nb_b = (N / 32) * (K / 32);
   split_ab_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B, ldb,

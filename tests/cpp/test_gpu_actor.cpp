@@ -294,6 +294,133 @@ int main() {
                 std::get<cafx::error>(bad).code == cafx::errc::interface_mismatch,
             "remote wrong arity -> error(interface_mismatch) reply over the wire");
     }
+
+    // 8. the spawn_cl surface: signature template checked
+    //    against the kernel, tuning overload, data-transformation overload
+    {
+      // (a) spawn_cl<float*(float*,float*)> -> typed (f32vec, f32vec) -> (f32vec)
+      const uint32_t n = 256;
+      auto mm = cafxg::spawn_cl<float*(float*, float*)>(sys, ctx, "matrix_multiply", {n, n});
+      cafxg::f32vec a(n * n, 0.0f), b(n * n, 0.0f);
+      for (uint32_t i = 0; i < n; ++i) {
+        a[i * n + i] = 2.0f;           // A = 2 I
+        b[i * n + (n - 1 - i)] = 1.0f;  // B = anti-identity
+      }
+      auto res = self->request(mm, cafx::make_message(a, b), 60s);
+      bool ok = std::holds_alternative<cafx::message>(res);
+      if (ok) {
+        const auto& c = std::get<cafx::message>(res).get<cafxg::f32vec>(0);
+        for (uint32_t i = 0; ok && i < n; ++i)
+          for (uint32_t j = 0; ok && j < n; ++j)
+            ok = c[i * n + j] == (j == n - 1 - i ? 2.0f : 0.0f);
+      }
+      auto& reg = cafx::type_registry::global();
+      cafx::rule want;
+      want.inputs = {cafx::type_spec::of(reg.id_of<cafxg::f32vec>()),
+                     cafx::type_spec::of(reg.id_of<cafxg::f32vec>())};
+      want.outputs = {cafx::type_spec::of(reg.id_of<cafxg::f32vec>())};
+      check(ok && mm.interface() == cafx::messaging_interface{want},
+            "spawn_cl<float*(float*,float*)>: typed (f32vec,f32vec)->(f32vec), reply exact");
+      // typed sends are checked at the sender (actor_system.cpp:85-91)
+      bool threw = false;
+      try {
+        sys.anon_send(mm, cafx::make_message(a));
+      } catch (const cafx::failure& f) {
+        threw = f.code() == cafx::errc::type_mismatch;
+      }
+      check(threw, "typed handle from the signature rejects a wrong send at the sender");
+    }
+    {
+      // (b) a signature that does not match the kernel's
+      bool threw = false;
+      try {
+        cafxg::spawn_cl<float*(float*)>(sys, ctx, "matrix_multiply", {64, 64});
+      } catch (const cafx::failure& f) {
+        threw = f.code() == cafx::errc::interface_mismatch;
+      }
+      bool threw2 = false;
+      try {
+        cafxg::spawn_cl<uint32_t*(float*, float*)>(sys, ctx, "matrix_multiply", {64, 64});
+      } catch (const cafx::failure& f) {
+        threw2 = f.code() == cafx::errc::interface_mismatch;
+      }
+      check(threw && threw2, "spawn_cl with a mismatched signature -> failure(interface_mismatch)");
+    }
+    {
+      // (c) tuning overload: launch-shape hints; bad values fail the spawn
+      auto mb = cafxg::spawn_cl<uint32_t*(cafxg_mandel_desc*)>(
+          sys, ctx, "mandelbrot", {}, cafxg::tuning().block_steps(24).max_ctas(64));
+      cafxg_mandel_desc d{};
+      d.x0 = -0.75; d.x1 = -0.73; d.y0 = 0.10; d.y1 = 0.12;
+      d.width = d.height = d.nrows = d.ncols = 192;
+      d.max_iter = 1000;
+      d.precision = CAFXG_FP64;
+      d.sampling = CAFXG_CENTRE;
+      auto res = self->request(mb, cafx::make_message(cafxg::mandel_tiles{{d}}), 60s);
+      bool ok = std::holds_alternative<cafx::message>(res);
+      if (ok) {
+        const auto& counts = std::get<cafx::message>(res).get<cafxg::u32vec>(0);
+        for (uint32_t r = 0; ok && r < 192; r += 7)
+          for (uint32_t c = 0; ok && c < 192; ++c) {
+            const double ci = d.y0 + (((double)r + 0.5) * (d.y1 - d.y0)) / 192;
+            const double cr = d.x0 + (((double)c + 0.5) * (d.x1 - d.x0)) / 192;
+            ok = counts[r * 192 + c] == cafx::bench::mandelbrot_cell(cr, ci, 1000);
+          }
+      }
+      bool threw = false;
+      try {
+        cafxg::spawn_cl<uint32_t*(cafxg_mandel_desc*)>(sys, ctx, "mandelbrot", {},
+                                                       cafxg::tuning().block_steps(20));
+      } catch (const cafx::failure& f) {
+        threw = f.code() == cafx::errc::config_error;
+      }
+      check(ok && threw,
+            "spawn_cl tuning overload: block_steps 24 / max_ctas 64 exact; block_steps 20 "
+            "-> failure(config_error)");
+    }
+    {
+      // (d) data-transformation overload: (uint32 size, uint32 max_iter) ->
+      //     run_mandelbrot's image on the GPU -> its collector checksum; the
+      //     kernel signature stays hidden behind the actor's own interface
+      auto rm = cafxg::spawn_cl<uint32_t*(cafxg_mandel_desc*)>(
+          sys, ctx, "mandelbrot", {},
+          cafx::behavior{[](uint32_t size, uint32_t it) {
+            return cafxg::mandel_tiles{{ref_desc(size, it)}};
+          }},
+          cafx::behavior{[](const cafxg::u32vec& counts) {
+            uint64_t h = cafx::detail::fnv1a_seed;
+            for (uint32_t c : counts)
+              h = cafx::detail::fnv1a_u32(h, c);
+            return h;
+          }});
+      auto res = self->request(rm, cafx::make_message(uint32_t{256}, uint32_t{100}), 60s);
+      bool ok = std::holds_alternative<cafx::message>(res) &&
+                std::get<cafx::message>(res).get<uint64_t>(0) == 12958954340663424292ull;
+      auto& reg = cafx::type_registry::global();
+      ok = ok && rm.interface().size() == 1 &&
+           rm.interface().rules()[0].inputs.size() == 2 &&
+           rm.interface().rules()[0].outputs ==
+               std::vector<cafx::type_spec>{cafx::type_spec::of(reg.id_of<uint64_t>())};
+      check(ok, "spawn_cl transformation: (uint32 256, uint32 100) -> checksum golden, "
+                "typed (u32,u32)->(u64)");
+      // a request the transformation does not match -> error reply
+      auto bad = self->request(cafx::actor_cast(rm), cafx::make_message(1.5f), 30s);
+      check(std::holds_alternative<cafx::error>(bad) &&
+                std::get<cafx::error>(bad).code == cafx::errc::type_mismatch,
+            "spawn_cl transformation: unmatched request -> error(type_mismatch)");
+      // map_args must produce the kernel's inputs
+      bool threw = false;
+      try {
+        cafxg::spawn_cl<uint32_t*(cafxg_mandel_desc*)>(
+            sys, ctx, "mandelbrot", {},
+            cafx::behavior{[](uint32_t n) { return cafxg::f32vec(n); }},
+            cafx::behavior{[](const cafxg::u32vec& c) { return (uint32_t)c.size(); }});
+      } catch (const cafx::failure& f) {
+        threw = f.code() == cafx::errc::interface_mismatch;
+      }
+      check(threw, "spawn_cl transformation whose map_args misses the kernel inputs -> "
+                   "failure(interface_mismatch)");
+    }
     // ~actor_system: hard-kills the gpu actors, which unregister (no hang)
   }
   std::printf("PASS actor_system shutdown with registered gpu actors\n");

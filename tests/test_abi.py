@@ -82,3 +82,16 @@ def test_header_is_plain_c_and_links(tmp_path):
     if not torch.cuda.is_available():
         out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
         assert out.returncode == 0 and "spawn_error" in out.stdout
+
+
+def test_kernel_signatures():
+    """spawn_cl's normalised signatures, no device needed."""
+    import paper_1505_07368_b200 as pkg
+    assert pkg.kernel_signature("matrix_multiply") == "f32*(f32*,f32*)"
+    assert pkg.kernel_signature("mandelbrot") == "u32*(mandel_desc*)"
+    with pytest.raises(pkg.CafxgError) as e:
+        pkg.kernel_signature("no_such_kernel")
+    assert e.value.code == 2
+    buf = ctypes.create_string_buffer(4)
+    assert pkg.lib().cafxg_kernel_signature(b"mandelbrot", buf, 4) == 4
+    assert ctypes.sizeof(pkg.Tuning) == 32

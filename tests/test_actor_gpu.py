@@ -393,3 +393,46 @@ def test_c_program_through_the_abi(tmp_path):
                            f"-Wl,-rpath,{os.path.dirname(b.LIB_PATH)}", "-o", str(exe)])
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "C ABI OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_spawn_cl_signature_and_tuning(ctx):
+    """cafxg_spawn_ex: the spawn_cl signature is checked against the kernel's
+    (interface_mismatch before any actor exists); tuning hints apply to every
+    request and out-of-range hints fail the spawn (config_error)."""
+    with pytest.raises(pkg.CafxgError) as e:
+        ctx.spawn("matrix_multiply", (64, 64), signature="f32*(f32*)")
+    assert e.value.code == 6
+    mm = ctx.spawn("matrix_multiply", (256, 256), signature="f32*(f32*,f32*)",
+                   tuning=pkg.Tuning(sgemm_mode=pkg.SGEMM_3XTF32, sgemm_splits=2))
+    A = oracle.fill_uniform(256 * 256, 91)
+    B = oracle.fill_uniform(256 * 256, 92)
+    C = np.zeros(256 * 256, dtype=np.float32)
+    mm.request([A, B], C).result(timeout=60)
+    rows = np.arange(0, 256, 11, dtype=np.uint32)
+    R = oracle.sgemm_ref_rows(A.reshape(256, 256), B.reshape(256, 256), rows, 256, 256)
+    assert oracle.sgemm_rel_err(C.reshape(256, 256), R, rows, 256) <= 1e-5
+    mm.release()
+    for bad in (pkg.Tuning(block_steps=20), pkg.Tuning(block_steps=72),
+                pkg.Tuning(sgemm_splits=3)):
+        with pytest.raises(pkg.CafxgError) as e:
+            ctx.spawn("mandelbrot", tuning=bad)
+        assert e.value.code == 8
+    # every block length and a CTA cap, exact against the oracle; batches of
+    # differently tuned actors never share a launch
+    d = pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 160, 96, 1000)
+    ref = _tile_ref(d)
+    actors = [ctx.spawn("mandelbrot", signature="u32*(mandel_desc*)",
+                        tuning=pkg.Tuning(block_steps=b, max_ctas=m))
+              for b, m in [(16, 0), (24, 8), (40, 1), (64, 0), (0, 3)]]
+    futs, outs = [], []
+    for a in actors:
+        for _ in range(3):
+            o = np.zeros(160 * 96, np.uint32)
+            futs.append(a.request([(pkg.MandelDesc * 1)(d)], o))
+            outs.append(o)
+    for f in futs:
+        f.result(timeout=60)
+    for o in outs:
+        assert np.array_equal(o.reshape(96, 160), ref)
+    for a in actors:
+        a.release()
