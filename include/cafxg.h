@@ -65,6 +65,12 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out);
  * releases everything. */
 int cafxg_close(cafxg_ctx* ctx);
 int cafxg_device_count(const cafxg_ctx* ctx);
+/* CAFXG_OK while the context is usable; CAFXG_E_DOWN after a sticky device
+ * error (illegal address, launch failure, ECC, ...: the CUDA context is
+ * gone), with the cause in cafxg_last_error(). From then on every submission
+ * fails with CAFXG_E_DOWN; an adapter should terminate its compute actors
+ * (monitors and pending requesters fire, abstract_actor.cpp:108-134). */
+int cafxg_ctx_status(cafxg_ctx* ctx);
 /* Blocks until every submission made before the call has completed and its
  * callback has returned. */
 int cafxg_sync(cafxg_ctx* ctx);

@@ -38,7 +38,9 @@
 //  * exit signals: a hard kill (actor_system.cpp:243-258) or a non-normal exit
 //    quits the backend actor, `finalize`s (monitors, links, request_down for
 //    pending requesters, abstract_actor.cpp:108-134) and unregisters, so
-//    ~actor_system does not wait forever (actor_system.cpp:21-30);
+//    ~actor_system does not wait forever (actor_system.cpp:21-30); a sticky
+//    device error (cafxg_ctx_status) terminates the actor the same way, with
+//    exit_reason::unhandled_error;
 //  * buffer types are registered with wire codecs (type_registry.hpp:74-80),
 //    so middleman::publish can serve a GPU actor to remote nodes;
 //  * reply relay: a reply leaves libcafxg's completion thread through a
@@ -357,6 +359,11 @@ class gpu_actor final : public cafx::abstract_actor {
                     cafx::make_message(cafx::error{static_cast<cafx::errc>(status),
                                                    cafxg_last_error()}),
                     true, false);
+      // a sticky device error: the backend cannot serve anything any more,
+      // so the actor terminates (monitors, links and pending requesters fire,
+      // abstract_actor.cpp:108-134) instead of failing requests one by one
+      if (cafxg_ctx_status(self->ctx_) != CAFXG_OK)
+        self->terminate(cafx::exit_reason::unhandled_error());
       return;
     }
     cafx::message reply = self->kernel_ == "mandelbrot"
@@ -473,6 +480,10 @@ class gpu_actor final : public cafx::abstract_actor {
       reason = env.content.get<cafx::exit_reason>(2);
     if (!env.hard_kill && reason.is_normal())
       return;  // normal exits do not terminate an actor that is not linked-dead
+    terminate(reason);
+  }
+
+  void terminate(const cafx::exit_reason& reason) {
     bool expected = false;
     if (!quitting_.compare_exchange_strong(expected, true))
       return;

@@ -34,7 +34,7 @@ SGEMM_AUTO, SGEMM_FFMA, SGEMM_3XTF32 = 0, 1, 2
 # Symbols include/cafxg.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "cafxg_abi_version", "cafxg_status_string", "cafxg_last_error",
-    "cafxg_open", "cafxg_close", "cafxg_device_count", "cafxg_sync",
+    "cafxg_open", "cafxg_close", "cafxg_device_count", "cafxg_ctx_status", "cafxg_sync",
     "cafxg_host_alloc", "cafxg_host_free", "cafxg_host_register", "cafxg_host_unregister",
     "cafxg_mandelbrot_submit", "cafxg_mandelbrot", "cafxg_mandelbrot_device",
     "cafxg_fnv1a_u32_device", "cafxg_run_mandelbrot",
@@ -106,6 +106,7 @@ def lib() -> C.CDLL:
         L.cafxg_open.argtypes = [u64, C.POINTER(vp)]
         L.cafxg_close.argtypes = [vp]
         L.cafxg_device_count.argtypes = [vp]
+        L.cafxg_ctx_status.argtypes = [vp]
         L.cafxg_sync.argtypes = [vp]
         L.cafxg_host_alloc.argtypes = [vp, sz, C.POINTER(vp)]
         L.cafxg_host_free.argtypes = [vp, vp]
@@ -280,6 +281,10 @@ class Context:
     @property
     def device_count(self) -> int:
         return lib().cafxg_device_count(self.handle)
+
+    def status(self) -> int:
+        """OK, or E_DOWN once a sticky device error made the context unusable."""
+        return lib().cafxg_ctx_status(self.handle)
 
     def sync(self) -> None:
         _check(lib().cafxg_sync(self.handle), "cafxg_sync")

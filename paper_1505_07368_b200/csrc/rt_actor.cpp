@@ -509,7 +509,7 @@ void dispatcher_loop(cafxg_ctx* ctx) {
     uint64_t px = 0;
     while (!queue.empty()) {
       Request* r = queue.front();
-      if (!r->actor->alive.load()) {
+      if (!r->actor->alive.load() || ctx->lost.load()) {
         queue.pop_front();
         queued_px -= r->pixels;
         push_completion(ctx, d, d->compute, [r](int) { finish_request(r, CAFXG_E_DOWN); });
@@ -731,6 +731,7 @@ int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in, const size_t* in_
   CAFXG_TRY(actor_check(a, in, in_bytes, n_in, &rb));
   if (!a->alive.load())
     return fail(CAFXG_E_DOWN, "enqueue: actor terminated");
+  CAFXG_TRY(check_alive(a->ctx));
   if (!out || out_bytes != rb)
     return fail(CAFXG_E_TYPE_MISMATCH, "enqueue: reply buffer must be %zu bytes", rb);
   auto* r = new Request;

@@ -89,9 +89,14 @@ void completion_loop(cafxg_ctx* ctx, Device* d) {
       d->cq.pop_front();
     }
     cudaError_t e = cudaEventSynchronize(c.ev);
+    const uint64_t nth = ctx->completions.fetch_add(1) + 1;
+    if (e == cudaSuccess && ctx->simulate_loss_at && nth >= ctx->simulate_loss_at)
+      e = cudaErrorLaunchFailure;  // CAFXG_SIMULATE_DEVICE_LOSS (tests)
     int status = CAFXG_OK;
-    if (e != cudaSuccess)
+    if (e != cudaSuccess) {
       status = cuda_status(e, "device work failed");
+      mark_lost(ctx, e, "device work failed");
+    }
     c.fn(status);
     {
       std::lock_guard<std::mutex> lk(d->cq_mu);
@@ -105,6 +110,47 @@ void completion_loop(cafxg_ctx* ctx, Device* d) {
     ctx->sync_cv.notify_all();
     ctx->disp_cv.notify_all();
   }
+}
+
+// Errors after which the CUDA context of the device is unusable: every later
+// call fails with the same error until the process exits.
+static bool sticky(cudaError_t e) {
+  switch (e) {
+    case cudaErrorIllegalAddress:
+    case cudaErrorLaunchFailure:
+    case cudaErrorHardwareStackError:
+    case cudaErrorIllegalInstruction:
+    case cudaErrorMisalignedAddress:
+    case cudaErrorInvalidAddressSpace:
+    case cudaErrorInvalidPc:
+    case cudaErrorECCUncorrectable:
+    case cudaErrorAssert:
+    case cudaErrorLaunchTimeout:
+    case cudaErrorContextIsDestroyed:
+    case cudaErrorDevicesUnavailable:
+      return true;
+    default:
+      return false;
+  }
+}
+
+void mark_lost(cafxg_ctx* ctx, cudaError_t e, const char* where) {
+  if (!sticky(e) || ctx->lost.load())
+    return;
+  {
+    std::lock_guard<std::mutex> g(ctx->lost_mu);
+    ctx->lost_why = std::string(where) + ": " + cudaGetErrorName(e);
+  }
+  ctx->lost.store(true);
+  ctx->disp_cv.notify_all();
+}
+
+int check_alive(cafxg_ctx* ctx) {
+  if (!ctx->lost.load(std::memory_order_relaxed))
+    return CAFXG_OK;
+  std::lock_guard<std::mutex> g(ctx->lost_mu);
+  return fail(CAFXG_E_DOWN, "context lost after a sticky device error (%s)",
+              ctx->lost_why.c_str());
 }
 
 // Records an event on `stream` and hands `fn` to the device's completion
@@ -301,6 +347,8 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
       return fail(CAFXG_E_SPAWN, "device_mask selects no visible device");
     const char* ex = getenv("CAFXG_EXACT_STEP");
     ctx->force_exact = ex && ex[0] == '1';
+    if (const char* sl = getenv("CAFXG_SIMULATE_DEVICE_LOSS"))
+      ctx->simulate_loss_at = (uint64_t)std::max(0, atoi(sl));
     cafxg_ctx* c = ctx.release();
     for (auto& d : c->devs)
       d->completer = std::thread(completion_loop, c, d.get());
@@ -412,6 +460,12 @@ int cafxg_close(cafxg_ctx* ctx) try {
 }
 
 int cafxg_device_count(const cafxg_ctx* ctx) { return ctx ? (int)ctx->devs.size() : 0; }
+
+int cafxg_ctx_status(cafxg_ctx* ctx) {
+  if (!ctx)
+    return fail(CAFXG_E_CONFIG, "ctx_status: null ctx");
+  return check_alive(ctx);
+}
 
 int cafxg_host_alloc(cafxg_ctx* ctx, size_t bytes, void** ptr) try {
   if (!ctx || !ptr)

@@ -637,6 +637,7 @@ int mandel_submit_impl(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles,
                               void* user, const cafxg_tuning* tune) {
   if (!ctx || (n && !tiles) || (n && !host_out))
     return fail(CAFXG_E_CONFIG, "mandelbrot_submit: null argument");
+  CAFXG_TRY(check_alive(ctx));
   uint64_t out_elems = 0;
   bool exact = false;
   for (size_t i = 0; i < n; ++i) {
@@ -715,6 +716,7 @@ int cafxg_mandelbrot_device(cafxg_ctx* ctx, int device, const cafxg_mandel_desc*
                             size_t n, uint32_t* dev_out, void* stream) {
   if (!ctx || device < 0 || device >= (int)ctx->devs.size() || (n && (!tiles || !dev_out)))
     return fail(CAFXG_E_CONFIG, "mandelbrot_device: bad argument");
+  CAFXG_TRY(check_alive(ctx));
   try {
     Device* d = ctx->devs[device].get();
     bool exact = false;

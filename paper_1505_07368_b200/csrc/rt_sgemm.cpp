@@ -442,6 +442,7 @@ int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
     return fail(CAFXG_E_CONFIG, "sgemm_submit: null argument");
   cafxg_sgemm_desc g = *desc;
   CAFXG_TRY(validate_sgemm(g));
+  CAFXG_TRY(check_alive(ctx));
   if ((g.M && g.K && !A) || (g.K && g.N && !B) || (g.M && g.N && !C))
     return fail(CAFXG_E_CONFIG, "sgemm_submit: null matrix");
   size_t G = ctx->devs.size();
@@ -651,6 +652,7 @@ int cafxg_sgemm_device(cafxg_ctx* ctx, int device, const cafxg_sgemm_desc* desc,
     return fail(CAFXG_E_CONFIG, "sgemm_device: bad argument");
   cafxg_sgemm_desc g = *desc;
   CAFXG_TRY(validate_sgemm(g));
+  CAFXG_TRY(check_alive(ctx));
   Device* d = ctx->devs[device].get();
   cudaSetDevice(d->ordinal);
   return sgemm_on_device(ctx, d, g, A, B, C, stream ? (cudaStream_t)stream : d->compute);

@@ -312,6 +312,18 @@ struct cafxg_ctx {
   bool cb_stop = false;
   std::vector<std::thread> cb_threads;
   bool force_exact = false;  // CAFXG_EXACT_STEP=1: always the 8-op step
+  // A sticky CUDA error (the CUDA context of a device is unusable) makes the
+  // whole context lost: later submissions fail at once with CAFXG_E_DOWN and
+  // cafxg_ctx_status reports it, so adapters can terminate their actors
+  // (abstract_actor.cpp:108-134) instead of failing every request one by one.
+  std::atomic<bool> lost{false};
+  std::mutex lost_mu;
+  std::string lost_why;
+  // CAFXG_SIMULATE_DEVICE_LOSS=<n> (read at cafxg_open; tests only): the n-th
+  // completion of the context reports cudaErrorLaunchFailure, as a real
+  // sticky fault would, without faulting the GPU
+  uint64_t simulate_loss_at = 0;
+  std::atomic<uint64_t> completions{0};
   // CAFXG_VIRTUAL_DEVICES=V: V context devices on one physical GPU (own
   // streams, scheduler ring and completion thread each) so the multi-device
   // split/join logic runs on a single-GPU box; B is then replicated by
@@ -361,6 +373,10 @@ inline void mark_used(cafxg_ctx* ctx, const Device* d) {
 }
 
 // ---- rt_core.cpp ----
+// marks the context lost after a sticky CUDA error (see cafxg_ctx::lost)
+void mark_lost(cafxg_ctx* ctx, cudaError_t e, const char* where);
+// CAFXG_E_DOWN (with the loss recorded as the error context) once lost
+int check_alive(cafxg_ctx* ctx);
 double trace_now_ms();
 bool trace_on();
 void note_max_batch(cafxg_ctx* ctx, uint64_t n);

@@ -5,6 +5,7 @@
 // libcafxg.so. Prints one PASS/FAIL line per check; exit code 0 iff all pass.
 // Built by tests/cpp/Makefile, run by tests/test_cafx_adapter_gpu.py.
 #include <atomic>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -15,6 +16,7 @@
 #include <vector>
 
 #include "cafx/actor_system.hpp"
+#include "cafx/atoms.hpp"
 #include "cafx/bench/bench.hpp"
 #include "cafx/detail/fnv.hpp"
 #include "cafx/io/middleman.hpp"
@@ -24,6 +26,7 @@
 using namespace std::chrono_literals;
 
 static int failures = 0;
+static cafxg_ctx* lost_ctx = nullptr;  // section 9's context (closed last)
 
 static void check(bool ok, const std::string& name) {
   std::printf("%s %s\n", ok ? "PASS" : "FAIL", name.c_str());
@@ -421,9 +424,57 @@ int main() {
       check(threw, "spawn_cl transformation whose map_args misses the kernel inputs -> "
                    "failure(interface_mismatch)");
     }
+
+    // 9. device loss: a sticky CUDA error (simulated on a second context:
+    //    CAFXG_SIMULATE_DEVICE_LOSS makes its 2nd completion report
+    //    cudaErrorLaunchFailure, as a real fault would) terminates the compute
+    //    actor: the failing request gets an error reply, monitors receive
+    //    down(unhandled_error), later requests get request_down
+    {
+      setenv("CAFXG_SIMULATE_DEVICE_LOSS", "2", 1);
+      const int os = cafxg_open(1, &lost_ctx);
+      unsetenv("CAFXG_SIMULATE_DEVICE_LOSS");
+      check(os == CAFXG_OK, "second context for the device-loss check");
+      auto mb = cafxg::spawn_gpu(sys, lost_ctx, "mandelbrot", {});
+      cafx::monitor(self.handle(), mb);
+      std::mt19937_64 rng(4242);
+      auto d = storm_tile(rng);
+      auto r1 = self->request(mb, cafx::make_message(cafxg::mandel_tiles{{d}}), 60s);
+      auto r2 = self->request(mb, cafx::make_message(cafxg::mandel_tiles{{d}}), 60s);
+      bool down = false, unhandled = false;
+      self->receive(cafx::behavior{[&](cafx::down_atom, cafx::actor_addr src,
+                                       cafx::exit_reason reason) {
+                      down = src == mb.address();
+                      unhandled = reason.k == cafx::exit_reason::kind::unhandled_error;
+                    }},
+                    30s);
+      auto r3 = self->request(mb, cafx::make_message(cafxg::mandel_tiles{{d}}), 30s);
+      auto code_of = [](const auto& r) {
+        return std::holds_alternative<cafx::error>(r) ? (int)std::get<cafx::error>(r).code : -1;
+      };
+      check(std::holds_alternative<cafx::message>(r1) &&
+                std::get<cafx::message>(r1).get<cafxg::u32vec>(0) == expect_tile(d),
+            "device loss: the request before the fault is answered exactly");
+      check(code_of(r2) == (int)cafx::errc::request_down,
+            "device loss: the faulting request gets error(request_down) (got " +
+                std::to_string(code_of(r2)) + ")");
+      check(down && unhandled, "device loss: monitors receive down(unhandled_error)");
+      check(code_of(r3) == (int)cafx::errc::request_down,
+            "device loss: later requests get request_down (got " + std::to_string(code_of(r3)) +
+                ")");
+      check(cafxg_ctx_status(lost_ctx) == CAFXG_E_DOWN, "device loss: ctx_status E_DOWN");
+      cafxg_mandel_desc t = d;
+      uint32_t out[4096];
+      check(cafxg_mandelbrot(lost_ctx, &t, 1, out) == CAFXG_E_DOWN,
+            "submissions on a lost context fail at once with request_down");
+      // (the context is closed after the actor system: the actor object
+      // may outlive this scope in a pending relay job)
+    }
     // ~actor_system: hard-kills the gpu actors, which unregister (no hang)
   }
   std::printf("PASS actor_system shutdown with registered gpu actors\n");
+  if (lost_ctx)
+    cafxg_close(lost_ctx);
   cafxg_close(ctx);
   std::printf("%s\n", failures ? "FAILED" : "ALL PASS");
   return failures ? 1 : 0;

@@ -154,6 +154,40 @@ print("ok")
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
 
 
+def test_sticky_device_error_loses_the_context():
+    """A sticky device error (CAFXG_SIMULATE_DEVICE_LOSS makes the 2nd
+    completion report cudaErrorLaunchFailure) loses the context: that request
+    fails with request_down, ctx_status reports it, later submissions fail at
+    once without reaching the device."""
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+d = pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 64, 64, 50)
+with pkg.Context(1) as c:
+    c.mandelbrot(d)
+    assert c.status() == 0
+    try:
+        c.mandelbrot(d)
+        raise SystemExit("no error")
+    except pkg.CafxgError as e:
+        assert e.code == 14, e.code
+    assert c.status() == 14
+    launches = c.stats().kernel_launches
+    try:
+        c.mandelbrot(d)
+        raise SystemExit("no error after the loss")
+    except pkg.CafxgError as e:
+        assert e.code == 14 and "lost" in str(e), str(e)
+    assert c.stats().kernel_launches == launches
+print("ok")
+""" % ROOT
+    env = dict(os.environ, CAFXG_SIMULATE_DEVICE_LOSS="2")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr[-3000:]
+
+
 def test_exact_and_fast_steps_agree():
     """The 7-op (fma-folded) and the 8-op step give identical counts."""
     code = r"""
