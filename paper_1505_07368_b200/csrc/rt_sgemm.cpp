@@ -189,7 +189,8 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
   // tensor maps encoded once per request: every block reuses Ah/Al (R rows)
   // and Bh/Bl
   SgemmTcMaps maps;
-  if (int me = sgemm_tc_make_maps(Ah, Al, (int)R, Bh, Bl, (int)N, (int)K, &maps))
+  const int bn = sgemm_tc_pick_bn((int)R, (int)N, d->sms);
+  if (int me = sgemm_tc_make_maps(Ah, Al, (int)R, Bh, Bl, (int)N, (int)K, bn, &maps))
     return cuda_status((cudaError_t)me, "sgemm: tensor maps");
   std::vector<cudaEvent_t> ev_split, ev_gemm, ev_down;
   auto mk = [d](std::vector<cudaEvent_t>& v) {
@@ -223,7 +224,7 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     if (e == 0)
       e = sgemm_tc_gemm_maps(&maps, dC[slot], (int)m, (int)N, (int)K, (int)N, cs,
                              g.splits ? (int)g.splits
-                                      : sgemm_tc_splits((int)m, (int)N, (int)K, d->sms));
+                                      : sgemm_tc_splits((int)m, (int)N, (int)K, d->sms, bn));
     if (e != 0)
       status = cuda_status((cudaError_t)e, "sgemm: 3xtf32 launch");
     ctx->st_launches += 2;
@@ -319,7 +320,7 @@ int sgemm_tiled2d_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
   CAFXG_CUDA_TRY(cudaMallocAsync((void**)&Bl, N * K * 4, cs));
   CAFXG_CUDA_TRY(cudaMallocAsync((void**)&dC, M * N * 4, cs));
   SgemmTcMaps maps;  // whole Ah/Al and Bh/Bl; blocks address rows by offset
-  if (int me = sgemm_tc_make_maps(Ah, Al, (int)M, Bh, Bl, (int)N, (int)K, &maps))
+  if (int me = sgemm_tc_make_maps(Ah, Al, (int)M, Bh, Bl, (int)N, (int)K, 256, &maps))
     return cuda_status((cudaError_t)me, "sgemm: tensor maps");
   CAFXG_TRY(stream_after_pooled(d, d->h2d, cs));  // buffers exist before uploads
   // CAFXG_TRACE=1: completion times of uploads, GEMM blocks and downloads
@@ -349,7 +350,7 @@ int sgemm_tiled2d_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     float* cblk = dC + (size_t)m0 * N + n0;
     int e = sgemm_tc_gemm_maps(&maps, cblk, (int)mi, (int)nj, (int)K, (int)N, cs,
                                g.splits ? (int)g.splits
-                                        : sgemm_tc_splits((int)mi, (int)nj, (int)K, d->sms),
+                                        : sgemm_tc_splits((int)mi, (int)nj, (int)K, d->sms, 256),
                                (int)m0, (int)n0);
     ctx->st_launches++;
     mark_used(ctx, d);

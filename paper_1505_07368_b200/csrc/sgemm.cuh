@@ -26,21 +26,25 @@ int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al
 int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl,
                      void* stream);
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl,
-                  float* C, int M, int N, int K, int ldc, void* stream, int splits = 1);
+                  float* C, int M, int N, int K, int ldc, void* stream, int splits = 1,
+                  int bn = 256);
 // The four TMA tensor maps of a GEMM (A_hi, A_lo over a_rows rows; B_hi,
 // B_lo), encoded once and reused by launches over the same buffers: a row
 // block of m <= a_rows rows only touches rows below m.
 struct SgemmTcMaps {
   alignas(64) unsigned char m[4][128];
+  int bn;  // tile width the maps were encoded for (B box rows)
 };
 int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
-                       const float* Bl, int N, int K, SgemmTcMaps* maps);
+                       const float* Bl, int N, int K, int bn, SgemmTcMaps* maps);
 // a_row0 / b_row0: this GEMM's first row inside the mapped A / B^T (block
 // (i, j) of a larger product whose maps were encoded once)
 int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
                        void* stream, int splits, int a_row0 = 0, int b_row0 = 0);
-// split-K factor (thread-block cluster size, <= 8) for small C grids
-int sgemm_tc_splits(int M, int N, int K, int sms);
+// tile width (256 or 128 columns) and split-K factor (thread-block cluster
+// size, <= 8) for a C grid
+int sgemm_tc_pick_bn(int M, int N, int sms);
+int sgemm_tc_splits(int M, int N, int K, int sms, int bn);
 
 // Device FNV-1a-64 over u32 cells hashed big-endian (fnv.cu).
 size_t fnv_scratch_bytes(uint64_t n, int sms);

@@ -35,23 +35,33 @@
 namespace cafxg {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4;
+constexpr int BM = 128, BK = 16, STAGES = 4;
 constexpr int A_TILE = BM * BK * 4;                       // 8 KiB
-constexpr int B_TILE = BN * BK * 4;                       // 16 KiB
-constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;      // 48 KiB
 constexpr int EPI_WARPS = 8;                              // 2 per TMEM lane quadrant
 constexpr int TC_THREADS = 64 + EPI_WARPS * 32;           // TMA + MMA + epilogue
 constexpr int GROUP_M = 16;
-constexpr uint32_t TMEM_COLS = 512;                       // 2 x 256-column accumulators
 // K chunk per accumulator: the tensor core's fp32 accumulation rounds toward
 // zero, so its error grows linearly with the number of MMAs into one
 // accumulator (measured: 3.9e-5 normwise at K=4096 with a single
 // accumulator). Chunks of 128 K are summed by the epilogue in fp32 with
 // round-to-nearest, which keeps the error at the per-chunk level.
 constexpr int CHUNK_KB = 8;                               // k-blocks per chunk (128 K)
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-static_assert(BM * BN * 4 <= STAGES * STAGE_BYTES, "split-K partial must fit the stages");
 constexpr int kMaxSplits = 8;  // portable cluster size
+
+// Tile width BN = 256 (large grids) or 128 (grids too small to fill the SMs:
+// twice the CTAs per split-K factor, half the partial tile to reduce).
+template <int BN>
+struct Cfg {
+  static constexpr int B_TILE = BN * BK * 4;                 // 16 / 8 KiB
+  static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;  // 48 / 32 KiB
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;              // two BN-column accumulators
+  static constexpr int COLS = BN / 2;                        // epilogue: half a tile row
+  // Instruction descriptor: D=f32, A=B=tf32, K-major both, M=128, N=BN.
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  static_assert(BM * BN * 4 <= STAGES * STAGE_BYTES, "split-K partial must fit the stages");
+};
 
 // ---- PTX helpers -----------------------------------------------------------
 
@@ -101,17 +111,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: D=f32, A=B=tf32, K-major both, M=128, N=256.
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                            ((uint32_t)(BM >> 4) << 24);
-
+template <uint32_t IDESC>
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db,
                                          uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+      "l"(da), "l"(db), "r"(IDESC), "r"(accumulate));
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -139,6 +146,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 // split-K partial tile (128 x 256 fp32) in shared memory, float4 granules:
 // row r, column granule c4 (0..63) XOR-swizzled by r % 8 so a warp storing
 // one granule of 32 consecutive rows hits 8 distinct 16-byte bank groups
+template <int BN>
 __device__ __forceinline__ int partial_index(int r, int c4) {
   return r * (BN / 4) + (c4 ^ (r & 7));
 }
@@ -163,6 +171,7 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t local, uint32_t rank) {
 
 // ---- the GEMM kernel --------------------------------------------------------
 
+template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     sgemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAh,
                         const __grid_constant__ CUtensorMap mAl,
@@ -170,6 +179,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
                         int M, int N, int K, int ldc, int splits, int a_row0,
                         int b_row0) {
+  using G = Cfg<BN>;
+  constexpr int STAGE_BYTES = G::STAGE_BYTES, B_TILE = G::B_TILE;
   // a_row0 / b_row0: first row of this GEMM's A / B^T block inside the
   // matrices the tensor maps describe (a sub-block of a larger product)
   // split-K: the `splits` CTAs of one C tile form a thread-block cluster; CTA
@@ -219,7 +230,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
+                 "r"(G::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -251,7 +262,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
       const int chunk = kb / CHUNK_KB, kin = kb % CHUNK_KB;
-      const uint32_t acc = tmem + (uint32_t)(chunk & 1) * 256;
+      const uint32_t acc = tmem + (uint32_t)(chunk & 1) * BN;
       if (kin == 0)  // the epilogue must have drained this accumulator
         mbar_wait(&acc_empty[chunk & 1], ((chunk >> 1) & 1) ^ 1);
       mbar_wait(&full[s], ph);
@@ -263,9 +274,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int k = 0; k < BK / 8; ++k) {
         const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K
         const uint32_t acc0 = (kin | k) != 0;
-        mma_tf32(acc, umma_desc_sw64(al + off), umma_desc_sw64(bh + off), acc0);
-        mma_tf32(acc, umma_desc_sw64(ah + off), umma_desc_sw64(bl + off), 1);
-        mma_tf32(acc, umma_desc_sw64(ah + off), umma_desc_sw64(bh + off), 1);
+        mma_tf32<G::IDESC>(acc, umma_desc_sw64(al + off), umma_desc_sw64(bh + off), acc0);
+        mma_tf32<G::IDESC>(acc, umma_desc_sw64(ah + off), umma_desc_sw64(bl + off), 1);
+        mma_tf32<G::IDESC>(acc, umma_desc_sw64(ah + off), umma_desc_sw64(bh + off), 1);
       }
       umma_commit(&empty[s]);  // the stage is free once these MMAs retire
       if (kin == CHUNK_KB - 1 || kb == nk - 1)
@@ -274,12 +285,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp >= 2) {
     // ---- epilogue: sum the chunk accumulators in fp32 (RN), then store ----
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
-    const int half = (warp - 2) >> 2;       // which 128 columns of the tile
+    const int half = (warp - 2) >> 2;       // which half of the tile's columns
     const int row = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    float sum[128];
+    float sum[G::COLS];
 #pragma unroll
-    for (int j = 0; j < 128; ++j)
+    for (int j = 0; j < G::COLS; ++j)
       sum[j] = 0.0f;
     const int nchunks = (nk + CHUNK_KB - 1) / CHUNK_KB;
     for (int chunk = 0; chunk < nchunks; ++chunk) {
@@ -287,9 +298,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&acc_full[b], (chunk >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < G::COLS / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tmem + lane_base + (uint32_t)(b * 256 + half * 128 + c * 32), r);
+        tmem_ld32(tmem + lane_base + (uint32_t)(b * BN + half * G::COLS + c * 32), r);
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           sum[c * 32 + j] = __fadd_rn(sum[c * 32 + j], __uint_as_float(r[j]));
@@ -301,9 +312,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                      : "memory");
     }
     if (splits == 1) {
-      float* crow = C + (size_t)(m0 + row) * ldc + n0 + half * 128;
+      float* crow = C + (size_t)(m0 + row) * ldc + n0 + half * G::COLS;
 #pragma unroll
-      for (int j = 0; j < 128; j += 4)
+      for (int j = 0; j < G::COLS; j += 4)
         *reinterpret_cast<float4*>(crow + j) =
             make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
     } else {
@@ -311,8 +322,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // commit follows every MMA, so no TMA write or MMA read is pending
       float4* part = reinterpret_cast<float4*>(smem);
 #pragma unroll
-      for (int j = 0; j < 128; j += 4)
-        part[partial_index(row, half * 32 + j / 4)] =
+      for (int j = 0; j < G::COLS; j += 4)
+        part[partial_index<BN>(row, half * (G::COLS / 4) + j / 4)] =
             make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
     }
   }
@@ -324,7 +335,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t mine = smem_u32(smem);
     for (int i = threadIdx.x; i < rows * (BN / 4); i += TC_THREADS) {
       const int r = kz * rows + i / (BN / 4), c4 = i % (BN / 4);
-      const uint32_t off = (uint32_t)partial_index(r, c4) * 16u;
+      const uint32_t off = (uint32_t)partial_index<BN>(r, c4) * 16u;
       float4 acc = ld_cluster_f4(mine + off, 0);
       for (int z = 1; z < splits; ++z) {
         const float4 v = ld_cluster_f4(mine + off, (uint32_t)z);
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
+                 "r"(G::TMEM_COLS));
 }
 
 // ---- hi/lo split ----------------------------------------------------------
@@ -480,7 +491,7 @@ bool make_map(CUtensorMap* m, const float* base, int rows, int cols, int box_row
 
 bool sgemm_tc_supported(int M, int N, int K, int lda, int ldb, int ldc) {
   (void)ldb;
-  return M >= BM && N >= BN && K >= BK && M % BM == 0 && N % BN == 0 && K % 32 == 0 &&
+  return M >= BM && N >= 128 && K >= BK && M % BM == 0 && N % 128 == 0 && K % 32 == 0 &&
          lda % 4 == 0 && ldc % 4 == 0 && get_encoder() != nullptr;
 }
 
@@ -505,20 +516,35 @@ int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl
   return (int)cudaGetLastError();
 }
 
+namespace {
+
+template <int BN>
+void configure_once() {
+  // once per device (the attribute is per-device state)
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !(configured.load() >> dev & 1)) {
+    cudaFuncSetAttribute(sgemm_3xtf32_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg<BN>::SMEM_BYTES);
+    configured.fetch_or(1ull << dev);
+  }
+}
+
 // How many clusters of `splits` CTAs of the GEMM kernel can be resident at
 // once (clusters are placed within one GPC / die, so this is less than
 // sms / splits: e.g. 8-CTA clusters do not all fit 148 SMs).
-static int max_active_clusters(int splits) {
+template <int BN>
+int max_active_clusters(int splits) {
   static std::atomic<int> cache[kMaxSplits + 1];
   int v = cache[splits].load();
   if (v)
     return v;
-  cudaFuncSetAttribute(sgemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       SMEM_BYTES);
+  configure_once<BN>();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(splits * 256));
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = Cfg<BN>::SMEM_BYTES;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)splits;
@@ -527,7 +553,8 @@ static int max_active_clusters(int splits) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, sgemm_3xtf32_kernel, &cfg) != cudaSuccess || n < 1) {
+  if (cudaOccupancyMaxActiveClusters(&n, sgemm_3xtf32_kernel<BN>, &cfg) != cudaSuccess ||
+      n < 1) {
     cudaGetLastError();
     n = 148 / splits;
   }
@@ -535,31 +562,8 @@ static int max_active_clusters(int splits) {
   return n;
 }
 
-// Split-K factor (cluster size) for C grids too small to fill the GPU: the
-// largest power of two <= 8 whose clusters (one per C tile) are all resident
-// at once and that keeps every split >= 128 deep in K (one accumulator chunk).
-int sgemm_tc_splits(int M, int N, int K, int sms) {
-  (void)sms;
-  const int tiles = (M / BM) * (N / BN);
-  int s = 1;
-  while (s < kMaxSplits && tiles <= max_active_clusters(s * 2) && K % (16 * s * 2) == 0 &&
-         K / (s * 2) >= 128)
-    s *= 2;
-  return s;
-}
-
-int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
-                       const float* Bl, int N, int K, SgemmTcMaps* maps) {
-  static_assert(sizeof(CUtensorMap) <= sizeof(maps->m[0]), "tensor map storage");
-  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(maps->m);
-  if (!make_map(&m[0], Ah, a_rows, K, BM) || !make_map(&m[1], Al, a_rows, K, BM) ||
-      !make_map(&m[2], Bh, N, K, BN) || !make_map(&m[3], Bl, N, K, BN))
-    return (int)cudaErrorInvalidValue;
-  return 0;
-}
-
 // CAFXG_SGEMM_PDL=0 launches the GEMM without programmatic dependent launch
-static bool pdl_enabled() {
+bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("CAFXG_SGEMM_PDL");
     return !(e && e[0] == '0');
@@ -567,20 +571,10 @@ static bool pdl_enabled() {
   return on;
 }
 
-int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
-                       void* stream, int splits, int a_row0, int b_row0) {
-  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
-  {
-    // once per device (the attribute is per-device state)
-    static std::atomic<uint64_t> configured{0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !(configured.load() >> dev & 1)) {
-      cudaFuncSetAttribute(sgemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES);
-      configured.fetch_or(1ull << dev);
-    }
-  }
+template <int BN>
+int launch(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, void* stream,
+           int splits, int a_row0, int b_row0) {
+  configure_once<BN>();
   if (splits < 1 || splits > kMaxSplits || (splits & (splits - 1)) ||
       K % (16 * splits) != 0)
     splits = 1;
@@ -588,7 +582,7 @@ int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, i
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(tiles * splits));
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = Cfg<BN>::SMEM_BYTES;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -601,15 +595,69 @@ int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, i
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel, m[0], m[1], m[2], m[3], C, M, N, K, ldc,
+  cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel<BN>, m[0], m[1], m[2], m[3], C, M, N, K, ldc,
                      splits, a_row0, b_row0);
   return (int)cudaGetLastError();
 }
 
+}  // namespace
+
+// Tile width: 256 columns; 128 only for N a multiple of 128 but not 256. (A
+// 128-column tile halves the split-K partial a cluster reduces, but each of
+// its MMAs reads as much A as a 256-column one for half the work: at 1024^3
+// with split-K 2 it measured 36.0 us against 34.6 us for 256 columns with
+// split-K 4, and 2048^3 0.140 against 0.102 ms.) CAFXG_SGEMM_BN=128 forces
+// the narrow tile (experiments).
+int sgemm_tc_pick_bn(int M, int N, int sms) {
+  (void)M;
+  (void)sms;
+  static const int env = [] {
+    const char* e = getenv("CAFXG_SGEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  if (N % 256 != 0 || env == 128)
+    return 128;
+  return 256;
+}
+
+// Split-K factor (thread-block cluster size) for C grids too small to fill
+// the GPU: the largest power of two <= 8 whose clusters (one per C tile) are
+// all resident at once and that keeps every split >= 128 deep in K (one
+// accumulator chunk).
+int sgemm_tc_splits(int M, int N, int K, int sms, int bn) {
+  (void)sms;
+  const int tiles = (M / BM) * (N / bn);
+  int s = 1;
+  while (s < kMaxSplits && K % (16 * s * 2) == 0 && K / (s * 2) >= 128 &&
+         tiles <= (bn == 256 ? max_active_clusters<256>(s * 2)
+                             : max_active_clusters<128>(s * 2)))
+    s *= 2;
+  return s;
+}
+
+int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
+                       const float* Bl, int N, int K, int bn, SgemmTcMaps* maps) {
+  static_assert(sizeof(CUtensorMap) <= sizeof(maps->m[0]), "tensor map storage");
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(maps->m);
+  maps->bn = bn;
+  if (!make_map(&m[0], Ah, a_rows, K, BM) || !make_map(&m[1], Al, a_rows, K, BM) ||
+      !make_map(&m[2], Bh, N, K, bn) || !make_map(&m[3], Bl, N, K, bn))
+    return (int)cudaErrorInvalidValue;
+  return 0;
+}
+
+int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
+                       void* stream, int splits, int a_row0, int b_row0) {
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
+  if (maps->bn == 256)
+    return launch<256>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0);
+  return launch<128>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0);
+}
+
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl, float* C,
-                  int M, int N, int K, int ldc, void* stream, int splits) {
+                  int M, int N, int K, int ldc, void* stream, int splits, int bn) {
   SgemmTcMaps maps;
-  if (int e = sgemm_tc_make_maps(Ah, Al, M, Bh, Bl, N, K, &maps))
+  if (int e = sgemm_tc_make_maps(Ah, Al, M, Bh, Bl, N, K, bn, &maps))
     return e;
   return sgemm_tc_gemm_maps(&maps, C, M, N, K, ldc, stream, splits);
 }
@@ -623,15 +671,16 @@ int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int 
   float* Bl = Bh + (size_t)N * K;
   if ((size_t)M * K / 4 >= (1ull << 32))
     return (int)cudaErrorInvalidValue;
-  const int splits =
-      splits_req > 0 ? splits_req : sgemm_tc_splits(M, N, K, sm_count > 0 ? sm_count : 148);
+  const int sms = sm_count > 0 ? sm_count : 148;
+  const int bn = sgemm_tc_pick_bn(M, N, sms);
+  const int splits = splits_req > 0 ? splits_req : sgemm_tc_splits(M, N, K, sms, bn);
   const int nb_a = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 8);
   const int nb_b = (N / 32) * (K / 32);
   split_ab_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B, ldb,
                                                                  N, Bh, Bl, nb_a);
   int e = (int)cudaGetLastError();
   if (e == 0)
-    e = sgemm_tc_gemm(Ah, Al, Bh, Bl, C, M, N, K, ldc, stream, splits);
+    e = sgemm_tc_gemm(Ah, Al, Bh, Bl, C, M, N, K, ldc, stream, splits, bn);
   if (launches)
     *launches = 2;
   return e;

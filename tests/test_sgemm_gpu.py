@@ -165,6 +165,38 @@ def test_sgemm_3xtf32_k16384(ctx):
     assert err <= TOL, err
 
 
+@pytest.mark.parametrize("bn", ["128", "256"])
+def test_sgemm_3xtf32_both_tile_widths(bn):
+    """Both tile widths within the tolerance, split-K clusters included: 256
+    columns by default, 128 for N % 256 != 0 shapes or when CAFXG_SGEMM_BN=128
+    forces it."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+for M, N, K in [(1024, 1024, 1024), (2048, 2048, 512), (512, 256, 4096), (256, 384, 640)]:
+    if N %% 256 and %r == "256":
+        continue
+    A = oracle.fill_uniform(M * K, 81).reshape(M, K)
+    B = oracle.fill_uniform(K * N, 82).reshape(K, N)
+    with pkg.Context(1) as c:
+        C = c.sgemm(A, B, mode=pkg.SGEMM_3XTF32)
+    rows = np.arange(0, M, 37, dtype=np.uint32)
+    R = oracle.sgemm_ref_rows(A, B, rows, N, K)
+    err = oracle.sgemm_rel_err(C, R, rows, N)
+    assert err <= 1e-5, (M, N, K, err)
+print("ok")
+""" % (root, bn)
+    env = dict(os.environ, CAFXG_SGEMM_BN=bn)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
+
+
 def test_sgemm_3xtf32_rejects_unsupported_shape(ctx):
     A = np.zeros((100, 64), np.float32)
     B = np.zeros((64, 256), np.float32)
