@@ -48,6 +48,19 @@ W_IMG = H_IMG = 16384
 MAX_ITER = 1000
 REGION = (-0.75, -0.73, 0.10, 0.12)
 BAND_ROWS = 64          # 64 x 16384 = 1M-pixel bands, the planner's band size
+# CAFXG_VIRTUAL_DEVICES=V (tests only): the N-device code path on ONE GPU --
+# the context presents V devices on device 0 (its own streams each), torch
+# tensors of "device k" live on cuda:0. Never a measurement: the line says so.
+VIRTUAL = int(os.environ.get("CAFXG_VIRTUAL_DEVICES", "0") or 0)
+
+
+def phys(k: int) -> int:
+    """CUDA ordinal behind context device k."""
+    return 0 if VIRTUAL > 1 else k
+
+
+def ctx_mask(n: int) -> int:
+    return 1 if VIRTUAL > 1 else (1 << n) - 1
 METRIC = "Mandelbrot Giter/s (BASELINE cfg3: 16384^2 fp32 max_iter=1000 zoom)"
 WORKLOAD = ("cfg3: one 16384x16384 fp32 Mandelbrot request, max_iter=1000, "
             "x[-0.75,-0.73] y[0.10,0.12], pixel centres")
@@ -360,12 +373,12 @@ def cfg3_device(ctx, ndev, fp64, steps, warmup, clocks=None):
     full = pkg.mandel_desc(*REGION, W_IMG, H_IMG, MAX_ITER, fp64=fp64, centre=True)
     tiles = [band_tiles(full, ndev, k, BAND_ROWS, global_offsets=False) for k in range(ndev)]
     npx = [sum(t.nrows * t.ncols for t in tk) for tk in tiles]
-    outs = [torch.empty(npx[k], dtype=torch.int32, device=f"cuda:{k}") for k in range(ndev)]
+    outs = [torch.empty(npx[k], dtype=torch.int32, device=f"cuda:{phys(k)}") for k in range(ndev)]
     # 256 MiB per device written between steps (untimed): > the 126 MB L2
-    flush = [torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{k}") for k in range(ndev)]
+    flush = [torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{phys(k)}") for k in range(ndev)]
     # real streams: torch's default stream is the legacy NULL stream (handle
     # 0), which the C ABI would read as "use the context's own stream"
-    streams = [torch.cuda.Stream(device=k) for k in range(ndev)]
+    streams = [torch.cuda.Stream(device=phys(k)) for k in range(ndev)]
 
     def launch_all():
         for k in range(ndev):
@@ -374,12 +387,12 @@ def cfg3_device(ctx, ndev, fp64, steps, warmup, clocks=None):
     for _ in range(max(warmup, 1)):
         launch_all()
     for k in range(ndev):
-        torch.cuda.synchronize(k)
+        torch.cuda.synchronize(phys(k))
     iters_dev = [float(o.to(torch.int64).sum().item()) for o in outs]
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(ndev)] for _ in range(steps)]
     for k in range(ndev):
-        torch.cuda.synchronize(k)
+        torch.cuda.synchronize(phys(k))
     st0 = ctx.stats()
     if clocks:
         clocks.start()
@@ -392,7 +405,7 @@ def cfg3_device(ctx, ndev, fp64, steps, warmup, clocks=None):
         for k in range(ndev):
             ev[s][k][1].record(streams[k])
     for k in range(ndev):
-        torch.cuda.synchronize(k)
+        torch.cuda.synchronize(phys(k))
     clk = clocks.stop() if clocks else None
     st1 = ctx.stats()
     per_dev = [[ev[s][k][0].elapsed_time(ev[s][k][1]) for s in range(steps)]
@@ -447,6 +460,8 @@ def run_ours(args):
         sys.exit(f"bench.py: --gpus {N} under a torchrun world of {D.world}")
     import torch
     visible = torch.cuda.device_count()
+    if VIRTUAL > 1 and N == VIRTUAL and visible >= 1:
+        visible = N  # test mode: N virtual devices on one GPU
     if N < 1 or N > visible:
         # fail loudly: a --gpus N run must not silently measure fewer devices
         sys.exit(f"bench.py: --gpus {N} but {visible} CUDA device(s) visible")
@@ -468,12 +483,12 @@ def measure(args, N):
     import paper_1505_07368_b200 as pkg
     from oracle import oracle
     probe = fp_peak_probe()
-    ctx = pkg.Context(device_mask=(1 << N) - 1)
+    ctx = pkg.Context(device_mask=ctx_mask(N))
     assert ctx.device_count == N, (ctx.device_count, N)
     torch.cuda.set_device(0)
 
     # ---- headline: cfg3 fp32, one request over N devices ----
-    clocks = ClockSampler(range(N))
+    clocks = ClockSampler(sorted({phys(k) for k in range(N)}))
     dev = cfg3_device(ctx, N, False, args.steps, args.warmup, clocks)
     clk = dev["clocks"]
     step_ms = dev["step_ms"]
@@ -572,7 +587,9 @@ def measure(args, N):
         "metric": METRIC, "value": round(value, 3), "unit": "Giter/s", "n_gpus": N,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (deterministic plane grid, BASELINE cfg3)",
+        "data": "synthetic (deterministic plane grid, BASELINE cfg3)"
+                + ("; VIRTUAL DEVICES on one GPU (code-path test, not a measurement)"
+                   if VIRTUAL > 1 else ""),
         "config": {"workload": WORKLOAD,
                    "multi_device": f"one request, {N} device(s): one cafxg context over "
                                    f"devices 0..{N - 1}, 1M-pixel row bands dealt cyclically",
@@ -701,10 +718,10 @@ def sec_sgemm(ctx, args, n, N):
     A_h = oracle.fill_uniform(n * n, 1).reshape(n, n)
     B_h = oracle.fill_uniform(n * n, 2).reshape(n, n)
     rows = n // N
-    streams = [torch.cuda.Stream(device=k) for k in range(N)]
-    As = [torch.from_numpy(A_h[k * rows:(k + 1) * rows]).to(f"cuda:{k}") for k in range(N)]
-    Bs = [torch.from_numpy(B_h).to(f"cuda:{k}") for k in range(N)]
-    Cs = [torch.empty(rows, n, device=f"cuda:{k}") for k in range(N)]
+    streams = [torch.cuda.Stream(device=phys(k)) for k in range(N)]
+    As = [torch.from_numpy(A_h[k * rows:(k + 1) * rows]).to(f"cuda:{phys(k)}") for k in range(N)]
+    Bs = [torch.from_numpy(B_h).to(f"cuda:{phys(k)}") for k in range(N)]
+    Cs = [torch.empty(rows, n, device=f"cuda:{phys(k)}") for k in range(N)]
     reps = 20 if n <= 2048 else 3
 
     def launch_all():
@@ -714,7 +731,7 @@ def sec_sgemm(ctx, args, n, N):
 
     launch_all()
     for k in range(N):
-        torch.cuda.synchronize(k)
+        torch.cuda.synchronize(phys(k))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(N)]
     for k in range(N):
@@ -724,7 +741,7 @@ def sec_sgemm(ctx, args, n, N):
     for k in range(N):
         ev[k][1].record(streams[k])
     for k in range(N):
-        torch.cuda.synchronize(k)
+        torch.cuda.synchronize(phys(k))
     ms = max(ev[k][0].elapsed_time(ev[k][1]) for k in range(N)) / reps
     tflops = 2.0 * n ** 3 / (ms / 1e3) / 1e12
     samp = np.arange(0, n, max(1, n // 16), dtype=np.uint32)
@@ -801,7 +818,7 @@ def sec_actor_cafx(N, cfg3_fnv, cfg3_e2e_ms):
     exe = os.path.join(ROOT, "build", "tests", "actor_request_cafx")
     if not os.path.exists(exe):
         return {"skipped": "build/tests/actor_request_cafx not built (needs /root/reference)"}
-    r = subprocess.run([exe, str((1 << N) - 1)], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([exe, str(ctx_mask(N))], capture_output=True, text=True, timeout=600)
     try:
         j = json.loads(r.stdout.strip().splitlines()[-1])
     except (ValueError, IndexError):
@@ -920,7 +937,7 @@ def sec_cfg4(ctx, args, N, clients=64, per=1600):
             # steal sweeps) and with a 20 us back-off (scheduler_config::steal_sleep)
             for mode, sleep_us in (("closed", None), ("closed", 20), ("open", None),
                                    ("open", 20)):
-                cmd = [exe, dpath, epath, str(clients), str(per), mode, str((1 << N) - 1)]
+                cmd = [exe, dpath, epath, str(clients), str(per), mode, str(ctx_mask(N))]
                 if sleep_us is not None:
                     cmd.append(str(sleep_us))
                 r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)

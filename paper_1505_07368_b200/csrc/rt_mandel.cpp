@@ -216,6 +216,12 @@ MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
   c.grid = (int)std::max<uint64_t>(1, std::min(want, full));
   if (tune && tune->max_ctas)
     c.grid = std::min(c.grid, (int)tune->max_ctas);
+  static const int occ_env = [] {  // CAFXG_OCC=<CTAs per SM>: experiments only
+    const char* e = getenv("CAFXG_OCC");
+    return e ? atoi(e) : 0;
+  }();
+  if (occ_env > 0)
+    c.grid = std::min(c.grid, d->sms * occ_env);
   return c;
 }
 
