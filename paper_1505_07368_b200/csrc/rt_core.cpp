@@ -153,6 +153,35 @@ int check_alive(cafxg_ctx* ctx) {
               ctx->lost_why.c_str());
 }
 
+void issuer_loop(Device* d) {
+  cudaSetDevice(d->ordinal);
+  while (true) {
+    std::function<void()> fn;
+    {
+      std::unique_lock<std::mutex> lk(d->iq_mu);
+      d->iq_cv.wait(lk, [&] { return d->iq_stop || !d->iq.empty(); });
+      if (d->iq.empty())
+        return;
+      fn = std::move(d->iq.front());
+      d->iq.pop_front();
+    }
+    fn();
+  }
+}
+
+void issue_async(cafxg_ctx* ctx, Device* d, std::function<void()> fn) {
+  ctx->issuing.fetch_add(1);
+  {
+    std::lock_guard<std::mutex> lk(d->iq_mu);
+    d->iq.push_back([ctx, fn = std::move(fn)] {
+      fn();
+      ctx->issuing.fetch_sub(1);
+      ctx->sync_cv.notify_all();
+    });
+  }
+  d->iq_cv.notify_one();
+}
+
 // Records an event on `stream` and hands `fn` to the device's completion
 // thread. Caller holds d->submit_mu (so records stay in stream order).
 int push_completion(cafxg_ctx* ctx, Device* d, cudaStream_t stream,
@@ -350,8 +379,11 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
     if (const char* sl = getenv("CAFXG_SIMULATE_DEVICE_LOSS"))
       ctx->simulate_loss_at = (uint64_t)std::max(0, atoi(sl));
     cafxg_ctx* c = ctx.release();
-    for (auto& d : c->devs)
+    for (auto& d : c->devs) {
       d->completer = std::thread(completion_loop, c, d.get());
+      if (c->devs.size() > 1)
+        d->issuer = std::thread(issuer_loop, d.get());
+    }
     c->dispatcher = std::thread(dispatcher_loop, c);
     unsigned hw = std::thread::hardware_concurrency();
     unsigned ncb = std::max(1u, std::min(8u, hw / 4));
@@ -368,7 +400,8 @@ int cafxg_sync(cafxg_ctx* ctx) {
   if (!ctx)
     return fail(CAFXG_E_CONFIG, "sync: null ctx");
   std::unique_lock<std::mutex> lk(ctx->sync_mu);
-  while (!(ctx->completed == ctx->submitted && ctx->actor_open.load() == 0))
+  while (!(ctx->completed == ctx->submitted && ctx->actor_open.load() == 0 &&
+           ctx->issuing.load() == 0))
     ctx->sync_cv.wait_for(lk, std::chrono::milliseconds(1));
   return CAFXG_OK;
 }
@@ -397,6 +430,17 @@ int cafxg_close(cafxg_ctx* ctx) try {
   ctx->disp_cv.notify_all();
   if (ctx->dispatcher.joinable())
     ctx->dispatcher.join();
+  // issuers drain their queues first: what they issue reports through the
+  // completion threads below
+  for (auto& d : ctx->devs) {
+    {
+      std::lock_guard<std::mutex> lk(d->iq_mu);
+      d->iq_stop = true;
+    }
+    d->iq_cv.notify_all();
+    if (d->issuer.joinable())
+      d->issuer.join();
+  }
   // completion threads may still hand slices to the callback threads, so
   // those stop last (after the completion threads below)
   for (auto& d : ctx->devs) {

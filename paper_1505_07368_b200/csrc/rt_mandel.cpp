@@ -671,6 +671,25 @@ int mandel_submit_impl(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles,
   }
   join->remaining = parts;
   ctx->st_requests++;
+  if (parts > 1) {
+    // every device's share on its own issuer thread, all at once; a share
+    // that fails before queueing anything reports through the join itself
+    const bool tuned = tune != nullptr;
+    const cafxg_tuning tcopy = tuned ? *tune : cafxg_tuning{};
+    for (size_t k = 0; k < plan.size(); ++k) {
+      if (plan[k].empty())
+        continue;
+      Device* d = ctx->devs[k].get();
+      issue_async(ctx, d, [ctx, d, subs = std::move(plan[k]), host_out, pinned, exact, join, tuned,
+                      tcopy] {
+        const int s = submit_mandel_device(ctx, d, subs, host_out, pinned, exact, join,
+                                           tuned ? &tcopy : nullptr);
+        if (s != CAFXG_OK)
+          join->part_done(s);
+      });
+    }
+    return CAFXG_OK;
+  }
   for (size_t k = 0; k < plan.size(); ++k) {
     if (plan[k].empty())
       continue;

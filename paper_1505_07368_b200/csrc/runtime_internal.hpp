@@ -250,6 +250,14 @@ struct Device {
   size_t sgemm_ws_bytes = 0;
   cudaEvent_t trace_ref = nullptr;  // CAFXG_TRACE time base
   double trace_ref_ms = 0;
+  // issuer thread (multi-device contexts): the per-device share of a request
+  // is issued here, so every device's first wave starts at once instead of
+  // after the previous devices' host-side issue (~20 us per wave)
+  std::mutex iq_mu;
+  std::condition_variable iq_cv;
+  std::deque<std::function<void()>> iq;
+  bool iq_stop = false;
+  std::thread issuer;
 
   // Self-resetting scheduler slots: slot i is free again once the launch that
   // last used it has finished; sched_acquire orders `stream` after that launch
@@ -305,6 +313,7 @@ struct cafxg_ctx {
   std::thread dispatcher;
   std::atomic<uint32_t> rr{0};
   std::atomic<uint64_t> actor_open{0};  // enqueued, not yet completed
+  std::atomic<uint64_t> issuing{0};     // issuer tasks queued or running (cafxg_sync)
   // reply-callback threads (finish_batch)
   std::mutex cb_mu;
   std::condition_variable cb_cv;
@@ -373,6 +382,9 @@ inline void mark_used(cafxg_ctx* ctx, const Device* d) {
 }
 
 // ---- rt_core.cpp ----
+// runs `fn` on device d's issuer thread (multi-device contexts)
+void issue_async(cafxg_ctx* ctx, Device* d, std::function<void()> fn);
+void issuer_loop(Device* d);
 // marks the context lost after a sticky CUDA error (see cafxg_ctx::lost)
 void mark_lost(cafxg_ctx* ctx, cudaError_t e, const char* where);
 // CAFXG_E_DOWN (with the loss recorded as the error context) once lost
