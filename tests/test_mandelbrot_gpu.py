@@ -70,6 +70,40 @@ def test_cfg3_sampled_rows(ctx):
         ctx.pinned_free(out)
 
 
+def test_cfg3_full_image_two_kernels_agree():
+    """Full-size property for cfg3 (all 268M pixels; the oracle checks sampled
+    rows above): the per-step-checked kernel and the deferred-escape kernel are
+    independent code paths of the same op sequence, so their images must be
+    identical -- compared through the device FNV-1a of the whole image and the
+    sum of all counts, in fp32 and fp64."""
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+res = []
+for fp64 in (False, True):
+    d = pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 16384, 16384, 1000, fp64=fp64)
+    out = torch.empty(16384 * 16384, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with pkg.Context(1) as c:
+        c.mandelbrot_device(d, out.data_ptr(), s.cuda_stream)
+        torch.cuda.synchronize()
+        h = c.fnv1a_u32_device(out.data_ptr(), out.numel(), stream=s.cuda_stream)
+    res.append((h, int(out.to(torch.int64).sum().item())))
+print(res)
+""" % ROOT
+    outs = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, CAFXG_DEFERRED=mode)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs[mode] = r.stdout.strip().splitlines()[-1]
+    assert outs["0"] == outs["1"], outs
+    sums = eval(outs["1"])
+    assert 1.7e11 < sums[0][1] < 1.95e11   # SURVEY §8a: ~1.82e11 iterations (fp32)
+
+
 @pytest.mark.parametrize("fp64", [False, True])
 @pytest.mark.parametrize("centre", [False, True])
 def test_random_regions_vs_oracle(ctx, fp64, centre):

@@ -197,6 +197,30 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
 
 
+def test_cfg5_full_size_row_sum_property(ctx):
+    """Full-size property for cfg5 (16384^3, the sampled-row check covers a
+    few rows): C.1 = A.(B.1) for every row. B.1 and A.(B.1) are computed in
+    fp64 on the host; each row sum of the GPU's C must match within the
+    fp32-GEMM tolerance scaled to the row's magnitude (sum_j |C_ij| bound)."""
+    import torch
+    n = 16384
+    A_h = oracle.fill_uniform(n * n, 1).reshape(n, n)
+    B_h = oracle.fill_uniform(n * n, 2).reshape(n, n)
+    A, B = torch.from_numpy(A_h).cuda(), torch.from_numpy(B_h).cuda()
+    C = torch.empty(n, n, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    ctx.sgemm_device(n, n, n, A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    got = C.to(torch.float64).sum(dim=1).cpu().numpy()
+    absrow = C.abs().to(torch.float64).sum(dim=1).cpu().numpy()
+    del A, B, C
+    b1 = B_h.astype(np.float64).sum(axis=1)
+    want = A_h.astype(np.float64) @ b1
+    err = np.abs(got - want) / absrow
+    assert float(err.max()) <= 1e-5, float(err.max())
+
+
 def test_sgemm_3xtf32_rejects_unsupported_shape(ctx):
     A = np.zeros((100, 64), np.float32)
     B = np.zeros((64, 256), np.float32)
