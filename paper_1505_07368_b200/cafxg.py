@@ -15,7 +15,8 @@ from concurrent.futures import Future
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcafxg.so")
+# CAFXG_LIB: another build of the library (A/B experiments only)
+LIB_PATH = os.environ.get("CAFXG_LIB") or os.path.join(HERE, "libcafxg.so")
 
 OK = 0
 E_UNKNOWN_TYPE = 2

@@ -25,6 +25,7 @@
 //    contract the reference's separate mul and add into one FMA.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "mandelbrot.cuh"
@@ -437,10 +438,20 @@ struct Feeder {
   using Cd = typename Slots::C;
   static constexpr int NS = Slots::kSlots;
   uint32_t cur = 0, cend = 0, orow = 0;
+  uint32_t c0 = 0;            // first column of the chunk (inline mode)
   const Cd* cxp = nullptr;    // column table (table mode)
-  const MTile* Tc = nullptr;  // current tile (inline-coordinate mode)
   Cd ci_row = Cd(0);
   bool exhausted = false;
+
+  // Inline-coordinate launches: the warp's real parts of its current chunk,
+  // computed by all 32 lanes when the chunk is claimed (4 per lane, the
+  // fp64 divides at full SIMT width) instead of per refilled slot inside the
+  // refill's divergent branches (cfg1: every refill round paid up to one
+  // masked fp64 divide sequence per slot for a handful of pixels).
+  __device__ __forceinline__ static Cd* chunk_table() {
+    __shared__ Cd tab[kMandelThreads / 32][kChunkPx];
+    return tab[threadIdx.x >> 5];
+  }
 
   __device__ __forceinline__ void refill(const MLaunch& L, Slots& sl, uint32_t (&n)[NS],
                                          uint32_t (&o)[NS], uint32_t& live, uint32_t lt_mask) {
@@ -474,8 +485,15 @@ struct Feeder {
         cur = (local - crow * cpr) * kChunk;
         cend = min(cur + kChunk, ncols);
         if constexpr (kInlineCoords) {
-          Tc = T;
           ci_row = (Cd)grid_coord(T->y0, T->yspan, T->s, T->row0 + crow, T->height);
+          Cd* tab = chunk_table();
+          __syncwarp();  // the previous chunk's entries are no longer read
+#pragma unroll
+          for (uint32_t j = lane; j < kChunkPx; j += 32)
+            if (cur + j < cend)
+              tab[j] = (Cd)grid_coord(T->x0, T->xspan, T->s, T->col0 + cur + j, T->width);
+          __syncwarp();
+          c0 = cur;
         } else {
           cxp = static_cast<const Cd*>(T->cx);
           ci_row = __ldg(static_cast<const Cd*>(T->cy) + crow);
@@ -493,7 +511,7 @@ struct Feeder {
         if (!(live >> s & 1u) && r < avail) {
           Cd cr;
           if constexpr (kInlineCoords)
-            cr = (Cd)grid_coord(Tc->x0, Tc->xspan, Tc->s, Tc->col0 + cur + r, Tc->width);
+            cr = chunk_table()[cur - c0 + r];
           else
             cr = __ldg(cxp + cur + r);
           sl.start(s, cr, ci_row);
@@ -860,22 +878,37 @@ int launch_t(const MLaunch& L, int grid, cudaStream_t s) {
   return (int)cudaGetLastError();
 }
 
+// Opts kernel `f` into `bytes` of dynamic shared memory on the current device
+// (the attribute is per-device state: once per device and kernel).
+template <class F>
+cudaError_t opt_in_smem(F* f, size_t bytes, std::atomic<uint64_t>& done_mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && (done_mask.load(std::memory_order_acquire) >> dev & 1))
+    return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && dev < 64)
+    done_mask.fetch_or(1ull << dev);
+  return e;
+}
+
 template <class A, int kUnit, bool kExact>
 int launch_deferred_t(const MLaunch& L, int grid, cudaStream_t s) {
   constexpr size_t smem = deferred_smem_bytes<A>();
   if (L.direct) {
-    // the direct-reply counters (static shared memory) push the fp32 kernel
-    // past the 48 KB that needs no opt-in
-    static const cudaError_t opt = cudaFuncSetAttribute(
-        mandel_deferred_kernel<A, kUnit, kExact, 2>,
-        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (opt != cudaSuccess)
-      return (int)opt;
+    // the direct-reply counters and the chunk coordinate tables (static
+    // shared memory) push the kernel past the 48 KB that needs no opt-in
+    static std::atomic<uint64_t> opted{0};
+    if (cudaError_t e = opt_in_smem(mandel_deferred_kernel<A, kUnit, kExact, 2>, smem, opted))
+      return (int)e;
     mandel_deferred_kernel<A, kUnit, kExact, 2><<<grid, kMandelThreads, smem, s>>>(L);
-  }
-  else if (L.inline_coords)
+  } else if (L.inline_coords) {
+    static std::atomic<uint64_t> opted{0};  // (the chunk coordinate tables, as above)
+    if (cudaError_t e = opt_in_smem(mandel_deferred_kernel<A, kUnit, kExact, 1>, smem, opted))
+      return (int)e;
     mandel_deferred_kernel<A, kUnit, kExact, 1><<<grid, kMandelThreads, smem, s>>>(L);
-  else
+  } else
     mandel_deferred_kernel<A, kUnit, kExact, 0><<<grid, kMandelThreads, smem, s>>>(L);
   return (int)cudaGetLastError();
 }
