@@ -330,8 +330,13 @@ class gpu_actor final : public cafx::abstract_actor {
     job->env = std::move(env);  // keeps the request payload alive
     int s = cafxg_actor_enqueue(backend_, in, in_bytes, n_in, out, reply, &gpu_actor::on_done,
                                 job.get());
-    if (s != CAFXG_OK)
-      return fail(*job->env, static_cast<cafx::errc>(s), cafxg_last_error());
+    if (s != CAFXG_OK) {
+      fail(*job->env, static_cast<cafx::errc>(s), cafxg_last_error());
+      // the context was lost through another actor's request: terminate too
+      if (s == CAFXG_E_DOWN && cafxg_ctx_status(ctx_) != CAFXG_OK)
+        terminate(cafx::exit_reason::unhandled_error());
+      return;
+    }
     job.release();  // owned by the backend until on_done
   }
 
@@ -355,10 +360,11 @@ class gpu_actor final : public cafx::abstract_actor {
     if (self->terminated())
       return;  // pending requesters already got request_down from finalize
     if (status != CAFXG_OK) {
+      // (delivered here, not through the relay: a terminating actor's
+      // requester gets the error before monitors get the down message)
       self->respond(*job->env,
                     cafx::make_message(cafx::error{static_cast<cafx::errc>(status),
-                                                   cafxg_last_error()}),
-                    true, false);
+                                                   cafxg_last_error()}));
       // a sticky device error: the backend cannot serve anything any more,
       // so the actor terminates (monitors, links and pending requesters fire,
       // abstract_actor.cpp:108-134) instead of failing requests one by one
@@ -634,7 +640,11 @@ cafx::typed_actor spawn_cl(cafx::actor_system& sys, cafxg_ctx* ctx, const std::s
 }
 
 /// spawn_cl's data-transformation overload: the actor shows other actors an
-/// interface of its own instead of the kernel signature. `map_args` maps a
+/// interface of its own instead of the kernel signature. map_args runs on the
+/// sender's thread (inside enqueue), map_result on a cafx worker (the reply
+/// relay), both possibly concurrently for different requests: they must not
+/// share unsynchronised state (stateless lambdas, as in the examples).
+/// `map_args` maps a
 /// request to the kernel's input message (each of its cases must produce
 /// exactly Sig's input buffers), `map_result` maps the kernel's output buffer
 /// to the reply (its one case takes Sig's output buffer). The typed handle's

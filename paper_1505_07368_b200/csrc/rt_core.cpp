@@ -108,6 +108,11 @@ void completion_loop(cafxg_ctx* ctx, Device* d) {
       ++ctx->completed;
     }
     ctx->sync_cv.notify_all();
+    // The dispatcher's wait predicate reads `inflight`: taking its mutex
+    // between the decrement and the notify keeps the notify from falling
+    // between its predicate check and its sleep (a lost wakeup stalled a
+    // closed-loop storm with every device at its in-flight cap).
+    { std::lock_guard<std::mutex> lk(ctx->disp_mu); }
     ctx->disp_cv.notify_all();
   }
 }
@@ -142,6 +147,7 @@ void mark_lost(cafxg_ctx* ctx, cudaError_t e, const char* where) {
     ctx->lost_why = std::string(where) + ": " + cudaGetErrorName(e);
   }
   ctx->lost.store(true);
+  { std::lock_guard<std::mutex> lk(ctx->disp_mu); }  // see completion_loop
   ctx->disp_cv.notify_all();
 }
 

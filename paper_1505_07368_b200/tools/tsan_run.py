@@ -29,12 +29,20 @@ def run(cmd, env):
 def main():
     import bench
     from oracle import oracle
+    supp = os.path.join(ROOT, "tests", "tsan.supp")
     env = dict(os.environ, TSAN_OPTIONS="halt_on_error=0 report_signal_unsafe=0 "
-                                        "second_deadlock_stack=1 history_size=4")
+                                        "second_deadlock_stack=1 history_size=4 "
+                                        f"suppressions={supp}")
     bt = os.path.join(ROOT, "build", "tests")
     total_w = 0
     rc, w = run([os.path.join(bt, "test_gpu_actor_tsan")], env)
     total_w += w
+    # the same checks on a 3-device context (virtual devices on one GPU):
+    # multi-device splitting, per-device issuer threads, peer-copy sgemm
+    rc3, w = run([os.path.join(bt, "test_gpu_actor_tsan")],
+                 dict(env, CAFXG_VIRTUAL_DEVICES="3"))
+    total_w += w
+    rc = rc or rc3
     clients, per = 16, 64
     arr = bench.storm_descs(clients * per, seed=77)
     import paper_1505_07368_b200 as pkg

@@ -425,6 +425,34 @@ int main() {
                    "failure(interface_mismatch)");
     }
 
+    // 10. a large request (>= 1M pixels leaves the batching path: row bands
+    //     over every device of the context -- with CAFXG_VIRTUAL_DEVICES, the
+    //     per-device issuer threads -- and overlapped waves into the reply)
+    {
+      auto big = cafxg::spawn_gpu(sys, ctx, "mandelbrot", {});
+      cafxg_mandel_desc d{};
+      d.x0 = -2.0; d.x1 = 1.0; d.y0 = -1.0; d.y1 = 1.0;
+      d.width = d.ncols = 1536;
+      d.height = d.nrows = 1024;
+      d.max_iter = 200;
+      d.precision = CAFXG_FP64;
+      d.sampling = CAFXG_CENTRE;
+      auto res = self->request(big, cafx::make_message(cafxg::mandel_tiles{{d}}), 60s);
+      bool ok = std::holds_alternative<cafx::message>(res);
+      if (ok) {
+        const auto& counts = std::get<cafx::message>(res).get<cafxg::u32vec>(0);
+        ok = counts.size() == 1536u * 1024u;
+        for (uint32_t r = 0; ok && r < 1024; r += 31)
+          for (uint32_t c = 0; ok && c < 1536; ++c) {
+            const double ci = d.y0 + (((double)r + 0.5) * (d.y1 - d.y0)) / 1024;
+            const double cr = d.x0 + (((double)c + 0.5) * (d.x1 - d.x0)) / 1536;
+            ok = counts[r * 1536 + c] == cafx::bench::mandelbrot_cell(cr, ci, 200);
+          }
+      }
+      check(ok, "large request (1.5M pixels) through the actor: bands over every device, "
+                "sampled rows = the reference's mandelbrot_cell");
+    }
+
     // 9. device loss: a sticky CUDA error (simulated on a second context:
     //    CAFXG_SIMULATE_DEVICE_LOSS makes its 2nd completion report
     //    cudaErrorLaunchFailure, as a real fault would) terminates the compute
@@ -442,12 +470,18 @@ int main() {
       auto r1 = self->request(mb, cafx::make_message(cafxg::mandel_tiles{{d}}), 60s);
       auto r2 = self->request(mb, cafx::make_message(cafxg::mandel_tiles{{d}}), 60s);
       bool down = false, unhandled = false;
-      self->receive(cafx::behavior{[&](cafx::down_atom, cafx::actor_addr src,
-                                       cafx::exit_reason reason) {
-                      down = src == mb.address();
-                      unhandled = reason.k == cafx::exit_reason::kind::unhandled_error;
-                    }},
-                    30s);
+      int reason_kind = -1;
+      const bool got = self->receive(cafx::behavior{[&](cafx::down_atom, cafx::actor_addr src,
+                                                        cafx::exit_reason reason) {
+                                       down = src == mb.address();
+                                       reason_kind = (int)reason.k;
+                                       unhandled =
+                                           reason.k == cafx::exit_reason::kind::unhandled_error;
+                                     }},
+                                     30s);
+      if (!(down && unhandled))
+        std::printf("  (down message received: %d, from the actor: %d, reason kind %d)\n",
+                    (int)got, (int)down, reason_kind);
       auto r3 = self->request(mb, cafx::make_message(cafxg::mandel_tiles{{d}}), 30s);
       auto code_of = [](const auto& r) {
         return std::holds_alternative<cafx::error>(r) ? (int)std::get<cafx::error>(r).code : -1;
