@@ -39,7 +39,7 @@ constexpr int BM = 128, BK = 16, STAGES = 4;
 constexpr int A_TILE = BM * BK * 4;                       // 8 KiB
 constexpr int EPI_WARPS = 8;                              // 2 per TMEM lane quadrant
 constexpr int TC_THREADS = 64 + EPI_WARPS * 32;           // TMA + MMA + epilogue
-constexpr int GROUP_M = 16;
+constexpr int GROUP_M = 16;  // default raster group (CAFXG_SGEMM_GROUP_M overrides)
 // K chunk per accumulator: the tensor core's fp32 accumulation rounds toward
 // zero, so its error grows linearly with the number of MMAs into one
 // accumulator (measured: 3.9e-5 normwise at K=4096 with a single
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         const __grid_constant__ CUtensorMap mBh,
                         const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
                         int M, int N, int K, int ldc, int splits, int a_row0,
-                        int b_row0) {
+                        int b_row0, int group_m) {
   using G = Cfg<BN>;
   constexpr int STAGE_BYTES = G::STAGE_BYTES, B_TILE = G::B_TILE;
   // a_row0 / b_row0: first row of this GEMM's A / B^T block inside the
@@ -201,11 +201,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   // grouped raster: GROUP_M consecutive M tiles share each N tile
   const int tiles_m = M / BM, tiles_n = N / BN;
-  const int per_group = GROUP_M * tiles_n;
+  const int per_group = group_m * tiles_n;
   const int kz = blockIdx.x % splits;   // == %cluster_ctarank (cluster = splits x 1 x 1)
   const int bid = blockIdx.x / splits;
-  const int first_m = (bid / per_group) * GROUP_M;
-  const int gsize = min(GROUP_M, tiles_m - first_m);
+  const int first_m = (bid / per_group) * group_m;
+  const int gsize = min(group_m, tiles_m - first_m);
   const int in_group = bid % per_group;
   const int m0 = (first_m + in_group % gsize) * BM;
   const int n0 = (in_group / gsize) * BN;
@@ -595,8 +595,13 @@ int launch(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, void* s
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  static const int group_m = [] {
+    const char* e = getenv("CAFXG_SGEMM_GROUP_M");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : GROUP_M;
+  }();
   cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel<BN>, m[0], m[1], m[2], m[3], C, M, N, K, ldc,
-                     splits, a_row0, b_row0);
+                     splits, a_row0, b_row0, group_m);
   return (int)cudaGetLastError();
 }
 
