@@ -201,6 +201,7 @@ inline uint64_t now_ns() {
 // reply), others by one scatter launch straight into the pinned reply buffers
 // (or one D2H into a pinned bounce buffer + host memcpy for pageable replies).
 void run_mandel_batch(cafxg_ctx* ctx, Device* d, std::vector<Request*> batch) {
+  NvtxRange nvtx_range("cafxg.actor.batch");
   const double t_begin = trace_now_ms();
   uint64_t ph = now_ns();
   auto phase = [&](int i) {

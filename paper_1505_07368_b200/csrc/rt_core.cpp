@@ -97,7 +97,10 @@ void completion_loop(cafxg_ctx* ctx, Device* d) {
       status = cuda_status(e, "device work failed");
       mark_lost(ctx, e, "device work failed");
     }
-    c.fn(status);
+    {
+      NvtxRange nvtx_range("cafxg.complete");
+      c.fn(status);
+    }
     {
       std::lock_guard<std::mutex> lk(d->cq_mu);
       d->ev_free.push_back(c.ev);

@@ -420,6 +420,7 @@ int submit_mandel_device(cafxg_ctx* ctx, Device* d,
                                 const std::vector<SubTile>& subs,
                                 uint32_t* host_out, bool out_pinned,
                                 bool exact, Join* join, const cafxg_tuning* tune) {
+  NvtxRange nvtx_range("cafxg.mandelbrot.device_share");
   cudaSetDevice(d->ordinal);
   std::lock_guard<std::mutex> g(d->submit_mu);
   static const uint64_t wave_px = [] {  // CAFXG_WAVE_MPX: experiments only
@@ -641,6 +642,7 @@ int submit_mandel_device(cafxg_ctx* ctx, Device* d,
 int mandel_submit_impl(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles,
                               size_t n, uint32_t* host_out, cafxg_done_fn done,
                               void* user, const cafxg_tuning* tune) {
+  NvtxRange nvtx_range("cafxg.mandelbrot.submit");
   if (!ctx || (n && !tiles) || (n && !host_out))
     return fail(CAFXG_E_CONFIG, "mandelbrot_submit: null argument");
   CAFXG_TRY(check_alive(ctx));
@@ -819,6 +821,7 @@ int cafxg_fnv1a_u32_device(cafxg_ctx* ctx, int device, const uint32_t* cells, ui
 // collector hash (bench.cpp:329-331) without moving the image off the GPUs.
 int cafxg_run_mandelbrot(cafxg_ctx* ctx, uint32_t size, uint32_t max_iter, uint64_t* checksum,
                          double* wall_ms) try {
+  NvtxRange nvtx_range("cafxg.run_mandelbrot");
   if (!ctx || !checksum || size == 0)
     return fail(CAFXG_E_CONFIG, "run_mandelbrot: bad argument");
   auto t0 = std::chrono::steady_clock::now();

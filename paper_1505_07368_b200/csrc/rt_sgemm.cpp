@@ -439,6 +439,7 @@ int sgemm_tiled2d_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
 int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
                              const float* A, const float* B, float* C,
                              cafxg_done_fn done, void* user) {
+  NvtxRange nvtx_range("cafxg.sgemm.submit");
   if (!ctx || !desc)
     return fail(CAFXG_E_CONFIG, "sgemm_submit: null argument");
   cafxg_sgemm_desc g = *desc;

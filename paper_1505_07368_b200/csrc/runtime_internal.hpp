@@ -8,6 +8,7 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -380,6 +381,15 @@ struct SubTile {
 inline void mark_used(cafxg_ctx* ctx, const Device* d) {
   ctx->st_dev_used.fetch_or(1ull << (d->index & 63), std::memory_order_relaxed);
 }
+
+// NVTX range over a host-side scope (request submission, batches, reply
+// callbacks): visible in Nsight Systems / ncu timelines, a no-op without a tool
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---- rt_core.cpp ----
 // runs `fn` on device d's issuer thread (multi-device contexts)
