@@ -30,9 +30,16 @@ def main():
     import bench
     from oracle import oracle
     supp = os.path.join(ROOT, "tests", "tsan.supp")
-    env = dict(os.environ, TSAN_OPTIONS="halt_on_error=0 report_signal_unsafe=0 "
-                                        "second_deadlock_stack=1 history_size=4 "
-                                        f"suppressions={supp}")
+    # CAFX_WORKERS=4: under TSAN's slowdown the reference scheduler's idle
+    # workers (hardware_concurrency of them, each sweeping the others' deques
+    # under mutexes, scheduler.hpp:374-402) starve the instrumented backend
+    # threads on a 16-core host with a 3-device context (the storm crawled:
+    # 60 s timeouts with 16 workers, 2.5 s with 4; without TSAN 16 workers run
+    # it in ~20 ms)
+    env = dict(os.environ, CAFX_WORKERS="4",
+               TSAN_OPTIONS="halt_on_error=0 report_signal_unsafe=0 "
+                            "second_deadlock_stack=1 history_size=4 "
+                            f"suppressions={supp}")
     bt = os.path.join(ROOT, "build", "tests")
     total_w = 0
     rc, w = run([os.path.join(bt, "test_gpu_actor_tsan")], env)

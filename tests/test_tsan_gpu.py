@@ -19,5 +19,5 @@ def test_no_thread_sanitizer_reports():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "paper_1505_07368_b200", "tools",
                                                      "tsan_run.py")],
                        capture_output=True, text=True, timeout=1500)
-    assert "TOTAL ThreadSanitizer warnings: 0; exit codes ok: True" in r.stdout, \
-        r.stdout[-4000:] + r.stderr[-2000:]
+    print(r.stdout)  # the whole log in the captured output of a failure
+    assert "TOTAL ThreadSanitizer warnings: 0; exit codes ok: True" in r.stdout
