@@ -236,6 +236,11 @@ int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in,
 /* Expected reply size in bytes for the given inputs (0 on error). */
 size_t cafxg_actor_reply_bytes(cafxg_actor* a, const void* const* in,
                                const size_t* in_bytes, size_t n_in);
+/* Inside a done callback of cafxg_actor_enqueue: how many request completions
+ * the backend is delivering together with this one on this thread (the
+ * requests of one launch), 1 for a lone reply. Lets an adapter batch the
+ * delivery of many replies and hand a lone one over at once. */
+size_t cafxg_completion_batch(void);
 /* Terminates the actor: queued (not yet launched) requests complete with
  * CAFXG_E_DOWN, launched ones finish normally; later enqueues fail with
  * CAFXG_E_DOWN. Mirrors the hard-kill exit path (actor_system.cpp:243-258). */

@@ -43,11 +43,12 @@
 //    exit_reason::unhandled_error;
 //  * buffer types are registered with wire codecs (type_registry.hpp:74-80),
 //    so middleman::publish can serve a GPU actor to remote nodes;
-//  * reply relay: a reply leaves libcafxg's completion thread through a
-//    lock-free per-actor queue drained by a job on the cafx scheduler
-//    (actor_system::schedule_job, scheduler.hpp:266-274), so the requesters
-//    are made runnable from a worker thread (its own deque) and a whole batch
-//    of replies costs one external enqueue instead of one each. External
+//  * reply relay: the replies of a batch (cafxg_completion_batch() > 1)
+//    leave libcafxg's completion thread through a lock-free per-actor queue
+//    drained by a job on the cafx scheduler (actor_system::schedule_job,
+//    scheduler.hpp:266-274), so the requesters are made runnable from a
+//    worker thread (its own deque) and a whole batch of replies costs one
+//    external enqueue instead of one each; a lone reply is delivered at once. External
 //    enqueues contend with the idle workers' steal sweeps over the deque
 //    mutexes (scheduler.hpp:374-402): delivering from a foreign thread cost
 //    ~15 us per reply against ~2.5-8 us relayed (a CPU probe of the pattern,
@@ -375,7 +376,12 @@ class gpu_actor final : public cafx::abstract_actor {
     cafx::message reply = self->kernel_ == "mandelbrot"
                               ? cafx::make_message(std::move(job->counts))
                               : cafx::make_message(std::move(job->floats));
-    self->respond(*job->env, std::move(reply), true, self->map_result_.defined());
+    // replies of a batch go through the relay (one external enqueue for all
+    // of them); a lone reply is delivered right here -- through the relay it
+    // would wait for an idle cafx worker to wake (up to the 1 ms steal
+    // back-off) for no saving. map_result always runs on a worker.
+    const bool relay = self->map_result_.defined() || cafxg_completion_batch() > 1;
+    self->respond(*job->env, std::move(reply), relay, self->map_result_.defined());
   }
 
   // local_actor::respond (local_actor.cpp:319-329). `relay`: hand the reply

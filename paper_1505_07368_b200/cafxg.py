@@ -41,7 +41,7 @@ EXPORTS = [
     "cafxg_fnv1a_u32_device", "cafxg_run_mandelbrot",
     "cafxg_sgemm_submit", "cafxg_sgemm", "cafxg_sgemm_device",
     "cafxg_spawn", "cafxg_spawn_ex", "cafxg_kernel_signature",
-    "cafxg_actor_enqueue", "cafxg_actor_reply_bytes",
+    "cafxg_actor_enqueue", "cafxg_actor_reply_bytes", "cafxg_completion_batch",
     "cafxg_actor_quit", "cafxg_actor_release", "cafxg_get_stats",
 ]
 
@@ -128,6 +128,7 @@ def lib() -> C.CDLL:
         L.cafxg_kernel_signature.argtypes = [C.c_char_p, C.c_char_p, sz]
         L.cafxg_actor_enqueue.argtypes = [vp, C.POINTER(vp), C.POINTER(sz), sz, vp, sz,
                                           DONE_FN, vp]
+        L.cafxg_completion_batch.restype = sz
         L.cafxg_actor_reply_bytes.restype = sz
         L.cafxg_actor_reply_bytes.argtypes = [vp, C.POINTER(vp), C.POINTER(sz), sz]
         L.cafxg_actor_quit.argtypes = [vp]

@@ -24,6 +24,10 @@ struct cafxg_actor {
 };
 
 namespace cafxg {
+// replies delivered together with the current done callback on this thread
+// (cafxg_completion_batch); 1 outside finish_batch's slices
+thread_local size_t t_completion_batch = 1;
+
 // requests of actors spawned with different tuning never share a launch
 static bool same_tuning(const cafxg_actor* a, const cafxg_actor* b) {
   return a == b || std::memcmp(&a->tune, &b->tune, sizeof(cafxg_tuning)) == 0;
@@ -107,6 +111,7 @@ void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* bounce,
   auto run_slice = [ctx, status](Request* const* rs, size_t cnt, uint64_t pix_off,
                                  const uint32_t* src) {
     uint64_t o = pix_off;
+    t_completion_batch = cnt;  // cafxg_completion_batch() inside the callbacks
     for (size_t i = 0; i < cnt; ++i) {
       Request* r = rs[i];
       if (src && status == CAFXG_OK)
@@ -114,6 +119,7 @@ void finish_batch(cafxg_ctx* ctx, std::vector<Request*> batch, uint32_t* bounce,
       o += r->pixels;
       finish_request(r, status, false);
     }
+    t_completion_batch = 1;
     ctx->st_requests += cnt;
     ctx->actor_open.fetch_sub(cnt);
     ctx->sync_cv.notify_all();
@@ -532,28 +538,6 @@ void dispatcher_loop(cafxg_ctx* ctx) {
         ctx->st_requests--;  // counted by finish_request
         break;
       }
-      if (r->pixels >= kLargeActorPx) {
-        // a large request is not batched: it takes the host-request path --
-        // 1M-pixel row bands dealt cyclically over every device of the
-        // context, waves whose copy-out overlaps the next wave's kernel --
-        // with the reply buffer as the output (its tiles are packed in order,
-        // cafxg_actor_enqueue recomputed their offsets)
-        if (!batch.empty())
-          break;
-        queue.pop_front();
-        queued_px -= r->pixels;
-        std::vector<cafxg_mandel_desc> tiles(r->ntiles);
-        for (uint32_t k = 0; k < r->ntiles; ++k)
-          tiles[k] = r->tile(k);
-        int s = mandel_submit_impl(
-            ctx, tiles.data(), tiles.size(), static_cast<uint32_t*>(r->out),
-            [](void* u, int st) { finish_request((Request*)u, st); }, r, &r->actor->tune);
-        if (s != CAFXG_OK)
-          push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); });
-        else
-          ctx->st_requests--;  // counted by finish_request
-        break;
-      }
       if (!batch.empty() &&
           (r->precision != batch[0]->precision || !same_tuning(r->actor, batch[0]->actor) ||
            px + r->pixels > kMaxBatchPx))
@@ -607,6 +591,8 @@ static int kernel_by_name(const char* name, Kernel* k) {
     return fail(CAFXG_E_UNKNOWN_TYPE, "spawn: no kernel named '%s'", name);
   return CAFXG_OK;
 }
+
+size_t cafxg_completion_batch(void) { return t_completion_batch; }
 
 int cafxg_kernel_signature(const char* kernel_name, char* buf, size_t cap) {
   if (!kernel_name || !buf)
@@ -768,6 +754,30 @@ int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in, const size_t* in_
   a->pending.fetch_add(1);
   cafxg_ctx* ctx = a->ctx;
   ctx->actor_open.fetch_add(1);
+  if (a->kernel == Kernel::mandelbrot && r->pixels >= kLargeActorPx) {
+    // a large request is never batched: submitted from the caller's thread
+    // straight into the host-request path (row bands over every device,
+    // overlapped waves), which saves the dispatcher hop (~10 us of a 0.2 ms
+    // cfg1 request); non-blocking like the inbox
+    std::vector<cafxg_mandel_desc> tiles(r->ntiles);
+    for (uint32_t k = 0; k < r->ntiles; ++k)
+      tiles[k] = r->tile(k);
+    const int s = mandel_submit_impl(
+        ctx, tiles.data(), tiles.size(), static_cast<uint32_t*>(r->out),
+        [](void* u, int st) { finish_request((Request*)u, st); }, r, &a->tune);
+    if (s != CAFXG_OK) {
+      std::string err = t_last_error;
+      Device* d = ctx->devs[0].get();
+      std::lock_guard<std::mutex> g(d->submit_mu);
+      if (push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); }) !=
+          CAFXG_OK)
+        finish_request(r, s);
+      t_last_error = err;
+    } else {
+      ctx->st_requests--;  // counted by finish_request
+    }
+    return CAFXG_OK;
+  }
   Request* head = ctx->inbox.load(std::memory_order_relaxed);
   do {
     r->next = head;
