@@ -933,14 +933,19 @@ def sec_cfg4(ctx, args, N, clients=64, per=1600):
             dpath, epath = os.path.join(td, "descs.bin"), os.path.join(td, "expect.u32")
             arr.tofile(dpath)
             expect.tofile(epath)
-            # the reference scheduler as shipped (idle workers sleep 1 ms between
-            # steal sweeps) and with a 20 us back-off (scheduler_config::steal_sleep)
-            for mode, sleep_us in (("closed", None), ("closed", 20), ("open", None),
-                                   ("open", 20)):
+            # the reference scheduler with its default configuration, and with
+            # CAFX_WORKERS set to the same worker count: left at 0, the
+            # worker count is re-derived from std::thread::hardware_concurrency()
+            # (a sysfs read) on every central enqueue and every steal sweep
+            # (scheduler.hpp:39-44,143-145,353,385), which costs the closed loop
+            # ~5x
+            cores = str(os.cpu_count() or 1)
+            base = {k: v for k, v in os.environ.items() if k != "CAFX_WORKERS"}
+            for mode, workers in (("closed", None), ("closed", cores), ("open", None),
+                                  ("open", cores)):
                 cmd = [exe, dpath, epath, str(clients), str(per), mode, str(ctx_mask(N))]
-                if sleep_us is not None:
-                    cmd.append(str(sleep_us))
-                r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+                env = base if workers is None else dict(base, CAFX_WORKERS=workers)
+                r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
                 try:
                     j = json.loads(r.stdout.strip().splitlines()[-1])
                 except (ValueError, IndexError):
@@ -953,7 +958,8 @@ def sec_cfg4(ctx, args, N, clients=64, per=1600):
                               "(multiset; async replies carry no request id)")
                 j["path"] = ("cafx event_based_actor clients (unmodified reference runtime) "
                              "-> gpu_actor (include/cafxg/gpu_actor.hpp) -> libcafxg")
-                tag = "" if sleep_us is None else f"_steal_sleep_{sleep_us}us"
+                j["cafx_workers_env"] = workers
+                tag = "" if workers is None else "_cafx_workers_set"
                 out[f"cfg4_request_storm_cafx_actors_{mode}_loop{tag}"] = j
     return out
 

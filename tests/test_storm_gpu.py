@@ -3,8 +3,8 @@ size -- the native driver in its three client disciplines (open loop, closed
 loop with one OS thread per client, closed loop with the clients multiplexed
 on worker threads like cafx actors) and the cafx client actors on the
 unmodified reference runtime (tools/storm_cafx.cpp, closed and open loop, the
-scheduler as shipped and with a short idle back-off); every reply of every
-mode checked against the reference's own mandelbrot_cell."""
+scheduler in its default configuration and with CAFX_WORKERS set); every
+reply of every mode checked against the reference's own mandelbrot_cell."""
 import os
 import types
 
