@@ -99,7 +99,7 @@ void callback_loop(cafxg_ctx* ctx) {
       job = std::move(ctx->cb_q.front());
       ctx->cb_q.pop_front();
     }
-    job();
+    run_guarded("reply callback", job);
   }
 }
 
@@ -530,12 +530,18 @@ void dispatcher_loop(cafxg_ctx* ctx) {
         g.M = g.N = g.K = (uint32_t)r->actor->dims[0];
         g.mode = r->actor->tune.sgemm_mode;
         g.splits = r->actor->tune.sgemm_splits;
-        int s = sgemm_submit_impl(
-            ctx, &g, r->a, r->b, (float*)r->out,
-            [](void* u, int st) { finish_request((Request*)u, st); }, r);
+        int s;
+        try {
+          s = sgemm_submit_impl(
+              ctx, &g, r->a, r->b, (float*)r->out,
+              [](void* u, int st) { finish_request((Request*)u, st); }, r);
+        } catch (const std::exception& ex) {
+          s = fail(CAFXG_E_CONFIG, "matrix_multiply: %s", ex.what());
+        }
         if (s != CAFXG_OK)
           push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); });
-        ctx->st_requests--;  // counted by finish_request
+        else
+          ctx->st_requests--;  // counted by finish_request
         break;
       }
       if (!batch.empty() &&
@@ -552,7 +558,7 @@ void dispatcher_loop(cafxg_ctx* ctx) {
         fprintf(stderr, "cafxg dispatch %.3f ms: batch %zu, %zu queued behind, inflight %d\n",
                 trace_now_ms(), batch.size(), queue.size(), (int)d->inflight.load());
       const auto b0 = std::chrono::steady_clock::now();
-      run_mandel_batch(ctx, d, std::move(batch));
+      run_guarded("actor batch", [&] { run_mandel_batch(ctx, d, std::move(batch)); });
       ctx->st_batch_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
                               std::chrono::steady_clock::now() - b0)
                               .count();
@@ -759,12 +765,17 @@ int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in, const size_t* in_
     // straight into the host-request path (row bands over every device,
     // overlapped waves), which saves the dispatcher hop (~10 us of a 0.2 ms
     // cfg1 request); non-blocking like the inbox
-    std::vector<cafxg_mandel_desc> tiles(r->ntiles);
-    for (uint32_t k = 0; k < r->ntiles; ++k)
-      tiles[k] = r->tile(k);
-    const int s = mandel_submit_impl(
-        ctx, tiles.data(), tiles.size(), static_cast<uint32_t*>(r->out),
-        [](void* u, int st) { finish_request((Request*)u, st); }, r, &a->tune);
+    int s;
+    try {
+      std::vector<cafxg_mandel_desc> tiles(r->ntiles);
+      for (uint32_t k = 0; k < r->ntiles; ++k)
+        tiles[k] = r->tile(k);
+      s = mandel_submit_impl(
+          ctx, tiles.data(), tiles.size(), static_cast<uint32_t*>(r->out),
+          [](void* u, int st) { finish_request((Request*)u, st); }, r, &a->tune);
+    } catch (const std::exception& ex) {
+      s = fail(CAFXG_E_CONFIG, "enqueue: %s", ex.what());
+    }
     if (s != CAFXG_OK) {
       std::string err = t_last_error;
       Device* d = ctx->devs[0].get();

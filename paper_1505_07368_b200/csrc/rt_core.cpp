@@ -99,7 +99,7 @@ void completion_loop(cafxg_ctx* ctx, Device* d) {
     }
     {
       NvtxRange nvtx_range("cafxg.complete");
-      c.fn(status);
+      run_guarded("completion callback", [&] { c.fn(status); });
     }
     {
       std::lock_guard<std::mutex> lk(d->cq_mu);
@@ -162,6 +162,18 @@ int check_alive(cafxg_ctx* ctx) {
               ctx->lost_why.c_str());
 }
 
+// Backend threads never let an exception escape (it would terminate the
+// process): a throwing callback or task is reported on stderr and skipped.
+void run_guarded(const char* what, const std::function<void()>& fn) {
+  try {
+    fn();
+  } catch (const std::exception& ex) {
+    fprintf(stderr, "cafxg: %s threw: %s\n", what, ex.what());
+  } catch (...) {
+    fprintf(stderr, "cafxg: %s threw a non-standard exception\n", what);
+  }
+}
+
 void issuer_loop(Device* d) {
   cudaSetDevice(d->ordinal);
   while (true) {
@@ -174,7 +186,7 @@ void issuer_loop(Device* d) {
       fn = std::move(d->iq.front());
       d->iq.pop_front();
     }
-    fn();
+    run_guarded("issue task", fn);
   }
 }
 

@@ -392,6 +392,8 @@ struct NvtxRange {
 };
 
 // ---- rt_core.cpp ----
+// runs fn, reporting (not propagating) an exception: backend threads
+void run_guarded(const char* what, const std::function<void()>& fn);
 // runs `fn` on device d's issuer thread (multi-device contexts)
 void issue_async(cafxg_ctx* ctx, Device* d, std::function<void()> fn);
 void issuer_loop(Device* d);
