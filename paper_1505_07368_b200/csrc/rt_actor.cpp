@@ -780,9 +780,7 @@ int cafxg_actor_enqueue(cafxg_actor* a, const void* const* in, const size_t* in_
       std::string err = t_last_error;
       Device* d = ctx->devs[0].get();
       std::lock_guard<std::mutex> g(d->submit_mu);
-      if (push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); }) !=
-          CAFXG_OK)
-        finish_request(r, s);
+      push_completion(ctx, d, d->compute, [r, s](int) { finish_request(r, s); });
       t_last_error = err;
     } else {
       ctx->st_requests--;  // counted by finish_request

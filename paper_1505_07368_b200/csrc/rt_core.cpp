@@ -88,20 +88,22 @@ void completion_loop(cafxg_ctx* ctx, Device* d) {
       c = std::move(d->cq.front());
       d->cq.pop_front();
     }
-    cudaError_t e = cudaEventSynchronize(c.ev);
-    const uint64_t nth = ctx->completions.fetch_add(1) + 1;
-    if (e == cudaSuccess && ctx->simulate_loss_at && nth >= ctx->simulate_loss_at)
-      e = cudaErrorLaunchFailure;  // CAFXG_SIMULATE_DEVICE_LOSS (tests)
-    int status = CAFXG_OK;
-    if (e != cudaSuccess) {
-      status = cuda_status(e, "device work failed");
-      mark_lost(ctx, e, "device work failed");
+    int status = c.status;
+    if (c.ev) {
+      cudaError_t e = cudaEventSynchronize(c.ev);
+      const uint64_t nth = ctx->completions.fetch_add(1) + 1;
+      if (e == cudaSuccess && ctx->simulate_loss_at && nth >= ctx->simulate_loss_at)
+        e = cudaErrorLaunchFailure;  // CAFXG_SIMULATE_DEVICE_LOSS (tests)
+      if (e != cudaSuccess) {
+        status = cuda_status(e, "device work failed");
+        mark_lost(ctx, e, "device work failed");
+      }
     }
     {
       NvtxRange nvtx_range("cafxg.complete");
       run_guarded("completion callback", [&] { c.fn(status); });
     }
-    {
+    if (c.ev) {
       std::lock_guard<std::mutex> lk(d->cq_mu);
       d->ev_free.push_back(c.ev);
     }
@@ -205,8 +207,15 @@ void issue_async(cafxg_ctx* ctx, Device* d, std::function<void()> fn) {
 
 // Records an event on `stream` and hands `fn` to the device's completion
 // thread. Caller holds d->submit_mu (so records stay in stream order).
-int push_completion(cafxg_ctx* ctx, Device* d, cudaStream_t stream,
-                           std::function<void(int)> fn) {
+__global__ void trap_kernel() { asm volatile("trap;"); }
+
+void push_completion(cafxg_ctx* ctx, Device* d, cudaStream_t stream,
+                     std::function<void(int)> fn) {
+  if (ctx->inject_trap_at && ctx->pushes.fetch_add(1) + 1 == ctx->inject_trap_at) {
+    trap_kernel<<<1, 32, 0, stream>>>();
+    if (ctx->inject_trap_sync)
+      cudaStreamSynchronize(stream);
+  }
   cudaEvent_t ev = nullptr;
   {
     std::lock_guard<std::mutex> lk(d->cq_mu);
@@ -215,9 +224,26 @@ int push_completion(cafxg_ctx* ctx, Device* d, cudaStream_t stream,
       d->ev_free.pop_back();
     }
   }
+  cudaError_t e = cudaSuccess;
   if (!ev)
-    CAFXG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  CAFXG_CUDA_TRY(cudaEventRecord(ev, stream));
+    e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess)
+    e = cudaEventRecord(ev, stream);
+  int status = CAFXG_OK;
+  if (e != cudaSuccess) {
+    // No event: the callback still runs, on the completion thread, after
+    // whatever is queued on the stream (best effort on a broken context) and
+    // with the error. Dropping it would leave the request's waiter asleep.
+    status = cuda_status(e, "completion event");
+    mark_lost(ctx, e, "completion event");
+    cudaStreamSynchronize(stream);
+    cudaGetLastError();
+    if (ev) {
+      std::lock_guard<std::mutex> lk(d->cq_mu);
+      d->ev_free.push_back(ev);
+    }
+    ev = nullptr;
+  }
   {
     std::lock_guard<std::mutex> lk(ctx->sync_mu);
     ++ctx->submitted;
@@ -225,10 +251,9 @@ int push_completion(cafxg_ctx* ctx, Device* d, cudaStream_t stream,
   d->inflight.fetch_add(1);
   {
     std::lock_guard<std::mutex> lk(d->cq_mu);
-    d->cq.push_back(Completion{ev, std::move(fn)});
+    d->cq.push_back(Completion{ev, std::move(fn), status});
   }
   d->cq_cv.notify_one();
-  return CAFXG_OK;
 }
 
 // Host -> device copy of small descriptor arrays through the device's pinned
@@ -399,6 +424,10 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
     ctx->force_exact = ex && ex[0] == '1';
     if (const char* sl = getenv("CAFXG_SIMULATE_DEVICE_LOSS"))
       ctx->simulate_loss_at = (uint64_t)std::max(0, atoi(sl));
+    if (const char* t = getenv("CAFXG_INJECT_TRAP"))
+      ctx->inject_trap_at = (uint64_t)std::max(0, atoi(t));
+    if (const char* t = getenv("CAFXG_INJECT_TRAP_SYNC"))
+      ctx->inject_trap_sync = t[0] == '1';
     cafxg_ctx* c = ctx.release();
     for (auto& d : c->devs) {
       d->completer = std::thread(completion_loop, c, d.get());

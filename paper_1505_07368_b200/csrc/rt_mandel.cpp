@@ -591,20 +591,12 @@ int submit_mandel_device(cafxg_ctx* ctx, Device* d,
     if (dout_live)
       cudaFreeAsync(dout_live, d->d2h);
     cudaGetLastError();
-    const int ps = push_completion(ctx, d, d->d2h, [ctx, staging, join, issued, err](int) {
+    push_completion(ctx, d, d->d2h, [ctx, staging, join, issued, err](int) {
       if (staging)
         ctx->pinned.free(staging);
       set_last_error("%s", err.c_str());
       join->part_done(issued);
     });
-    if (ps != CAFXG_OK) {
-      // not even an event could be recorded: wait here for what is queued
-      cudaStreamSynchronize(d->d2h);
-      if (staging)
-        ctx->pinned.free(staging);
-      set_last_error("%s", err.c_str());
-      join->part_done(issued);
-    }
     return CAFXG_OK;
   }
   if (trace && !tev.empty()) {
@@ -627,16 +619,17 @@ int submit_mandel_device(cafxg_ctx* ctx, Device* d,
         cudaEventDestroy(e);
     cudaGetLastError();
   }
-  return push_completion(ctx, d, d->d2h,
-                         [ctx, staging, scat = std::move(scat), host_out, join](int st) {
-                           if (staging) {
-                             if (st == CAFXG_OK)
-                               for (auto& s : scat)
-                                 std::memcpy(host_out + s[1], staging + s[0], s[2] * 4);
-                             ctx->pinned.free(staging);
-                           }
-                           join->part_done(st);
-                         });
+  push_completion(ctx, d, d->d2h,
+                  [ctx, staging, scat = std::move(scat), host_out, join](int st) {
+                    if (staging) {
+                      if (st == CAFXG_OK)
+                        for (auto& s : scat)
+                          std::memcpy(host_out + s[1], staging + s[0], s[2] * 4);
+                      ctx->pinned.free(staging);
+                    }
+                    join->part_done(st);
+                  });
+  return CAFXG_OK;
 }
 
 int mandel_submit_impl(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles,
@@ -669,7 +662,8 @@ int mandel_submit_impl(cafxg_ctx* ctx, const cafxg_mandel_desc* tiles,
     Device* d = ctx->devs[0].get();
     cudaSetDevice(d->ordinal);
     std::lock_guard<std::mutex> g(d->submit_mu);
-    return push_completion(ctx, d, d->compute, [join](int st) { join->part_done(st); });
+    push_completion(ctx, d, d->compute, [join](int st) { join->part_done(st); });
+    return CAFXG_OK;
   }
   join->remaining = parts;
   ctx->st_requests++;

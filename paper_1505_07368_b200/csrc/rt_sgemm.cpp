@@ -474,13 +474,12 @@ int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
     std::lock_guard<std::mutex> lk(d->submit_mu);
     cudaSetDevice(d->ordinal);
     int s = sgemm_tiled2d_device(ctx, d, g, A, B, C);
-    if (s != CAFXG_OK) {
-      // queued work may still read the host buffers: report after it
+    // a failure is reported after the queued work: it may still read the
+    // host buffers
+    if (s != CAFXG_OK)
       push_completion(ctx, d, d->d2h, [join, s](int) { join->part_done(s); });
-      return CAFXG_OK;
-    }
-    if (push_completion(ctx, d, d->d2h, [join](int st) { join->part_done(st); }) != CAFXG_OK)
-      join->part_done(CAFXG_E_DOWN);
+    else
+      push_completion(ctx, d, d->d2h, [join](int st) { join->part_done(st); });
     return CAFXG_OK;
   }
   const size_t bytesB = (size_t)g.K * g.ldb * 4;
@@ -577,9 +576,8 @@ int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
       cudaFreeAsync(dB[k], d->d2h);
       if (s != CAFXG_OK)
         push_completion(ctx, d, d->d2h, [join, s](int) { join->part_done(s); });
-      else if (push_completion(ctx, d, d->d2h, [join](int st) { join->part_done(st); }) !=
-               CAFXG_OK)
-        join->part_done(CAFXG_E_DOWN);
+      else
+        push_completion(ctx, d, d->d2h, [join](int st) { join->part_done(st); });
       continue;
     }
     if (s == CAFXG_OK && part.M) {
@@ -608,14 +606,11 @@ int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
     if (dA) cudaFreeAsync(dA, d->compute);
     if (dC) cudaFreeAsync(dC, d->compute);
     if (dB[k]) cudaFreeAsync(dB[k], d->compute);
-    if (s != CAFXG_OK) {
-      // still route the failure through the completion thread
+    // a failure is still routed through the completion thread
+    if (s != CAFXG_OK)
       push_completion(ctx, d, d->compute, [join, s](int) { join->part_done(s); });
-    } else {
-      int ps = push_completion(ctx, d, d->compute, [join](int st) { join->part_done(st); });
-      if (ps != CAFXG_OK)
-        join->part_done(ps);
-    }
+    else
+      push_completion(ctx, d, d->compute, [join](int st) { join->part_done(st); });
   }
   return CAFXG_OK;
 }

@@ -172,8 +172,9 @@ struct NcclApi {
 // ---- devices and completion -----------------------------------------------------------
 
 struct Completion {
-  cudaEvent_t ev;
+  cudaEvent_t ev;  // null: no event could be recorded, `status` is the outcome
   std::function<void(int)> fn;
+  int status = 0;
 };
 
 constexpr uint32_t kSchedSlots = 1024;
@@ -333,6 +334,13 @@ struct cafxg_ctx {
   // completion of the context reports cudaErrorLaunchFailure, as a real
   // sticky fault would, without faulting the GPU
   uint64_t simulate_loss_at = 0;
+  // CAFXG_INJECT_TRAP=n (tests): a trapping kernel is queued ahead of the
+  // n-th completion event, a real sticky device fault; with
+  // CAFXG_INJECT_TRAP_SYNC=1 the fault is waited for first, so recording the
+  // completion event itself fails
+  uint64_t inject_trap_at = 0;
+  bool inject_trap_sync = false;
+  std::atomic<uint64_t> pushes{0};
   std::atomic<uint64_t> completions{0};
   // CAFXG_VIRTUAL_DEVICES=V: V context devices on one physical GPU (own
   // streams, scheduler ring and completion thread each) so the multi-device
@@ -408,7 +416,11 @@ void raise_priority();
 void completion_loop(cafxg_ctx* ctx, Device* d);
 // Records an event on `stream` and hands `fn` to the device's completion
 // thread. Caller holds d->submit_mu (so records stay in stream order).
-int push_completion(cafxg_ctx* ctx, Device* d, cudaStream_t stream, std::function<void(int)> fn);
+// Runs fn(status) on the device's completion thread once the work queued on
+// `stream` so far has finished. fn is called exactly once on every path: when
+// not even an event can be recorded (a dead context), the stream is drained
+// here and fn receives the error.
+void push_completion(cafxg_ctx* ctx, Device* d, cudaStream_t stream, std::function<void(int)> fn);
 // Host -> device copy of small descriptor arrays through the device's pinned
 // staging ring, so the call never waits for earlier work on `stream`.
 int upload(Device* d, void* dst, const void* src, size_t bytes, cudaStream_t stream);

@@ -408,8 +408,64 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const float* __res
 }
 
 // Both operands in one launch (device-API requests): blocks [0, nb_a) split
-// A's rows, the rest split + transpose 32 x 32 tiles of B.
+// A's rows, the rest split + transpose 64 x 64 tiles of B (K % 64 == 0).
 __global__ void __launch_bounds__(256) split_ab_kernel(const float* __restrict__ A, int lda,
+                                                       int M, int K, float* __restrict__ Ah,
+                                                       float* __restrict__ Al,
+                                                       const float* __restrict__ B, int ldb,
+                                                       int N, float* __restrict__ Bth,
+                                                       float* __restrict__ Btl, int nb_a) {
+  if ((int)blockIdx.x < nb_a) {
+    // rows of A in float4 steps; 32-bit index math (sgemm_tc_launch checks
+    // M * K / 4 < 2^32)
+    const uint32_t k4 = (uint32_t)K / 4, total = (uint32_t)M * k4;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (uint32_t)nb_a * blockDim.x) {
+      const uint32_t r = i / k4, c = (i - r * k4) * 4;
+      float4 v = *reinterpret_cast<const float4*>(A + (size_t)r * lda + c);
+      float4 h, l;
+      split_tf32(v.x, h.x, l.x);
+      split_tf32(v.y, h.y, l.y);
+      split_tf32(v.z, h.z, l.z);
+      split_tf32(v.w, h.w, l.w);
+      *reinterpret_cast<float4*>(Ah + (size_t)i * 4) = h;
+      *reinterpret_cast<float4*>(Al + (size_t)i * 4) = l;
+    }
+    asm volatile("griddepcontrol.launch_dependents;");
+    return;
+  }
+  // B: 64 x 64 tiles of (k, n), float4 loads along n and float4 stores
+  // along k of the transposed halves (16-byte accesses both ways; 64 x 65
+  // shared tiles keep the column reads conflict-free)
+  __shared__ float th[64][65], tl[64][65];
+  const int t = (int)blockIdx.x - nb_a, tn = N / 64;
+  const int k0 = (t / tn) * 64, n0 = (t % tn) * 64;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int f = threadIdx.x + i * 256;          // float4 index in the 64 x 16 grid
+    const int kk = f >> 4, nn = (f & 15) * 4;
+    const float4 v = *reinterpret_cast<const float4*>(B + (size_t)(k0 + kk) * ldb + n0 + nn);
+    float h, l;
+    split_tf32(v.x, h, l); th[kk][nn + 0] = h; tl[kk][nn + 0] = l;
+    split_tf32(v.y, h, l); th[kk][nn + 1] = h; tl[kk][nn + 1] = l;
+    split_tf32(v.z, h, l); th[kk][nn + 2] = h; tl[kk][nn + 2] = l;
+    split_tf32(v.w, h, l); th[kk][nn + 3] = h; tl[kk][nn + 3] = l;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int f = threadIdx.x + i * 256;          // float4 index in the 64 (n) x 16 (k) grid
+    const int nn = f >> 4, kk = (f & 15) * 4;
+    const float4 h = make_float4(th[kk][nn], th[kk + 1][nn], th[kk + 2][nn], th[kk + 3][nn]);
+    const float4 l = make_float4(tl[kk][nn], tl[kk + 1][nn], tl[kk + 2][nn], tl[kk + 3][nn]);
+    *reinterpret_cast<float4*>(Bth + (size_t)(n0 + nn) * K + k0 + kk) = h;
+    *reinterpret_cast<float4*>(Btl + (size_t)(n0 + nn) * K + k0 + kk) = l;
+  }
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
+// The same with 32 x 32 tiles of B (K not a multiple of 64).
+__global__ void __launch_bounds__(256) split_ab32_kernel(const float* __restrict__ A, int lda,
                                                        int M, int K, float* __restrict__ Ah,
                                                        float* __restrict__ Al,
                                                        const float* __restrict__ B, int ldb,
@@ -680,9 +736,15 @@ int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int 
   const int bn = sgemm_tc_pick_bn(M, N, sms);
   const int splits = splits_req > 0 ? splits_req : sgemm_tc_splits(M, N, K, sms, bn);
   const int nb_a = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 8);
-  const int nb_b = (N / 32) * (K / 32);
-  split_ab_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B, ldb,
-                                                                 N, Bh, Bl, nb_a);
+  if (K % 64 == 0 && ldb % 4 == 0 && ((uintptr_t)B & 15) == 0) {
+    const int nb_b = (N / 64) * (K / 64);
+    split_ab_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B,
+                                                                   ldb, N, Bh, Bl, nb_a);
+  } else {
+    const int nb_b = (N / 32) * (K / 32);
+    split_ab32_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B,
+                                                                     ldb, N, Bh, Bl, nb_a);
+  }
   int e = (int)cudaGetLastError();
   if (e == 0)
     e = sgemm_tc_gemm(Ah, Al, Bh, Bl, C, M, N, K, ldc, stream, splits, bn);
