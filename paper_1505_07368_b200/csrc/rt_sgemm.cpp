@@ -46,7 +46,7 @@ int sgemm_on_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     return fail(CAFXG_E_CONFIG,
                 "sgemm: shape not supported by the 3xTF32 kernel (see cafxg.h)");
   if (tc) {
-    size_t sb = sgemm_tc_scratch_bytes(g.M, g.N, g.K);
+    size_t sb = sgemm_tc_scratch_bytes(g.M, g.N, g.K, d->sms, (int)g.splits);
     void* scratch = nullptr;
     CAFXG_CUDA_TRY(cudaMallocAsync(&scratch, sb, stream));
     int launches = 0;

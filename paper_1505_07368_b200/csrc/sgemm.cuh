@@ -13,7 +13,7 @@ int sgemm_simt_launch(const float* A, const float* B, float* C, int M, int N,
 // sgemm_tc_supported; scratch holds the tf32 hi/lo splits of A and B^T
 // (sgemm_tc_scratch_bytes).
 bool sgemm_tc_supported(int M, int N, int K, int lda, int ldb, int ldc);
-size_t sgemm_tc_scratch_bytes(int M, int N, int K);
+size_t sgemm_tc_scratch_bytes(int M, int N, int K, int sm_count, int splits_req = 0);
 // splits: split-K cluster size (1/2/4/8), 0 = sgemm_tc_splits' choice
 int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N,
                     int K, int lda, int ldb, int ldc, void* scratch,
@@ -33,14 +33,26 @@ int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float
 // block of m <= a_rows rows only touches rows below m.
 struct SgemmTcMaps {
   alignas(64) unsigned char m[4][128];
-  int bn;  // tile width the maps were encoded for (B box rows)
+  int bn;           // tile width the maps were encoded for (B box rows)
+  bool b_mn_major;  // B operands as they lie (K x N) rather than B^T (N x K)
 };
 int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
                        const float* Bl, int N, int K, int bn, SgemmTcMaps* maps);
+// The same for raw operands: A (pitch lda) and B (K x N, pitch ldb) are read
+// as their own hi halves (the tensor core truncates fp32 to tf32); Al (pitch
+// K) and Bl (K x N, pitch N) hold the lo halves. b_row0 of a launch is then
+// B's first column.
+int sgemm_tc_make_maps_raw(const float* A, int lda, const float* Al, int a_rows,
+                           const float* B, int ldb, const float* Bl, int N, int K, int bn,
+                           SgemmTcMaps* maps);
 // a_row0 / b_row0: this GEMM's first row inside the mapped A / B^T (block
 // (i, j) of a larger product whose maps were encoded once)
+// ws: split-K workspace (sgemm_tc_ws_bytes) for a reduction through L2;
+// null reduces through distributed shared memory
 int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
-                       void* stream, int splits, int a_row0 = 0, int b_row0 = 0);
+                       void* stream, int splits, int a_row0 = 0, int b_row0 = 0,
+                       float* ws = nullptr);
+size_t sgemm_tc_ws_bytes(int M, int N, int splits, int bn);
 // tile width (256 or 128 columns) and split-K factor (thread-block cluster
 // size, <= 8) for a C grid
 int sgemm_tc_pick_bn(int M, int N, int sms);

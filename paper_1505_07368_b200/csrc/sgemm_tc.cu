@@ -1,26 +1,37 @@
 // 3xTF32 fp32 GEMM on the 5th-generation tensor cores (tcgen05) for the
 // `matrix_multiply` compute actor: C = A * B, row-major.
 //
-// fp32 operands are split once per request into tf32 hi/lo halves
-// (hi = rna_tf32(x), lo = rna_tf32(x - hi)); the kernel accumulates
-// lo(A)*hi(B) + hi(A)*lo(B) + hi(A)*hi(B) in fp32 TMEM, which recovers ~22
-// mantissa bits per product (the dropped lo*lo term is ~2^-22 relative).
+// Each operand is taken as hi + lo tf32 halves and the kernel accumulates
+// lo(A)*hi(B) + hi(A)*lo(B) + hi(A)*hi(B) in fp32 TMEM (~22 mantissa bits
+// per product). Two operand forms, chosen per request by size:
+//   split:  a pass writes hi = rna_tf32(x), lo = rna_tf32(x - hi) of A and of
+//           B transposed (B^T, K-major); large GEMMs, where the pass is
+//           cheap against the GEMM and K-major B feeds the MMA fastest;
+//   raw:    the tensor core reads a 32-bit operand as tf32 by dropping its
+//           low 13 mantissa bits, so A and B themselves are the hi halves;
+//           a pass writes only lo = rna_tf32(x - trunc_tf32(x)), in place
+//           layout (B stays K x N, an MN-major operand): half the pass's
+//           writes, no transpose; small and mid-size GEMMs.
 //
-// Kernel (one 128x256 C tile per CTA, 6 warps, warp-specialised):
-//   warp 0 lane 0 : TMA producer -- 4-stage ring of {A_hi, A_lo, Bt_hi, Bt_lo}
-//                   16-deep K slices (SWIZZLE_64B, K-major), mbarrier
-//                   complete_tx;
-//   warp 1        : allocates 512 TMEM columns (two 128x256 fp32
+// Kernel (one 128 x BN C tile per CTA, BN = 256 or 128, 10 warps,
+// warp-specialised):
+//   warp 0 lane 0 : TMA producer -- 4-stage ring of {A_hi, A_lo, B_hi, B_lo}
+//                   16-deep K slices (A and B^T K-major SWIZZLE_64B; raw B
+//                   MN-major SWIZZLE_128B_ATOM_32B, one 3-D box per half),
+//                   mbarrier complete_tx;
+//   warp 1        : allocates 2 * BN TMEM columns (two 128 x BN fp32
 //                   accumulators); lane 0 issues tcgen05.mma.cta_group::1
-//                   .kind::tf32 (M=128, N=256, K=8), 6 per stage, alternating
+//                   .kind::tf32 (M=128, N=BN, K=8), 6 per stage, alternating
 //                   accumulators every 128 K; tcgen05.commit frees stages and
 //                   hands finished chunks to the epilogue;
 //   warps 2..9    : epilogue -- tcgen05.ld 32x32b.x32 TMEM -> registers,
 //                   fp32 round-to-nearest sum of the K chunks (the tensor
 //                   core accumulates with truncation), then global stores
 //                   (each thread owns half a C row of the tile).
-// Grid: grouped raster over (M/128) x (N/256) tiles so the CTAs in flight
-// share A row-blocks and B column-blocks in L2.
+// Grid: grouped raster over (M/128) x (N/BN) tiles so the CTAs in flight
+// share A row-blocks and B column-blocks in L2. Grids too small to fill the
+// GPU split K over a thread-block cluster; the partial tiles are reduced
+// through an L2 workspace (device-API requests) or distributed shared memory.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -50,15 +61,17 @@ constexpr int kMaxSplits = 8;  // portable cluster size
 
 // Tile width BN = 256 (large grids) or 128 (grids too small to fill the SMs:
 // twice the CTAs per split-K factor, half the partial tile to reduce).
-template <int BN>
+template <int BN, bool BMN>
 struct Cfg {
   static constexpr int B_TILE = BN * BK * 4;                 // 16 / 8 KiB
   static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;  // 48 / 32 KiB
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;              // two BN-column accumulators
   static constexpr int COLS = BN / 2;                        // epilogue: half a tile row
-  // Instruction descriptor: D=f32, A=B=tf32, K-major both, M=128, N=BN.
+  // Instruction descriptor: D=f32, A=B=tf32, A K-major, B K-major (B^T
+  // split operands) or MN-major (BMN: raw B and its lo half), M=128, N=BN.
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    ((BMN ? 1u : 0u) << 16) |
                                     ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   static_assert(BM * BN * 4 <= STAGES * STAGE_BYTES, "split-K partial must fit the stages");
 };
@@ -89,6 +102,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int x, int y) {
   asm volatile(
@@ -108,6 +130,26 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   d |= (uint64_t)(512 >> 4) << 32;        // SBO
   d |= (uint64_t)1 << 46;                 // version
   d |= (uint64_t)4 << 61;                 // SWIZZLE_64B
+  return d;
+}
+
+// UMMA descriptor of an MN-major B operand (B as it lies in memory: K rows
+// of N contiguous floats; no transpose). For 32-bit (tf32) MN-major operands
+// the tensor core takes only the SWIZZLE_128B_BASE32B layout (type 1):
+// 128-byte rows of 32 consecutive N columns with 32-byte granules XOR-ed by
+// the row inside 4-row (512 B) atoms, which TMA writes with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B. A stage holds BN / 32 such 32-column
+// chunks of BK rows, B_CHUNK bytes apart (LBO); 4-row K atoms are 512 B
+// apart (SBO); one MMA of K = 8 spans two atoms (1024 B). (With the plain
+// SWIZZLE_128B layout the MMA returns zeros.)
+constexpr int B_CHUNK = 32 * BK * 4;  // 32 columns x BK rows: 2 KiB
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128b32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(B_CHUNK >> 4) << 16;  // LBO: next 32 N columns
+  d |= (uint64_t)(512 >> 4) << 32;      // SBO: next 4 K rows
+  d |= (uint64_t)1 << 46;               // version
+  d |= (uint64_t)1 << 61;               // SWIZZLE_128B_BASE32B
   return d;
 }
 
@@ -156,30 +198,109 @@ __device__ __forceinline__ void cluster_sync() {
                "barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// 16-byte load from the shared memory of cluster CTA `rank` at the address
-// that `local` has in this CTA
-__device__ __forceinline__ float4 ld_cluster_f4(uint32_t local, uint32_t rank) {
+// address in the shared memory of cluster CTA `rank` of the byte that
+// `local` addresses in this CTA (windows are linear: offsets carry over)
+__device__ __forceinline__ uint32_t cluster_map(uint32_t local, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  return remote;
+}
+
+// 16-byte distributed-shared-memory load (no memory clobber: the cluster
+// barriers around the reduction order it against the partials' stores;
+// volatile keeps the issue order the reduction loop writes)
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t remote) {
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(remote)
-               : "memory");
+               : "r"(remote));
   return v;
+}
+
+// Phase timestamps for tuning (build with -DCAFXG_SGEMM_PHASES, `make
+// phases`; tools/sgemm_phases.py reads them): %globaltimer per CTA at fixed
+// points of the kernel, and the first start / last end of the split pass.
+#ifdef CAFXG_SGEMM_PHASES
+__device__ unsigned long long g_sgemm_phase[1024][16];  // [0, 8) globaltimer, [8, 16) clock64
+__device__ unsigned long long g_split_span[2];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SGEMM_PHASE(i)                                   \
+  do {                                                   \
+    if (blockIdx.x < 1024) {                             \
+      g_sgemm_phase[blockIdx.x][i] = gtimer();           \
+      g_sgemm_phase[blockIdx.x][8 + i] = clock64();      \
+    }                                                    \
+  } while (0)
+#define SPLIT_SPAN_BEGIN() \
+  if (threadIdx.x == 0) atomicMin(&g_split_span[0], gtimer())
+#define SPLIT_SPAN_END()  \
+  __syncthreads();        \
+  if (threadIdx.x == 0) atomicMax(&g_split_span[1], gtimer())
+#else
+#define SGEMM_PHASE(i) \
+  do {                 \
+  } while (0)
+#define SPLIT_SPAN_BEGIN()
+#define SPLIT_SPAN_END()
+#endif
+
+// Split-K reduction through L2 (S = splits): this CTA (rank kz of cluster
+// `bid`) sums rows [kz * BM / S, (kz + 1) * BM / S) of its tile over its own
+// parked partial (shared memory) and the S - 1 slices its peers wrote to the
+// workspace, in fixed z order. Every load of a thread's batch of granules is
+// issued before the first add: the loop is L2-latency-bound otherwise.
+template <int BN, int S>
+__device__ __forceinline__ void reduce_ws(const float* __restrict__ ws, const uint8_t* smem,
+                                          int bid, int kz, float* __restrict__ ctile, int ldc) {
+  constexpr int ROWS = BM / S, N4 = ROWS * (BN / 4), PER = 4;
+  const float4* mine = reinterpret_cast<const float4*>(ws) + ((size_t)bid * S + kz) * S * N4;
+  for (int i0 = threadIdx.x; i0 < N4; i0 += PER * TC_THREADS) {
+    float4 v[PER][S];
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int i = i0 + p * TC_THREADS;
+#pragma unroll
+      for (int z = 0; z < S; ++z)
+        if (i < N4 && z != kz)
+          v[p][z] = __ldcg(mine + (size_t)z * N4 + i);
+    }
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int i = i0 + p * TC_THREADS;
+      if (i >= N4)
+        break;
+      const int j4 = i / ROWS, rr = i - j4 * ROWS;
+      const float4 l = *reinterpret_cast<const float4*>(
+          smem + (uint32_t)partial_index<BN>(kz * ROWS + rr, j4) * 16u);
+      float4 a = kz == 0 ? l : v[p][0];
+#pragma unroll
+      for (int z = 1; z < S; ++z) {
+        const float4 w = z == kz ? l : v[p][z];
+        a.x = __fadd_rn(a.x, w.x);
+        a.y = __fadd_rn(a.y, w.y);
+        a.z = __fadd_rn(a.z, w.z);
+        a.w = __fadd_rn(a.w, w.w);
+      }
+      *reinterpret_cast<float4*>(ctile + (size_t)(kz * ROWS + rr) * ldc + j4 * 4) = a;
+    }
+  }
 }
 
 // ---- the GEMM kernel --------------------------------------------------------
 
-template <int BN>
+template <int BN, bool BMN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     sgemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAh,
                         const __grid_constant__ CUtensorMap mAl,
                         const __grid_constant__ CUtensorMap mBh,
                         const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
                         int M, int N, int K, int ldc, int splits, int a_row0,
-                        int b_row0, int group_m) {
-  using G = Cfg<BN>;
+                        int b_row0, int group_m, float* __restrict__ ws) {
+  using G = Cfg<BN, BMN>;
   constexpr int STAGE_BYTES = G::STAGE_BYTES, B_TILE = G::B_TILE;
   // a_row0 / b_row0: first row of this GEMM's A / B^T block inside the
   // matrices the tensor maps describe (a sub-block of a larger product)
@@ -198,6 +319,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0)
+    SGEMM_PHASE(0);
 
   // grouped raster: GROUP_M consecutive M tiles share each N tile
   const int tiles_m = M / BM, tiles_n = N / BN;
@@ -241,48 +364,73 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // allocation, tensor-map prefetch) overlaps the tail of the operand split;
   // no global memory is touched before the split grid has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0)
+    SGEMM_PHASE(1);
 
-  if (warp == 0 && lane == 0) {
+  // Roles are warp-uniform branches (lane 0 works, the warp waits at
+  // __syncwarp): the __syncthreads below is bar.sync, which PTX defines only
+  // for warps that reach it converged.
+  if (warp == 0) {
     // ---- TMA producer ----
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      uint8_t* st = smem + s * STAGE_BYTES;
-      mbar_expect_tx(&full[s], STAGE_BYTES);
-      const int kx = k_base + kb * BK;
-      tma_load_2d(st, &mAh, &full[s], kx, a_row0 + m0);
-      tma_load_2d(st + A_TILE, &mAl, &full[s], kx, a_row0 + m0);
-      tma_load_2d(st + 2 * A_TILE, &mBh, &full[s], kx, b_row0 + n0);
-      tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], kx, b_row0 + n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer ----
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      const int chunk = kb / CHUNK_KB, kin = kb % CHUNK_KB;
-      const uint32_t acc = tmem + (uint32_t)(chunk & 1) * BN;
-      if (kin == 0)  // the epilogue must have drained this accumulator
-        mbar_wait(&acc_empty[chunk & 1], ((chunk >> 1) & 1) ^ 1);
-      mbar_wait(&full[s], ph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
-      const uint32_t ah = base, al = base + A_TILE;
-      const uint32_t bh = base + 2 * A_TILE, bl = bh + B_TILE;
-#pragma unroll
-      for (int k = 0; k < BK / 8; ++k) {
-        const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K
-        const uint32_t acc0 = (kin | k) != 0;
-        mma_tf32<G::IDESC>(acc, umma_desc_sw64(al + off), umma_desc_sw64(bh + off), acc0);
-        mma_tf32<G::IDESC>(acc, umma_desc_sw64(ah + off), umma_desc_sw64(bl + off), 1);
-        mma_tf32<G::IDESC>(acc, umma_desc_sw64(ah + off), umma_desc_sw64(bh + off), 1);
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        const int kx = k_base + kb * BK;
+        tma_load_2d(st, &mAh, &full[s], kx, a_row0 + m0);
+        tma_load_2d(st + A_TILE, &mAl, &full[s], kx, a_row0 + m0);
+        if constexpr (BMN) {
+          // raw B and its lo half as they lie (K rows of N floats): BN / 32
+          // chunks of 32 columns each; b_row0 is the first column
+          // (one 3-D box: 32 columns x BK rows x BN / 32 chunks)
+          tma_load_3d(st + 2 * A_TILE, &mBh, &full[s], 0, kx, (b_row0 + n0) / 32);
+          tma_load_3d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], 0, kx, (b_row0 + n0) / 32);
+        } else {
+          tma_load_2d(st + 2 * A_TILE, &mBh, &full[s], kx, b_row0 + n0);
+          tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], kx, b_row0 + n0);
+        }
       }
-      umma_commit(&empty[s]);  // the stage is free once these MMAs retire
-      if (kin == CHUNK_KB - 1 || kb == nk - 1)
-        umma_commit(&acc_full[chunk & 1]);
     }
-  } else if (warp >= 2) {
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---- MMA issuer ----
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        const int chunk = kb / CHUNK_KB, kin = kb % CHUNK_KB;
+        const uint32_t acc = tmem + (uint32_t)(chunk & 1) * BN;
+        if (kin == 0)  // the epilogue must have drained this accumulator
+          mbar_wait(&acc_empty[chunk & 1], ((chunk >> 1) & 1) ^ 1);
+        mbar_wait(&full[s], ph);
+        if (kb == 0)
+          SGEMM_PHASE(2);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t ah = base, al = base + A_TILE;
+        const uint32_t bh = base + 2 * A_TILE, bl = bh + B_TILE;
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K
+          const uint32_t acc0 = (kin | k) != 0;
+          // B: 8 more K along a K-major row, or 8 more 128-byte rows (MN-major)
+          const uint64_t dbh = BMN ? umma_desc_mn_sw128b32(bh + k * 1024) : umma_desc_sw64(bh + off);
+          const uint64_t dbl = BMN ? umma_desc_mn_sw128b32(bl + k * 1024) : umma_desc_sw64(bl + off);
+          mma_tf32<G::IDESC>(acc, umma_desc_sw64(al + off), dbh, acc0);  // small terms first
+          mma_tf32<G::IDESC>(acc, umma_desc_sw64(ah + off), dbl, 1);
+          mma_tf32<G::IDESC>(acc, umma_desc_sw64(ah + off), dbh, 1);
+        }
+        umma_commit(&empty[s]);  // the stage is free once these MMAs retire
+        if (kin == CHUNK_KB - 1 || kb == nk - 1)
+          umma_commit(&acc_full[chunk & 1]);
+      }
+      SGEMM_PHASE(3);
+    }
+    __syncwarp();
+  } else {
     // ---- epilogue: sum the chunk accumulators in fp32 (RN), then store ----
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const int half = (warp - 2) >> 2;       // which half of the tile's columns
@@ -311,43 +459,104 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&acc_empty[b]))
                      : "memory");
     }
+    if (warp == 2 && lane == 0)
+      SGEMM_PHASE(4);
     if (splits == 1) {
       float* crow = C + (size_t)(m0 + row) * ldc + n0 + half * G::COLS;
 #pragma unroll
       for (int j = 0; j < G::COLS; j += 4)
         *reinterpret_cast<float4*>(crow + j) =
             make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
-    } else {
+    } else if (ws == nullptr || row / (BM / splits) == kz) {
       // partial tile into the (now idle) stage buffers: the last acc_full
-      // commit follows every MMA, so no TMA write or MMA read is pending
+      // commit follows every MMA, so no TMA write or MMA read is pending.
+      // (With a workspace only the rows this CTA reduces stay here.)
       float4* part = reinterpret_cast<float4*>(smem);
 #pragma unroll
       for (int j = 0; j < G::COLS; j += 4)
         part[partial_index<BN>(row, half * (G::COLS / 4) + j / 4)] =
             make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+    } else {
+      // rows another CTA of the cluster reduces: to its workspace slice,
+      // granule-major (lanes = consecutive rows = consecutive 16 bytes)
+      const int rows = BM / splits, owner = row / rows;
+      float4* slice = reinterpret_cast<float4*>(ws) +
+                      (((size_t)bid * splits + owner) * splits + kz) * (size_t)(rows * BN / 4);
+#pragma unroll
+      for (int j = 0; j < G::COLS; j += 4)
+        __stcg(slice + (size_t)(half * (G::COLS / 4) + j / 4) * rows + (row - owner * rows),
+               make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (splits > 1) {
+  if (threadIdx.x == 0)
+    SGEMM_PHASE(5);
+  if (splits > 1 && ws != nullptr) {
+    // split-K through L2: every CTA's slices for the peers went to the
+    // workspace; after the cluster barrier (release / acquire: the peers'
+    // global stores are visible) each CTA sums its rows in fixed z order
+    cluster_sync();
+    if (threadIdx.x == 0)
+      SGEMM_PHASE(6);
+    float* crow = C + (size_t)m0 * ldc + n0;
+    switch (splits) {
+      case 2: reduce_ws<BN, 2>(ws, smem, bid, kz, crow, ldc); break;
+      case 4: reduce_ws<BN, 4>(ws, smem, bid, kz, crow, ldc); break;
+      default: reduce_ws<BN, 8>(ws, smem, bid, kz, crow, ldc); break;
+    }
+  } else if (splits > 1) {
     cluster_sync();  // every partial of the cluster is written
+    if (threadIdx.x == 0)
+      SGEMM_PHASE(6);
     const int rows = BM / splits;
-    const uint32_t mine = smem_u32(smem);
-    for (int i = threadIdx.x; i < rows * (BN / 4); i += TC_THREADS) {
-      const int r = kz * rows + i / (BN / 4), c4 = i % (BN / 4);
-      const uint32_t off = (uint32_t)partial_index<BN>(r, c4) * 16u;
-      float4 acc = ld_cluster_f4(mine + off, 0);
-      for (int z = 1; z < splits; ++z) {
-        const float4 v = ld_cluster_f4(mine + off, (uint32_t)z);
-        acc.x = __fadd_rn(acc.x, v.x);
-        acc.y = __fadd_rn(acc.y, v.y);
-        acc.z = __fadd_rn(acc.z, v.z);
-        acc.w = __fadd_rn(acc.w, v.w);
-      }
-      *reinterpret_cast<float4*>(C + (size_t)(m0 + r) * ldc + n0 + c4 * 4) = acc;
+    // every peer's window once; the loads of all peers (and of two granules)
+    // are issued before the first add, so the distributed-shared-memory
+    // latency is paid once per pair of granules rather than once per peer
+    uint32_t peer[kMaxSplits];
+#pragma unroll
+    for (int z = 0; z < kMaxSplits; ++z)
+      peer[z] = z < splits ? cluster_map(smem_u32(smem), (uint32_t)z) : 0u;
+    const int n4 = rows * (BN / 4);
+    for (int i = threadIdx.x; i < n4; i += 2 * TC_THREADS) {
+      const int i2 = i + TC_THREADS;
+      const bool two = i2 < n4;
+      const int r0 = kz * rows + i / (BN / 4), c0 = i % (BN / 4);
+      const int r1 = kz * rows + i2 / (BN / 4), c1 = i2 % (BN / 4);
+      const uint32_t off0 = (uint32_t)partial_index<BN>(r0, c0) * 16u;
+      const uint32_t off1 = two ? (uint32_t)partial_index<BN>(r1, c1) * 16u : off0;
+      float4 v0[kMaxSplits], v1[kMaxSplits];
+#pragma unroll
+      for (int z = 0; z < kMaxSplits; ++z)
+        if (z < splits && z != kz) {
+          v0[z] = ld_dsmem_f4(peer[z] + off0);
+          v1[z] = ld_dsmem_f4(peer[z] + off1);
+        }
+      // this CTA's own partial through the local shared-memory path
+      const float4 l0 = *reinterpret_cast<const float4*>(smem + off0);
+      const float4 l1 = *reinterpret_cast<const float4*>(smem + off1);
+      float4 a0 = kz == 0 ? l0 : v0[0], a1 = kz == 0 ? l1 : v1[0];
+#pragma unroll
+      for (int z = 1; z < kMaxSplits; ++z)
+        if (z < splits) {
+          const float4 w0 = z == kz ? l0 : v0[z], w1 = z == kz ? l1 : v1[z];
+          a0.x = __fadd_rn(a0.x, w0.x);
+          a0.y = __fadd_rn(a0.y, w0.y);
+          a0.z = __fadd_rn(a0.z, w0.z);
+          a0.w = __fadd_rn(a0.w, w0.w);
+          a1.x = __fadd_rn(a1.x, w1.x);
+          a1.y = __fadd_rn(a1.y, w1.y);
+          a1.z = __fadd_rn(a1.z, w1.z);
+          a1.w = __fadd_rn(a1.w, w1.w);
+        }
+      *reinterpret_cast<float4*>(C + (size_t)(m0 + r0) * ldc + n0 + c0 * 4) = a0;
+      if (two)
+        *reinterpret_cast<float4*>(C + (size_t)(m0 + r1) * ldc + n0 + c1 * 4) = a1;
     }
     cluster_sync();  // the peers are done reading this CTA's partial
   }
+  if (threadIdx.x == 0)
+    SGEMM_PHASE(7);
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(G::TMEM_COLS));
@@ -415,6 +624,7 @@ __global__ void __launch_bounds__(256) split_ab_kernel(const float* __restrict__
                                                        const float* __restrict__ B, int ldb,
                                                        int N, float* __restrict__ Bth,
                                                        float* __restrict__ Btl, int nb_a) {
+  SPLIT_SPAN_BEGIN();
   if ((int)blockIdx.x < nb_a) {
     // rows of A in float4 steps; 32-bit index math (sgemm_tc_launch checks
     // M * K / 4 < 2^32)
@@ -431,6 +641,7 @@ __global__ void __launch_bounds__(256) split_ab_kernel(const float* __restrict__
       *reinterpret_cast<float4*>(Ah + (size_t)i * 4) = h;
       *reinterpret_cast<float4*>(Al + (size_t)i * 4) = l;
     }
+    SPLIT_SPAN_END();
     asm volatile("griddepcontrol.launch_dependents;");
     return;
   }
@@ -461,6 +672,7 @@ __global__ void __launch_bounds__(256) split_ab_kernel(const float* __restrict__
     *reinterpret_cast<float4*>(Bth + (size_t)(n0 + nn) * K + k0 + kk) = h;
     *reinterpret_cast<float4*>(Btl + (size_t)(n0 + nn) * K + k0 + kk) = l;
   }
+  SPLIT_SPAN_END();
   asm volatile("griddepcontrol.launch_dependents;");
 }
 
@@ -508,6 +720,69 @@ __global__ void __launch_bounds__(256) split_ab32_kernel(const float* __restrict
   asm volatile("griddepcontrol.launch_dependents;");
 }
 
+// lo half for operands the GEMM reads raw: the tensor core takes a 32-bit
+// operand as tf32 by dropping its low 13 mantissa bits, so the fp32 value
+// itself is hi = trunc_tf32(x); lo = rna_tf32(x - hi) (the difference is
+// exact in fp32). Dropped terms: lo(A)*lo(B) <= 2^-20 relative and lo's own
+// rounding <= 2^-21, below the fp32 accumulation's error.
+__device__ __forceinline__ float lo_tf32(float x) {
+  const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  uint32_t l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(__fsub_rn(x, hi)));
+  return __uint_as_float(l);
+}
+
+__device__ __forceinline__ float4 lo_tf32(float4 v) {
+  return make_float4(lo_tf32(v.x), lo_tf32(v.y), lo_tf32(v.z), lo_tf32(v.w));
+}
+
+// rows x cols (pitch ld_in, float4-aligned) -> lo halves packed (pitch cols);
+// thread t of `nthreads` takes float4 granules t, t + nthreads, ... four at
+// a time (four loads in flight before the first store)
+__device__ __forceinline__ void lo_rows(const float* __restrict__ in, int ld_in, int rows,
+                                        int cols, float* __restrict__ out, uint32_t t,
+                                        uint32_t nthreads) {
+  const uint32_t c4 = (uint32_t)cols / 4, total = (uint32_t)rows * c4;
+  for (uint32_t i = t; i < total; i += 4 * nthreads) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t j = i + u * nthreads;
+      if (j < total) {
+        const uint32_t r = j / c4, c = (j - r * c4) * 4;
+        v[u] = __ldcs(reinterpret_cast<const float4*>(in + (size_t)r * ld_in + c));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t j = i + u * nthreads;
+      if (j < total)
+        *reinterpret_cast<float4*>(out + (size_t)j * 4) = lo_tf32(v[u]);
+    }
+  }
+}
+
+// One launch for both operands: blocks [0, nb_a) make lo(A) (M x K), the
+// rest lo(B) (K x N, B's own layout). The grid is at most 4 CTAs of 256
+// threads per SM, so the dependent GEMM's CTAs (320 threads) fit beside it:
+// the trigger comes first, the GEMM's prologue (barriers, TMEM, tensor-map
+// prefetch) overlaps this pass and its griddepcontrol.wait still waits for
+// the whole grid.
+__global__ void __launch_bounds__(256) split_lo_kernel(const float* __restrict__ A, int lda,
+                                                       int M, int K, float* __restrict__ Al,
+                                                       const float* __restrict__ B, int ldb,
+                                                       int N, float* __restrict__ Bl,
+                                                       int nb_a) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  SPLIT_SPAN_BEGIN();
+  if ((int)blockIdx.x < nb_a)
+    lo_rows(A, lda, M, K, Al, blockIdx.x * blockDim.x + threadIdx.x, (uint32_t)nb_a * blockDim.x);
+  else
+    lo_rows(B, ldb, K, N, Bl, (blockIdx.x - nb_a) * blockDim.x + threadIdx.x,
+            (gridDim.x - (uint32_t)nb_a) * blockDim.x);
+  SPLIT_SPAN_END();
+}
+
 // ---- tensor maps (driver entry point fetched through the runtime) ---------
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -528,19 +803,41 @@ EncodeTiled get_encoder() {
   return fn;
 }
 
-// rows x cols fp32 row-major (cols contiguous); box = box_rows x BK
-bool make_map(CUtensorMap* m, const float* base, int rows, int cols, int box_rows) {
+// rows x cols fp32 row-major with row pitch `ld` floats; box = box_cols
+// (contiguous) x box_rows
+bool make_map(CUtensorMap* m, const float* base, int rows, int cols, int ld, int box_cols,
+              int box_rows, CUtensorMapSwizzle swz) {
   EncodeTiled enc = get_encoder();
   if (!enc)
     return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// K-major operand (rows of K): BK x box_rows boxes, SWIZZLE_64B
+bool make_map_kmajor(CUtensorMap* m, const float* base, int rows, int K, int ld, int box_rows) {
+  return make_map(m, base, rows, K, ld, BK, box_rows, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+// MN-major B (K rows of N) as a 3-D tensor (32 columns, K rows, N / 32
+// column chunks): one box of 32 x BK x bn / 32 fills a stage's B tile in
+// the chunked SWIZZLE_128B_ATOM_32B layout with one TMA request
+bool make_map_mnmajor(CUtensorMap* m, const float* base, int K, int N, int ld, int bn) {
+  EncodeTiled enc = get_encoder();
+  if (!enc || N % 32)
+    return false;
+  cuuint64_t dims[3] = {32, (cuuint64_t)K, (cuuint64_t)N / 32};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, 128};
+  cuuint32_t box[3] = {32, (cuuint32_t)BK, (cuuint32_t)bn / 32};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -551,10 +848,22 @@ bool sgemm_tc_supported(int M, int N, int K, int lda, int ldb, int ldc) {
          lda % 4 == 0 && ldc % 4 == 0 && get_encoder() != nullptr;
 }
 
-size_t sgemm_tc_scratch_bytes(int M, int N, int K) {
-  // hi/lo splits of A and B^T (split-K reduces through distributed shared
-  // memory and needs no workspace)
-  return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float);
+size_t sgemm_tc_ws_bytes(int M, int N, int splits, int bn) {
+  // per cluster (one C tile): for every reducing CTA one slice of BM / splits
+  // rows per source CTA (its own slot unused), i.e. `splits` partial tiles
+  if (splits <= 1)
+    return 0;
+  return (size_t)(M / BM) * (N / bn) * splits * BM * bn * sizeof(float);
+}
+
+size_t sgemm_tc_scratch_bytes(int M, int N, int K, int sm_count, int splits_req) {
+  // hi/lo splits of A and B^T (the raw-operand path uses the first half: lo
+  // of A and B) and the split-K workspace
+  const int sms = sm_count > 0 ? sm_count : 148;
+  const int bn = sgemm_tc_pick_bn(M, N, sms);
+  const int splits = splits_req > 0 ? splits_req : sgemm_tc_splits(M, N, K, sms, bn);
+  return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float) +
+         sgemm_tc_ws_bytes(M, N, splits, bn);
 }
 
 int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al,
@@ -574,15 +883,15 @@ int sgemm_tc_split_b(const float* B, int ldb, int K, int N, float* Bh, float* Bl
 
 namespace {
 
-template <int BN>
+template <int BN, bool BMN>
 void configure_once() {
   // once per device (the attribute is per-device state)
   static std::atomic<uint64_t> configured{0};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 64 && !(configured.load() >> dev & 1)) {
-    cudaFuncSetAttribute(sgemm_3xtf32_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg<BN>::SMEM_BYTES);
+    cudaFuncSetAttribute(sgemm_3xtf32_kernel<BN, BMN>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, BMN>::SMEM_BYTES);
     configured.fetch_or(1ull << dev);
   }
 }
@@ -596,11 +905,11 @@ int max_active_clusters(int splits) {
   int v = cache[splits].load();
   if (v)
     return v;
-  configure_once<BN>();
+  configure_once<BN, false>();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(splits * 256));
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = Cfg<BN>::SMEM_BYTES;
+  cfg.dynamicSmemBytes = Cfg<BN, false>::SMEM_BYTES;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)splits;
@@ -609,13 +918,41 @@ int max_active_clusters(int splits) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, sgemm_3xtf32_kernel<BN>, &cfg) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveClusters(&n, sgemm_3xtf32_kernel<BN, false>, &cfg) != cudaSuccess ||
       n < 1) {
     cudaGetLastError();
     n = 148 / splits;
   }
   cache[splits].store(n);
   return n;
+}
+
+// Raw operands: the GEMM reads A and B through TMA as they lie (both
+// 16-byte aligned with 16-byte row pitches) and only their lo halves are
+// materialised -- half the split pass's writes and no transpose -- but the
+// MN-major B operand costs ~5% of MMA throughput (2048^3: 64 against 61 us
+// of MMA). Taken where the split pass weighs more than that: the pass
+// scales with M + N, the GEMM with M * N, and M N / (M + N) < 3200 covers up
+// to ~6400^2 (measured: 4096^3 0.622 -> 0.590 ms, 16384^3 38.4 -> 40.4 ms).
+// CAFXG_SGEMM_RAW=0 / 1 forces either way (experiments).
+bool use_raw_operands(const float* A, int lda, const float* B, int ldb, int M, int N) {
+  static const int env = [] {
+    const char* e = getenv("CAFXG_SGEMM_RAW");
+    return e ? atoi(e) : -1;
+  }();
+  if (((uintptr_t)A & 15) || ((uintptr_t)B & 15) || lda % 4 || ldb % 4 || env == 0)
+    return false;
+  return env == 1 || (double)M * N / ((double)M + N) < 3200.0;
+}
+
+// CAFXG_SGEMM_WS=0: split-K reduces through distributed shared memory even
+// where a workspace is available (experiments)
+bool ws_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CAFXG_SGEMM_WS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // CAFXG_SGEMM_PDL=0 launches the GEMM without programmatic dependent launch
@@ -627,10 +964,10 @@ bool pdl_enabled() {
   return on;
 }
 
-template <int BN>
+template <int BN, bool BMN>
 int launch(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, void* stream,
-           int splits, int a_row0, int b_row0) {
-  configure_once<BN>();
+           int splits, int a_row0, int b_row0, float* ws) {
+  configure_once<BN, BMN>();
   if (splits < 1 || splits > kMaxSplits || (splits & (splits - 1)) ||
       K % (16 * splits) != 0)
     splits = 1;
@@ -638,7 +975,7 @@ int launch(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, void* s
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(tiles * splits));
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = Cfg<BN>::SMEM_BYTES;
+  cfg.dynamicSmemBytes = Cfg<BN, BMN>::SMEM_BYTES;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -656,8 +993,8 @@ int launch(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, void* s
     const int v = e ? atoi(e) : 0;
     return v > 0 ? v : GROUP_M;
   }();
-  cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel<BN>, m[0], m[1], m[2], m[3], C, M, N, K, ldc,
-                     splits, a_row0, b_row0, group_m);
+  cudaLaunchKernelEx(&cfg, sgemm_3xtf32_kernel<BN, BMN>, m[0], m[1], m[2], m[3], C, M, N, K, ldc,
+                     splits, a_row0, b_row0, group_m, splits > 1 ? ws : nullptr);
   return (int)cudaGetLastError();
 }
 
@@ -701,18 +1038,37 @@ int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float
   static_assert(sizeof(CUtensorMap) <= sizeof(maps->m[0]), "tensor map storage");
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(maps->m);
   maps->bn = bn;
-  if (!make_map(&m[0], Ah, a_rows, K, BM) || !make_map(&m[1], Al, a_rows, K, BM) ||
-      !make_map(&m[2], Bh, N, K, bn) || !make_map(&m[3], Bl, N, K, bn))
+  maps->b_mn_major = false;
+  if (!make_map_kmajor(&m[0], Ah, a_rows, K, K, BM) ||
+      !make_map_kmajor(&m[1], Al, a_rows, K, K, BM) ||
+      !make_map_kmajor(&m[2], Bh, N, K, K, bn) || !make_map_kmajor(&m[3], Bl, N, K, K, bn))
+    return (int)cudaErrorInvalidValue;
+  return 0;
+}
+
+int sgemm_tc_make_maps_raw(const float* A, int lda, const float* Al, int a_rows,
+                           const float* B, int ldb, const float* Bl, int N, int K, int bn,
+                           SgemmTcMaps* maps) {
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(maps->m);
+  maps->bn = bn;
+  maps->b_mn_major = true;
+  if (!make_map_kmajor(&m[0], A, a_rows, K, lda, BM) ||
+      !make_map_kmajor(&m[1], Al, a_rows, K, K, BM) || !make_map_mnmajor(&m[2], B, K, N, ldb, bn) ||
+      !make_map_mnmajor(&m[3], Bl, K, N, N, bn))
     return (int)cudaErrorInvalidValue;
   return 0;
 }
 
 int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
-                       void* stream, int splits, int a_row0, int b_row0) {
+                       void* stream, int splits, int a_row0, int b_row0, float* ws) {
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
-  if (maps->bn == 256)
-    return launch<256>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0);
-  return launch<128>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0);
+  if (maps->b_mn_major)
+    return maps->bn == 256
+               ? launch<256, true>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws)
+               : launch<128, true>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws);
+  return maps->bn == 256
+             ? launch<256, false>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws)
+             : launch<128, false>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws);
 }
 
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl, float* C,
@@ -726,31 +1082,69 @@ int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float
 int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int K, int lda,
                     int ldb, int ldc, void* scratch, int sm_count, void* stream,
                     int* launches, int splits_req) {
-  float* Ah = static_cast<float*>(scratch);
-  float* Al = Ah + (size_t)M * K;
-  float* Bh = Al + (size_t)M * K;
-  float* Bl = Bh + (size_t)N * K;
-  if ((size_t)M * K / 4 >= (1ull << 32))
+  if ((size_t)M * K / 4 >= (1ull << 32) || (size_t)K * N / 4 >= (1ull << 32))
     return (int)cudaErrorInvalidValue;
   const int sms = sm_count > 0 ? sm_count : 148;
   const int bn = sgemm_tc_pick_bn(M, N, sms);
   const int splits = splits_req > 0 ? splits_req : sgemm_tc_splits(M, N, K, sms, bn);
-  const int nb_a = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 8);
-  if (K % 64 == 0 && ldb % 4 == 0 && ((uintptr_t)B & 15) == 0) {
-    const int nb_b = (N / 64) * (K / 64);
-    split_ab_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B,
-                                                                   ldb, N, Bh, Bl, nb_a);
+  float* Ah = static_cast<float*>(scratch);
+  float* Al = Ah + (size_t)M * K;
+  float* Bh = Al + (size_t)M * K;
+  float* Bl = Bh + (size_t)N * K;
+  float* ws = Bl + (size_t)N * K;  // split-K workspace (sgemm_tc_scratch_bytes)
+  // maps before the first launch: the two launches then go out back to back
+  // (encoding between them left the GPU idle for the host's encode time)
+  SgemmTcMaps maps;
+  if (use_raw_operands(A, lda, B, ldb, M, N)) {
+    // lo halves only, into the first half of the scratch; the GEMM reads A
+    // and B themselves as the hi halves
+    float* Alo = Ah;
+    float* Blo = Alo + (size_t)M * K;
+    if (int me = sgemm_tc_make_maps_raw(A, lda, Alo, M, B, ldb, Blo, N, K, bn, &maps))
+      return me;
+    const size_t ga = (size_t)M * K / 4, gb = (size_t)K * N / 4;
+    const int grid = std::max<int>(2, (int)std::min<size_t>((ga + gb + 1023) / 1024,
+                                                            (size_t)sms * 4));
+    const int nb_a = std::clamp((int)((double)grid * ga / (ga + gb) + 0.5), 1, grid - 1);
+    split_lo_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Alo, B, ldb, N, Blo,
+                                                            nb_a);
   } else {
-    const int nb_b = (N / 32) * (K / 32);
-    split_ab32_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B,
+    if (int me = sgemm_tc_make_maps(Ah, Al, M, Bh, Bl, N, K, bn, &maps))
+      return me;
+    const int nb_a = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 8);
+    if (K % 64 == 0 && ldb % 4 == 0 && ((uintptr_t)B & 15) == 0) {
+      const int nb_b = (N / 64) * (K / 64);
+      split_ab_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B,
                                                                      ldb, N, Bh, Bl, nb_a);
+    } else {
+      const int nb_b = (N / 32) * (K / 32);
+      split_ab32_kernel<<<nb_a + nb_b, 256, 0, (cudaStream_t)stream>>>(A, lda, M, K, Ah, Al, B,
+                                                                       ldb, N, Bh, Bl, nb_a);
+    }
   }
   int e = (int)cudaGetLastError();
   if (e == 0)
-    e = sgemm_tc_gemm(Ah, Al, Bh, Bl, C, M, N, K, ldc, stream, splits, bn);
+    e = sgemm_tc_gemm_maps(&maps, C, M, N, K, ldc, stream, splits, 0, 0,
+                           ws_enabled() ? ws : nullptr);
   if (launches)
     *launches = 2;
   return e;
 }
 
 }  // namespace cafxg
+
+#ifdef CAFXG_SGEMM_PHASES
+// tools/sgemm_phases.py: reset before a launch, read after it
+extern "C" int cafxg_debug_sgemm_phases(unsigned long long* out, int nblocks,
+                                        unsigned long long* split_span, int reset) {
+  using namespace cafxg;
+  if (reset) {
+    static unsigned long long zero[1024][16];
+    unsigned long long span0[2] = {~0ull, 0ull};
+    cudaMemcpyToSymbol(g_sgemm_phase, zero, sizeof(zero));
+    return (int)cudaMemcpyToSymbol(g_split_span, span0, sizeof(span0));
+  }
+  cudaMemcpyFromSymbol(out, g_sgemm_phase, (size_t)std::min(nblocks, 1024) * 16 * 8);
+  return (int)cudaMemcpyFromSymbol(split_span, g_split_span, 16);
+}
+#endif

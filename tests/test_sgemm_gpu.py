@@ -197,6 +197,62 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
 
 
+@pytest.mark.parametrize("raw", ["0", "1"])
+@pytest.mark.parametrize("ws", ["0", "1"])
+def test_sgemm_3xtf32_operand_forms(raw, ws):
+    """Both operand forms (split + transposed B, or raw A / B read as their own
+    hi halves with only lo materialised, B MN-major) and both split-K
+    reductions (L2 workspace, distributed shared memory), forced through
+    CAFXG_SGEMM_RAW / CAFXG_SGEMM_WS, on device-API GEMMs: split-K clusters of
+    2 / 4 / 8, both tile widths, padded row pitches, K = 8192; every result
+    within the tolerance, and the two reductions bit-identical."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+out = []
+with pkg.Context(1) as c:
+    for M, N, K, pad, splits in [(1024, 1024, 1024, 0, 0), (256, 256, 2048, 0, 8),
+                                 (512, 768, 512, 4, 2), (128, 128, 8192, 0, 0),
+                                 (2048, 512, 256, 8, 4)]:
+        A_h = oracle.fill_uniform(M * (K + pad), 91).reshape(M, K + pad)
+        B_h = oracle.fill_uniform(K * (N + pad), 92).reshape(K, N + pad)
+        A, B = torch.from_numpy(A_h).cuda(), torch.from_numpy(B_h).cuda()
+        C = torch.full((M, N + pad), float("nan"), device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        c.sgemm_device(M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream,
+                       mode=pkg.SGEMM_3XTF32, lda=K + pad, ldb=N + pad, ldc=N + pad,
+                       splits=splits)
+        torch.cuda.synchronize()
+        Ch = C.cpu().numpy()
+        assert not np.isnan(Ch[:, :N]).any(), (M, N, K)
+        if pad:
+            assert np.isnan(Ch[:, N:]).all(), (M, N, K)
+        rows = np.unique(np.linspace(0, M - 1, 40).astype(np.uint32))
+        R = oracle.sgemm_ref_rows(np.ascontiguousarray(A_h[:, :K]),
+                                  np.ascontiguousarray(B_h[:, :N]), rows, N, K)
+        err = oracle.sgemm_rel_err(np.ascontiguousarray(Ch[:, :N]), R, rows, N)
+        assert err <= 1e-5, (M, N, K, err)
+        out.append(Ch[:, :N].copy())
+np.save(sys.argv[1], np.concatenate([o.ravel() for o in out]))
+print("ok")
+""" % root
+    env = dict(os.environ, CAFXG_SGEMM_RAW=raw, CAFXG_SGEMM_WS=ws)
+    path = f"/tmp/cafxg_forms_{raw}_{ws}.npy"
+    r = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
+    if ws == "1":
+        other = f"/tmp/cafxg_forms_{raw}_0.npy"
+        if os.path.exists(other):
+            assert np.array_equal(np.load(path), np.load(other))
+
+
 def test_cfg5_full_size_row_sum_property(ctx):
     """Full-size property for cfg5 (16384^3, the sampled-row check covers a
     few rows): C.1 = A.(B.1) for every row. B.1 and A.(B.1) are computed in
