@@ -35,6 +35,7 @@ struct SgemmTcMaps {
   alignas(64) unsigned char m[4][128];
   int bn;           // tile width the maps were encoded for (B box rows)
   bool b_mn_major;  // B operands as they lie (K x N) rather than B^T (N x K)
+  bool pair;        // CTA-pair kernel (bn = its per-CTA half of the pair tile's columns)
 };
 int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
                        const float* Bl, int N, int K, int bn, SgemmTcMaps* maps);

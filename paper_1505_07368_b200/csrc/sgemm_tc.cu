@@ -462,11 +462,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (warp == 2 && lane == 0)
       SGEMM_PHASE(4);
     if (splits == 1) {
-      float* crow = C + (size_t)(m0 + row) * ldc + n0 + half * G::COLS;
+      // through the idle stage buffers (swizzled float4 granules, conflict
+      // free both ways) so each warp stores whole rows: a thread's own row
+      // would take one 16-byte segment per lane and instruction
+      float4* part = reinterpret_cast<float4*>(smem);
 #pragma unroll
       for (int j = 0; j < G::COLS; j += 4)
-        *reinterpret_cast<float4*>(crow + j) =
+        part[partial_index<BN>(row, half * (G::COLS / 4) + j / 4)] =
             make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+      for (int r = warp - 2; r < BM; r += EPI_WARPS) {
+        float* crow = C + (size_t)(m0 + r) * ldc + n0;
+#pragma unroll
+        for (int c4 = lane; c4 < BN / 4; c4 += 32)
+          *reinterpret_cast<float4*>(crow + c4 * 4) = part[partial_index<BN>(r, c4)];
+      }
     } else if (ws == nullptr || row / (BM / splits) == kz) {
       // partial tile into the (now idle) stage buffers: the last acc_full
       // commit follows every MMA, so no TMA write or MMA read is pending.
@@ -559,6 +569,306 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     SGEMM_PHASE(7);
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(G::TMEM_COLS));
+}
+
+// ---- the 2-SM (CTA pair) GEMM kernel ------------------------------------------
+// For C grids too small to fill the GPU (cfg2: 1024^3). A pair of CTAs on
+// the two SMs of a TPC computes a 256 x BNP tile with tcgen05.mma
+// .cta_group::2 (M = 256): each CTA loads its 128 rows of A and its BNP / 2
+// columns of B, the leader's single thread issues the MMAs over both CTAs'
+// shared memory, and each CTA's TMEM holds its 128 x BNP accumulator. Per SM
+// this reads half as much B from shared memory as a 1-SM 128 x BNP tile, so
+// a 256 x 128 pair tile runs the tensor core at the 1-SM 128 x 256 rate with
+// half the accumulator: twice the tiles, half the split-K factor, and a
+// third of the partial-tile bytes to exchange (the exchange bounds the small
+// grids). Split-K pairs form a cluster of 2 x splits CTAs: rank = 2 z + q
+// (z the K split, q the pair rank; rank 2 z is the pair's leader).
+//
+// Synchronisation: full[s] lives in the leader only; both CTAs' TMA loads
+// (.cta_group::2) signal it, the leader arms it with both CTAs' bytes.
+// empty[s] and acc_full[b] live in both CTAs; the leader's tcgen05.commit
+// multicasts to the pair. acc_empty[b] lives in the leader and counts both
+// CTAs' epilogue warps (remote arrives).
+template <int BNP, bool BMN>
+struct PairCfg {
+  static constexpr int BH = BNP / 2;                           // B columns per CTA
+  static constexpr int B_TILE = BH * BK * 4;                   // 4 / 8 KiB
+  static constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;  // 24 / 32 KiB
+  static constexpr int PSTAGES = BNP == 256 ? 6 : 8;
+  static constexpr int SMEM_BYTES = PSTAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t TMEM_COLS = 2 * BNP;               // two accumulators
+  static constexpr int COLS = BNP / 2;                         // epilogue: half a row
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    ((BMN ? 1u : 0u) << 16) |
+                                    ((uint32_t)(BNP >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+  static_assert(BM * BNP * 4 <= PSTAGES * STAGE_BYTES, "split-K partial must fit the stages");
+  static_assert(!BMN || BH % 32 == 0, "MN-major B halves are 32-column chunks");
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t bar_cluster, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t bar_cluster, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+               : "memory");
+}
+
+template <int BNP, bool BMN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    sgemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap mAh,
+                             const __grid_constant__ CUtensorMap mAl,
+                             const __grid_constant__ CUtensorMap mBh,
+                             const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
+                             int M, int N, int K, int ldc, int splits, int a_row0, int b_row0,
+                             int group_m, float* __restrict__ ws) {
+  using G = PairCfg<BNP, BMN>;
+  constexpr int STAGE_BYTES = G::STAGE_BYTES, B_TILE = G::B_TILE, BH = G::BH;
+  constexpr int PSTAGES = G::PSTAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + PSTAGES * STAGE_BYTES);
+  uint64_t* empty = full + PSTAGES;
+  uint64_t* acc_full = empty + PSTAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0)
+    SGEMM_PHASE(0);
+  const uint32_t rank = cluster_rank();
+  const int q = (int)(rank & 1), kz = (int)(rank >> 1);
+  const uint32_t leader = rank & ~1u;
+  const uint16_t pair_mask = (uint16_t)(3u << leader);
+
+  // grouped raster over 256 x BNP pair tiles
+  const int tiles_m = M / 256, tiles_n = N / BNP;
+  const int per_group = group_m * tiles_n;
+  const int bid = blockIdx.x / (2 * splits);  // pair tile (cluster) index
+  const int first_m = (bid / per_group) * group_m;
+  const int gsize = min(group_m, tiles_m - first_m);
+  const int in_group = bid % per_group;
+  const int m0 = (first_m + in_group % gsize) * 256 + q * BM;  // this CTA's rows
+  const int n0 = (in_group / gsize) * BNP;                     // the pair tile's columns
+  const int nb0 = n0 + q * BH;                                 // this CTA's B columns
+  const int ksplit = K / splits;
+  const int k_base = kz * ksplit;
+  const int nk = ksplit / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (const CUtensorMap* m : {&mAh, &mAl, &mBh, &mBl})
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m))
+                   : "memory");
+    for (int s = 0; s < PSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 2 * EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // both CTAs of the pair allocate together
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(G::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();  // the peers' barriers are initialised before any remote use
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0)
+    SGEMM_PHASE(1);
+
+  if (warp == 0) {
+    // ---- TMA producer (both CTAs): this CTA's halves into its own stage,
+    // completion counted on the leader's full[s]
+    if (lane == 0) {
+      const uint32_t full_leader = cluster_map(smem_u32(full), leader);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % PSTAGES;
+        const uint32_t ph = (kb / PSTAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        const uint32_t fb = full_leader + 8u * s;
+        if (q == 0)
+          mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+        const int kx = k_base + kb * BK;
+        tma_load_2d_pair(st, &mAh, fb, kx, a_row0 + m0);
+        tma_load_2d_pair(st + A_TILE, &mAl, fb, kx, a_row0 + m0);
+        if constexpr (BMN) {
+          tma_load_3d_pair(st + 2 * A_TILE, &mBh, fb, 0, kx, (b_row0 + nb0) / 32);
+          tma_load_3d_pair(st + 2 * A_TILE + B_TILE, &mBl, fb, 0, kx, (b_row0 + nb0) / 32);
+        } else {
+          tma_load_2d_pair(st + 2 * A_TILE, &mBh, fb, kx, b_row0 + nb0);
+          tma_load_2d_pair(st + 2 * A_TILE + B_TILE, &mBl, fb, kx, b_row0 + nb0);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---- MMA issuer: the leader's lane 0 drives the pair ----
+    if (lane == 0 && q == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % PSTAGES;
+        const uint32_t ph = (kb / PSTAGES) & 1;
+        const int chunk = kb / CHUNK_KB, kin = kb % CHUNK_KB;
+        const uint32_t acc = tmem + (uint32_t)(chunk & 1) * BNP;
+        if (kin == 0)  // both CTAs' epilogues must have drained this accumulator
+          mbar_wait(&acc_empty[chunk & 1], ((chunk >> 1) & 1) ^ 1);
+        mbar_wait(&full[s], ph);
+        if (kb == 0)
+          SGEMM_PHASE(2);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t ah = base, al = base + A_TILE;
+        const uint32_t bh = base + 2 * A_TILE, bl = bh + B_TILE;
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          const uint32_t off = k * 32;
+          const uint32_t acc0 = (kin | k) != 0;
+          const uint64_t dbh = BMN ? umma_desc_mn_sw128b32(bh + k * 1024) : umma_desc_sw64(bh + off);
+          const uint64_t dbl = BMN ? umma_desc_mn_sw128b32(bl + k * 1024) : umma_desc_sw64(bl + off);
+          mma_tf32_pair<G::IDESC>(acc, umma_desc_sw64(al + off), dbh, acc0);
+          mma_tf32_pair<G::IDESC>(acc, umma_desc_sw64(ah + off), dbl, 1);
+          mma_tf32_pair<G::IDESC>(acc, umma_desc_sw64(ah + off), dbh, 1);
+        }
+        umma_commit_pair(&empty[s], pair_mask);  // both CTAs' stage s is free
+        if (kin == CHUNK_KB - 1 || kb == nk - 1)
+          umma_commit_pair(&acc_full[chunk & 1], pair_mask);
+      }
+      SGEMM_PHASE(3);
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue (both CTAs): this CTA's 128 rows from its own TMEM ----
+    const int q4 = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const uint32_t acc_empty_leader = cluster_map(smem_u32(acc_empty), leader);
+    float sum[G::COLS];
+#pragma unroll
+    for (int j = 0; j < G::COLS; ++j)
+      sum[j] = 0.0f;
+    const int nchunks = (nk + CHUNK_KB - 1) / CHUNK_KB;
+    for (int chunk = 0; chunk < nchunks; ++chunk) {
+      const int b = chunk & 1;
+      mbar_wait(&acc_full[b], (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < G::COLS / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + (uint32_t)(b * BNP + half * G::COLS + c * 32), r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          sum[c * 32 + j] = __fadd_rn(sum[c * 32 + j], __uint_as_float(r[j]));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        mbar_arrive_cluster(acc_empty_leader + 8u * b);
+    }
+    if (warp == 2 && lane == 0)
+      SGEMM_PHASE(4);
+    if (splits == 1) {
+      // through the idle stage buffers (swizzled float4 granules, conflict
+      // free both ways) so each warp stores whole rows: a thread's own row
+      // would take one 16-byte segment per lane and instruction
+      float4* part = reinterpret_cast<float4*>(smem);
+#pragma unroll
+      for (int j = 0; j < G::COLS; j += 4)
+        part[partial_index<BNP>(row, half * (G::COLS / 4) + j / 4)] =
+            make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+      for (int r = warp - 2; r < BM; r += EPI_WARPS) {
+        float* crow = C + (size_t)(m0 + r) * ldc + n0;
+#pragma unroll
+        for (int c4 = lane; c4 < BNP / 4; c4 += 32)
+          *reinterpret_cast<float4*>(crow + c4 * 4) = part[partial_index<BNP>(r, c4)];
+      }
+    } else if (row / (BM / splits) == kz) {
+      float4* part = reinterpret_cast<float4*>(smem);
+#pragma unroll
+      for (int j = 0; j < G::COLS; j += 4)
+        part[partial_index<BNP>(row, half * (G::COLS / 4) + j / 4)] =
+            make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+    } else {
+      // rows the same-q CTA of split `owner` reduces: to the workspace; the
+      // 128-row half tiles (pair tile * 2 + q) index it like 1-SM tiles
+      const int rows = BM / splits, owner = row / rows;
+      const int htile = bid * 2 + q;
+      float4* slice = reinterpret_cast<float4*>(ws) +
+                      (((size_t)htile * splits + owner) * splits + kz) * (size_t)(rows * BNP / 4);
+#pragma unroll
+      for (int j = 0; j < G::COLS; j += 4)
+        __stcg(slice + (size_t)(half * (G::COLS / 4) + j / 4) * rows + (row - owner * rows),
+               make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0)
+    SGEMM_PHASE(5);
+  cluster_sync();  // partials visible; the pair's MMAs and TMEM reads are over
+  if (threadIdx.x == 0)
+    SGEMM_PHASE(6);
+  if (splits > 1) {
+    float* crow = C + (size_t)m0 * ldc + n0;
+    const int htile = bid * 2 + q;
+    switch (splits) {
+      case 2: reduce_ws<BNP, 2>(ws, smem, htile, kz, crow, ldc); break;
+      default: reduce_ws<BNP, 4>(ws, smem, htile, kz, crow, ldc); break;
+    }
+  }
+  if (threadIdx.x == 0)
+    SGEMM_PHASE(7);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(G::TMEM_COLS));
 }
 
@@ -856,15 +1166,13 @@ size_t sgemm_tc_ws_bytes(int M, int N, int splits, int bn) {
   return (size_t)(M / BM) * (N / bn) * splits * BM * bn * sizeof(float);
 }
 
-size_t sgemm_tc_scratch_bytes(int M, int N, int K, int sm_count, int splits_req) {
-  // hi/lo splits of A and B^T (the raw-operand path uses the first half: lo
-  // of A and B) and the split-K workspace
-  const int sms = sm_count > 0 ? sm_count : 148;
-  const int bn = sgemm_tc_pick_bn(M, N, sms);
-  const int splits = splits_req > 0 ? splits_req : sgemm_tc_splits(M, N, K, sms, bn);
-  return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float) +
-         sgemm_tc_ws_bytes(M, N, splits, bn);
-}
+namespace {
+struct TcPlan;
+TcPlan tc_plan(int M, int N, int K, int sms, int splits_req);
+}  // namespace
+
+size_t sgemm_tc_scratch_bytes(int M, int N, int K, int sm_count, int splits_req);
+
 
 int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al,
                      void* stream) {
@@ -998,7 +1306,145 @@ int launch(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, void* s
   return (int)cudaGetLastError();
 }
 
+// ---- CTA-pair kernel (256 x 128 pair tiles) ----
+
+constexpr int kMaxPairSplits = 4;  // cluster of 2 x 4 CTAs: the portable maximum
+
+// pair tile width (columns): CAFXG_SGEMM_PAIR_BN=128 / 256 (experiments)
+int pair_bn() {
+  static const int v = [] {
+    const char* e = getenv("CAFXG_SGEMM_PAIR_BN");
+    return e && atoi(e) == 128 ? 128 : 256;
+  }();
+  return v;
+}
+
+template <int BNP, bool BMN>
+void configure_pair_once() {
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !(configured.load() >> dev & 1)) {
+    cudaFuncSetAttribute(sgemm_3xtf32_pair_kernel<BNP, BMN>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         PairCfg<BNP, BMN>::SMEM_BYTES);
+    configured.fetch_or(1ull << dev);
+  }
+}
+
+template <int BNP>
+int max_active_pair_clusters(int splits) {
+  static std::atomic<int> cache[kMaxPairSplits + 1];
+  int v = cache[splits].load();
+  if (v)
+    return v;
+  configure_pair_once<BNP, false>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * splits * 128));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = PairCfg<BNP, false>::SMEM_BYTES;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)(2 * splits);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, sgemm_3xtf32_pair_kernel<BNP, false>, &cfg) !=
+          cudaSuccess ||
+      n < 1) {
+    cudaGetLastError();
+    n = 148 / (2 * splits);
+  }
+  cache[splits].store(n);
+  return n;
+}
+
+// CAFXG_SGEMM_PAIR=0 never takes the CTA-pair kernel, =1 takes it for every
+// eligible shape (experiments); default: grids that fill the GPU without
+// split-K (measured, b2b: 2048^3 79.8 -> 78.5 us, 4096^3 0.585 -> 0.568 ms,
+// 16384^3 41.0 -> 39.9 ms; at 1024^3, where the 1-SM grid splits K 4 ways,
+// the pair kernel's 256 x 256 tiles need the same 4-way exchange and its
+// 8-CTA clusters fit fewer at once: 31 against 23 us)
+bool pair_allowed(int force) {
+  static const int env = [] {
+    const char* e = getenv("CAFXG_SGEMM_PAIR");
+    return e ? atoi(e) : -1;
+  }();
+  return force ? env == 1 : env != 0;
+}
+
+int pair_splits(int M, int N, int K, int bnp) {
+  const int tiles = (M / 256) * (N / bnp);
+  int s = 1;
+  while (s < kMaxPairSplits && K % (16 * s * 2) == 0 && K / (s * 2) >= 128 &&
+         tiles <= (bnp == 256 ? max_active_pair_clusters<256>(s * 2)
+                              : max_active_pair_clusters<128>(s * 2)))
+    s *= 2;
+  return s;
+}
+
+template <int BNP, bool BMN>
+int launch_pair(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, void* stream,
+                int splits, float* ws) {
+  configure_pair_once<BNP, BMN>();
+  if (splits < 1 || splits > kMaxPairSplits || (splits & (splits - 1)) ||
+      K % (16 * splits) != 0 || ws == nullptr)
+    splits = 1;  // split-K pairs reduce through the workspace only
+  const int tiles = (M / 256) * (N / BNP);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(tiles * 2 * splits));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = PairCfg<BNP, BMN>::SMEM_BYTES;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)(2 * splits);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, sgemm_3xtf32_pair_kernel<BNP, BMN>, m[0], m[1], m[2], m[3], C, M,
+                     N, K, ldc, splits, 0, 0, GROUP_M, ws);
+  return (int)cudaGetLastError();
+}
+
+// Which kernel, tile width and split-K factor a device-API GEMM takes (the
+// scratch size and the launch must agree): the CTA-pair kernel (256 x 256
+// pair tiles) where the 1-SM grid needs no split-K, else 1-SM tiles.
+struct TcPlan {
+  bool pair;
+  int bn;
+  int splits;
+};
+
+TcPlan tc_plan(int M, int N, int K, int sms, int splits_req) {
+  TcPlan p{false, sgemm_tc_pick_bn(M, N, sms), 1};
+  const int s1 = sgemm_tc_splits(M, N, K, sms, p.bn);
+  const int bnp = pair_bn();
+  const bool eligible = M % 256 == 0 && N % bnp == 0 && splits_req <= kMaxPairSplits;
+  if (eligible && pair_allowed(0) && (s1 == 1 || pair_allowed(1))) {
+    p.pair = true;
+    p.bn = bnp;
+    p.splits = splits_req > 0 ? splits_req : pair_splits(M, N, K, bnp);
+    return p;
+  }
+  p.splits = splits_req > 0 ? splits_req : s1;
+  return p;
+}
+
 }  // namespace
+
+size_t sgemm_tc_scratch_bytes(int M, int N, int K, int sm_count, int splits_req) {
+  // hi/lo splits of A and B^T (the raw-operand path uses the first half: lo
+  // of A and B) and the split-K workspace
+  const TcPlan p = tc_plan(M, N, K, sm_count > 0 ? sm_count : 148, splits_req);
+  return ((size_t)M * K * 2 + (size_t)N * K * 2) * sizeof(float) +
+         sgemm_tc_ws_bytes(M, N, p.splits, p.bn);
+}
 
 // Tile width: 256 columns; 128 only for N a multiple of 128 but not 256. (A
 // 128-column tile halves the split-K partial a cluster reduces, but each of
@@ -1039,6 +1485,7 @@ int sgemm_tc_make_maps(const float* Ah, const float* Al, int a_rows, const float
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(maps->m);
   maps->bn = bn;
   maps->b_mn_major = false;
+  maps->pair = false;
   if (!make_map_kmajor(&m[0], Ah, a_rows, K, K, BM) ||
       !make_map_kmajor(&m[1], Al, a_rows, K, K, BM) ||
       !make_map_kmajor(&m[2], Bh, N, K, K, bn) || !make_map_kmajor(&m[3], Bl, N, K, K, bn))
@@ -1052,6 +1499,7 @@ int sgemm_tc_make_maps_raw(const float* A, int lda, const float* Al, int a_rows,
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(maps->m);
   maps->bn = bn;
   maps->b_mn_major = true;
+  maps->pair = false;
   if (!make_map_kmajor(&m[0], A, a_rows, K, lda, BM) ||
       !make_map_kmajor(&m[1], Al, a_rows, K, K, BM) || !make_map_mnmajor(&m[2], B, K, N, ldb, bn) ||
       !make_map_mnmajor(&m[3], Bl, K, N, N, bn))
@@ -1062,6 +1510,13 @@ int sgemm_tc_make_maps_raw(const float* A, int lda, const float* Al, int a_rows,
 int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, int ldc,
                        void* stream, int splits, int a_row0, int b_row0, float* ws) {
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
+  if (maps->pair) {  // maps->bn: each CTA's half of the pair tile's columns
+    if (maps->bn == 128)
+      return maps->b_mn_major ? launch_pair<256, true>(m, C, M, N, K, ldc, stream, splits, ws)
+                              : launch_pair<256, false>(m, C, M, N, K, ldc, stream, splits, ws);
+    return maps->b_mn_major ? launch_pair<128, true>(m, C, M, N, K, ldc, stream, splits, ws)
+                            : launch_pair<128, false>(m, C, M, N, K, ldc, stream, splits, ws);
+  }
   if (maps->b_mn_major)
     return maps->bn == 256
                ? launch<256, true>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws)
@@ -1082,11 +1537,13 @@ int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float
 int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int K, int lda,
                     int ldb, int ldc, void* scratch, int sm_count, void* stream,
                     int* launches, int splits_req) {
-  if ((size_t)M * K / 4 >= (1ull << 32) || (size_t)K * N / 4 >= (1ull << 32))
+  if ((size_t)M * K / 4 >= (1ull << 32))  // the A split indexes float4s in 32 bits
     return (int)cudaErrorInvalidValue;
   const int sms = sm_count > 0 ? sm_count : 148;
-  const int bn = sgemm_tc_pick_bn(M, N, sms);
-  const int splits = splits_req > 0 ? splits_req : sgemm_tc_splits(M, N, K, sms, bn);
+  const TcPlan plan = tc_plan(M, N, K, sms, splits_req);
+  // the pair kernel's CTAs each load half of the pair tile's B columns
+  const int bn = plan.pair ? plan.bn / 2 : plan.bn;
+  const int splits = plan.splits;
   float* Ah = static_cast<float*>(scratch);
   float* Al = Ah + (size_t)M * K;
   float* Bh = Al + (size_t)M * K;
@@ -1095,7 +1552,7 @@ int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int 
   // maps before the first launch: the two launches then go out back to back
   // (encoding between them left the GPU idle for the host's encode time)
   SgemmTcMaps maps;
-  if (use_raw_operands(A, lda, B, ldb, M, N)) {
+  if (use_raw_operands(A, lda, B, ldb, M, N) && (size_t)K * N / 4 < (1ull << 32)) {
     // lo halves only, into the first half of the scratch; the GEMM reads A
     // and B themselves as the hi halves
     float* Alo = Ah;
@@ -1122,10 +1579,11 @@ int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N, int 
                                                                        ldb, N, Bh, Bl, nb_a);
     }
   }
+  maps.pair = plan.pair;
   int e = (int)cudaGetLastError();
   if (e == 0)
     e = sgemm_tc_gemm_maps(&maps, C, M, N, K, ldc, stream, splits, 0, 0,
-                           ws_enabled() ? ws : nullptr);
+                           ws_enabled() || plan.pair ? ws : nullptr);
   if (launches)
     *launches = 2;
   return e;

@@ -197,15 +197,18 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
 
 
+@pytest.mark.parametrize("pair", ["0", "1"])
 @pytest.mark.parametrize("raw", ["0", "1"])
 @pytest.mark.parametrize("ws", ["0", "1"])
-def test_sgemm_3xtf32_operand_forms(raw, ws):
+def test_sgemm_3xtf32_operand_forms(pair, raw, ws):
     """Both operand forms (split + transposed B, or raw A / B read as their own
-    hi halves with only lo materialised, B MN-major) and both split-K
-    reductions (L2 workspace, distributed shared memory), forced through
-    CAFXG_SGEMM_RAW / CAFXG_SGEMM_WS, on device-API GEMMs: split-K clusters of
-    2 / 4 / 8, both tile widths, padded row pitches, K = 8192; every result
-    within the tolerance, and the two reductions bit-identical."""
+    hi halves with only lo materialised, B MN-major), both split-K reductions
+    (L2 workspace, distributed shared memory) and both kernels (1-SM tiles, or
+    CTA pairs with tcgen05 .cta_group::2, which always reduce through the
+    workspace), forced through CAFXG_SGEMM_RAW / _WS / _PAIR, on device-API
+    GEMMs: split-K clusters of 2 / 4 / 8, both tile widths, padded row pitches,
+    K = 8192; every result within the tolerance, and the two reductions
+    bit-identical."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -242,13 +245,13 @@ with pkg.Context(1) as c:
 np.save(sys.argv[1], np.concatenate([o.ravel() for o in out]))
 print("ok")
 """ % root
-    env = dict(os.environ, CAFXG_SGEMM_RAW=raw, CAFXG_SGEMM_WS=ws)
-    path = f"/tmp/cafxg_forms_{raw}_{ws}.npy"
+    env = dict(os.environ, CAFXG_SGEMM_RAW=raw, CAFXG_SGEMM_WS=ws, CAFXG_SGEMM_PAIR=pair)
+    path = f"/tmp/cafxg_forms_{pair}_{raw}_{ws}.npy"
     r = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
     if ws == "1":
-        other = f"/tmp/cafxg_forms_{raw}_0.npy"
+        other = f"/tmp/cafxg_forms_{pair}_{raw}_0.npy"
         if os.path.exists(other):
             assert np.array_equal(np.load(path), np.load(other))
 
