@@ -322,6 +322,11 @@ int sgemm_tiled2d_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
   SgemmTcMaps maps;  // whole Ah/Al and Bh/Bl; blocks address rows by offset
   if (int me = sgemm_tc_make_maps(Ah, Al, (int)M, Bh, Bl, (int)N, (int)K, 256, &maps))
     return cuda_status((cudaError_t)me, "sgemm: tensor maps");
+  // the same operands for the CTA-pair kernel (blocks of whole 256 x 256
+  // pair tiles whose grid needs no split-K)
+  SgemmTcMaps pmaps;
+  const bool pair_ok =
+      sgemm_tc_make_pair_maps(Ah, Al, (int)M, Bh, Bl, (int)N, (int)K, &pmaps) == 0;
   CAFXG_TRY(stream_after_pooled(d, d->h2d, cs));  // buffers exist before uploads
   // CAFXG_TRACE=1: completion times of uploads, GEMM blocks and downloads
   std::vector<std::pair<char, cudaEvent_t>> tev;
@@ -348,9 +353,14 @@ int sgemm_tiled2d_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     const uint32_t mi = (uint32_t)std::min<size_t>(Mb, M - m0);
     const uint32_t nj = (uint32_t)std::min<size_t>(Nb, N - n0);
     float* cblk = dC + (size_t)m0 * N + n0;
-    int e = sgemm_tc_gemm_maps(&maps, cblk, (int)mi, (int)nj, (int)K, (int)N, cs,
-                               g.splits ? (int)g.splits
-                                        : sgemm_tc_splits((int)mi, (int)nj, (int)K, d->sms, 256),
+    const bool pair = pair_ok && !g.splits && mi % 256 == 0 && nj % 256 == 0 &&
+                      sgemm_tc_pair_wanted((int)mi, (int)nj, (int)K, d->sms);
+    int e = sgemm_tc_gemm_maps(pair ? &pmaps : &maps, cblk, (int)mi, (int)nj, (int)K, (int)N,
+                               cs,
+                               pair ? 1
+                               : g.splits
+                                   ? (int)g.splits
+                                   : sgemm_tc_splits((int)mi, (int)nj, (int)K, d->sms, 256),
                                (int)m0, (int)n0);
     ctx->st_launches++;
     mark_used(ctx, d);

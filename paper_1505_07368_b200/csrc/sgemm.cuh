@@ -54,6 +54,13 @@ int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, i
                        void* stream, int splits, int a_row0 = 0, int b_row0 = 0,
                        float* ws = nullptr);
 size_t sgemm_tc_ws_bytes(int M, int N, int splits, int bn);
+// CTA-pair kernel (256 x 256 pair tiles, tcgen05 .cta_group::2) for split
+// operands: whether an M x N x K product should take it (a grid that needs no
+// split-K), and its maps (launched by sgemm_tc_gemm_maps with splits 1; blocks
+// of it need M % 256 == N % 256 == 0)
+bool sgemm_tc_pair_wanted(int M, int N, int K, int sms);
+int sgemm_tc_make_pair_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
+                            const float* Bl, int N, int K, SgemmTcMaps* maps);
 // tile width (256 or 128 columns) and split-K factor (thread-block cluster
 // size, <= 8) for a C grid
 int sgemm_tc_pick_bn(int M, int N, int sms);

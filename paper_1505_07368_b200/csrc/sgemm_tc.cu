@@ -1387,7 +1387,7 @@ int pair_splits(int M, int N, int K, int bnp) {
 
 template <int BNP, bool BMN>
 int launch_pair(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, void* stream,
-                int splits, float* ws) {
+                int splits, int a_row0, int b_row0, float* ws) {
   configure_pair_once<BNP, BMN>();
   if (splits < 1 || splits > kMaxPairSplits || (splits & (splits - 1)) ||
       K % (16 * splits) != 0 || ws == nullptr)
@@ -1408,7 +1408,7 @@ int launch_pair(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, vo
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaLaunchKernelEx(&cfg, sgemm_3xtf32_pair_kernel<BNP, BMN>, m[0], m[1], m[2], m[3], C, M,
-                     N, K, ldc, splits, 0, 0, GROUP_M, ws);
+                     N, K, ldc, splits, a_row0, b_row0, GROUP_M, ws);
   return (int)cudaGetLastError();
 }
 
@@ -1512,10 +1512,12 @@ int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, i
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps->m);
   if (maps->pair) {  // maps->bn: each CTA's half of the pair tile's columns
     if (maps->bn == 128)
-      return maps->b_mn_major ? launch_pair<256, true>(m, C, M, N, K, ldc, stream, splits, ws)
-                              : launch_pair<256, false>(m, C, M, N, K, ldc, stream, splits, ws);
-    return maps->b_mn_major ? launch_pair<128, true>(m, C, M, N, K, ldc, stream, splits, ws)
-                            : launch_pair<128, false>(m, C, M, N, K, ldc, stream, splits, ws);
+      return maps->b_mn_major
+                 ? launch_pair<256, true>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws)
+                 : launch_pair<256, false>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws);
+    return maps->b_mn_major
+               ? launch_pair<128, true>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws)
+               : launch_pair<128, false>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws);
   }
   if (maps->b_mn_major)
     return maps->bn == 256
@@ -1524,6 +1526,20 @@ int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, i
   return maps->bn == 256
              ? launch<256, false>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws)
              : launch<128, false>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws);
+}
+
+bool sgemm_tc_pair_wanted(int M, int N, int K, int sms) {
+  const TcPlan p = tc_plan(M, N, K, sms > 0 ? sms : 148, 0);
+  return p.pair && p.splits == 1 && p.bn == 256;
+}
+
+int sgemm_tc_make_pair_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
+                            const float* Bl, int N, int K, SgemmTcMaps* maps) {
+  // each CTA of a pair loads 128 of the pair tile's 256 B^T rows
+  if (int e = sgemm_tc_make_maps(Ah, Al, a_rows, Bh, Bl, N, K, 128, maps))
+    return e;
+  maps->pair = true;
+  return 0;
 }
 
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl, float* C,
