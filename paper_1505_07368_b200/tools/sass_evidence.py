@@ -22,6 +22,10 @@ KERNELS = [
     (r"sgemm_3xtf32_kernel",
      "3xTF32 GEMM: sgemm_3xtf32_kernel",
      ["UTCHMMA", "UTCQMMA", "UTCBAR", "UTMALDG", "UTMAPF", "LDTM", "SYNCS", "FADD", "HMMA"]),
+    (r"sgemm_3xtf32_pair_kernelILi256ELb0E",
+     "3xTF32 GEMM on CTA pairs: sgemm_3xtf32_pair_kernel<256, B^T> (tcgen05 .cta_group::2)",
+     ["UTCHMMA.2CTA", "UTCHMMA", "UTCBAR.2CTA.MULTICAST", "UTMALDG.2D.2CTA", "UTMALDG",
+      "UTCATOMSWS.2CTA", "LDTM"]),
 ]
 
 
@@ -53,14 +57,18 @@ def main():
             print(f"== {title}: not found")
             continue
         name, body = hits[0]
-        hist = collections.Counter()
+        hist, full = collections.Counter(), collections.Counter()
         for line in body:
             op = opcode(line)
             if op:
                 hist[op.split(".")[0]] += 1
+                full[op] += 1
         print(f"== {title}\n   {name}\n   {sum(hist.values())} instructions")
         for op in ops:
-            print(f"   {op:8s} {hist.get(op, 0)}")
+            # dotted names count the opcodes with that qualified prefix
+            n = sum(v for k, v in full.items() if k.startswith(op)) if "." in op \
+                else hist.get(op, 0)
+            print(f"   {op:8s} {n}")
         if "sgemm" in pat:
             lines = [ln.strip() for ln in body if re.search(r"UTCHMMA|UTMALDG|LDTM", ln)][:8]
         else:
