@@ -1407,8 +1407,16 @@ int launch_pair(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, vo
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  // raster groups of 4 pair tiles (1024 A rows). At 16384^3 (ncu, DRAM read
+  // per GEMM; CUDA events back to back): 16 pair tiles 84 GB, 40.1 ms; 8:
+  // 57 GB, 38.1 ms; 4: 54 GB, 37.4 ms; 2: 38.9 ms
+  static const int group_m = [] {
+    const char* e = getenv("CAFXG_SGEMM_GROUP_M");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 4;
+  }();
   cudaLaunchKernelEx(&cfg, sgemm_3xtf32_pair_kernel<BNP, BMN>, m[0], m[1], m[2], m[3], C, M,
-                     N, K, ldc, splits, a_row0, b_row0, GROUP_M, ws);
+                     N, K, ldc, splits, a_row0, b_row0, group_m, ws);
   return (int)cudaGetLastError();
 }
 

@@ -35,6 +35,13 @@ WORK = {
     "storm_fp64_16x64sq_it256": storm(16, 256),
     "storm_fp64_64x64sq_it256": storm(64, 256),
     "cfg1_fp32_1920x1080_it100": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)],
+    # cfg1's two host waves: the first 273 rows (512K pixels), then the rest
+    "cfg1_wave0_rows0_273": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100, nrows=273)],
+    "cfg1_wave1_rows273_1080": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100,
+                                                row0=273)],
+    "tiny_fp32_64x64_it100": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 64, 64, 100)],
+    "cfg1_middle_rows405_675": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100,
+                                                row0=405, nrows=270)],
     "cfg3reg_fp32_4096_it3000": [pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 4096, 4096, 3000)],
     "deep_fp32_4096_it2000": [pkg.mandel_desc(-0.7487, -0.7485, 0.0650, 0.0652, 4096, 4096,
                                               2000)],
