@@ -115,7 +115,10 @@ constexpr unsigned kFull = 0xffffffffu;
 #define CAFXG_X4(S) S S S S
 #define CAFXG_X8(S) CAFXG_X4(S) CAFXG_X4(S)
 #define CAFXG_X16(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S) CAFXG_X4(S)
+#define CAFXG_X12(S) CAFXG_X8(S) CAFXG_X4(S)
+#define CAFXG_X20(S) CAFXG_X16(S) CAFXG_X4(S)
 #define CAFXG_X24(S) CAFXG_X16(S) CAFXG_X8(S)
+#define CAFXG_X28(S) CAFXG_X24(S) CAFXG_X4(S)
 #define CAFXG_X32(S) CAFXG_X16(S) CAFXG_X16(S)
 #define CAFXG_X40(S) CAFXG_X32(S) CAFXG_X8(S)
 #define CAFXG_X48(S) CAFXG_X32(S) CAFXG_X16(S)
@@ -127,8 +130,11 @@ constexpr unsigned kFull = 0xffffffffu;
 #define CAFXG_STEPS_SWITCH(K, BODY)                    \
   if constexpr (K == 4) { BODY(CAFXG_X4); }            \
   else if constexpr (K == 8) { BODY(CAFXG_X8); }       \
+  else if constexpr (K == 12) { BODY(CAFXG_X12); }     \
   else if constexpr (K == 16) { BODY(CAFXG_X16); }     \
+  else if constexpr (K == 20) { BODY(CAFXG_X20); }     \
   else if constexpr (K == 24) { BODY(CAFXG_X24); }     \
+  else if constexpr (K == 28) { BODY(CAFXG_X28); }     \
   else if constexpr (K == 32) { BODY(CAFXG_X32); }     \
   else if constexpr (K == 40) { BODY(CAFXG_X40); }     \
   else if constexpr (K == 48) { BODY(CAFXG_X48); }     \
@@ -244,6 +250,26 @@ struct F32Slots {
   __device__ __forceinline__ float zi_of(int s) const { return get_half(zi[s >> 1], s & 1); }
   __device__ __forceinline__ float cr_of(int s) const { return get_half(cr[s >> 1], s & 1); }
   __device__ __forceinline__ float ci_of(int s) const { return get_half(ci[s >> 1], s & 1); }
+  // mid-block checkpoint (deferred kernel): both pairs' packed z per lane
+  struct Mid {
+    uint64_t zr[2][32], zi[2][32];
+  };
+  __device__ __forceinline__ void save_mid(Mid& m, uint32_t lane) const {
+    m.zr[0][lane] = zr[0];
+    m.zr[1][lane] = zr[1];
+    m.zi[0][lane] = zi[0];
+    m.zi[1][lane] = zi[1];
+  }
+  static __device__ __forceinline__ float mid_zr(const Mid& m, int s, uint32_t lane) {
+    return get_half(m.zr[s >> 1][lane], s & 1);
+  }
+  static __device__ __forceinline__ float mid_zi(const Mid& m, int s, uint32_t lane) {
+    return get_half(m.zi[s >> 1][lane], s & 1);
+  }
+  // the block-end test on a saved z: fl(fl(zr^2) + fl(zi^2)) > 4 or NaN
+  static __device__ __forceinline__ bool escaped_at(float r, float i) {
+    return !(__fadd_rn(__fmul_rn(r, r), __fmul_rn(i, i)) <= 4.0f);
+  }
   // bit s: fl(zr^2 + zi^2) > 4 or NaN (an orbit that overflowed)
   __device__ __forceinline__ uint32_t escaped() const {
     uint32_t m = 0;
@@ -379,6 +405,22 @@ struct F64Slots {
   __device__ __forceinline__ double zi_of(int s) const { return s ? zi.y : zi.x; }
   __device__ __forceinline__ double cr_of(int s) const { return s ? cr.y : cr.x; }
   __device__ __forceinline__ double ci_of(int s) const { return s ? ci.y : ci.x; }
+  struct Mid {
+    double2 zr[32], zi[32];
+  };
+  __device__ __forceinline__ void save_mid(Mid& m, uint32_t lane) const {
+    m.zr[lane] = zr;
+    m.zi[lane] = zi;
+  }
+  static __device__ __forceinline__ double mid_zr(const Mid& m, int s, uint32_t lane) {
+    return s ? m.zr[lane].y : m.zr[lane].x;
+  }
+  static __device__ __forceinline__ double mid_zi(const Mid& m, int s, uint32_t lane) {
+    return s ? m.zi[lane].y : m.zi[lane].x;
+  }
+  static __device__ __forceinline__ bool escaped_at(double r, double i) {
+    return !(__dadd_rn(__dmul_rn(r, r), __dmul_rn(i, i)) <= 4.0);
+  }
   __device__ __forceinline__ uint32_t escaped() const {
     double s0 = __dadd_rn(zr2.x, zi2.x), s1 = __dadd_rn(zr2.y, zi2.y);
     return ((!(s0 <= 4.0)) ? 1u : 0u) | ((!(s1 <= 4.0)) ? 2u : 0u);
@@ -704,10 +746,23 @@ struct ReplayQueue {
   uint32_t n[kCap], o[kCap];
 };
 
+// Per warp: the replay queue and the mid-block checkpoint (the live slots'
+// z after half a block; see mandel_deferred_kernel).
+template <class Slots>
+struct DeferredWarp {
+  ReplayQueue<Slots> q;
+  typename Slots::Mid mid;
+};
+
 template <class Slots>
 constexpr size_t deferred_smem_bytes() {
-  return sizeof(ReplayQueue<Slots>) * (kMandelThreads / 32);
+  return sizeof(DeferredWarp<Slots>) * (kMandelThreads / 32);
 }
+
+// Replay window: the deferred kernel checkpoints z halfway through a fully
+// unrolled block, so an escaped block replays at most half its steps (8-step
+// units with runtime repeats keep whole-block replays).
+__host__ __device__ constexpr int deferred_replay_steps(int unit) { return unit == 8 ? 8 : unit / 2; }
 
 template <class Slots, int kUnit, bool kExact, bool kDirect>
 __device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
@@ -737,7 +792,7 @@ __device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
     for (uint32_t r = 0; r < L.block_reps; ++r)
       rp.template run<kUnit, kExact>(rn);
   } else {
-    rp.template run<kUnit, kExact>(rn);
+    rp.template run<deferred_replay_steps(kUnit), kExact>(rn);
   }
   constexpr uint32_t omask = kDirect ? (1u << kDirectShift) - 1u : 0xffffffffu;
 #pragma unroll
@@ -762,7 +817,9 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
   constexpr uint32_t kBatch = 32 * NS;
   using Cd = typename Slots::C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ReplayQueue<Slots>& q = reinterpret_cast<ReplayQueue<Slots>*>(smem_raw)[threadIdx.x >> 5];
+  DeferredWarp<Slots>& ws = reinterpret_cast<DeferredWarp<Slots>*>(smem_raw)[threadIdx.x >> 5];
+  ReplayQueue<Slots>& q = ws.q;
+  constexpr int kHalf = deferred_replay_steps(kUnit);
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t maxit = L.max_iter;
@@ -802,8 +859,12 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
         sl.template run_free<kUnit, kExact>();
     } else {
       // fully unrolled block (the host sets block_reps = 1): no runtime loop,
-      // which also spared ptxas a second copy of the block-start save
-      sl.template run_free<kUnit, kExact>();
+      // which also spared ptxas a second copy of the block-start save. The
+      // z halfway through goes to shared memory: an escaped block then
+      // replays only the half its escape lies in.
+      sl.template run_free<kHalf, kExact>();
+      sl.save_mid(ws.mid, lane);
+      sl.template run_free<kUnit - kHalf, kExact>();
     }
     const uint32_t esc = sl.escaped() & live;
     uint32_t done = esc;
@@ -832,11 +893,23 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
         const uint32_t b = __ballot_sync(kFull, esc >> s & 1u);
         if (esc >> s & 1u) {
           const uint32_t e = base + __popc(b & lt_mask);
-          q.zr[e] = szr[s];
-          q.zi[e] = szi[s];
+          Cd rz = szr[s], iz = szi[s];
+          uint32_t rn = n[s];
+          if constexpr (kUnit != 8) {
+            // not yet escaped halfway (the orbit stays out once out, see
+            // above): the escape lies in the second half
+            const Cd mr = Slots::mid_zr(ws.mid, s, lane), mi = Slots::mid_zi(ws.mid, s, lane);
+            if (!Slots::escaped_at(mr, mi)) {
+              rz = mr;
+              iz = mi;
+              rn += kHalf;
+            }
+          }
+          q.zr[e] = rz;
+          q.zi[e] = iz;
           q.cr[e] = sl.cr_of(s);
           q.ci[e] = sl.ci_of(s);
-          q.n[e] = n[s];
+          q.n[e] = rn;
           q.o[e] = o[s];
         }
         base += __popc(b);
@@ -908,8 +981,12 @@ int launch_deferred_t(const MLaunch& L, int grid, cudaStream_t s) {
     if (cudaError_t e = opt_in_smem(mandel_deferred_kernel<A, kUnit, kExact, 1>, smem, opted))
       return (int)e;
     mandel_deferred_kernel<A, kUnit, kExact, 1><<<grid, kMandelThreads, smem, s>>>(L);
-  } else
+  } else {
+    static std::atomic<uint64_t> opted{0};  // queues + checkpoints: > 48 KB
+    if (cudaError_t e = opt_in_smem(mandel_deferred_kernel<A, kUnit, kExact, 0>, smem, opted))
+      return (int)e;
     mandel_deferred_kernel<A, kUnit, kExact, 0><<<grid, kMandelThreads, smem, s>>>(L);
+  }
   return (int)cudaGetLastError();
 }
 
@@ -923,6 +1000,8 @@ int occ_t() {
 
 template <class A, int kUnit, bool kExact>
 int occ_deferred_t() {
+  static std::atomic<uint64_t> opted{0};
+  opt_in_smem(mandel_deferred_kernel<A, kUnit, kExact, 0>, deferred_smem_bytes<A>(), opted);
   int n = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &n, mandel_deferred_kernel<A, kUnit, kExact, 0>, kMandelThreads,
@@ -930,8 +1009,9 @@ int occ_deferred_t() {
   return n;
 }
 
-static_assert(deferred_smem_bytes<F32Slots>() <= 48 * 1024, "replay queues exceed 48 KB");
-static_assert(deferred_smem_bytes<F64Slots>() <= 48 * 1024, "replay queues exceed 48 KB");
+// two CTAs per SM with their static chunk tables
+static_assert(deferred_smem_bytes<F32Slots>() <= 96 * 1024, "replay queues exceed 96 KB");
+static_assert(deferred_smem_bytes<F64Slots>() <= 96 * 1024, "replay queues exceed 96 KB");
 
 }  // namespace
 
