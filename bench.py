@@ -514,17 +514,18 @@ def measure(args, N):
     peak_gpu = sms * 128 * sm_max * 1e6 / 1e12
     achieved = 8.0 * iters / (step_ms / 1e3) / 1e12
     # DRAM traffic of the escape kernel from the committed ncu capture of the
-    # full-image launch (profiles/round1/mandel_cfg3_v20_full.txt:
-    # 1.021409 GB written + 10.748672 MB read), the whole image over N devices
-    traffic = round(1.021409e9 + 10.748672e6)
-    # The same capture: FMA pipe busy 92.5% of active cycles, 6.42 executed
-    # lane-ops per iteration (6 in the unchecked step, the rest block-end
-    # tests, refills and exact replays) against the algorithmic 8.
-    exec_ops_per_iter = 6.42
+    # full-image launch (profiles/round2/mandel_cfg3_mid_r2_full.txt:
+    # 1.023902 GB written + 10.715136 MB read), the whole image over N devices
+    traffic = round(1.023902e9 + 10.715136e6)
+    # The same capture: FMA pipe busy 91.7% of active cycles over 33.71 ms at
+    # 1.963 GHz = 6.31 executed lane-ops per iteration (6 in the unchecked
+    # step, the rest block-end tests, refills and exact replays) against the
+    # algorithmic 8.
+    exec_ops_per_iter = 6.31
     roof = {"bound": "fp32_pipe", "achieved": round(achieved, 3),
             "peak": round(N * peak_gpu, 3), "unit": "TFLOP/s",
             "frac": round(achieved / (N * peak_gpu), 4), "traffic": traffic,
-            "traffic_note": "dram read+write bytes per image (ncu, profiles/round1); "
+            "traffic_note": "dram read+write bytes per image (ncu, profiles/round2); "
                             "algorithmic output is 4 B/pixel",
             "ops_per_step": 8.0 * iters,
             "peak_basis": f"{N} x {sms} SMs x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz of "
@@ -534,8 +535,8 @@ def measure(args, N):
             "frac_note": "frac counts the reference's 8 FP ops per iteration, so it can exceed "
                          "1: the kernel executes 6 per iteration (escape test deferred to the "
                          "ends of unchecked blocks, 2*zr*zi+ci as one FMA) plus block-end tests "
-                         "and exact replays, 6.42 lane-ops/iteration measured (ncu FMA pipe "
-                         "busy 92.5%, profiles/round1/mandel_cfg3_v20_full.txt); "
+                         "and exact replays, 6.31 lane-ops/iteration measured (ncu FMA pipe "
+                         "busy 91.7%, profiles/round2/mandel_cfg3_mid_r2_full.txt); "
                          "frac_executed is the pipe fraction doing that executed work"}
     if probe and probe.get("fp32_lane_tops"):
         pp = N * probe["fp32_lane_tops"]
