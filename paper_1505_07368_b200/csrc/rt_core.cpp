@@ -459,6 +459,9 @@ int cafxg_sync(cafxg_ctx* ctx) {
 int cafxg_close(cafxg_ctx* ctx) try {
   if (!ctx)
     return CAFXG_OK;
+  if (trace_on() || getenv("CAFXG_STATS"))
+    fprintf(stderr, "cafxg: pinned pool: %llu driver allocations\n",
+            (unsigned long long)ctx->pinned.new_allocs());
   if ((trace_on() || getenv("CAFXG_STATS")) && ctx->st_batches.load())
     fprintf(stderr, "cafxg: %llu batches, dispatcher submit time %.3f ms (%.2f us/batch)\n",
             (unsigned long long)ctx->st_batches.load(), ctx->st_batch_ns.load() / 1e6,

@@ -40,44 +40,66 @@ extern thread_local std::string t_last_error;
 // ---- pinned host pool -----------------------------------------------------------
 // Page-locked, portable, device-mapped buffers cached by power-of-two size
 // class. Reply buffers that live here are written by DMA or by the reply
-// scatter kernel directly.
+// scatter kernel directly. Classes up to kSlabClassMax are carved out of
+// 64 MB slabs: one driver call per slab instead of one per buffer (a storm
+// of 102,400 outstanding 16 KB replies made ~100K cudaHostAlloc calls, which
+// serialise on the driver lock against the dispatcher's launches and copies).
 class PinnedPool {
  public:
+  static constexpr size_t kSlabBytes = 64ull << 20;
+  static constexpr size_t kSlabClassMax = 1ull << 20;
+
   ~PinnedPool() {
     std::lock_guard<std::mutex> g(mu_);
-    for (auto& kv : free_)
-      for (void* p : kv.second)
-        cudaFreeHost(p);
-    for (auto& kv : live_)
-      cudaFreeHost(kv.first);
+    for (void* p : slabs_)
+      cudaFreeHost(p);
+    for (void* p : large_)
+      cudaFreeHost(p);
   }
 
   void* alloc(size_t bytes) {
     size_t cls = size_class(bytes);
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      auto it = free_.find(cls);
-      if (it != free_.end() && !it->second.empty()) {
-        void* p = it->second.back();
-        it->second.pop_back();
-        live_[p] = cls;
-        return p;
-      }
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = free_.find(cls);
+    if (it != free_.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      live_[p] = cls;
+      return p;
     }
     void* p = nullptr;
-    if (cudaHostAlloc(&p, cls, cudaHostAllocPortable | cudaHostAllocMapped) !=
-        cudaSuccess) {
-      cudaGetLastError();
-      return nullptr;
+    if (cls <= kSlabClassMax) {
+      if (!slab_ || slab_used_ + cls > kSlabBytes) {
+        void* s = nullptr;
+        new_allocs_.fetch_add(1, std::memory_order_relaxed);
+        if (cudaHostAlloc(&s, kSlabBytes, cudaHostAllocPortable | cudaHostAllocMapped) !=
+            cudaSuccess) {
+          cudaGetLastError();
+          return nullptr;
+        }
+        slabs_.push_back(s);
+        slab_ = (uint8_t*)s;
+        slab_used_ = 0;
+        add_range(s, kSlabBytes);
+      }
+      p = slab_ + slab_used_;  // classes are multiples of 4 KB: page-aligned
+      slab_used_ += cls;
+    } else {
+      new_allocs_.fetch_add(1, std::memory_order_relaxed);
+      if (cudaHostAlloc(&p, cls, cudaHostAllocPortable | cudaHostAllocMapped) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      large_.push_back(p);
+      add_range(p, cls);
     }
-    std::lock_guard<std::mutex> g(mu_);
     live_[p] = cls;
-    {
-      std::unique_lock<std::shared_mutex> w(ranges_mu_);
-      ranges_[(uintptr_t)p] = cls;
-    }
     return p;
   }
+
+  // driver allocations so far (CAFXG_STATS=1 prints them at close)
+  uint64_t new_allocs() const { return new_allocs_.load(std::memory_order_relaxed); }
 
   bool free(void* p) {
     std::lock_guard<std::mutex> g(mu_);
@@ -89,7 +111,7 @@ class PinnedPool {
     return true;
   }
 
-  // [p, p+bytes) inside one pool buffer (no driver call). Every client
+  // [p, p+bytes) inside one pool slab or buffer (no driver call). Every client
   // thread classifies its reply buffer here, so the common case takes no lock
   // at all: a thread-local cache of the last buffer hit (pool buffers stay
   // pinned and device-mapped until the context closes, so a cached range
@@ -123,11 +145,19 @@ class PinnedPool {
       c <<= 1;
     return c;
   }
+  void add_range(void* p, size_t bytes) {
+    std::unique_lock<std::shared_mutex> w(ranges_mu_);
+    ranges_[(uintptr_t)p] = bytes;
+  }
   std::mutex mu_;
+  std::atomic<uint64_t> new_allocs_{0};
   std::unordered_map<void*, size_t> live_;
   std::map<size_t, std::vector<void*>> free_;
+  std::vector<void*> slabs_, large_;  // what the driver allocated
+  uint8_t* slab_ = nullptr;           // the slab small classes are carved from
+  size_t slab_used_ = 0;
   mutable std::shared_mutex ranges_mu_;
-  std::map<uintptr_t, size_t> ranges_;  // every buffer ever allocated
+  std::map<uintptr_t, size_t> ranges_;  // every slab and large buffer
   // unique per pool instance (never reused), so a thread-local cache entry of
   // a closed context can never match a later one
   static inline std::atomic<uint64_t> next_id_{1};
