@@ -1166,14 +1166,6 @@ size_t sgemm_tc_ws_bytes(int M, int N, int splits, int bn) {
   return (size_t)(M / BM) * (N / bn) * splits * BM * bn * sizeof(float);
 }
 
-namespace {
-struct TcPlan;
-TcPlan tc_plan(int M, int N, int K, int sms, int splits_req);
-}  // namespace
-
-size_t sgemm_tc_scratch_bytes(int M, int N, int K, int sm_count, int splits_req);
-
-
 int sgemm_tc_split_a(const float* A, int lda, int M, int K, float* Ah, float* Al,
                      void* stream) {
   int grid = (int)std::min<size_t>(((size_t)M * K / 4 + 255) / 256, 148 * 16);
