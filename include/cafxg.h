@@ -149,6 +149,11 @@ int cafxg_run_mandelbrot(cafxg_ctx* ctx, uint32_t size, uint32_t max_iter,
 /* ---- fp32 matrix multiply --------------------------------------------------
  * C = A * B, row-major, the OpenCL `matrix_multiply(matrix1, matrix2, output)`
  * contract. */
+/* The 3xTF32 path takes M % 128 == 0, N % 128 == 0, K % 32 == 0 (M, N >= 128),
+ * lda, ldc multiples of 4 and, for device-resident calls, A and C 16-byte
+ * aligned; AUTO runs the FFMA kernel otherwise and 3XTF32 fails with
+ * CAFXG_E_CONFIG. Results are within 1e-5 normwise of an fp64-accumulated
+ * product either way. */
 enum {
   CAFXG_SGEMM_AUTO = 0,   /* 3xTF32 tensor cores when shapes allow, else FFMA */
   CAFXG_SGEMM_FFMA = 1,   /* register-tiled SIMT fp32 FFMA */

@@ -40,11 +40,14 @@ int sgemm_on_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     const char* e = getenv("CAFXG_SGEMM_AUTO_TC");
     return !(e && e[0] == '0');
   }();
-  bool supported = sgemm_tc_supported(g.M, g.N, g.K, g.lda, g.ldb, g.ldc);
+  // the tensor-core path reads A and writes C in 16-byte vectors (device-API
+  // callers pass arbitrary pointers; host requests use the pool's buffers)
+  const bool aligned = ((uintptr_t)A & 15) == 0 && ((uintptr_t)C & 15) == 0;
+  bool supported = aligned && sgemm_tc_supported(g.M, g.N, g.K, g.lda, g.ldb, g.ldc);
   bool tc = supported && (g.mode == CAFXG_SGEMM_3XTF32 || (g.mode == CAFXG_SGEMM_AUTO && auto_tc));
   if (g.mode == CAFXG_SGEMM_3XTF32 && !tc)
     return fail(CAFXG_E_CONFIG,
-                "sgemm: shape not supported by the 3xTF32 kernel (see cafxg.h)");
+                "sgemm: shape or alignment not supported by the 3xTF32 kernel (see cafxg.h)");
   if (tc) {
     size_t sb = sgemm_tc_scratch_bytes(g.M, g.N, g.K, d->sms, (int)g.splits);
     void* scratch = nullptr;

@@ -256,6 +256,33 @@ print("ok")
             assert np.array_equal(np.load(path), np.load(other))
 
 
+def test_sgemm_device_misaligned_pointers(ctx):
+    """Device-API operands at a 4-byte (not 16-byte) offset: AUTO falls back
+    to the FFMA kernel and stays within the tolerance, 3XTF32 refuses with
+    E_CONFIG -- neither may fault the device (the tensor-core path reads A
+    and writes C in 16-byte vectors)."""
+    import torch
+    M = N = K = 256
+    A_h = oracle.fill_uniform(M * K, 31).reshape(M, K)
+    B_h = oracle.fill_uniform(K * N, 32).reshape(K, N)
+    Abuf = torch.zeros(M * K + 4, device="cuda")
+    Cbuf = torch.zeros(M * N + 4, device="cuda")
+    Abuf[1:1 + M * K] = torch.from_numpy(A_h.ravel()).cuda()
+    B = torch.from_numpy(B_h).cuda()
+    a_ptr, c_ptr = Abuf.data_ptr() + 4, Cbuf.data_ptr() + 4
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with pytest.raises(pkg.CafxgError) as e:
+        ctx.sgemm_device(M, N, K, a_ptr, B.data_ptr(), c_ptr, s.cuda_stream,
+                         mode=pkg.SGEMM_3XTF32)
+    assert e.value.code == 8
+    ctx.sgemm_device(M, N, K, a_ptr, B.data_ptr(), c_ptr, s.cuda_stream, mode=pkg.SGEMM_AUTO)
+    torch.cuda.synchronize()
+    C = Cbuf[1:1 + M * N].cpu().numpy().reshape(M, N)
+    assert check(A_h, B_h, C) <= TOL
+    assert ctx.status() == 0
+
+
 def test_cfg5_full_size_row_sum_property(ctx):
     """Full-size property for cfg5 (16384^3, the sampled-row check covers a
     few rows): C.1 = A.(B.1) for every row. B.1 and A.(B.1) are computed in
