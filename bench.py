@@ -711,7 +711,9 @@ def sec_sgemm(ctx, args, n, N):
     """fp32 matmul C = A.B (cfg2: 1024^3, cfg5: 16384^3). Device-resident:
     each device's row block of A (M/N rows) times the whole of B, CUDA events
     per device, max over devices. End to end: cafxg_sgemm over the N-device
-    context (1/N of B up per device + NCCL all-gather at N > 1)."""
+    context (1/N of B up per device; at N > 1 every device's GEMM reads the
+    other slices from the peers in place -- peer_gemms -- or, without peer
+    access, B is replicated by the NCCL all-gather)."""
     import numpy as np
     import torch
 
@@ -775,6 +777,8 @@ def sec_sgemm(ctx, args, n, N):
            "e2e_ms": round(e2e, 3),
            "e2e_tflops": round(2.0 * n ** 3 / (e2e / 1e3) / 1e12, 2),
            "nccl_collectives": int(st1.nccl_collectives - st0.nccl_collectives),
+           # N > 1: GEMMs that read B's K slices from the peers in place (no all-gather)
+           "peer_gemms": int(st1.peer_gemms - st0.peer_gemms),
            "max_rel_err_sampled_rows": err, "max_rel_err_e2e": err_e2e, "tolerance": 1e-5}
     if N == 1 and not args.no_cpu_baseline:
         tf, cores, sample, srows, full = cpu_sgemm(n, A_h, B_h, 10.0)

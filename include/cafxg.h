@@ -28,7 +28,8 @@
 extern "C" {
 #endif
 
-#define CAFXG_ABI_VERSION 2  /* 2: cafxg_stats grew nccl_collectives, devices_used */
+#define CAFXG_ABI_VERSION 3  /* 2: cafxg_stats grew nccl_collectives, devices_used;
+                                3: peer_gemms */
 
 /* ---- status codes: numeric values of cafx::errc (error.hpp:11-29) --------- */
 enum {
@@ -263,6 +264,7 @@ typedef struct {
   uint64_t direct_batches; /* batches whose escape kernel wrote the replies itself */
   uint64_t nccl_collectives; /* NCCL collectives issued (multi-device B all-gather) */
   uint64_t devices_used;   /* bit i set: context device i has run a kernel */
+  uint64_t peer_gemms;     /* multi-device GEMMs that read B's slices from the peers in place */
 } cafxg_stats;
 int cafxg_get_stats(cafxg_ctx* ctx, cafxg_stats* out);
 

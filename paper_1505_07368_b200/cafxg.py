@@ -84,7 +84,7 @@ class Stats(C.Structure):
                 ("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64),
                 ("d2h_bytes", C.c_uint64), ("max_batch", C.c_uint64),
                 ("direct_batches", C.c_uint64), ("nccl_collectives", C.c_uint64),
-                ("devices_used", C.c_uint64)]
+                ("devices_used", C.c_uint64), ("peer_gemms", C.c_uint64)]
 
 
 DONE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int)

@@ -615,6 +615,7 @@ int cafxg_get_stats(cafxg_ctx* ctx, cafxg_stats* out) {
   out->max_batch = ctx->st_max_batch.load();
   out->direct_batches = ctx->st_direct.load();
   out->nccl_collectives = ctx->st_nccl.load();
+  out->peer_gemms = ctx->st_p2p.load();
   out->devices_used = ctx->st_dev_used.load();
   return CAFXG_OK;
 }

@@ -102,6 +102,170 @@ int ensure_nccl(cafxg_ctx* ctx) {
   return CAFXG_OK;
 }
 
+// ---- multi-device GEMM fused with the exchange of B ----------------------------
+// B is uploaded in K slices, 1/G per device (each device also makes the lo
+// halves of its slice); every device then multiplies its row block of A by
+// the whole of B with sgemm_tc_peer_gemm, whose TMA loads read each k-block
+// from the device that holds its slice -- over NVLink for the peers' slices.
+// The all-gather of the NCCL path disappears into the GEMM: remote tiles are
+// fetched as the tensor cores consume them, overlapped with the MMAs of the
+// earlier stages, and no device holds a full copy of B. Needs peer access
+// between every pair of the context's GPUs (virtual devices share one GPU,
+// where the "peer" slices are local: the same code path, tested on one GPU).
+// CAFXG_SGEMM_P2P=0 keeps the NCCL all-gather path.
+static bool p2p_wanted() {
+  static const bool on = [] {
+    const char* e = getenv("CAFXG_SGEMM_P2P");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static bool peer_access_all(cafxg_ctx* ctx) {
+  std::lock_guard<std::mutex> g(ctx->nccl_mu);  // (serialises the one-time enabling)
+  if (ctx->p2p_state)
+    return ctx->p2p_state > 0;
+  int ok = 1;
+  for (auto& a : ctx->devs)
+    for (auto& b : ctx->devs) {
+      if (a->ordinal == b->ordinal)
+        continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, a->ordinal, b->ordinal) != cudaSuccess || !can) {
+        ok = -1;
+        continue;
+      }
+      cudaSetDevice(a->ordinal);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b->ordinal, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        ok = -1;
+    }
+  cudaGetLastError();
+  ctx->p2p_state = ok;
+  return ok > 0;
+}
+
+static bool p2p_eligible(cafxg_ctx* ctx, const cafxg_sgemm_desc& g, uint32_t rows_per) {
+  const int G = (int)ctx->devs.size();
+  return G > 1 && p2p_wanted() && g.mode != CAFXG_SGEMM_FFMA && g.K % G == 0 &&
+         g.M % 128 == 0 && rows_per % 128 == 0 && sgemm_tc_peer_supported(128, g.N, g.K, G) &&
+         peer_access_all(ctx);
+}
+
+static int sgemm_p2p_submit(cafxg_ctx* ctx, const cafxg_sgemm_desc& g, const float* A,
+                            const float* B, float* C, uint32_t rows_per, Join* join) {
+  const size_t G = ctx->devs.size(), M = g.M, N = g.N, K = g.K, ks = K / G;
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (auto& d : ctx->devs)
+    locks.emplace_back(d->submit_mu);
+  int status = CAFXG_OK;
+  auto note = [&](int s) {
+    if (status == CAFXG_OK && s != CAFXG_OK)
+      status = s;
+  };
+  std::vector<float*> dB(G, nullptr), dBl(G, nullptr);
+  std::vector<cudaEvent_t> ready(G, nullptr), done(G, nullptr);
+  // 1. each device: its K slice of B (and the slice's lo halves)
+  for (size_t k = 0; k < G; ++k) {
+    Device* d = ctx->devs[k].get();
+    cudaSetDevice(d->ordinal);
+    cudaStream_t cs = d->compute;
+    if (status == CAFXG_OK &&
+        (cudaMallocAsync((void**)&dB[k], ks * N * 4, cs) != cudaSuccess ||
+         cudaMallocAsync((void**)&dBl[k], ks * N * 4, cs) != cudaSuccess))
+      note(cuda_status(cudaGetLastError(), "sgemm p2p: B slice allocation"));
+    if (status == CAFXG_OK) {
+      note(cuda_status(cudaMemcpy2DAsync(dB[k], N * 4, B + k * ks * g.ldb, (size_t)g.ldb * 4,
+                                         N * 4, ks, cudaMemcpyHostToDevice, cs),
+                       "sgemm p2p: B slice upload"));
+      ctx->st_h2d += ks * N * 4;
+    }
+    if (status == CAFXG_OK) {
+      const int e = sgemm_tc_lo(dB[k], (int)N, (int)ks, (int)N, dBl[k], d->sms, cs);
+      note(e ? cuda_status((cudaError_t)e, "sgemm p2p: B lo pass") : CAFXG_OK);
+      ctx->st_launches++;
+    }
+    ready[k] = pooled_event(d);
+    if (ready[k])
+      cudaEventRecord(ready[k], cs);
+  }
+  // 2. each device: its rows of A times all of B (peer slices read in place)
+  for (size_t k = 0; k < G; ++k) {
+    Device* d = ctx->devs[k].get();
+    cudaSetDevice(d->ordinal);
+    cudaStream_t cs = d->compute;
+    for (size_t j = 0; j < G; ++j)
+      if (ready[j])
+        cudaStreamWaitEvent(cs, ready[j], 0);
+    const size_t r0 = std::min<size_t>(M, rows_per * k), r1 = std::min<size_t>(M, rows_per * (k + 1));
+    const size_t m = r1 - r0;
+    if (status == CAFXG_OK && m) {
+      float *dA = nullptr, *dAl = nullptr, *dC = nullptr;
+      if (cudaMallocAsync((void**)&dA, m * K * 4, cs) != cudaSuccess ||
+          cudaMallocAsync((void**)&dAl, m * K * 4, cs) != cudaSuccess ||
+          cudaMallocAsync((void**)&dC, m * N * 4, cs) != cudaSuccess)
+        note(cuda_status(cudaGetLastError(), "sgemm p2p: A / C allocation"));
+      if (status == CAFXG_OK) {
+        note(cuda_status(cudaMemcpy2DAsync(dA, K * 4, A + r0 * g.lda, (size_t)g.lda * 4, K * 4,
+                                           m, cudaMemcpyHostToDevice, cs),
+                         "sgemm p2p: A upload"));
+        ctx->st_h2d += m * K * 4;
+      }
+      if (status == CAFXG_OK) {
+        int e = sgemm_tc_lo(dA, (int)K, (int)m, (int)K, dAl, d->sms, cs);
+        if (!e)
+          e = sgemm_tc_peer_gemm(dA, (int)K, dAl, (int)m, (int)N, (int)K, dB.data(), dBl.data(),
+                                 (int)G, dC, (int)N, cs);
+        note(e ? cuda_status((cudaError_t)e, "sgemm p2p: GEMM launch") : CAFXG_OK);
+        ctx->st_launches += 2;
+        mark_used(ctx, d);
+      }
+      if (status == CAFXG_OK) {
+        note(cuda_status(cudaMemcpy2DAsync(C + r0 * g.ldc, (size_t)g.ldc * 4, dC, N * 4, N * 4,
+                                           m, cudaMemcpyDeviceToHost, cs),
+                         "sgemm p2p: C download"));
+        ctx->st_d2h += m * N * 4;
+      }
+      for (float* p : {dA, dAl, dC})
+        if (p)
+          cudaFreeAsync(p, cs);
+    }
+    done[k] = pooled_event(d);
+    if (done[k])
+      cudaEventRecord(done[k], cs);
+  }
+  // 3. a slice is freed once every device's GEMM has read it; each device's
+  // part completes behind that (so behind every device's download)
+  for (size_t k = 0; k < G; ++k) {
+    Device* d = ctx->devs[k].get();
+    cudaSetDevice(d->ordinal);
+    for (size_t j = 0; j < G; ++j)
+      if (done[j])
+        cudaStreamWaitEvent(d->compute, done[j], 0);
+    if (dB[k])
+      cudaFreeAsync(dB[k], d->compute);
+    if (dBl[k])
+      cudaFreeAsync(dBl[k], d->compute);
+  }
+  // every wait on the events is enqueued: back to their pools
+  for (size_t k = 0; k < G; ++k) {
+    Device* d = ctx->devs[k].get();
+    for (cudaEvent_t e : {ready[k], done[k]})
+      if (e)
+        d->ev_pool.push_back(e);
+  }
+  const int st = status;
+  for (size_t k = 0; k < G; ++k) {
+    Device* d = ctx->devs[k].get();
+    cudaSetDevice(d->ordinal);
+    if (st != CAFXG_OK)
+      push_completion(ctx, d, d->compute, [join, st](int) { join->part_done(st); });
+    else
+      push_completion(ctx, d, d->compute, [join](int s) { join->part_done(s); });
+  }
+  return CAFXG_OK;
+}
+
 // Host-request pipeline for one device's C rows [r0, r1) with B already in
 // device memory (dB, K x N): B is split once (tf32 hi/lo, transposed), then
 // per block of R rows: H2D of A_i on the upload stream -> hi/lo split + 3xTF32
@@ -466,6 +630,20 @@ int sgemm_submit_impl(cafxg_ctx* ctx, const cafxg_sgemm_desc* desc,
   bool nccl = false;
   if (G > 1 && g.M >= G * 128 && g.K % G == 0 && g.ldb == g.N) {
     use = G;
+    // the GEMM that reads B's slices from the peers in place (above)
+    const uint32_t rp = (uint32_t)((g.M + use - 1) / use);
+    const uint32_t rows_per = (rp + 127) / 128 * 128;
+    if (p2p_eligible(ctx, g, rows_per)) {
+      clear_last_error();
+      Join* join = new Join;
+      join->done = done;
+      join->user = user;
+      join->remaining = (int)use;
+      ctx->st_requests++;
+      ctx->st_p2p++;
+      return sgemm_p2p_submit(ctx, g, A, B, C, rows_per, join);
+    }
+    clear_last_error();
     // NCCL all-gather over NVLink; without it (virtual devices, or NCCL not
     // loadable) the slices are replicated by peer copies on the copy engines
     nccl = ensure_nccl(ctx) == CAFXG_OK;

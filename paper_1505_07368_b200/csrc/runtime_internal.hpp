@@ -334,6 +334,7 @@ struct cafxg_ctx {
   std::atomic<uint64_t> st_batch_ns{0};  // dispatcher time spent submitting batches
   std::atomic<uint64_t> st_direct{0};    // batches replied by the escape kernel itself
   std::atomic<uint64_t> st_nccl{0};      // NCCL collectives issued (B all-gathers)
+  std::atomic<uint64_t> st_p2p{0};       // multi-device GEMMs reading B's slices in place
   std::atomic<uint64_t> st_dev_used{0};  // bit i: context device i ran a kernel
   std::atomic<uint64_t> st_phase_ns[6] = {};  // run_mandel_batch phases (CAFXG_STATS)
   // actor dispatcher
@@ -380,6 +381,7 @@ struct cafxg_ctx {
   // NCCL communicators for multi-device sgemm (one per device)
   std::mutex nccl_mu;
   bool nccl_failed = false;
+  int p2p_state = 0;  // peer access between every pair of GPUs: 0 unknown, 1 yes, -1 no
   NcclApi nccl;
   std::vector<ncclComm_t> comms;
 };

@@ -54,6 +54,19 @@ int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, i
                        void* stream, int splits, int a_row0 = 0, int b_row0 = 0,
                        float* ws = nullptr);
 size_t sgemm_tc_ws_bytes(int M, int N, int splits, int bn);
+// lo halves of one operand (rows x cols, pitch ld) for the raw-operand GEMMs:
+// lo = rna_tf32(x - trunc_tf32(x)), packed (pitch cols)
+int sgemm_tc_lo(const float* X, int ld, int rows, int cols, float* out, int sm_count,
+                void* stream);
+// The multi-device fused GEMM: C (M x N) = A (M x K, raw + lo) times B whose
+// K slices (K / nslices rows of N floats each, raw + lo, pitch N) live in the
+// memory of the context's devices -- the kernel's TMA loads pull each k-block
+// from the slice's device over NVLink (peer access enabled), so B is never
+// gathered. M % 128 == 0, N % 256 == 0, K / nslices a multiple of 16.
+bool sgemm_tc_peer_supported(int M, int N, int K, int nslices);
+int sgemm_tc_peer_gemm(const float* A, int lda, const float* Alo, int M, int N, int K,
+                       const float* const* Bs, const float* const* Blos, int nslices, float* C,
+                       int ldc, void* stream);
 // CTA-pair kernel (256 x 256 pair tiles, tcgen05 .cta_group::2) for split
 // operands: whether an M x N x K product should take it (a grid that needs no
 // split-K), and its maps (launched by sgemm_tc_gemm_maps with splits 1; blocks

@@ -292,14 +292,65 @@ __device__ __forceinline__ void reduce_ws(const float* __restrict__ ws, const ui
 
 // ---- the GEMM kernel --------------------------------------------------------
 
-template <int BN, bool BMN>
-__global__ void __launch_bounds__(TC_THREADS, 1)
-    sgemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAh,
-                        const __grid_constant__ CUtensorMap mAl,
-                        const __grid_constant__ CUtensorMap mBh,
-                        const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
-                        int M, int N, int K, int ldc, int splits, int a_row0,
-                        int b_row0, int group_m, float* __restrict__ ws) {
+// Where the 1-SM kernel's B stages come from. OneB: one (hi, lo) pair of
+// tensor maps over the whole of B (or B^T). PeerBLoad (the multi-device fused
+// path): one pair per K slice, each slice resident in the memory of the
+// device that uploaded it; the producer picks the slice of each k-block, so
+// the TMA engine pulls remote slices over NVLink tile by tile as the MMAs
+// consume them -- the all-gather of B becomes the GEMM's own loads.
+struct OneB {
+  const CUtensorMap* h;
+  const CUtensorMap* l;
+  __device__ __forceinline__ void prefetch() const {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(h)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(l)) : "memory");
+  }
+  template <bool BMN>
+  __device__ __forceinline__ void load(uint8_t* dh, uint8_t* dl, uint64_t* bar, int kx,
+                                       int ncol) const {
+    if constexpr (BMN) {
+      // (one 3-D box: 32 columns x BK rows x BN / 32 chunks)
+      tma_load_3d(dh, h, bar, 0, kx, ncol / 32);
+      tma_load_3d(dl, l, bar, 0, kx, ncol / 32);
+    } else {
+      tma_load_2d(dh, h, bar, kx, ncol);
+      tma_load_2d(dl, l, bar, kx, ncol);
+    }
+  }
+};
+
+constexpr int kMaxPeerSlices = 8;
+struct PeerB {
+  CUtensorMap h[kMaxPeerSlices], l[kMaxPeerSlices];  // raw B / lo(B), MN-major
+  int kslice;                                          // K rows per slice
+  int n;                                               // slices
+};
+
+struct PeerBLoad {
+  const PeerB* p;
+  __device__ __forceinline__ void prefetch() const {
+    for (int i = 0; i < p->n; ++i) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p->h[i]))
+                   : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p->l[i]))
+                   : "memory");
+    }
+  }
+  template <bool BMN>
+  __device__ __forceinline__ void load(uint8_t* dh, uint8_t* dl, uint64_t* bar, int kx,
+                                       int ncol) const {
+    static_assert(BMN, "peer slices are raw MN-major B");
+    const int src = kx / p->kslice, k = kx - src * p->kslice;
+    tma_load_3d(dh, &p->h[src], bar, 0, k, ncol / 32);
+    tma_load_3d(dl, &p->l[src], bar, 0, k, ncol / 32);
+  }
+};
+
+template <int BN, bool BMN, class BSrc>
+__device__ __forceinline__ void gemm_body(const CUtensorMap& mAh, const CUtensorMap& mAl,
+                                          const BSrc& bsrc, float* __restrict__ C, int M,
+                                          int N, int K, int ldc, int splits, int a_row0,
+                                          int b_row0, int group_m, float* __restrict__ ws) {
   using G = Cfg<BN, BMN>;
   constexpr int STAGE_BYTES = G::STAGE_BYTES, B_TILE = G::B_TILE;
   // a_row0 / b_row0: first row of this GEMM's A / B^T block inside the
@@ -337,9 +388,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int nk = ksplit / BK;
 
   if (warp == 0 && lane == 0) {
-    for (const CUtensorMap* m : {&mAh, &mAl, &mBh, &mBl})
+    for (const CUtensorMap* m : {&mAh, &mAl})
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m))
                    : "memory");
+    bsrc.prefetch();
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -382,16 +434,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int kx = k_base + kb * BK;
         tma_load_2d(st, &mAh, &full[s], kx, a_row0 + m0);
         tma_load_2d(st + A_TILE, &mAl, &full[s], kx, a_row0 + m0);
-        if constexpr (BMN) {
-          // raw B and its lo half as they lie (K rows of N floats): BN / 32
-          // chunks of 32 columns each; b_row0 is the first column
-          // (one 3-D box: 32 columns x BK rows x BN / 32 chunks)
-          tma_load_3d(st + 2 * A_TILE, &mBh, &full[s], 0, kx, (b_row0 + n0) / 32);
-          tma_load_3d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], 0, kx, (b_row0 + n0) / 32);
-        } else {
-          tma_load_2d(st + 2 * A_TILE, &mBh, &full[s], kx, b_row0 + n0);
-          tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, &full[s], kx, b_row0 + n0);
-        }
+        // B^T rows, or (BMN) raw B and its lo half as they lie (K rows of N
+        // floats, BN / 32 chunks of 32 columns; b_row0 is then the first column)
+        bsrc.template load<BMN>(st + 2 * A_TILE, st + 2 * A_TILE + B_TILE, &full[s], kx,
+                                b_row0 + n0);
       }
     }
     __syncwarp();
@@ -570,6 +616,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(G::TMEM_COLS));
+}
+
+template <int BN, bool BMN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    sgemm_3xtf32_kernel(const __grid_constant__ CUtensorMap mAh,
+                        const __grid_constant__ CUtensorMap mAl,
+                        const __grid_constant__ CUtensorMap mBh,
+                        const __grid_constant__ CUtensorMap mBl, float* __restrict__ C,
+                        int M, int N, int K, int ldc, int splits, int a_row0,
+                        int b_row0, int group_m, float* __restrict__ ws) {
+  gemm_body<BN, BMN>(mAh, mAl, OneB{&mBh, &mBl}, C, M, N, K, ldc, splits, a_row0, b_row0,
+                     group_m, ws);
+}
+
+// The multi-device fused path: this device's rows of A (raw + lo) times B
+// whose K slices live on the context's devices (PeerB).
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    sgemm_3xtf32_peer_kernel(const __grid_constant__ CUtensorMap mAh,
+                             const __grid_constant__ CUtensorMap mAl,
+                             const __grid_constant__ PeerB pb, float* __restrict__ C, int M,
+                             int N, int K, int ldc, int group_m) {
+  gemm_body<BN, true>(mAh, mAl, PeerBLoad{&pb}, C, M, N, K, ldc, 1, 0, 0, group_m, nullptr);
 }
 
 // ---- the 2-SM (CTA pair) GEMM kernel ------------------------------------------
@@ -1412,6 +1481,31 @@ int launch_pair(const CUtensorMap* m, float* C, int M, int N, int K, int ldc, vo
   return (int)cudaGetLastError();
 }
 
+int launch_peer(const CUtensorMap* mA, const PeerB& pb, float* C, int M, int N, int K, int ldc,
+                void* stream) {
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !(configured.load() >> dev & 1)) {
+    cudaFuncSetAttribute(sgemm_3xtf32_peer_kernel<256>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<256, true>::SMEM_BYTES);
+    configured.fetch_or(1ull << dev);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((M / BM) * (N / 256)));
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = Cfg<256, true>::SMEM_BYTES;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, sgemm_3xtf32_peer_kernel<256>, mA[0], mA[1], pb, C, M, N, K, ldc,
+                     GROUP_M);
+  return (int)cudaGetLastError();
+}
+
 // Which kernel, tile width and split-K factor a device-API GEMM takes (the
 // scratch size and the launch must agree): the CTA-pair kernel (256 x 256
 // pair tiles) where the 1-SM grid needs no split-K, else 1-SM tiles.
@@ -1540,6 +1634,49 @@ int sgemm_tc_make_pair_maps(const float* Ah, const float* Al, int a_rows, const 
     return e;
   maps->pair = true;
   return 0;
+}
+
+int sgemm_tc_lo(const float* X, int ld, int rows, int cols, float* out, int sm_count,
+                void* stream) {
+  if (rows <= 0 || cols <= 0)
+    return 0;
+  if (((uintptr_t)X & 15) || ((uintptr_t)out & 15) || ld % 4 || cols % 4 ||
+      (size_t)rows * cols / 4 >= (1ull << 32))
+    return (int)cudaErrorInvalidValue;
+  const int sms = sm_count > 0 ? sm_count : 148;
+  const size_t g4 = (size_t)rows * cols / 4;
+  const int grid = std::max(1, (int)std::min<size_t>((g4 + 1023) / 1024, (size_t)sms * 4));
+  // every block takes the first operand; the second is empty
+  split_lo_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(X, ld, rows, cols, out, nullptr, 0, 0,
+                                                          nullptr, grid);
+  return (int)cudaGetLastError();
+}
+
+bool sgemm_tc_peer_supported(int M, int N, int K, int nslices) {
+  return nslices >= 1 && nslices <= kMaxPeerSlices && M % BM == 0 && N % 256 == 0 &&
+         K % nslices == 0 && (K / nslices) % BK == 0 && get_encoder() != nullptr;
+}
+
+int sgemm_tc_peer_gemm(const float* A, int lda, const float* Alo, int M, int N, int K,
+                       const float* const* Bs, const float* const* Blos, int nslices, float* C,
+                       int ldc, void* stream) {
+  if (!sgemm_tc_peer_supported(M, N, K, nslices) || lda % 4 || ldc % 4 ||
+      ((uintptr_t)A & 15) || ((uintptr_t)C & 15))
+    return (int)cudaErrorInvalidValue;
+  if (M == 0)
+    return 0;
+  const int kslice = K / nslices;
+  CUtensorMap mA[2];
+  PeerB pb{};
+  pb.kslice = kslice;
+  pb.n = nslices;
+  if (!make_map_kmajor(&mA[0], A, M, K, lda, BM) || !make_map_kmajor(&mA[1], Alo, M, K, K, BM))
+    return (int)cudaErrorInvalidValue;
+  for (int i = 0; i < nslices; ++i)
+    if (!make_map_mnmajor(&pb.h[i], Bs[i], kslice, N, N, 256) ||
+        !make_map_mnmajor(&pb.l[i], Blos[i], kslice, N, N, 256))
+      return (int)cudaErrorInvalidValue;
+  return launch_peer(mA, pb, C, M, N, K, ldc, stream);
 }
 
 int sgemm_tc_gemm(const float* Ah, const float* Al, const float* Bh, const float* Bl, float* C,

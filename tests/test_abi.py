@@ -44,7 +44,7 @@ def test_status_codes_are_errc_values():
     # cafx::errc (error.hpp:11-29): unknown_type=2, out_of_range=4,
     # type_mismatch=5, interface_mismatch=6, config_error=8, spawn_error=9,
     # request_timeout=13, request_down=14
-    assert b.lib().cafxg_abi_version() == 2
+    assert b.lib().cafxg_abi_version() == 3
     for code, name in [(0, "none"), (2, "unknown_type"), (4, "out_of_range"),
                        (5, "type_mismatch"), (6, "interface_mismatch"), (8, "config_error"),
                        (9, "spawn_error"), (13, "request_timeout"), (14, "request_down")]:
@@ -65,7 +65,7 @@ def test_struct_layouts_match_header():
     import paper_1505_07368_b200.cafxg as b
     assert ctypes.sizeof(b.MandelDesc) == 4 * 8 + 10 * 4 + 8
     assert ctypes.sizeof(b.SgemmDesc) == 32
-    assert ctypes.sizeof(b.Stats) == 9 * 8
+    assert ctypes.sizeof(b.Stats) == 10 * 8
 
 
 def test_header_is_plain_c_and_links(tmp_path):

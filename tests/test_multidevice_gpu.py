@@ -70,15 +70,21 @@ def test_run_mandelbrot_chain(vctx, golden, size, it):
     assert h == want
 
 
-@pytest.mark.parametrize("M,N,K", [(768, 512, 384),      # one launch per device
-                                   (3072, 1024, 768),    # per-device H2D/GEMM/D2H pipeline
-                                   (3 * 128, 256, 3)])    # smallest split
-def test_sgemm_row_blocks(vctx, M, N, K):
+@pytest.mark.parametrize("M,N,K,peer", [(768, 512, 384, True),    # B slices read in place
+                                        (3072, 1024, 768, True),
+                                        (3 * 128, 256, 3, False),  # K / V < 16: replicated B
+                                        (384, 384, 768, False)])   # N % 256: replicated B
+def test_sgemm_row_blocks(vctx, M, N, K, peer):
+    """Row blocks of A per device. Where the shapes allow, the fused path:
+    each device uploads 1/V of B's rows and every device's GEMM reads the K
+    slices where they lie (peer_gemms); else B is replicated by peer copies
+    (the NCCL all-gather on real GPUs)."""
     A = oracle.fill_uniform(M * K, 31).reshape(M, K)
     B = oracle.fill_uniform(K * N, 32).reshape(K, N)
     before = vctx.stats()
     C = vctx.sgemm(A, B)
     after = vctx.stats()
+    assert after.peer_gemms - before.peer_gemms == (1 if peer else 0)
     # B crossed PCIe once in total (1/V per device), A once
     assert after.h2d_bytes - before.h2d_bytes == (M * K + K * N) * 4
     rows = np.unique(np.concatenate([np.arange(0, M, 61), [M // V - 1, M // V, M - 1]]))
@@ -210,10 +216,34 @@ def test_two_gpu_context_nccl_and_bands():
         before = c.stats()
         C = c.sgemm(A, B)
         after = c.stats()
-        assert after.nccl_collectives - before.nccl_collectives == 2
+        # with peer access between the GPUs, each GEMM reads B's other slice
+        # over NVLink in place; without it, the NCCL all-gather replicates B
+        assert (after.peer_gemms - before.peer_gemms == 1 or
+                after.nccl_collectives - before.nccl_collectives == 2)
         rows = np.arange(0, M, 127, dtype=np.uint32)
         R = oracle.sgemm_ref_rows(A, B, rows, N, K)
         assert oracle.sgemm_rel_err(C, R, rows, N) <= 1e-5
+        # the same product through the NCCL all-gather path
+        code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+M = N = K = 4096
+A = oracle.fill_uniform(M * K, 61).reshape(M, K)
+B = oracle.fill_uniform(K * N, 62).reshape(K, N)
+with pkg.Context(device_mask=0b11) as c:
+    C = c.sgemm(A, B)
+    assert c.stats().peer_gemms == 0
+rows = np.arange(0, M, 127, dtype=np.uint32)
+assert oracle.sgemm_rel_err(C, oracle.sgemm_ref_rows(A, B, rows, N, K), rows, N) <= 1e-5
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        import subprocess
+        import sys
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                           timeout=600, env=dict(os.environ, CAFXG_SGEMM_P2P="0"))
+        assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
         d = pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, 2048, 2048, 1000)
         out = c.mandelbrot(d).reshape(2048, 2048)
         ref = oracle.tile(-0.75, -0.73, 0.10, 0.12, 2048, 2048, 1000, fp64=False, centre=True)
