@@ -15,7 +15,8 @@ from concurrent.futures import Future
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# CAFXG_LIB: another build of the library (A/B experiments only)
+# CAFXG_LIB: another build of the library (A/B experiments, and the checked
+# build with device-side bounds checks, tests/test_checked_build_gpu.py)
 LIB_PATH = os.environ.get("CAFXG_LIB") or os.path.join(HERE, "libcafxg.so")
 
 OK = 0

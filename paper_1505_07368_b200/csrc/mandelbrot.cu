@@ -612,6 +612,8 @@ __device__ __forceinline__ void direct_finish(const MLaunch& L) {
     fins &= fins - 1;
     const MTile& T = L.inl[t];
     const uint32_t nv = T.nrows * T.ncols / 4;
+    CAFXG_DCHECK(t < L.n && (uint64_t)T.out_off + 4ull * nv <= L.out_limit &&
+                 ((uintptr_t)T.reply & 15) == 0);
     const uint4* from = reinterpret_cast<const uint4*>(L.out + T.out_off);
     uint4* to = reinterpret_cast<uint4*>(T.reply);
     for (uint32_t i0 = 0; i0 < nv; i0 += 32 * 8) {
@@ -696,6 +698,7 @@ __global__ void __launch_bounds__(kMandelThreads, kMode == 2 ? 2 : 4)
       for (int s = 0; s < NS; ++s) {
         if (done >> s & 1u) {
           uint32_t c = (int32_t)n[s] < 0 ? (n[s] & 0x7fffffffu) + 1u : n[s];
+          CAFXG_DCHECK((o[s] & omask) < L.out_limit);
           L.out[o[s] & omask] = min(c, maxit);
         }
       }
@@ -799,6 +802,7 @@ __device__ __forceinline__ void replay(const MLaunch& L, ReplayQueue<Slots>& q,
   for (int s = 0; s < NS; ++s) {
     if (ro[s] != 0xffffffffu) {
       uint32_t c = (int32_t)rn[s] < 0 ? (rn[s] & 0x7fffffffu) + 1u : rn[s];
+      CAFXG_DCHECK((ro[s] & omask) < L.out_limit);
       L.out[ro[s] & omask] = min(c, maxit);
     }
   }
@@ -882,8 +886,10 @@ __global__ void __launch_bounds__(kMandelThreads, 2)
     if (hitm) {
 #pragma unroll
       for (int s = 0; s < NS; ++s)
-        if (hitm >> s & 1u)
+        if (hitm >> s & 1u) {
+          CAFXG_DCHECK((o[s] & omask) < L.out_limit);
           out[o[s] & omask] = maxit;
+        }
     }
     done |= hitm;
     if (__any_sync(kFull, esc != 0)) {

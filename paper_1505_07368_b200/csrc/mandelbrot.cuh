@@ -3,6 +3,8 @@
 #pragma once
 #include <cstdint>
 
+#include "dcheck.cuh"
+
 namespace cafxg {
 
 // One tile of a batch, as the kernel sees it. Built on the host from
@@ -58,6 +60,7 @@ struct MLaunch {
   // finished pixels (zero at launch, reset by the warp that copies the tile).
   uint32_t direct;
   uint32_t* tile_done;
+  uint64_t out_limit;   // elements of `out` the launch may write (checked build)
 };
 static_assert(sizeof(MLaunch) <= 4096, "MLaunch is passed by value");
 constexpr int kDirectShift = 26;

@@ -310,6 +310,15 @@ int launch_mandel_group(cafxg_ctx* ctx, Device* d, uint32_t* out_base,
   L.total_chunks = chunks;
   L.max_iter = tiles[0].max_iter;
   L.out = out_base;
+  for (auto& t : tiles)  // (the checked build traps on stores past it)
+    L.out_limit = std::max<uint64_t>(L.out_limit, (uint64_t)t.out_off + (uint64_t)t.nrows * t.ncols);
+#ifdef CAFXG_DEVICE_CHECKS
+  // CAFXG_DCHECK_SELFTEST=1: a limit the launch must overrun, so a test can
+  // see the checks fire
+  static const bool dcheck_selftest = getenv("CAFXG_DCHECK_SELFTEST") != nullptr;
+  if (dcheck_selftest)
+    L.out_limit = 1;
+#endif
   L.zero = 0.0f;
   L.inline_coords = tiles[0].cx == nullptr;
   if (direct_counters) {

@@ -41,6 +41,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "dcheck.cuh"
 #include "sgemm.cuh"
 
 namespace cafxg {
@@ -341,6 +342,7 @@ struct PeerBLoad {
                                        int ncol) const {
     static_assert(BMN, "peer slices are raw MN-major B");
     const int src = kx / p->kslice, k = kx - src * p->kslice;
+    CAFXG_DCHECK(src < p->n && k + BK <= p->kslice);
     tma_load_3d(dh, &p->h[src], bar, 0, k, ncol / 32);
     tma_load_3d(dl, &p->l[src], bar, 0, k, ncol / 32);
   }
@@ -386,6 +388,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& mAh, const CUtensor
   const int ksplit = K / splits;
   const int k_base = kz * ksplit;
   const int nk = ksplit / BK;
+  CAFXG_DCHECK(bid < tiles_m * tiles_n && m0 + BM <= M && n0 + BN <= N && nk > 0 &&
+               ksplit % BK == 0);
 
   if (warp == 0 && lane == 0) {
     for (const CUtensorMap* m : {&mAh, &mAl})
@@ -763,6 +767,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int ksplit = K / splits;
   const int k_base = kz * ksplit;
   const int nk = ksplit / BK;
+  CAFXG_DCHECK(bid < tiles_m * tiles_n && m0 + BM <= M && n0 + BNP <= N && nk > 0 &&
+               ksplit % BK == 0);
 
   if (warp == 0 && lane == 0) {
     for (const CUtensorMap* m : {&mAh, &mAl, &mBh, &mBl})
