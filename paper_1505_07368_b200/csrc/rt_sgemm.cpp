@@ -294,7 +294,16 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     return e ? (uint32_t)atoi(e) : 256u;
   }();
   R = std::max<uint32_t>(R, rmin);
-  float *Bh = nullptr, *Bl = nullptr, *Ah = nullptr, *Al = nullptr;
+  // Raw operands (the device-API size rule): A blocks and B are read as they
+  // lie and only their lo halves are made (no transpose of B, half the
+  // writes); split-K reduces through an L2 workspace (one more piece).
+  // 1024^3 end to end: the four block GEMMs were the critical path (~40 us
+  // each through the split + transpose pass and the DSMEM reduction).
+  const bool raw = sgemm_tc_raw_wanted((int)rows, (int)N);
+  const int bn = sgemm_tc_pick_bn((int)R, (int)N, d->sms);
+  const int splits_max = g.splits ? (int)g.splits : sgemm_tc_splits((int)R, (int)N, (int)K, d->sms, bn);
+  const size_t ws_bytes = raw ? sgemm_tc_ws_bytes((int)R, (int)N, splits_max, bn) : 0;
+  float *Bh = nullptr, *Bl = nullptr, *Ah = nullptr, *Al = nullptr, *wsk = nullptr;
   float* dA[2] = {nullptr, nullptr};
   float* dC[2] = {nullptr, nullptr};
   cudaStream_t cs = d->compute;
@@ -302,8 +311,8 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
   // allocation and free per buffer and request cost more host time than the
   // GEMMs of a 1024^3 request); 256-byte aligned pieces
   {
-    const size_t pieces[8] = {N * K, N * K, (size_t)R * K, (size_t)R * K, (size_t)R * K,
-                              (size_t)R * K, (size_t)R * N, (size_t)R * N};
+    const size_t pieces[9] = {N * K, N * K, (size_t)R * K, (size_t)R * K, (size_t)R * K,
+                              (size_t)R * K, (size_t)R * N, (size_t)R * N, ws_bytes / 4};
     size_t need = 0;
     for (size_t p : pieces)
       need += (p * 4 + 255) / 256 * 256;
@@ -319,9 +328,9 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
       CAFXG_CUDA_TRY(cudaMalloc((void**)&d->sgemm_ws, need));
       d->sgemm_ws_bytes = need;
     }
-    float** dst[8] = {&Bh, &Bl, &Ah, &Al, &dA[0], &dA[1], &dC[0], &dC[1]};
+    float** dst[9] = {&Bh, &Bl, &Ah, &Al, &dA[0], &dA[1], &dC[0], &dC[1], &wsk};
     uint8_t* base = reinterpret_cast<uint8_t*>(d->sgemm_ws);
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 9; ++i) {
       *dst[i] = reinterpret_cast<float*>(base);
       base += (pieces[i] * 4 + 255) / 256 * 256;
     }
@@ -349,16 +358,24 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     tmark("B up", d->h2d);
     CAFXG_TRY(stream_after_pooled(d, cs, d->h2d));
   }
-  int e = sgemm_tc_split_b(dB, (int)N, (int)K, (int)N, Bh, Bl, cs);
-  if (e != 0)
-    return cuda_status((cudaError_t)e, "sgemm: B split");
-  ctx->st_launches++;
   // tensor maps encoded once per request: every block reuses Ah/Al (R rows)
-  // and Bh/Bl
-  SgemmTcMaps maps;
-  const int bn = sgemm_tc_pick_bn((int)R, (int)N, d->sms);
-  if (int me = sgemm_tc_make_maps(Ah, Al, (int)R, Bh, Bl, (int)N, (int)K, bn, &maps))
-    return cuda_status((cudaError_t)me, "sgemm: tensor maps");
+  // and Bh/Bl; raw: one set per A slot (the maps read the slot itself), Bl
+  // holds lo(B) in B's layout, Al lo of the current block
+  SgemmTcMaps maps, rmaps[2];
+  int e = 0;
+  if (raw) {
+    e = sgemm_tc_lo(dB, (int)N, (int)K, (int)N, Bl, d->sms, cs);
+    for (int sl = 0; sl < 2 && !e; ++sl)
+      e = sgemm_tc_make_maps_raw(dA[sl], (int)K, Al, (int)R, dB, (int)N, Bl, (int)N, (int)K, bn,
+                                 &rmaps[sl]);
+  } else {
+    e = sgemm_tc_split_b(dB, (int)N, (int)K, (int)N, Bh, Bl, cs);
+    if (!e)
+      e = sgemm_tc_make_maps(Ah, Al, (int)R, Bh, Bl, (int)N, (int)K, bn, &maps);
+  }
+  if (e != 0)
+    return cuda_status((cudaError_t)e, "sgemm: B split / tensor maps");
+  ctx->st_launches++;
   std::vector<cudaEvent_t> ev_split, ev_gemm, ev_down;
   auto mk = [d](std::vector<cudaEvent_t>& v) {
     cudaEvent_t ev = pooled_event(d);
@@ -370,9 +387,10 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
   for (uint32_t b0 = 0; b0 < rows && status == CAFXG_OK; b0 += R, ++i) {
     const uint32_t m = std::min(R, rows - b0);
     const int slot = i & 1;
-    // upload A block (slot free once block i-2's split consumed it)
+    // upload A block (slot free once block i-2's split -- raw: its GEMM --
+    // consumed it)
     if (i >= 2)
-      cudaStreamWaitEvent(d->h2d, ev_split[i - 2], 0);
+      cudaStreamWaitEvent(d->h2d, raw ? ev_gemm[i - 2] : ev_split[i - 2], 0);
     const float* src = A + (size_t)(r0 + b0) * g.lda;
     if (g.lda == K)
       status = cuda_status(cudaMemcpyAsync(dA[slot], src, (size_t)m * K * 4,
@@ -386,12 +404,16 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     CAFXG_TRY(stream_after_pooled(d, cs, d->h2d));
     if (i >= 2)
       cudaStreamWaitEvent(cs, ev_down[i - 2], 0);  // C slot drained
-    e = sgemm_tc_split_a(dA[slot], (int)K, (int)m, (int)K, Ah, Al, cs);
+    e = raw ? sgemm_tc_lo(dA[slot], (int)K, (int)m, (int)K, Al, d->sms, cs)
+            : sgemm_tc_split_a(dA[slot], (int)K, (int)m, (int)K, Ah, Al, cs);
     cudaEventRecord(mk(ev_split), cs);
-    if (e == 0)
-      e = sgemm_tc_gemm_maps(&maps, dC[slot], (int)m, (int)N, (int)K, (int)N, cs,
-                             g.splits ? (int)g.splits
-                                      : sgemm_tc_splits((int)m, (int)N, (int)K, d->sms, bn));
+    if (e == 0) {
+      int sp = g.splits ? (int)g.splits : sgemm_tc_splits((int)m, (int)N, (int)K, d->sms, bn);
+      if (raw && sp > splits_max)
+        sp = splits_max;  // (the workspace is sized for R-row blocks)
+      e = sgemm_tc_gemm_maps(raw ? &rmaps[slot] : &maps, dC[slot], (int)m, (int)N, (int)K,
+                             (int)N, cs, sp, 0, 0, raw ? wsk : nullptr);
+    }
     if (e != 0)
       status = cuda_status((cudaError_t)e, "sgemm: 3xtf32 launch");
     ctx->st_launches += 2;
@@ -400,10 +422,13 @@ int sgemm_pipeline_device(cafxg_ctx* ctx, Device* d, const cafxg_sgemm_desc& g,
     cudaEventRecord(mk(ev_gemm), cs);
     cudaStreamWaitEvent(d->d2h, ev_gemm.back(), 0);
     if (status == CAFXG_OK)
-      status = cuda_status(cudaMemcpy2DAsync(C + (size_t)(r0 + b0) * g.ldc, (size_t)g.ldc * 4,
-                                             dC[slot], N * 4, N * 4, m,
-                                             cudaMemcpyDeviceToHost, d->d2h),
-                           "sgemm: C download");
+      status = cuda_status(
+          g.ldc == N ? cudaMemcpyAsync(C + (size_t)(r0 + b0) * g.ldc, dC[slot], (size_t)m * N * 4,
+                                       cudaMemcpyDeviceToHost, d->d2h)
+                     : cudaMemcpy2DAsync(C + (size_t)(r0 + b0) * g.ldc, (size_t)g.ldc * 4,
+                                         dC[slot], N * 4, N * 4, m, cudaMemcpyDeviceToHost,
+                                         d->d2h),
+          "sgemm: C download");
     ctx->st_d2h += (size_t)m * N * 4;
     tmark("C down", d->d2h);
     cudaEventRecord(mk(ev_down), d->d2h);

@@ -72,6 +72,9 @@ int sgemm_tc_peer_gemm(const float* A, int lda, const float* Alo, int M, int N, 
 // split-K), and its maps (launched by sgemm_tc_gemm_maps with splits 1; blocks
 // of it need M % 256 == N % 256 == 0)
 bool sgemm_tc_pair_wanted(int M, int N, int K, int sms);
+// whether an M x N product should take the raw-operand form (lo-only pass,
+// MN-major B): the device-API size rule, for the runtime's own buffers
+bool sgemm_tc_raw_wanted(int M, int N);
 int sgemm_tc_make_pair_maps(const float* Ah, const float* Al, int a_rows, const float* Bh,
                             const float* Bl, int N, int K, SgemmTcMaps* maps);
 // tile width (256 or 128 columns) and split-K factor (thread-block cluster

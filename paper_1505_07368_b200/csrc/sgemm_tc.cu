@@ -1628,6 +1628,18 @@ int sgemm_tc_gemm_maps(const SgemmTcMaps* maps, float* C, int M, int N, int K, i
              : launch<128, false>(m, C, M, N, K, ldc, stream, splits, a_row0, b_row0, ws);
 }
 
+bool sgemm_tc_raw_wanted(int M, int N) {
+  // the size rule of use_raw_operands for buffers the runtime allocates
+  // (16-byte aligned, packed)
+  static const int env = [] {
+    const char* e = getenv("CAFXG_SGEMM_RAW");
+    return e ? atoi(e) : -1;
+  }();
+  if (env == 0)
+    return false;
+  return env == 1 || (double)M * N / ((double)M + N) < 3200.0;
+}
+
 bool sgemm_tc_pair_wanted(int M, int N, int K, int sms) {
   const TcPlan p = tc_plan(M, N, K, sms > 0 ? sms : 148, 0);
   return p.pair && p.splits == 1 && p.bn == 256;
