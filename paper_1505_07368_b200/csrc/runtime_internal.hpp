@@ -58,44 +58,41 @@ class PinnedPool {
   }
 
   void* alloc(size_t bytes) {
-    size_t cls = size_class(bytes);
-    std::lock_guard<std::mutex> g(mu_);
-    auto it = free_.find(cls);
-    if (it != free_.end() && !it->second.empty()) {
-      void* p = it->second.back();
-      it->second.pop_back();
-      live_[p] = cls;
-      return p;
+    const size_t cls = size_class(bytes);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      if (void* p = take_locked(cls))
+        return p;
     }
-    void* p = nullptr;
-    if (cls <= kSlabClassMax) {
-      if (!slab_ || slab_used_ + cls > kSlabBytes) {
-        void* s = nullptr;
-        new_allocs_.fetch_add(1, std::memory_order_relaxed);
-        if (cudaHostAlloc(&s, kSlabBytes, cudaHostAllocPortable | cudaHostAllocMapped) !=
-            cudaSuccess) {
-          cudaGetLastError();
-          return nullptr;
-        }
-        slabs_.push_back(s);
-        slab_ = (uint8_t*)s;
-        slab_used_ = 0;
-        add_range(s, kSlabBytes);
-      }
-      p = slab_ + slab_used_;  // classes are multiples of 4 KB: page-aligned
-      slab_used_ += cls;
-    } else {
+    // driver calls outside the lock: a pinned allocation takes milliseconds
+    // (a 1 GiB image ~0.1 s) and completion threads free buffers meanwhile
+    if (cls > kSlabClassMax) {
+      void* p = nullptr;
       new_allocs_.fetch_add(1, std::memory_order_relaxed);
-      if (cudaHostAlloc(&p, cls, cudaHostAllocPortable | cudaHostAllocMapped) !=
-          cudaSuccess) {
+      if (cudaHostAlloc(&p, cls, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
       }
+      std::lock_guard<std::mutex> g(mu_);
       large_.push_back(p);
       add_range(p, cls);
+      live_[p] = cls;
+      return p;
     }
-    live_[p] = cls;
-    return p;
+    void* s = nullptr;
+    new_allocs_.fetch_add(1, std::memory_order_relaxed);
+    if (cudaHostAlloc(&s, kSlabBytes, cudaHostAllocPortable | cudaHostAllocMapped) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    std::lock_guard<std::mutex> g(mu_);
+    slabs_.push_back(s);
+    add_range(s, kSlabBytes);
+    // (a slab another thread installed meanwhile keeps its tail unused)
+    slab_ = (uint8_t*)s;
+    slab_used_ = 0;
+    return take_locked(cls);
   }
 
   // driver allocations so far (CAFXG_STATS=1 prints them at close)
@@ -144,6 +141,23 @@ class PinnedPool {
     while (c < bytes)
       c <<= 1;
     return c;
+  }
+  // a cached buffer of class cls, or one carved from the current slab
+  void* take_locked(size_t cls) {
+    auto it = free_.find(cls);
+    if (it != free_.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      live_[p] = cls;
+      return p;
+    }
+    if (cls <= kSlabClassMax && slab_ && slab_used_ + cls <= kSlabBytes) {
+      void* p = slab_ + slab_used_;  // classes are multiples of 4 KB: page-aligned
+      slab_used_ += cls;
+      live_[p] = cls;
+      return p;
+    }
+    return nullptr;
   }
   void add_range(void* p, size_t bytes) {
     std::unique_lock<std::shared_mutex> w(ranges_mu_);
