@@ -39,6 +39,9 @@ WORK = {
     "cfg1_wave0_rows0_273": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100, nrows=273)],
     "cfg1_wave1_rows273_1080": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100,
                                                 row0=273)],
+    # every pixel inside the main cardioid: no escapes, no replays (the main
+    # loop alone)
+    "inset_fp32_4096_it1000": [pkg.mandel_desc(-0.3, -0.1, -0.1, 0.1, 4096, 4096, 1000)],
     "tiny_fp32_64x64_it100": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 64, 64, 100)],
     "cfg1_middle_rows405_675": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100,
                                                 row0=405, nrows=270)],
