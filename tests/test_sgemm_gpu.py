@@ -283,6 +283,59 @@ def test_sgemm_device_misaligned_pointers(ctx):
     assert ctx.status() == 0
 
 
+@pytest.mark.parametrize("env", [{}, {"CAFXG_SGEMM_PAIR": "1"}, {"CAFXG_SGEMM_RAW": "0"},
+                                 {"CAFXG_SGEMM_RAW": "1", "CAFXG_SGEMM_WS": "0"}])
+def test_sgemm_device_randomised_kernel_paths(env):
+    """Seeded random tensor-core shapes through the device API under each
+    kernel / operand / reduction choice (forced by environment, one process
+    each): M, N multiples of 128, K a multiple of 32, padded row pitches,
+    random split-K requests; every result within the tolerance and padding
+    never written."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+rng = np.random.default_rng(2024)
+with pkg.Context(1) as c:
+    for case in range(24):
+        M = int(rng.integers(1, 9)) * 128
+        N = int(rng.integers(1, 9)) * 128
+        K = int(rng.integers(1, 33)) * 32
+        pa, pb, pc = (int(rng.integers(0, 3)) * 4 for _ in range(3))
+        splits = int(rng.choice([0, 0, 1, 2, 4, 8]))
+        if splits and (K %% (16 * splits) or K // splits < 16):
+            splits = 0
+        A_h = oracle.fill_uniform(M * (K + pa), 300 + case).reshape(M, K + pa)
+        B_h = oracle.fill_uniform(K * (N + pb), 400 + case).reshape(K, N + pb)
+        A, B = torch.from_numpy(A_h).cuda(), torch.from_numpy(B_h).cuda()
+        C = torch.full((M, N + pc), float("nan"), device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        c.sgemm_device(M, N, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream,
+                       mode=pkg.SGEMM_3XTF32, lda=K + pa, ldb=N + pb, ldc=N + pc,
+                       splits=splits)
+        torch.cuda.synchronize()
+        Ch = C.cpu().numpy()
+        assert not np.isnan(Ch[:, :N]).any(), (case, M, N, K, splits)
+        if pc:
+            assert np.isnan(Ch[:, N:]).all(), (case, M, N, K)
+        rows = np.unique(np.linspace(0, M - 1, 12).astype(np.uint32))
+        R = oracle.sgemm_ref_rows(np.ascontiguousarray(A_h[:, :K]),
+                                  np.ascontiguousarray(B_h[:, :N]), rows, N, K)
+        err = oracle.sgemm_rel_err(np.ascontiguousarray(Ch[:, :N]), R, rows, N)
+        assert err <= 1e-5, (case, M, N, K, splits, err)
+    assert c.status() == 0
+print("ok")
+""" % root
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
+
+
 def test_cfg5_full_size_row_sum_property(ctx):
     """Full-size property for cfg5 (16384^3, the sampled-row check covers a
     few rows): C.1 = A.(B.1) for every row. B.1 and A.(B.1) are computed in
