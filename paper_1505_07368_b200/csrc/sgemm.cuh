@@ -10,11 +10,14 @@ int sgemm_simt_launch(const float* A, const float* B, float* C, int M, int N,
                       int K, int lda, int ldb, int ldc, void* stream);
 
 // 3xTF32 tcgen05 path (sgemm_tc.cu). Shape constraints are checked by
-// sgemm_tc_supported; scratch holds the tf32 hi/lo splits of A and B^T
-// (sgemm_tc_scratch_bytes).
+// sgemm_tc_supported (the caller also checks 16-byte alignment of A and C);
+// scratch holds the tf32 hi/lo splits of A and B^T, or the lo halves of A and
+// B for raw operands, and the split-K workspace (sgemm_tc_scratch_bytes).
+// sgemm_tc_launch picks the kernel (1-SM tiles or CTA pairs), the operand form
+// and the split-K factor per shape (tc_plan).
 bool sgemm_tc_supported(int M, int N, int K, int lda, int ldb, int ldc);
 size_t sgemm_tc_scratch_bytes(int M, int N, int K, int sm_count, int splits_req = 0);
-// splits: split-K cluster size (1/2/4/8), 0 = sgemm_tc_splits' choice
+// splits: split-K cluster size (1/2/4/8), 0 = the plan's choice
 int sgemm_tc_launch(const float* A, const float* B, float* C, int M, int N,
                     int K, int lda, int ldb, int ldc, void* scratch,
                     int sm_count, void* stream, int* launches, int splits = 0);
