@@ -470,13 +470,13 @@ def run_ours(args):
         D.barrier()
         D.close()
         return
-    line = measure(args, N)
+    line = measure(args, N, D)
     print(json.dumps(line), flush=True)
     D.barrier()
     D.close()
 
 
-def measure(args, N):
+def measure(args, N, dist=None):
     import numpy as np
     import torch
 
@@ -579,11 +579,6 @@ def measure(args, N):
             same["ratio_vs_cpu_reference"] = round(v64 / v, 1)
             same["e2e_ratio_vs_cpu_reference"] = round(same["e2e"]["value"] / v, 1)
 
-    secondary = {}
-    if not args.no_secondary:
-        secondary = run_secondary(ctx, args, N)
-        secondary["actor_requests_cafx"] = sec_actor_cafx(N, img_fnv, e2e["ms"])
-
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Giter/s", "n_gpus": N,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
@@ -613,7 +608,16 @@ def measure(args, N):
     }
     if cpu:
         line["cpu_baseline"] = cpu
-    if secondary:
+    if not args.no_secondary:
+        # the headline is complete here: a secondary that fails records its
+        # error, and one that hangs (first N>1 run on real NVLink peers) cannot
+        # take the headline with it -- the watchdog prints the line without the
+        # unfinished secondaries, joins the ranks' barrier and exits
+        dog = Watchdog(line, SECONDARY_BUDGET_S, dist)
+        secondary = run_secondary(ctx, args, N, dog.out)
+        guarded(secondary, "actor_requests_cafx",
+                lambda: sec_actor_cafx(N, img_fnv, e2e["ms"]))
+        dog.cancel()
         line["secondary"] = secondary
     ctx.close()
     return line
@@ -645,18 +649,62 @@ def median_wall(fn, n):
     return statistics.median(walls) * 1e3
 
 
-def run_secondary(ctx, args, N):
+# seconds the secondaries may take after the headline is measured (a 1-GPU
+# run needs ~60 s of them)
+SECONDARY_BUDGET_S = float(os.environ.get("CAFXG_BENCH_SECONDARY_S", "900"))
+
+
+class Watchdog:
+    """Prints the headline line with the secondaries finished so far if they
+    overrun their budget, then releases the other ranks and exits 0."""
+
+    def __init__(self, line, budget_s, dist):
+        import threading
+        self.line, self.dist, self.out = line, dist, {}
+        self.timer = threading.Timer(budget_s, self._fire)
+        self.timer.daemon = True
+        self.timer.start()
+
+    def _fire(self):
+        sec = dict(self.out)
+        sec["watchdog"] = (f"secondaries stopped after {SECONDARY_BUDGET_S:.0f} s; "
+                           "the entries present finished")
+        self.line["secondary"] = sec
+        print(json.dumps(self.line), flush=True)
+        try:
+            if self.dist is not None:
+                self.dist.barrier()
+        finally:
+            os._exit(0)
+
+    def cancel(self):
+        self.timer.cancel()
+
+
+def guarded(out, name, fn):
+    """out[name] = fn(), or the error it raised: one failing secondary must not
+    cost the others or the headline."""
+    try:
+        out[name] = fn()
+    except Exception as e:  # noqa: BLE001 -- recorded in the line
+        out[name] = {"error": f"{type(e).__name__}: {e}"[:500]}
+
+
+def run_secondary(ctx, args, N, out=None):
     """cfg1/cfg2/paper scale (one-GPU configs) at N=1; cfg5 and cfg4 (the
     1/2/4/8-GPU configs) at every N on the N-device context; cfg3 through a
     compute actor."""
-    out = {}
+    out = {} if out is None else out
     if N == 1:
-        out["cfg1_mandelbrot_1920x1080_fp32"] = sec_cfg1(ctx, args)
-        out["cfg2_sgemm_1024"] = sec_sgemm(ctx, args, 1024, N)
-        out["paper_scale_run_mandelbrot_16000_500"] = sec_paper_scale(ctx)
-    out["cfg5_sgemm_16384"] = sec_sgemm(ctx, args, 16384, N)
-    out["cfg3_through_compute_actor"] = sec_cfg3_actor(ctx)
-    out.update(sec_cfg4(ctx, args, N))
+        guarded(out, "cfg1_mandelbrot_1920x1080_fp32", lambda: sec_cfg1(ctx, args))
+        guarded(out, "cfg2_sgemm_1024", lambda: sec_sgemm(ctx, args, 1024, N))
+        guarded(out, "paper_scale_run_mandelbrot_16000_500", lambda: sec_paper_scale(ctx))
+    guarded(out, "cfg5_sgemm_16384", lambda: sec_sgemm(ctx, args, 16384, N))
+    guarded(out, "cfg3_through_compute_actor", lambda: sec_cfg3_actor(ctx))
+    try:
+        out.update(sec_cfg4(ctx, args, N))
+    except Exception as e:  # noqa: BLE001
+        out["cfg4_request_storm"] = {"error": f"{type(e).__name__}: {e}"[:500]}
     return out
 
 
