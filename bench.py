@@ -619,7 +619,10 @@ def measure(args, N, dist=None):
                 lambda: sec_actor_cafx(N, img_fnv, e2e["ms"]))
         dog.cancel()
         line["secondary"] = secondary
-    ctx.close()
+    try:
+        ctx.close()
+    except Exception as e:  # noqa: BLE001 -- e.g. a secondary left a sticky fault
+        line.setdefault("secondary", {})["close_error"] = f"{type(e).__name__}: {e}"[:300]
     return line
 
 
