@@ -195,7 +195,11 @@ MandelLaunchCfg mandel_cfg(Device* d, int precision, uint32_t max_iter,
   if (ks_env == 4 || ks_env == 16 || ks_env == 32)
     c.ksteps = ks_env;
   c.exact = exact;
-  c.deferred = safe && max_iter >= 256 && deferred_enabled();
+  static const uint32_t def_min = [] {  // CAFXG_DEFERRED_MIN=<max_iter>: experiments only
+    const char* e = getenv("CAFXG_DEFERRED_MIN");
+    return e ? (uint32_t)atoi(e) : 256u;
+  }();
+  c.deferred = safe && max_iter >= def_min && deferred_enabled();
   if (c.deferred) {
     pick_block(max_iter, precision, c);
     if (tune && tune->block_steps) {  // spawn_cl tuning (validated at spawn)

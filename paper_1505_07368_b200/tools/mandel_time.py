@@ -42,6 +42,9 @@ WORK = {
     # every pixel inside the main cardioid: no escapes, no replays (the main
     # loop alone)
     "inset_fp32_4096_it1000": [pkg.mandel_desc(-0.3, -0.1, -0.1, 0.1, 4096, 4096, 1000)],
+    # cfg1's pitch without the columns near |c| = 2 (x >= -1.7: the deferred
+    # escape test's safe box)
+    "cfg1safe_fp32_1728x1080_it100": [pkg.mandel_desc(-1.7, 1.0, -1.0, 1.0, 1728, 1080, 100)],
     "tiny_fp32_64x64_it100": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 64, 64, 100)],
     "cfg1_middle_rows405_675": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100,
                                                 row0=405, nrows=270)],
