@@ -52,19 +52,22 @@ def test_cfg1_fp32_full_image(ctx):
     assert 6.0e7 < int(out.sum(dtype=np.uint64)) < 6.6e7   # 6.29e7
 
 
-def test_cfg3_sampled_rows(ctx):
-    """BASELINE config 3 (16384^2, fp32, it=1000, boundary zoom): full image on
-    the GPU, every 256th row checked bit-exactly against the oracle."""
+def test_cfg3_full_image_vs_oracle(ctx):
+    """BASELINE config 3 (16384^2, fp32, it=1000, boundary zoom) at full size:
+    the image through the C ABI against the oracle restatement, every one of
+    the 268,435,456 pixels bit-exactly (the oracle runs on every host thread,
+    ~1-2 min on the GPU box's 16 cores)."""
     W = H = 16384
     d = pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, W, H, 1000)
     out = ctx.pinned_empty((H, W), np.uint32)
     try:
         ctx.mandelbrot(d, out)
-        ref = oracle.tile(-0.75, -0.73, 0.10, 0.12, W, H, 1000, fp64=False, centre=True,
-                          sample_stride=256)
-        for r in range(0, H, 256):
-            assert np.array_equal(out[r], ref[r]), r
-        mean = float(out[::64].mean())
+        ref = oracle.tile(-0.75, -0.73, 0.10, 0.12, W, H, 1000, fp64=False, centre=True)
+        bad = np.count_nonzero(out != ref)
+        if bad:
+            r = int(np.argwhere(out != ref)[0][0])
+            pytest.fail(f"{bad} of {W * H} pixels differ; first in row {r}")
+        mean = float(out.mean(dtype=np.float64))
         assert 600 < mean < 760   # SURVEY §8a: mean 678.6
     finally:
         ctx.pinned_free(out)

@@ -337,10 +337,12 @@ print("ok")
 
 
 def test_cfg5_full_size_row_sum_property(ctx):
-    """Full-size property for cfg5 (16384^3, the sampled-row check covers a
-    few rows): C.1 = A.(B.1) for every row. B.1 and A.(B.1) are computed in
-    fp64 on the host; each row sum of the GPU's C must match within the
-    fp32-GEMM tolerance scaled to the row's magnitude (sum_j |C_ij| bound)."""
+    """cfg5 at full size (16384^3): 32 sampled rows (first, last and 30 random)
+    against the fp64-accumulated oracle, normwise <= 1e-5 as BASELINE states;
+    then the size-independent property C.1 = A.(B.1) for every row. B.1 and
+    A.(B.1) are computed in fp64 on the host; each row sum of the GPU's C must
+    match within the fp32-GEMM tolerance scaled to the row's magnitude
+    (sum_j |C_ij| bound)."""
     import torch
     n = 16384
     A_h = oracle.fill_uniform(n * n, 1).reshape(n, n)
@@ -351,6 +353,8 @@ def test_cfg5_full_size_row_sum_property(ctx):
     s.wait_stream(torch.cuda.current_stream())
     ctx.sgemm_device(n, n, n, A.data_ptr(), B.data_ptr(), C.data_ptr(), s.cuda_stream)
     torch.cuda.synchronize()
+    err_rows = check(A_h, B_h, C.cpu().numpy(), nrows=30, seed=5)
+    assert err_rows <= TOL, err_rows
     got = C.to(torch.float64).sum(dim=1).cpu().numpy()
     absrow = C.abs().to(torch.float64).sum(dim=1).cpu().numpy()
     del A, B, C
