@@ -139,6 +139,17 @@ static bool peer_access_all(cafxg_ctx* ctx) {
       const cudaError_t e = cudaDeviceEnablePeerAccess(b->ordinal, 0);
       if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
         ok = -1;
+      // The slices of B come from b's stream-ordered pool (cudaMallocAsync),
+      // which cudaDeviceEnablePeerAccess does not cover: the pool itself
+      // must map its allocations for a, or a's TMA loads of them fault.
+      cudaMemPool_t pool;
+      cudaMemAccessDesc acc = {};
+      acc.location.type = cudaMemLocationTypeDevice;
+      acc.location.id = a->ordinal;
+      acc.flags = cudaMemAccessFlagsProtReadWrite;
+      if (cudaDeviceGetDefaultMemPool(&pool, b->ordinal) != cudaSuccess ||
+          cudaMemPoolSetAccess(pool, &acc, 1) != cudaSuccess)
+        ok = -1;
     }
   cudaGetLastError();
   ctx->p2p_state = ok;
