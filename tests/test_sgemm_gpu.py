@@ -377,7 +377,9 @@ def test_sgemm_randomised_shapes(ctx):
     shapes (multiples of 128 / 256 / 32) and odd ones (FFMA), host arrays
     with padded rows; every result within the fp32 tolerance."""
     rng = np.random.default_rng(int(os.environ.get("CAFXG_FUZZ_SEED", "11")))
-    for case in range(int(os.environ.get("CAFXG_FUZZ_CASES", "40"))):
+    cases = int(os.environ.get("CAFXG_FUZZ_CASES", "40"))
+    tc_shapes = 0
+    for case in range(cases):
         if rng.integers(0, 2):
             M, N, K = (int(rng.integers(1, 9)) * 128, int(rng.integers(1, 5)) * 256,
                        int(rng.integers(1, 33)) * 32)
@@ -396,3 +398,5 @@ def test_sgemm_randomised_shapes(ctx):
             (case, M, N, K, mode)
         if pc:
             assert np.isnan(Cbig[:, N:]).all()
+        tc_shapes += M % 128 == 0 and N % 256 == 0 and K % 32 == 0
+    print(f"sgemm fuzz: {cases} requests ({tc_shapes} tcgen05-eligible shapes) within {TOL}")
