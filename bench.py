@@ -703,6 +703,8 @@ def run_secondary(ctx, args, N, out=None):
         guarded(out, "cfg2_sgemm_1024", lambda: sec_sgemm(ctx, args, 1024, N))
         guarded(out, "paper_scale_run_mandelbrot_16000_500", lambda: sec_paper_scale(ctx))
     guarded(out, "cfg5_sgemm_16384", lambda: sec_sgemm(ctx, args, 16384, N))
+    if N > 1:
+        guarded(out, "cfg5_sgemm_16384_nccl_exchange", lambda: sec_sgemm_nccl(N))
     guarded(out, "cfg3_through_compute_actor", lambda: sec_cfg3_actor(ctx))
     try:
         out.update(sec_cfg4(ctx, args, N))
@@ -840,6 +842,53 @@ def sec_sgemm(ctx, args, n, N):
     for h in (hA, hB, hC):
         ctx.pinned_free(h)
     return res
+
+
+def sec_sgemm_nccl(N, n=16384):
+    """N > 1: cfg5 end to end on a second N-device context opened with
+    CAFXG_SGEMM_P2P=0, i.e. B replicated by the NCCL all-gather over NVLink
+    (ncclCommInitAll over the N GPUs) before each device's GEMM -- the
+    baseline the fused exchange (cfg5_sgemm_16384: every device's GEMM reads
+    B's slices from the peers in place) is measured against."""
+    import numpy as np
+
+    import paper_1505_07368_b200 as pkg
+    from oracle import oracle
+    old = os.environ.get("CAFXG_SGEMM_P2P")
+    os.environ["CAFXG_SGEMM_P2P"] = "0"   # read by cafxg_open, per context
+    try:
+        c2 = pkg.Context(device_mask=ctx_mask(N))
+    finally:
+        if old is None:
+            os.environ.pop("CAFXG_SGEMM_P2P", None)
+        else:
+            os.environ["CAFXG_SGEMM_P2P"] = old
+    try:
+        A_h = oracle.fill_uniform(n * n, 1).reshape(n, n)
+        B_h = oracle.fill_uniform(n * n, 2).reshape(n, n)
+        hA = c2.pinned_empty((n, n), np.float32)
+        hB = c2.pinned_empty((n, n), np.float32)
+        hC = c2.pinned_empty((n, n), np.float32)
+        hA[...] = A_h
+        hB[...] = B_h
+        st0 = c2.stats()
+        e2e = median_wall(lambda: c2.sgemm(hA, hB, hC), 3)
+        st1 = c2.stats()
+        samp = np.arange(0, n, max(1, n // 16), dtype=np.uint32)
+        R = oracle.sgemm_ref_rows(A_h, B_h, samp, n, n)
+        res = {"e2e_ms": round(e2e, 3),
+               "e2e_tflops": round(2.0 * n ** 3 / (e2e / 1e3) / 1e12, 2),
+               "n_gpus": N,
+               "nccl_collectives": int(st1.nccl_collectives - st0.nccl_collectives),
+               "peer_gemms": int(st1.peer_gemms - st0.peer_gemms),
+               "max_rel_err_e2e": oracle.sgemm_rel_err(hC, R, samp, n), "tolerance": 1e-5,
+               "path": "cafxg_sgemm over an N-device context with CAFXG_SGEMM_P2P=0: 1/N of B "
+                       "up per device, in-place ncclAllGather, then each device's GEMM"}
+        for h in (hA, hB, hC):
+            c2.pinned_free(h)
+        return res
+    finally:
+        c2.close()
 
 
 def sec_cfg3_actor(ctx):

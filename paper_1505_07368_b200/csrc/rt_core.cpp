@@ -383,6 +383,8 @@ int cafxg_open(uint64_t device_mask, cafxg_ctx** out) {
     for (int i = 0; i < n && i < 64; ++i)
       if (!device_mask || (device_mask >> i & 1))
         ords.push_back(i);
+    const char* p2p = getenv("CAFXG_SGEMM_P2P");
+    ctx->p2p_off = p2p && p2p[0] == '0';
     const char* vd = getenv("CAFXG_VIRTUAL_DEVICES");
     int vcount = vd ? atoi(vd) : 0;
     if (vcount > 1 && ords.size() == 1) {

@@ -112,14 +112,8 @@ int ensure_nccl(cafxg_ctx* ctx) {
 // earlier stages, and no device holds a full copy of B. Needs peer access
 // between every pair of the context's GPUs (virtual devices share one GPU,
 // where the "peer" slices are local: the same code path, tested on one GPU).
-// CAFXG_SGEMM_P2P=0 keeps the NCCL all-gather path.
-static bool p2p_wanted() {
-  static const bool on = [] {
-    const char* e = getenv("CAFXG_SGEMM_P2P");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+// CAFXG_SGEMM_P2P=0 at cafxg_open keeps that context on the NCCL all-gather
+// path (read per context, so one process can compare both exchanges).
 
 static bool peer_access_all(cafxg_ctx* ctx) {
   std::lock_guard<std::mutex> g(ctx->nccl_mu);  // (serialises the one-time enabling)
@@ -158,7 +152,7 @@ static bool peer_access_all(cafxg_ctx* ctx) {
 
 static bool p2p_eligible(cafxg_ctx* ctx, const cafxg_sgemm_desc& g, uint32_t rows_per) {
   const int G = (int)ctx->devs.size();
-  return G > 1 && p2p_wanted() && g.mode != CAFXG_SGEMM_FFMA && g.K % G == 0 &&
+  return G > 1 && !ctx->p2p_off && g.mode != CAFXG_SGEMM_FFMA && g.K % G == 0 &&
          g.M % 128 == 0 && rows_per % 128 == 0 && sgemm_tc_peer_supported(128, g.N, g.K, G) &&
          peer_access_all(ctx);
 }

@@ -395,6 +395,7 @@ struct cafxg_ctx {
   // NCCL communicators for multi-device sgemm (one per device)
   std::mutex nccl_mu;
   bool nccl_failed = false;
+  bool p2p_off = false;  // CAFXG_SGEMM_P2P=0 at open: B exchanged by NCCL, not read in place
   int p2p_state = 0;  // peer access between every pair of GPUs: 0 unknown, 1 yes, -1 no
   NcclApi nccl;
   std::vector<ncclComm_t> comms;
