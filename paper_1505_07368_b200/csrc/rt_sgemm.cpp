@@ -168,33 +168,78 @@ static int sgemm_p2p_submit(cafxg_ctx* ctx, const cafxg_sgemm_desc& g, const flo
     if (status == CAFXG_OK && s != CAFXG_OK)
       status = s;
   };
-  std::vector<float*> dB(G, nullptr), dBl(G, nullptr);
+  std::vector<float*> dB(G, nullptr), dBl(G, nullptr), dA(G, nullptr), dAl(G, nullptr),
+      dC(G, nullptr);
   std::vector<cudaEvent_t> ready(G, nullptr), done(G, nullptr);
-  // 1. each device: its K slice of B (and the slice's lo halves)
+  std::vector<std::vector<cudaEvent_t>> held(G);  // per device: events back to its pool
+  auto ev = [&](size_t k, cudaStream_t sm) {
+    cudaEvent_t e = pooled_event(ctx->devs[k].get());
+    if (e) {
+      cudaEventRecord(e, sm);
+      held[k].push_back(e);
+    }
+    return e;
+  };
+  auto rows_of = [&](size_t k) {
+    const size_t r0 = std::min<size_t>(M, rows_per * k), r1 = std::min<size_t>(M, rows_per * (k + 1));
+    return std::make_pair(r0, r1 - r0);
+  };
+  // A row blocks per device (whole 128-row tiles): uploads, GEMMs and
+  // downloads of consecutive blocks overlap on the three streams
+  auto blocks_of = [](size_t m) {
+    std::vector<size_t> b;
+    const size_t R = std::max<size_t>(128, (m / 4 + 127) / 128 * 128);
+    for (size_t r = 0; r < m; r += R)
+      b.push_back(std::min(R, m - r));
+    return b;
+  };
+  // 1. each device: buffers; its K slice of B up on the upload stream, then
+  // the slice's lo halves; its A row blocks up behind the slice
+  std::vector<std::vector<cudaEvent_t>> a_up(G);
   for (size_t k = 0; k < G; ++k) {
     Device* d = ctx->devs[k].get();
     cudaSetDevice(d->ordinal);
     cudaStream_t cs = d->compute;
+    const size_t m = rows_of(k).second;
     if (status == CAFXG_OK &&
         (cudaMallocAsync((void**)&dB[k], ks * N * 4, cs) != cudaSuccess ||
-         cudaMallocAsync((void**)&dBl[k], ks * N * 4, cs) != cudaSuccess))
-      note(cuda_status(cudaGetLastError(), "sgemm p2p: B slice allocation"));
+         cudaMallocAsync((void**)&dBl[k], ks * N * 4, cs) != cudaSuccess ||
+         (m && (cudaMallocAsync((void**)&dA[k], m * K * 4, cs) != cudaSuccess ||
+                cudaMallocAsync((void**)&dAl[k], m * K * 4, cs) != cudaSuccess ||
+                cudaMallocAsync((void**)&dC[k], m * N * 4, cs) != cudaSuccess))))
+      note(cuda_status(cudaGetLastError(), "sgemm p2p: allocation"));
+    if (status == CAFXG_OK)
+      note(stream_after_pooled(d, d->h2d, cs));
     if (status == CAFXG_OK) {
       note(cuda_status(cudaMemcpy2DAsync(dB[k], N * 4, B + k * ks * g.ldb, (size_t)g.ldb * 4,
-                                         N * 4, ks, cudaMemcpyHostToDevice, cs),
+                                         N * 4, ks, cudaMemcpyHostToDevice, d->h2d),
                        "sgemm p2p: B slice upload"));
       ctx->st_h2d += ks * N * 4;
     }
+    cudaEvent_t b_up = status == CAFXG_OK ? ev(k, d->h2d) : nullptr;
+    size_t r = rows_of(k).first;
+    for (size_t mb : blocks_of(m)) {
+      if (status != CAFXG_OK)
+        break;
+      note(cuda_status(cudaMemcpy2DAsync(dA[k] + (r - rows_of(k).first) * K, K * 4,
+                                         A + r * g.lda, (size_t)g.lda * 4, K * 4, mb,
+                                         cudaMemcpyHostToDevice, d->h2d),
+                       "sgemm p2p: A upload"));
+      ctx->st_h2d += mb * K * 4;
+      a_up[k].push_back(ev(k, d->h2d));
+      r += mb;
+    }
     if (status == CAFXG_OK) {
+      if (b_up)
+        cudaStreamWaitEvent(cs, b_up, 0);
       const int e = sgemm_tc_lo(dB[k], (int)N, (int)ks, (int)N, dBl[k], d->sms, cs);
       note(e ? cuda_status((cudaError_t)e, "sgemm p2p: B lo pass") : CAFXG_OK);
       ctx->st_launches++;
     }
-    ready[k] = pooled_event(d);
-    if (ready[k])
-      cudaEventRecord(ready[k], cs);
+    ready[k] = ev(k, cs);
   }
-  // 2. each device: its rows of A times all of B (peer slices read in place)
+  // 2. each device: its A row blocks times all of B (peer slices read in
+  // place), each block's C down as soon as its GEMM is done
   for (size_t k = 0; k < G; ++k) {
     Device* d = ctx->devs[k].get();
     cudaSetDevice(d->ordinal);
@@ -202,42 +247,42 @@ static int sgemm_p2p_submit(cafxg_ctx* ctx, const cafxg_sgemm_desc& g, const flo
     for (size_t j = 0; j < G; ++j)
       if (ready[j])
         cudaStreamWaitEvent(cs, ready[j], 0);
-    const size_t r0 = std::min<size_t>(M, rows_per * k), r1 = std::min<size_t>(M, rows_per * (k + 1));
-    const size_t m = r1 - r0;
-    if (status == CAFXG_OK && m) {
-      float *dA = nullptr, *dAl = nullptr, *dC = nullptr;
-      if (cudaMallocAsync((void**)&dA, m * K * 4, cs) != cudaSuccess ||
-          cudaMallocAsync((void**)&dAl, m * K * 4, cs) != cudaSuccess ||
-          cudaMallocAsync((void**)&dC, m * N * 4, cs) != cudaSuccess)
-        note(cuda_status(cudaGetLastError(), "sgemm p2p: A / C allocation"));
+    const auto [r0, m] = rows_of(k);
+    size_t off = 0, bi = 0;
+    for (size_t mb : blocks_of(m)) {
+      if (status != CAFXG_OK)
+        break;
+      if (bi < a_up[k].size() && a_up[k][bi])
+        cudaStreamWaitEvent(cs, a_up[k][bi], 0);
+      int e = sgemm_tc_lo(dA[k] + off * K, (int)K, (int)mb, (int)K, dAl[k] + off * K, d->sms,
+                          cs);
+      if (!e)
+        e = sgemm_tc_peer_gemm(dA[k] + off * K, (int)K, dAl[k] + off * K, (int)mb, (int)N,
+                               (int)K, dB.data(), dBl.data(), (int)G, dC[k] + off * N, (int)N,
+                               cs);
+      note(e ? cuda_status((cudaError_t)e, "sgemm p2p: GEMM launch") : CAFXG_OK);
+      ctx->st_launches += 2;
+      mark_used(ctx, d);
+      if (cudaEvent_t gdone = ev(k, cs))
+        cudaStreamWaitEvent(d->d2h, gdone, 0);
       if (status == CAFXG_OK) {
-        note(cuda_status(cudaMemcpy2DAsync(dA, K * 4, A + r0 * g.lda, (size_t)g.lda * 4, K * 4,
-                                           m, cudaMemcpyHostToDevice, cs),
-                         "sgemm p2p: A upload"));
-        ctx->st_h2d += m * K * 4;
-      }
-      if (status == CAFXG_OK) {
-        int e = sgemm_tc_lo(dA, (int)K, (int)m, (int)K, dAl, d->sms, cs);
-        if (!e)
-          e = sgemm_tc_peer_gemm(dA, (int)K, dAl, (int)m, (int)N, (int)K, dB.data(), dBl.data(),
-                                 (int)G, dC, (int)N, cs);
-        note(e ? cuda_status((cudaError_t)e, "sgemm p2p: GEMM launch") : CAFXG_OK);
-        ctx->st_launches += 2;
-        mark_used(ctx, d);
-      }
-      if (status == CAFXG_OK) {
-        note(cuda_status(cudaMemcpy2DAsync(C + r0 * g.ldc, (size_t)g.ldc * 4, dC, N * 4, N * 4,
-                                           m, cudaMemcpyDeviceToHost, cs),
+        note(cuda_status(cudaMemcpy2DAsync(C + (r0 + off) * g.ldc, (size_t)g.ldc * 4,
+                                           dC[k] + off * N, N * 4, N * 4, mb,
+                                           cudaMemcpyDeviceToHost, d->d2h),
                          "sgemm p2p: C download"));
-        ctx->st_d2h += m * N * 4;
+        ctx->st_d2h += mb * N * 4;
       }
-      for (float* p : {dA, dAl, dC})
-        if (p)
-          cudaFreeAsync(p, cs);
+      off += mb;
+      ++bi;
     }
-    done[k] = pooled_event(d);
-    if (done[k])
-      cudaEventRecord(done[k], cs);
+    done[k] = ev(k, cs);
+    // the part completes on the download stream, behind every kernel and
+    // copy of this device (also on failure: queued copies may still target
+    // the caller's buffers)
+    stream_after_pooled(d, d->d2h, cs);
+    for (float* p : {dA[k], dAl[k], dC[k]})
+      if (p)
+        cudaFreeAsync(p, d->d2h);
   }
   // 3. a slice is freed once every device's GEMM has read it; each device's
   // part completes behind that (so behind every device's download)
@@ -255,18 +300,17 @@ static int sgemm_p2p_submit(cafxg_ctx* ctx, const cafxg_sgemm_desc& g, const flo
   // every wait on the events is enqueued: back to their pools
   for (size_t k = 0; k < G; ++k) {
     Device* d = ctx->devs[k].get();
-    for (cudaEvent_t e : {ready[k], done[k]})
-      if (e)
-        d->ev_pool.push_back(e);
+    for (cudaEvent_t e : held[k])
+      d->ev_pool.push_back(e);
   }
   const int st = status;
   for (size_t k = 0; k < G; ++k) {
     Device* d = ctx->devs[k].get();
     cudaSetDevice(d->ordinal);
     if (st != CAFXG_OK)
-      push_completion(ctx, d, d->compute, [join, st](int) { join->part_done(st); });
+      push_completion(ctx, d, d->d2h, [join, st](int) { join->part_done(st); });
     else
-      push_completion(ctx, d, d->compute, [join](int s) { join->part_done(s); });
+      push_completion(ctx, d, d->d2h, [join](int s) { join->part_done(s); });
   }
   return CAFXG_OK;
 }
