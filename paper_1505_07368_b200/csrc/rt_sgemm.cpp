@@ -275,10 +275,11 @@ static int sgemm_p2p_submit(cafxg_ctx* ctx, const cafxg_sgemm_desc& g, const flo
       off += mb;
       ++bi;
     }
-    done[k] = ev(k, cs);
     // the part completes on the download stream, behind every kernel and
-    // copy of this device (also on failure: queued copies may still target
-    // the caller's buffers)
+    // copy of this device (also on failure: queued uploads may still read
+    // the caller's A and B, queued downloads write its C)
+    stream_after_pooled(d, cs, d->h2d);
+    done[k] = ev(k, cs);
     stream_after_pooled(d, d->d2h, cs);
     for (float* p : {dA[k], dAl[k], dC[k]})
       if (p)
