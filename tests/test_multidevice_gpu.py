@@ -72,6 +72,10 @@ def test_run_mandelbrot_chain(vctx, golden, size, it):
 
 @pytest.mark.parametrize("M,N,K,peer", [(768, 512, 384, True),    # B slices read in place
                                         (3072, 1024, 768, True),
+                                        # ragged shares (512 / 512 / 384 rows) and
+                                        # row blocks (4 / 4 / 3 of 128 per device)
+                                        (1408, 512, 384, True),
+                                        (1280, 768, 96, True),
                                         (3 * 128, 256, 3, False),  # K / V < 16: replicated B
                                         (384, 384, 768, False)])   # N % 256: replicated B
 def test_sgemm_row_blocks(vctx, M, N, K, peer):
@@ -87,7 +91,8 @@ def test_sgemm_row_blocks(vctx, M, N, K, peer):
     assert after.peer_gemms - before.peer_gemms == (1 if peer else 0)
     # B crossed PCIe once in total (1/V per device), A once
     assert after.h2d_bytes - before.h2d_bytes == (M * K + K * N) * 4
-    rows = np.unique(np.concatenate([np.arange(0, M, 61), [M // V - 1, M // V, M - 1]]))
+    rows = np.unique(np.concatenate([np.arange(0, M, 61), [M // V - 1, M // V, M - 1],
+                                     np.arange(127, M, 128), np.arange(128, M, 128)]))
     R = oracle.sgemm_ref_rows(A, B, rows.astype(np.uint32), N, K)
     assert oracle.sgemm_rel_err(C, R, rows.astype(np.uint32), N) <= 1e-5
 
