@@ -664,11 +664,18 @@ class Watchdog:
     def __init__(self, line, budget_s, dist):
         import threading
         self.line, self.dist, self.out = line, dist, {}
+        # the line is printed once: by the timer (which then exits) or, after
+        # cancel(), by the caller
+        self.lock, self.cancelled = threading.Lock(), False
         self.timer = threading.Timer(budget_s, self._fire)
         self.timer.daemon = True
         self.timer.start()
 
     def _fire(self):
+        self.lock.acquire()   # held until os._exit: cancel() then never returns
+        if self.cancelled:
+            self.lock.release()
+            return
         sec = dict(self.out)
         sec["watchdog"] = (f"secondaries stopped after {SECONDARY_BUDGET_S:.0f} s; "
                            "the entries present finished")
@@ -682,6 +689,8 @@ class Watchdog:
 
     def cancel(self):
         self.timer.cancel()
+        with self.lock:
+            self.cancelled = True
 
 
 def guarded(out, name, fn):
