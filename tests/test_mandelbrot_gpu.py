@@ -73,6 +73,24 @@ def test_cfg3_full_image_vs_oracle(ctx):
         ctx.pinned_free(out)
 
 
+def test_cfg3_region_fp64_full_image_vs_oracle(ctx):
+    """cfg3's region and size in fp64 (the bench's same-precision companion,
+    the reference's own precision): all 268,435,456 pixels against the fp64
+    oracle restatement, bit-exactly (~40 s of oracle on 16 host cores)."""
+    W = H = 16384
+    d = pkg.mandel_desc(-0.75, -0.73, 0.10, 0.12, W, H, 1000, fp64=True)
+    out = ctx.pinned_empty((H, W), np.uint32)
+    try:
+        ctx.mandelbrot(d, out)
+        ref = oracle.tile(-0.75, -0.73, 0.10, 0.12, W, H, 1000, fp64=True, centre=True)
+        bad = np.count_nonzero(out != ref)
+        if bad:
+            r = int(np.argwhere(out != ref)[0][0])
+            pytest.fail(f"{bad} of {W * H} pixels differ; first in row {r}")
+    finally:
+        ctx.pinned_free(out)
+
+
 def test_cfg3_full_image_two_kernels_agree():
     """Full-size property for cfg3 (all 268M pixels; the oracle checks sampled
     rows above): the per-step-checked kernel and the deferred-escape kernel are
