@@ -61,7 +61,7 @@ def test_multi_tile_request_over_devices(vctx):
         assert np.array_equal(got, r)
 
 
-@pytest.mark.parametrize("size,it", [(256, 100), (1024, 500)])
+@pytest.mark.parametrize("size,it", [(256, 100), (1024, 500), (16000, 500)])
 def test_run_mandelbrot_chain(vctx, golden, size, it):
     """Blocks on different devices, FNV chained block to block in row order."""
     want = int([g for g in golden["run_mandelbrot"]
