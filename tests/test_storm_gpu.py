@@ -34,3 +34,20 @@ def test_storm_all_modes(ctx):
             r = res[k]
             assert r["status"] == 0, (k, r)
             assert r["good"] == 8 * 64 and r["bad"] == 0 and r["errors"] == 0, (k, r)
+
+
+def test_storm_full_size_every_reply(ctx):
+    """BASELINE config 4 at its full size: 64 clients x 1,600 requests =
+    102,400 fp64 64x64 tiles in every client discipline, each reply checked
+    against the unmodified reference's mandelbrot_cell (the bench's own
+    measurement path, run here as a parity test)."""
+    args = types.SimpleNamespace(no_cpu_baseline=False)
+    res = bench.sec_cfg4(ctx, args, 1)
+    for k in ["cfg4_request_storm", "cfg4_request_storm_closed_loop",
+              "cfg4_request_storm_closed_loop_os_threads"]:
+        r = res[k]
+        assert r["status"] == 0 and r["errors"] == 0, (k, r)
+        assert r["checked_tiles"] == 102400 and r["mismatched_tiles"] == 0, (k, r)
+    for k in [k for k in res if k.startswith("cfg4_request_storm_cafx_actors")]:
+        r = res[k]
+        assert r["status"] == 0 and r["good"] == 102400 and r["bad"] == 0, (k, r)
