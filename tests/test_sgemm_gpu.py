@@ -400,3 +400,17 @@ def test_sgemm_randomised_shapes(ctx):
             assert np.isnan(Cbig[:, N:]).all()
         tc_shapes += M % 128 == 0 and N % 256 == 0 and K % 32 == 0
     print(f"sgemm fuzz: {cases} requests ({tc_shapes} tcgen05-eligible shapes) within {TOL}")
+
+
+def test_cfg2_every_row(ctx):
+    """BASELINE config 2 (C = A.B, 1024^3, A and B uniform[-1,1) from a seeded
+    generator) through the host request, EVERY row of C against the
+    fp64-accumulated oracle, normwise <= 1e-5."""
+    n = 1024
+    A = oracle.fill_uniform(n * n, 1).reshape(n, n)
+    B = oracle.fill_uniform(n * n, 2).reshape(n, n)
+    C = ctx.sgemm(A, B)
+    rows = np.arange(n, dtype=np.uint32)
+    R = oracle.sgemm_ref_rows(A, B, rows, n, n)
+    err = oracle.sgemm_rel_err(C, R, rows, n)
+    assert err <= TOL, err
