@@ -185,10 +185,21 @@ static int sgemm_p2p_submit(cafxg_ctx* ctx, const cafxg_sgemm_desc& g, const flo
     return std::make_pair(r0, r1 - r0);
   };
   // A row blocks per device (whole 128-row tiles): uploads, GEMMs and
-  // downloads of consecutive blocks overlap on the three streams
+  // downloads of consecutive blocks overlap on the three streams. Every
+  // block's GEMM streams all of B again (its K slices, 7/8 of them over
+  // NVLink at 8 GPUs), so blocks keep >= 1024 rows: B's bytes then stay at
+  // about 1/(3 x 1024 / 8) of the block's tensor flops (a quarter of cfg5's
+  // 2048 rows per device at 8 GPUs would re-read B 4x per device).
+  // CAFXG_P2P_RMIN overrides the minimum (tests: several blocks on small
+  // shapes).
+  static const size_t rmin = [] {
+    const char* e = getenv("CAFXG_P2P_RMIN");
+    const long v = e ? atol(e) : 0;
+    return v > 0 ? (size_t)(v + 127) / 128 * 128 : (size_t)1024;
+  }();
   auto blocks_of = [](size_t m) {
     std::vector<size_t> b;
-    const size_t R = std::max<size_t>(128, (m / 4 + 127) / 128 * 128);
+    const size_t R = std::max<size_t>(rmin, (m / 4 + 127) / 128 * 128);
     for (size_t r = 0; r < m; r += R)
       b.push_back(std::min(R, m - r));
     return b;

@@ -254,3 +254,34 @@ print("ok")
         ref = oracle.tile(-0.75, -0.73, 0.10, 0.12, 2048, 2048, 1000, fp64=False, centre=True)
         assert np.array_equal(out, ref)
         assert c.stats().devices_used == 0b11
+
+
+def test_sgemm_peer_path_several_row_blocks():
+    """The fused peer path's per-device pipeline with several A row blocks per
+    device (CAFXG_P2P_RMIN=128 lowers the 1024-row minimum block for these
+    small shapes), ragged shares included; every 128-row block boundary
+    checked against the fp64-accumulated oracle."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_1505_07368_b200 as pkg
+from oracle import oracle
+with pkg.Context(device_mask=1) as c:
+    for M, N, K in [(1408, 512, 384), (1280, 768, 96), (3072, 1024, 768)]:
+        A = oracle.fill_uniform(M * K, 41).reshape(M, K)
+        B = oracle.fill_uniform(K * N, 42).reshape(K, N)
+        s0 = c.stats(); C = c.sgemm(A, B); s1 = c.stats()
+        assert s1.peer_gemms - s0.peer_gemms == 1, (M, N, K)
+        rows = np.unique(np.concatenate([np.arange(127, M, 128), np.arange(128, M, 128),
+                                         [0, M - 1]])).astype(np.uint32)
+        err = oracle.sgemm_rel_err(C, oracle.sgemm_ref_rows(A, B, rows, N, K), rows, N)
+        assert err <= 1e-5, (M, N, K, err)
+print("ok")
+""" % root
+    env = dict(os.environ, CAFXG_VIRTUAL_DEVICES="3", CAFXG_P2P_RMIN="128")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
