@@ -187,9 +187,9 @@ static int sgemm_p2p_submit(cafxg_ctx* ctx, const cafxg_sgemm_desc& g, const flo
   // A row blocks per device (whole 128-row tiles): uploads, GEMMs and
   // downloads of consecutive blocks overlap on the three streams. Every
   // block's GEMM streams all of B again (its K slices, 7/8 of them over
-  // NVLink at 8 GPUs), so blocks keep >= 1024 rows: B's bytes then stay at
-  // about 1/(3 x 1024 / 8) of the block's tensor flops (a quarter of cfg5's
-  // 2048 rows per device at 8 GPUs would re-read B 4x per device).
+  // NVLink at 8 GPUs), so blocks keep >= 1024 rows: each block then does
+  // >= 6 x 1024 tensor flops (3 MMAs) per 8 bytes of B it streams (quarter
+  // blocks of cfg5's 2048 rows per device at 8 GPUs would read B 4x over).
   // CAFXG_P2P_RMIN overrides the minimum (tests: several blocks on small
   // shapes).
   static const size_t rmin = [] {
