@@ -14,11 +14,11 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 import paper_1505_07368_b200 as pkg  # noqa: E402
 
 
-def storm(n, it):
+def storm(n, it, kx_min=0):
     rng = np.random.default_rng(7)
     tiles = []
     for k in range(n):
-        kx, ky = int(rng.integers(0, 1473)), int(rng.integers(0, 961))
+        kx, ky = int(rng.integers(kx_min, 1473)), int(rng.integers(0, 961))
         x0, y0 = -2.0 + kx / 512, -1.0 + ky / 512
         tiles.append(pkg.mandel_desc(x0, x0 + 0.125, y0, y0 + 0.125, 64, 64, it, fp64=True,
                                      out_offset=k * 4096))
@@ -33,6 +33,9 @@ WORK = {
                                               5000)],
     "storm_fp64_4096x64sq_it256": storm(4096, 256),
     "storm_fp64_16x64sq_it256": storm(16, 256),
+    # the same storm with every tile at x >= -1.7 (all tiles clear of |c| ~ 2,
+    # so the deferred escape test may serve the whole batch)
+    "stormsafe_fp64_4096x64sq_it256": storm(4096, 256, kx_min=154),
     "storm_fp64_64x64sq_it256": storm(64, 256),
     "cfg1_fp32_1920x1080_it100": [pkg.mandel_desc(-2.0, 1.0, -1.0, 1.0, 1920, 1080, 100)],
     # cfg1's two host waves: the first 273 rows (512K pixels), then the rest
